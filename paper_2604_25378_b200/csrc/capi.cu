@@ -1,0 +1,464 @@
+// C-ABI implementation (include/mvsk_gpu.h): lifecycle, row sharding, the
+// oracle method set of mvsk::Oracle (oracle.hpp:29-149) and line_model
+// (linesearch.hpp:62-81). Host vectors cross the boundary; caches stay in HBM.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "host_ops.hpp"
+
+using namespace mvsk_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int32_t guard(mvsk_gpu_ctx* ctx, F&& f) {
+    try {
+        f();
+        return MVSK_OK;
+    } catch (const ApiError& e) {
+        if (ctx) ctx->err = e.what();
+        g_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        g_err = e.what();
+        return MVSK_INTERNAL_ERROR;
+    }
+}
+
+void set_device(mvsk_gpu_ctx* ctx) { MVSK_CUDA(cudaSetDevice(ctx->device)); }
+
+bool finite(const double* v, long long n) {
+    for (long long i = 0; i < n; ++i)
+        if (!std::isfinite(v[i])) return false;
+    return true;
+}
+
+void alloc_workspaces(mvsk_gpu_ctx* ctx) {
+    const size_t ld = (size_t)ctx->ld;
+    MVSK_CUDA(cudaMalloc(&ctx->mu_dev, ld * sizeof(double)));
+    MVSK_CUDA(cudaMemset(ctx->mu_dev, 0, ld * sizeof(double)));
+    MVSK_CUDA(cudaMemcpy(ctx->mu_dev, ctx->mu.data(), ctx->n * sizeof(double), cudaMemcpyHostToDevice));
+    MVSK_CUDA(cudaMalloc(&ctx->vin, (size_t)MVSK_GPU_MAX_RHS * 2 * ld * sizeof(double)));
+    MVSK_CUDA(cudaMemset(ctx->vin, 0, (size_t)MVSK_GPU_MAX_RHS * 2 * ld * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ctx->part_sc, (size_t)ctx->nsm * 4 * kNumScalars * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ctx->red, ((size_t)MVSK_GPU_MAX_RHS * ld + kNumScalars) * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ctx->outd, (size_t)MVSK_GPU_MAX_RHS * ld * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ctx->tvec, (size_t)std::max<long long>(1, ctx->T_local) * sizeof(double)));
+    for (auto& s : ctx->slots) {
+        MVSK_CUDA(cudaMalloc(&s.z, (size_t)std::max<long long>(1, ctx->T_local) * sizeof(double)));
+        MVSK_CUDA(cudaMalloc(&s.g, ld * sizeof(double)));
+        MVSK_CUDA(cudaMalloc(&s.sc, 8 * sizeof(double)));
+    }
+    ensure_host_staging(ctx, std::max<size_t>((size_t)MVSK_GPU_MAX_RHS * 2 * ld, (size_t)ctx->T_local + 16));
+}
+
+void free_all(mvsk_gpu_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->owns_X && ctx->X) cudaFree(ctx->X);
+    for (double* p : {ctx->mu_dev, ctx->zoff_dev, ctx->vin, ctx->part_acc, ctx->part_sc, ctx->red, ctx->outd,
+                      ctx->tvec, ctx->gram, ctx->gram_part, ctx->tvec2, ctx->pmat})
+        if (p) cudaFree(p);
+    for (auto& s : ctx->slots) {
+        if (s.z) cudaFree(s.z);
+        if (s.g) cudaFree(s.g);
+        if (s.sc) cudaFree(s.sc);
+    }
+    if (ctx->h_in) cudaFreeHost(ctx->h_in);
+    if (ctx->h_out) cudaFreeHost(ctx->h_out);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+mvsk_gpu_ctx* make_ctx(long long T_local, long long row0, long long T_global, long long n, const double* mu,
+                       const mvsk_coeffs* c, int device, int nranks, int rank, const void* id) {
+    if (n < 1) throw ApiError(MVSK_DIMENSION_ERROR, "oracle: need at least one asset");
+    if (T_global < 1 || T_local < 0 || row0 < 0 || row0 + T_local > T_global)
+        throw ApiError(MVSK_DIMENSION_ERROR, "oracle: bad row block");
+    if (!mu || !c) throw ApiError(MVSK_DIMENSION_ERROR, "oracle: mu length does not match panel columns");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw ApiError(MVSK_DOMAIN_ERROR, "bad rank / nranks");
+    int ndev = 0;
+    MVSK_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw ApiError(MVSK_CUDA_ERROR, "no such CUDA device");
+    auto* ctx = new mvsk_gpu_ctx();
+    try {
+        ctx->device = device;
+        MVSK_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        MVSK_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            throw ApiError(MVSK_CUDA_ERROR, "device is not Blackwell (sm_100a build)");
+        ctx->nsm = prop.multiProcessorCount;
+        ctx->max_smem = prop.sharedMemPerBlockOptin;
+        MVSK_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+        ctx->stream = ctx->own_stream;
+        ctx->T_local = T_local;
+        ctx->T_global = T_global;
+        ctx->row0 = row0;
+        ctx->n = n;
+        ctx->ld = (n + 1) / 2 * 2;
+        ctx->pub_face.m = n;
+        ctx->mu.assign(mu, mu + n);
+        ctx->c = *c;
+        ctx->nranks = nranks;
+        ctx->rank = rank;
+        if (nranks > 1) {
+            if (!id) throw ApiError(MVSK_DOMAIN_ERROR, "nccl unique id required for nranks > 1");
+            ncclUniqueId uid;
+            std::memcpy(&uid, id, sizeof(uid));
+            MVSK_NCCL(ncclCommInitRank(&ctx->comm, nranks, uid, rank));
+        }
+        return ctx;
+    } catch (...) {
+        free_all(ctx);
+        throw;
+    }
+}
+
+void upload_panel(mvsk_gpu_ctx* ctx, const double* A_rows) {
+    const size_t bytes = (size_t)std::max<long long>(1, ctx->T_local) * ctx->ld * sizeof(double);
+    MVSK_CUDA(cudaMalloc(&ctx->X, bytes));
+    ctx->owns_X = true;
+    if (ctx->T_local == 0) return;
+    if (ctx->ld == ctx->n) {
+        MVSK_CUDA(cudaMemcpy(ctx->X, A_rows, (size_t)ctx->T_local * ctx->n * sizeof(double), cudaMemcpyHostToDevice));
+    } else {
+        MVSK_CUDA(cudaMemset(ctx->X, 0, bytes));
+        MVSK_CUDA(cudaMemcpy2D(ctx->X, ctx->ld * sizeof(double), A_rows, ctx->n * sizeof(double),
+                               ctx->n * sizeof(double), ctx->T_local, cudaMemcpyHostToDevice));
+    }
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int32_t mvsk_gpu_abi_version(void) { return MVSK_GPU_ABI_VERSION; }
+
+const char* mvsk_gpu_status_string(int32_t s) {
+    switch (s) {
+    case MVSK_OK: return "ok";
+    case MVSK_DIMENSION_ERROR: return "dimension_error";
+    case MVSK_DOMAIN_ERROR: return "domain_error";
+    case MVSK_DATA_ERROR: return "data_error";
+    case MVSK_NUMERIC_ERROR: return "numeric_error";
+    case MVSK_CUDA_ERROR: return "cuda_error";
+    case MVSK_NCCL_ERROR: return "nccl_error";
+    default: return "internal_error";
+    }
+}
+
+int32_t mvsk_gpu_nccl_unique_id(void* out) {
+    return guard(nullptr, [&] {
+        ncclUniqueId id;
+        MVSK_NCCL(ncclGetUniqueId(&id));
+        static_assert(sizeof(id) == MVSK_NCCL_UNIQUE_ID_BYTES, "nccl id size");
+        std::memcpy(out, &id, sizeof(id));
+    });
+}
+
+int32_t mvsk_gpu_create(const double* A, int64_t T, int64_t n, const double* mu, const mvsk_coeffs* c,
+                        int32_t device, mvsk_gpu_ctx** out) {
+    return mvsk_gpu_create_sharded(A, T, 0, T, n, mu, c, device, 1, 0, nullptr, out);
+}
+
+int32_t mvsk_gpu_create_sharded(const double* A_rows, int64_t T_local, int64_t row0, int64_t T_global, int64_t n,
+                                const double* mu, const mvsk_coeffs* c, int32_t device, int32_t nranks,
+                                int32_t rank, const void* nccl_unique_id, mvsk_gpu_ctx** out) {
+    return guard(nullptr, [&] {
+        if (!out) throw ApiError(MVSK_DOMAIN_ERROR, "null out");
+        *out = nullptr;
+        mvsk_gpu_ctx* ctx = make_ctx(T_local, row0, T_global, n, mu, c, device, nranks, rank, nccl_unique_id);
+        try {
+            upload_panel(ctx, A_rows);
+            alloc_workspaces(ctx);
+        } catch (...) {
+            free_all(ctx);
+            throw;
+        }
+        *out = ctx;
+    });
+}
+
+int32_t mvsk_gpu_create_from_device(const double* A_dev, int64_t ld, int64_t T_local, int64_t row0,
+                                    int64_t T_global, int64_t n, const double* mu, const mvsk_coeffs* c,
+                                    int32_t device, int32_t nranks, int32_t rank, const void* nccl_unique_id,
+                                    mvsk_gpu_ctx** out) {
+    return guard(nullptr, [&] {
+        if (!out) throw ApiError(MVSK_DOMAIN_ERROR, "null out");
+        *out = nullptr;
+        if (ld < n || (ld & 1) || (reinterpret_cast<uintptr_t>(A_dev) & 15))
+            throw ApiError(MVSK_DIMENSION_ERROR, "device panel needs even ld >= n and a 16-byte aligned base");
+        mvsk_gpu_ctx* ctx = make_ctx(T_local, row0, T_global, n, mu, c, device, nranks, rank, nccl_unique_id);
+        try {
+            ctx->ld = ld;
+            ctx->X = const_cast<double*>(A_dev);
+            ctx->owns_X = false;
+            alloc_workspaces(ctx);
+        } catch (...) {
+            free_all(ctx);
+            throw;
+        }
+        *out = ctx;
+    });
+}
+
+int32_t mvsk_gpu_destroy(mvsk_gpu_ctx* ctx) {
+    free_all(ctx);
+    return MVSK_OK;
+}
+
+const char* mvsk_gpu_last_error(const mvsk_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int32_t mvsk_gpu_set_stream(mvsk_gpu_ctx* ctx, void* stream) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    });
+}
+
+int32_t mvsk_gpu_synchronize(mvsk_gpu_ctx* ctx) {
+    return guard(ctx, [&] { MVSK_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int32_t mvsk_gpu_dims(const mvsk_gpu_ctx* ctx, int64_t* T_global, int64_t* T_local, int64_t* n) {
+    if (T_global) *T_global = ctx->T_global;
+    if (T_local) *T_local = ctx->T_local;
+    if (n) *n = ctx->n;
+    return MVSK_OK;
+}
+
+int32_t mvsk_gpu_set_offset(mvsk_gpu_ctx* ctx, const double* zoff, double value_offset) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        if (zoff) {
+            if (!ctx->zoff_dev)
+                MVSK_CUDA(cudaMalloc(&ctx->zoff_dev, (size_t)std::max<long long>(1, ctx->T_local) * sizeof(double)));
+            MVSK_CUDA(cudaMemcpy(ctx->zoff_dev, zoff, ctx->T_local * sizeof(double), cudaMemcpyHostToDevice));
+        } else if (ctx->zoff_dev) {
+            MVSK_CUDA(cudaFree(ctx->zoff_dev));
+            ctx->zoff_dev = nullptr;
+        }
+        ctx->value_offset = value_offset;
+        for (auto& s : ctx->slots) s.valid = false;
+    });
+}
+
+int32_t mvsk_gpu_set_face(mvsk_gpu_ctx* ctx, const int64_t* free_idx, int64_t nf, double tau) {
+    return guard(ctx, [&] {
+        if (nf < 1 || nf > ctx->n) throw ApiError(MVSK_DOMAIN_ERROR, "degenerate face, all coordinates pinned");
+        FaceMap f;
+        f.tau = tau;
+        f.m = nf;
+        if (nf == ctx->n && !free_idx) {
+            f.active = false;
+        } else {
+            if (!free_idx) throw ApiError(MVSK_DOMAIN_ERROR, "face needs free indices");
+            f.idx.assign(free_idx, free_idx + nf);
+            for (long long j = 0; j < nf; ++j)
+                if (f.idx[j] < 0 || f.idx[j] >= ctx->n || (j && f.idx[j] <= f.idx[j - 1]))
+                    throw ApiError(MVSK_DOMAIN_ERROR, "free indices must be increasing and in range");
+            f.active = nf != ctx->n;
+        }
+        ctx->pub_face = f;
+        for (auto& s : ctx->slots) s.valid = false;
+    });
+}
+
+int32_t mvsk_gpu_make_cache(mvsk_gpu_ctx* ctx, int32_t slot, const double* x, double* f_out) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        const double f = op_make_cache(ctx, slot, ctx->pub_face, x);
+        if (f_out) *f_out = f;
+    });
+}
+
+int32_t mvsk_gpu_value(mvsk_gpu_ctx* ctx, int32_t slot, double* f_out) {
+    return guard(ctx, [&] {
+        check_slot(ctx, slot);
+        *f_out = ctx->slots[slot].f;
+    });
+}
+
+int32_t mvsk_gpu_moments(mvsk_gpu_ctx* ctx, int32_t slot, double out[4]) {
+    return guard(ctx, [&] { op_moments(ctx, slot, out); });
+}
+
+int32_t mvsk_gpu_gradient(mvsk_gpu_ctx* ctx, int32_t slot, double* g_out) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        op_gradient(ctx, slot, ctx->pub_face, g_out);
+    });
+}
+
+int32_t mvsk_gpu_hvp(mvsk_gpu_ctx* ctx, int32_t slot, const double* V, int32_t k, double* HV) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        op_hvp(ctx, slot, ctx->pub_face, V, k, HV);
+    });
+}
+
+int32_t mvsk_gpu_third_action(mvsk_gpu_ctx* ctx, int32_t slot, const double* U, const double* V, int32_t k,
+                              double* out) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        op_third(ctx, slot, ctx->pub_face, U, V, k, out);
+    });
+}
+
+int32_t mvsk_gpu_hessian_diag_weights(mvsk_gpu_ctx* ctx, int32_t slot, double* out) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        op_psi2(ctx, slot, out);
+    });
+}
+
+int32_t mvsk_gpu_sample_direction(mvsk_gpu_ctx* ctx, const double* d, double* out) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        op_sample_direction(ctx, ctx->pub_face, d, out);
+    });
+}
+
+int32_t mvsk_gpu_line_model(mvsk_gpu_ctx* ctx, int32_t slot, const double* d, double cap, double out[14]) {
+    (void)cap;  // alpha_cap only parameterises the host-side minimisation
+    return guard(ctx, [&] {
+        set_device(ctx);
+        op_line_model(ctx, slot, ctx->pub_face, d, out);
+    });
+}
+
+int32_t mvsk_gpu_weighted_gram(mvsk_gpu_ctx* ctx, int32_t slot, double* G_out) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        op_weighted_gram(ctx, slot, ctx->pub_face, G_out);
+    });
+}
+
+int32_t mvsk_gpu_weighted_gram_device(mvsk_gpu_ctx* ctx, int32_t slot, double* G_dev) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        check_slot(ctx, slot);
+        run_psi2(ctx, ctx->slots[slot].z, ctx->tvec, ctx->T_local);
+        run_weighted_gram(ctx, ctx->tvec, G_dev, 1.0 / (double)ctx->T_global);
+        ctx->fwd += 1;
+    });
+}
+
+int32_t mvsk_gpu_passes(const mvsk_gpu_ctx* ctx, uint64_t* forward, uint64_t* transpose, uint64_t* physical) {
+    if (forward) *forward = ctx->fwd;
+    if (transpose) *transpose = ctx->tr;
+    if (physical) *physical = ctx->phys;
+    return MVSK_OK;
+}
+
+int32_t mvsk_gpu_reset_passes(mvsk_gpu_ctx* ctx) {
+    ctx->fwd = ctx->tr = ctx->phys = 0;
+    return MVSK_OK;
+}
+
+// ---- device-resident fast path ---------------------------------------------
+int32_t mvsk_gpu_make_cache_device(mvsk_gpu_ctx* ctx, int32_t slot, const double* x_dev) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        check_slot(ctx, slot, false);
+        if (ctx->pub_face.active) throw ApiError(MVSK_DOMAIN_ERROR, "device path works on the full problem (no face)");
+        MVSK_CUDA(cudaMemcpyAsync(ctx->vin, x_dev, ctx->n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        PassIO io;
+        io.vin = ctx->vin;
+        io.slot = slot;
+        io.x_for_mux = ctx->vin;
+        run_pass(ctx, Op::FGRAD, 1, io);
+        ctx->fwd += 1;
+        ctx->slots[slot].valid = true;  // scalars stay on device (slot sc)
+        ctx->slots[slot].grad_counted = false;
+    });
+}
+
+int32_t mvsk_gpu_hvp_device(mvsk_gpu_ctx* ctx, int32_t slot, const double* V_dev, int32_t k, double* HV_dev) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        check_slot(ctx, slot);
+        if (k < 1 || k > MVSK_GPU_MAX_RHS) throw ApiError(MVSK_DIMENSION_ERROR, "hvp: k out of range");
+        const double* vin = V_dev;
+        if (ctx->ld != ctx->n) {
+            MVSK_CUDA(cudaMemcpy2DAsync(ctx->vin, ctx->ld * sizeof(double), V_dev, ctx->n * sizeof(double),
+                                        ctx->n * sizeof(double), k, cudaMemcpyDeviceToDevice, ctx->stream));
+            vin = ctx->vin;
+        }
+        PassIO io;
+        io.vin = vin;
+        io.z = ctx->slots[slot].z;
+        io.out = HV_dev;
+        io.ldo = ctx->n;
+        run_pass(ctx, Op::HVP, k, io);
+        ctx->fwd += k;
+        ctx->tr += k;
+    });
+}
+
+int32_t mvsk_gpu_third_action_device(mvsk_gpu_ctx* ctx, int32_t slot, const double* U_dev, const double* V_dev,
+                                     int32_t k, double* out_dev) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        check_slot(ctx, slot);
+        if (k < 1 || k > MVSK_GPU_MAX_RHS) throw ApiError(MVSK_DIMENSION_ERROR, "third_action: k out of range");
+        const double* u = U_dev;
+        const double* v = V_dev;
+        if (ctx->ld != ctx->n) {
+            MVSK_CUDA(cudaMemcpy2DAsync(ctx->vin, ctx->ld * sizeof(double), U_dev, ctx->n * sizeof(double),
+                                        ctx->n * sizeof(double), k, cudaMemcpyDeviceToDevice, ctx->stream));
+            MVSK_CUDA(cudaMemcpy2DAsync(ctx->vin + (size_t)MVSK_GPU_MAX_RHS * ctx->ld, ctx->ld * sizeof(double), V_dev,
+                                        ctx->n * sizeof(double), ctx->n * sizeof(double), k, cudaMemcpyDeviceToDevice,
+                                        ctx->stream));
+            u = ctx->vin;
+            v = ctx->vin + (size_t)MVSK_GPU_MAX_RHS * ctx->ld;
+        }
+        PassIO io;
+        io.vin = u;
+        io.vin2 = v;
+        io.z = ctx->slots[slot].z;
+        io.out = out_dev;
+        io.ldo = ctx->n;
+        run_pass(ctx, Op::THIRD, k, io);
+        ctx->fwd += 2 * k;
+        ctx->tr += k;
+    });
+}
+
+int32_t mvsk_gpu_line_sums_device(mvsk_gpu_ctx* ctx, int32_t slot, const double* d_dev, double* sums_dev) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        check_slot(ctx, slot);
+        const double* d = d_dev;
+        if (ctx->ld != ctx->n) {
+            MVSK_CUDA(cudaMemcpyAsync(ctx->vin, d_dev, ctx->n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+            d = ctx->vin;
+        }
+        PassIO io;
+        io.vin = d;
+        io.z = ctx->slots[slot].z;
+        io.out = sums_dev;
+        run_pass(ctx, Op::LINESUMS, 1, io);
+        ctx->fwd += 1;
+    });
+}
+
+int32_t mvsk_gpu_slot_pointers(mvsk_gpu_ctx* ctx, int32_t slot, double** z, double** grad, double** scalars) {
+    return guard(ctx, [&] {
+        check_slot(ctx, slot, false);
+        if (z) *z = ctx->slots[slot].z;
+        if (grad) *grad = ctx->slots[slot].g;
+        if (scalars) *scalars = ctx->slots[slot].sc;
+    });
+}
+
+}  // extern "C"

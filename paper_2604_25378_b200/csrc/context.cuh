@@ -1,0 +1,106 @@
+// Device context behind the C-ABI: resident panel shard, per-slot caches,
+// workspaces, stream and the NCCL communicator of the row-shard group.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mvsk_gpu.h"
+#include "stream_kernels.cuh"
+
+namespace mvsk_b200 {
+
+struct ApiError : std::runtime_error {
+    int code;
+    ApiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define MVSK_CUDA(call)                                                                             \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            throw ::mvsk_b200::ApiError(MVSK_CUDA_ERROR, std::string(#call " failed: ") +           \
+                                                             cudaGetErrorString(e_));               \
+    } while (0)
+
+#define MVSK_NCCL(call)                                                                              \
+    do {                                                                                             \
+        ncclResult_t r_ = (call);                                                                    \
+        if (r_ != ncclSuccess)                                                                       \
+            throw ::mvsk_b200::ApiError(MVSK_NCCL_ERROR, std::string(#call " failed: ") +            \
+                                                             ncclGetErrorString(r_));                \
+    } while (0)
+
+struct Slot {
+    double* z = nullptr;   // T_local
+    double* g = nullptr;   // ld (gradient, full coordinates)
+    double* sc = nullptr;  // [f, mu'x, Ez2, Ez3, Ez4, ...] (8)
+    bool valid = false;
+    bool grad_counted = false;
+    double f = 0.0;
+    double mom[4] = {0, 0, 0, 0};
+    std::vector<double> x_full;  // host copy of the cached point (full coordinates)
+};
+
+// Face view over the resident panel (replaces the column-gathered face panel of
+// solver.hpp:343-363): vectors in face coordinates map to full coordinates with
+// the pinned entries fixed (tau for iterates, 0 for directions).
+struct FaceMap {
+    bool active = false;
+    std::vector<int64_t> idx;  // free coordinates, increasing
+    double tau = 0.0;
+    long long m = 0;           // vector length in face coordinates
+};
+
+}  // namespace mvsk_b200
+
+struct mvsk_gpu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    int nsm = 148;
+    size_t max_smem = 227 * 1024;
+
+    long long T_global = 0, T_local = 0, row0 = 0;
+    long long n = 0, ld = 0;
+    double* X = nullptr;
+    bool owns_X = false;
+    double* mu_dev = nullptr;  // ld, zero padded
+    std::vector<double> mu;    // n
+    mvsk_coeffs c{};
+    double* zoff_dev = nullptr;  // T_local or null
+    double value_offset = 0.0;
+
+    // face selected through the C-ABI (mvsk_gpu_set_face)
+    mvsk_b200::FaceMap pub_face;
+
+    mvsk_b200::Slot slots[MVSK_GPU_MAX_SLOTS];
+
+    // workspaces (device)
+    double* vin = nullptr;  // MVSK_GPU_MAX_RHS * 2 * ld input staging
+    double* part_acc = nullptr;
+    size_t part_acc_elems = 0;
+    double* part_sc = nullptr;
+    double* red = nullptr;   // MVSK_GPU_MAX_RHS * ld + kNumScalars
+    double* outd = nullptr;  // MVSK_GPU_MAX_RHS * ld output staging
+    double* tvec = nullptr;  // T_local scratch (sample directions / weights)
+    double* gram = nullptr;  // n x n (lazy)
+    double* tvec2 = nullptr; // T_local scratch (lazy)
+    double* pmat = nullptr;  // ld x ld (lazy)
+    double* gram_part = nullptr;
+    size_t gram_part_elems = 0;
+    // pinned host staging
+    double* h_in = nullptr;
+    double* h_out = nullptr;
+    size_t h_elems = 0;
+
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+
+    uint64_t fwd = 0, tr = 0, phys = 0;
+    std::string err;
+};

@@ -1,0 +1,273 @@
+// Dense contractions of the direct branch (affine_normal.hpp:151-188):
+//   * weighted Gram  G = X^T diag(w) X        — fp64 tensor cores (DMMA,
+//     mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4), 128x128 output tiles, lower
+//     triangle only, cp.async double-buffered row chunks, deterministic
+//     split-K over samples;
+//   * per-row quadratic forms q_t = x_t^T P x_t (the diag(W M^-1 W^T) of
+//     affine_normal.hpp:175-176, with P = UQ M^-1 (UQ)^T).
+// fp64 has no tcgen05 kind on sm_100a (CUDA 12.9 exposes f16/tf32/f8f6f4/i8/
+// mxf4 only), so DMMA through mma.sync is the tensor-core path for fp64.
+#include <algorithm>
+
+#include "oracle_ops.cuh"
+
+namespace mvsk_b200 {
+
+namespace {
+
+constexpr int GBM = 128;            // output tile (square)
+constexpr int GBK = 16;             // sample rows per chunk
+constexpr int GPAD = 4;             // smem row pad (doubles): conflict-free fragment loads
+constexpr int GLDS = GBM + GPAD;    // smem row stride
+constexpr int GTHREADS = 256;       // 8 warps: 4 (m) x 2 (n), warp tile 32 x 64
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+struct GramArgs {
+    const double* X;  // T x ld
+    const double* w;  // T sample weights
+    long long T;
+    int ld;
+    int ntile;          // tiles per dimension
+    int nsplit;         // sample splits
+    double* part;       // [nsplit][npairs][GBM*GBM]
+};
+
+// tile pair index -> (ti, tj), ti >= tj
+__device__ __forceinline__ void pair_of(int p, int& ti, int& tj) {
+    int i = (int)((sqrt(8.0 * p + 1.0) - 1.0) * 0.5);
+    while ((i + 1) * (i + 2) / 2 <= p) ++i;
+    while (i * (i + 1) / 2 > p) --i;
+    ti = i;
+    tj = p - i * (i + 1) / 2;
+}
+
+__global__ void __launch_bounds__(GTHREADS, 1) syrk_dmma_kernel(const GramArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* sA = reinterpret_cast<double*>(smem_raw);           // [2][GBK][GLDS]
+    double* sB = sA + 2 * GBK * GLDS;                            // [2][GBK][GLDS]
+    double* sw = sB + 2 * GBK * GLDS;                            // [2][GBK]
+    int ti, tj;
+    pair_of(blockIdx.x, ti, tj);
+    const int i0 = ti * GBM, j0 = tj * GBM;
+    const int split = blockIdx.y;
+    const long long t_lo = a.T * split / a.nsplit, t_hi = a.T * (split + 1) / a.nsplit;
+    const int nchunk = (int)((t_hi - t_lo + GBK - 1) / GBK);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;  // warp tile origin (wm*32, wn*64)
+
+    auto load_chunk = [&](int c, int buf) {
+        const long long t0 = t_lo + (long long)c * GBK;
+        // 16 rows x 128 doubles per operand = 1024 16-byte pieces each; 256 threads -> 4 + 4
+        for (int e = tid; e < GBK * (GBM / 2); e += GTHREADS) {
+            const int r = e / (GBM / 2), cp = e - r * (GBM / 2);
+            const long long t = t0 + r;
+            const bool rv = t < t_hi;
+            const int ca = i0 + 2 * cp, cb = j0 + 2 * cp;
+            const double* ga = a.X + (rv ? t : 0) * (long long)a.ld + (ca < a.ld ? ca : 0);
+            const double* gb = a.X + (rv ? t : 0) * (long long)a.ld + (cb < a.ld ? cb : 0);
+            cp_async16(sA + (buf * GBK + r) * GLDS + 2 * cp, ga, (rv && ca < a.ld) ? 16 : 0);
+            cp_async16(sB + (buf * GBK + r) * GLDS + 2 * cp, gb, (rv && cb < a.ld) ? 16 : 0);
+        }
+        if (tid < GBK) {
+            const long long t = t0 + tid;
+            sw[buf * GBK + tid] = t < t_hi ? a.w[t] : 0.0;
+        }
+    };
+
+    double acc[4][8][2];
+#pragma unroll
+    for (int fm = 0; fm < 4; ++fm)
+#pragma unroll
+        for (int fn = 0; fn < 8; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
+
+    if (nchunk > 0) load_chunk(0, 0);
+    cp_async_commit();
+    for (int c = 0; c < nchunk; ++c) {
+        const int buf = c & 1;
+        if (c + 1 < nchunk) load_chunk(c + 1, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const double* A = sA + buf * GBK * GLDS;
+        const double* B = sB + buf * GBK * GLDS;
+        const double* W = sw + buf * GBK;
+#pragma unroll
+        for (int k0 = 0; k0 < GBK; k0 += 4) {
+            const int kr = k0 + (lane & 3);
+            const double wk = W[kr];
+            double af[4], bf[8];
+#pragma unroll
+            for (int fm = 0; fm < 4; ++fm) af[fm] = A[kr * GLDS + wm * 32 + fm * 8 + (lane >> 2)];
+#pragma unroll
+            for (int fn = 0; fn < 8; ++fn) bf[fn] = wk * B[kr * GLDS + wn * 64 + fn * 8 + (lane >> 2)];
+#pragma unroll
+            for (int fm = 0; fm < 4; ++fm)
+#pragma unroll
+                for (int fn = 0; fn < 8; ++fn) dmma_8x8x4(acc[fm][fn], af[fm], bf[fn]);
+        }
+        __syncthreads();
+    }
+    // partial tile out (row-major 128 x 128)
+    double* out = a.part + ((size_t)split * gridDim.x + blockIdx.x) * (GBM * GBM);
+#pragma unroll
+    for (int fm = 0; fm < 4; ++fm)
+#pragma unroll
+        for (int fn = 0; fn < 8; ++fn) {
+            const int r = wm * 32 + fm * 8 + (lane >> 2);
+            const int cc = wn * 64 + fn * 8 + (lane & 3) * 2;
+            *reinterpret_cast<double2*>(out + r * GBM + cc) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+        }
+}
+
+// sum splits in order, scale, mirror into the dense n x n result
+__global__ void gram_finish_kernel(const double* part, int npairs, int nsplit, int n, double scale, double* G,
+                                   long long ldg) {
+    const int p = blockIdx.x;
+    int ti, tj;
+    pair_of(p, ti, tj);
+    for (int e = threadIdx.x; e < GBM * GBM; e += blockDim.x) {
+        const int r = e / GBM, c = e - r * GBM;
+        const int i = ti * GBM + r, j = tj * GBM + c;
+        if (i >= n || j >= n) continue;
+        double v = 0.0;
+        for (int s = 0; s < nsplit; ++s) v += part[((size_t)s * npairs + p) * (GBM * GBM) + e];
+        v *= scale;
+        if (ti == tj) {
+            if (j <= i) {
+                G[(long long)i * ldg + j] = v;
+                G[(long long)j * ldg + i] = v;
+            }
+        } else {
+            G[(long long)i * ldg + j] = v;
+            G[(long long)j * ldg + i] = v;
+        }
+    }
+}
+
+// q_t = x_t^T P x_t for RB rows per block; P is ld x ld (zero outside the face)
+template <int RB>
+__global__ void quadform_kernel(const double* X, long long T, int ld, const double* P, double* q) {
+    extern __shared__ __align__(16) double xs[];  // [RB][ld]
+    const long long t0 = (long long)blockIdx.x * RB;
+    const int rows = (int)min((long long)RB, T - t0);
+    for (int e = threadIdx.x; e < RB * ld; e += blockDim.x) {
+        const int r = e / ld;
+        xs[e] = r < rows ? X[(t0 + r) * ld + (e - r * ld)] : 0.0;
+    }
+    __syncthreads();
+    double part[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) part[r] = 0.0;
+    for (int c = threadIdx.x; c < ld; c += blockDim.x) {
+        double y[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) y[r] = 0.0;
+        for (int i = 0; i < ld; ++i) {
+            const double pic = P[(long long)i * ld + c];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) y[r] = fma(xs[r * ld + i], pic, y[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < RB; ++r) part[r] = fma(y[r], xs[r * ld + c], part[r]);
+    }
+    __shared__ double red[RB][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+        double v = part[r];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[r][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < RB && threadIdx.x < rows) {
+        double v = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[threadIdx.x][w];
+        q[t0 + threadIdx.x] = v;
+    }
+}
+
+// tw_t = psi'''(z_t) q_t / T   (affine_normal.hpp:174-177)
+__global__ void third_weights_kernel(const double* z, const double* q, double* tw, long long T, double c3, double c4,
+                                     double Tg) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < T; t += (long long)gridDim.x * blockDim.x) {
+        const double psi3 = -6.0 * c3 + 24.0 * c4 * z[t];
+        tw[t] = psi3 * q[t] / Tg;
+    }
+}
+
+}  // namespace
+
+void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, double scale) {
+    const int n = (int)ctx->n;
+    const int ntile = (n + GBM - 1) / GBM;
+    const int npairs = ntile * (ntile + 1) / 2;
+    // split the sample range so that >= 1 wave of CTAs is busy, min 256 rows / split
+    int nsplit = std::max(1, ctx->nsm / npairs);
+    nsplit = (int)std::max<long long>(1, std::min<long long>(nsplit, ctx->T_local / 256));
+    const size_t need = (size_t)nsplit * npairs * GBM * GBM;
+    if (ctx->gram_part_elems < need) {
+        if (ctx->gram_part) MVSK_CUDA(cudaFree(ctx->gram_part));
+        ctx->gram_part = nullptr;
+        MVSK_CUDA(cudaMalloc(&ctx->gram_part, need * sizeof(double)));
+        ctx->gram_part_elems = need;
+    }
+    GramArgs a{};
+    a.X = ctx->X;
+    a.w = w_rows;
+    a.T = ctx->T_local;
+    a.ld = (int)ctx->ld;
+    a.ntile = ntile;
+    a.nsplit = nsplit;
+    a.part = ctx->gram_part;
+    const size_t smem = (size_t)(4 * GBK * GLDS + 2 * GBK) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        MVSK_CUDA(cudaFuncSetAttribute(syrk_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    syrk_dmma_kernel<<<dim3(npairs, nsplit), GTHREADS, smem, ctx->stream>>>(a);
+    MVSK_CUDA(cudaGetLastError());
+    gram_finish_kernel<<<npairs, 256, 0, ctx->stream>>>(ctx->gram_part, npairs, nsplit, n, scale, G_dev, n);
+    MVSK_CUDA(cudaGetLastError());
+    ctx->phys += 1;
+    if (ctx->nranks > 1)
+        MVSK_NCCL(ncclAllReduce(G_dev, G_dev, (size_t)n * n, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+}
+
+void run_quadform(mvsk_gpu_ctx* ctx, const double* P_dev, double* q_dev) {
+    constexpr int RB = 16;
+    const long long T = ctx->T_local;
+    if (T <= 0) return;
+    const int nb = (int)((T + RB - 1) / RB);
+    const size_t smem = (size_t)RB * ctx->ld * sizeof(double);
+    if (smem > 48 * 1024)
+        MVSK_CUDA(cudaFuncSetAttribute(quadform_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    quadform_kernel<RB><<<nb, 256, smem, ctx->stream>>>(ctx->X, T, (int)ctx->ld, P_dev, q_dev);
+    MVSK_CUDA(cudaGetLastError());
+}
+
+void run_third_weights(mvsk_gpu_ctx* ctx, const double* z, const double* q, double* tw) {
+    const long long T = ctx->T_local;
+    if (T <= 0) return;
+    const int nb = (int)std::min<long long>(4 * ctx->nsm, (T + 255) / 256);
+    third_weights_kernel<<<nb, 256, 0, ctx->stream>>>(z, q, tw, T, ctx->c.c3, ctx->c.c4, (double)ctx->T_global);
+    MVSK_CUDA(cudaGetLastError());
+}
+
+}  // namespace mvsk_b200

@@ -1,0 +1,248 @@
+// Face-aware host layer of the oracle (see host_ops.hpp). Each call stages its
+// n-vector inputs into pinned memory, issues ONE fused streaming pass (plus the
+// fixed-order reduction kernel) on the context stream and reads back the
+// n-vector / scalar results. Logical pass counts follow the reference cost
+// contract (common.hpp:27-37, oracle.hpp:127,134,138); physical passes are
+// counted by run_pass.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "host_ops.hpp"
+
+namespace mvsk_b200 {
+
+FaceMap full_face(const mvsk_gpu_ctx* ctx) {
+    FaceMap f;
+    f.active = false;
+    f.m = ctx->n;
+    return f;
+}
+
+void check_slot(const mvsk_gpu_ctx* ctx, int slot, bool need_valid) {
+    if (slot < 0 || slot >= MVSK_GPU_MAX_SLOTS) throw ApiError(MVSK_DOMAIN_ERROR, "slot out of range");
+    if (need_valid && !ctx->slots[slot].valid) throw ApiError(MVSK_DOMAIN_ERROR, "slot holds no cache");
+}
+
+namespace {
+
+void to_full(const mvsk_gpu_ctx* ctx, const FaceMap& fm, const double* v, double fill, double* full) {
+    std::fill(full, full + ctx->ld, 0.0);
+    if (!fm.active) {
+        std::memcpy(full, v, sizeof(double) * ctx->n);
+        return;
+    }
+    for (long long i = 0; i < ctx->n; ++i) full[i] = fill;
+    for (long long j = 0; j < fm.m; ++j) full[fm.idx[j]] = v[j];
+}
+
+void from_full(const mvsk_gpu_ctx* ctx, const FaceMap& fm, const double* full, double* v) {
+    if (!fm.active) {
+        std::memcpy(v, full, sizeof(double) * ctx->n);
+        return;
+    }
+    for (long long j = 0; j < fm.m; ++j) v[j] = full[fm.idx[j]];
+}
+
+bool finite(const double* v, long long n) {
+    for (long long i = 0; i < n; ++i)
+        if (!std::isfinite(v[i])) return false;
+    return true;
+}
+
+// H2D of k host vectors (face coordinates) into vin rows [base, base + k)
+void stage_in(mvsk_gpu_ctx* ctx, const FaceMap& fm, const double* V, int k, double fill, size_t base) {
+    const size_t ld = (size_t)ctx->ld;
+    ensure_host_staging(ctx, (base + (size_t)k) * ld);
+    for (int i = 0; i < k; ++i) to_full(ctx, fm, V + (size_t)i * fm.m, fill, ctx->h_in + (base + i) * ld);
+    MVSK_CUDA(cudaMemcpyAsync(ctx->vin + base * ld, ctx->h_in + base * ld, (size_t)k * ld * sizeof(double),
+                              cudaMemcpyHostToDevice, ctx->stream));
+}
+
+void fetch_out(mvsk_gpu_ctx* ctx, const FaceMap& fm, const double* dev, int k, long long stride_dev, double* out) {
+    ensure_host_staging(ctx, (size_t)k * stride_dev);
+    MVSK_CUDA(cudaMemcpyAsync(ctx->h_out, dev, (size_t)k * stride_dev * sizeof(double), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < k; ++i) from_full(ctx, fm, ctx->h_out + (size_t)i * stride_dev, out + (size_t)i * fm.m);
+}
+
+void ensure_tvec2(mvsk_gpu_ctx* ctx) {
+    if (!ctx->tvec2) MVSK_CUDA(cudaMalloc(&ctx->tvec2, (size_t)std::max<long long>(1, ctx->T_local) * sizeof(double)));
+}
+
+}  // namespace
+
+double op_make_cache(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* x) {
+    check_slot(ctx, slot, false);
+    Slot& s = ctx->slots[slot];
+    s.valid = false;
+    stage_in(ctx, fm, x, 1, fm.tau, 0);
+    s.x_full.assign(ctx->h_in, ctx->h_in + ctx->ld);
+    PassIO io;
+    io.vin = ctx->vin;
+    io.slot = slot;
+    io.x_for_mux = ctx->vin;
+    run_pass(ctx, Op::FGRAD, 1, io);
+    ctx->fwd += 1;  // oracle.hpp:127
+    double h[5];
+    MVSK_CUDA(cudaMemcpyAsync(h, s.sc, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+    s.f = h[0];
+    for (int i = 0; i < 4; ++i) s.mom[i] = h[1 + i];
+    s.grad_counted = false;
+    if (!std::isfinite(s.f)) throw ApiError(MVSK_NUMERIC_ERROR, "oracle: non-finite objective value");  // :66-67
+    s.valid = true;
+    return s.f;
+}
+
+void op_moments(const mvsk_gpu_ctx* ctx, int slot, double out[4]) {
+    check_slot(ctx, slot);
+    for (int i = 0; i < 4; ++i) out[i] = ctx->slots[slot].mom[i];
+}
+
+void op_gradient(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, double* g) {
+    check_slot(ctx, slot);
+    Slot& s = ctx->slots[slot];
+    // make_cache's fused pass already produced g; the reference's memoised
+    // transpose pass (oracle.hpp:80-89) is counted on the first request
+    if (!s.grad_counted) {
+        ctx->tr += 1;
+        s.grad_counted = true;
+    }
+    fetch_out(ctx, fm, s.g, 1, ctx->ld, g);
+    if (!finite(g, fm.m)) throw ApiError(MVSK_NUMERIC_ERROR, "oracle: non-finite gradient");  // :85-86
+}
+
+void op_hvp(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* V, int k, double* HV) {
+    check_slot(ctx, slot);
+    if (k < 1 || k > MVSK_GPU_MAX_RHS) throw ApiError(MVSK_DIMENSION_ERROR, "hvp: k out of range");
+    stage_in(ctx, fm, V, k, 0.0, 0);
+    PassIO io;
+    io.vin = ctx->vin;
+    io.z = ctx->slots[slot].z;
+    io.out = ctx->outd;
+    io.ldo = ctx->ld;
+    run_pass(ctx, Op::HVP, k, io);
+    ctx->fwd += k;  // oracle.hpp:134
+    ctx->tr += k;   // oracle.hpp:138
+    fetch_out(ctx, fm, ctx->outd, k, ctx->ld, HV);
+    if (!finite(HV, (long long)k * fm.m)) throw ApiError(MVSK_NUMERIC_ERROR, "oracle: non-finite Hessian product");
+}
+
+void op_third(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* U, const double* V, int k, double* out) {
+    check_slot(ctx, slot);
+    if (k < 1 || k > MVSK_GPU_MAX_RHS) throw ApiError(MVSK_DIMENSION_ERROR, "third_action: k out of range");
+    stage_in(ctx, fm, U, k, 0.0, 0);
+    stage_in(ctx, fm, V, k, 0.0, MVSK_GPU_MAX_RHS);
+    PassIO io;
+    io.vin = ctx->vin;
+    io.vin2 = ctx->vin + (size_t)MVSK_GPU_MAX_RHS * ctx->ld;
+    io.z = ctx->slots[slot].z;
+    io.out = ctx->outd;
+    io.ldo = ctx->ld;
+    run_pass(ctx, Op::THIRD, k, io);
+    ctx->fwd += 2 * k;
+    ctx->tr += k;
+    fetch_out(ctx, fm, ctx->outd, k, ctx->ld, out);
+    if (!finite(out, (long long)k * fm.m)) throw ApiError(MVSK_NUMERIC_ERROR, "oracle: non-finite third-order action");
+}
+
+void op_psi2(mvsk_gpu_ctx* ctx, int slot, double* out) {
+    check_slot(ctx, slot);
+    run_psi2(ctx, ctx->slots[slot].z, ctx->tvec, ctx->T_local);
+    MVSK_CUDA(cudaMemcpyAsync(out, ctx->tvec, ctx->T_local * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void op_sample_direction(mvsk_gpu_ctx* ctx, const FaceMap& fm, const double* d, double* out) {
+    stage_in(ctx, fm, d, 1, 0.0, 0);
+    PassIO io;
+    io.vin = ctx->vin;
+    io.z = ctx->tvec;  // power sums are discarded here; only A d (zout) is kept
+    io.zout = ctx->tvec;
+    io.out = ctx->outd;
+    MVSK_CUDA(cudaMemsetAsync(ctx->tvec, 0, std::max<long long>(1, ctx->T_local) * sizeof(double), ctx->stream));
+    run_pass(ctx, Op::LINESUMS, 1, io);
+    ctx->fwd += 1;  // oracle.hpp:134 (sample_direction -> forward_tangent)
+    MVSK_CUDA(cudaMemcpyAsync(out, ctx->tvec, ctx->T_local * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void op_line_model(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* d, double out[14]) {
+    check_slot(ctx, slot);
+    const long long m = fm.m;
+    // linesearch.hpp:64-67
+    double dn2 = 0.0, dsum = 0.0;
+    for (long long i = 0; i < m; ++i) {
+        dn2 += d[i] * d[i];
+        dsum += d[i];
+    }
+    const double dn = std::sqrt(dn2);
+    if (!(dn > 0)) throw ApiError(MVSK_DOMAIN_ERROR, "line_model: zero direction");
+    if (std::abs(dsum) > 1e-10 * dn) throw ApiError(MVSK_DOMAIN_ERROR, "line_model: direction is not tangent to the simplex");
+    stage_in(ctx, fm, d, 1, 0.0, 0);
+    PassIO io;
+    io.vin = ctx->vin;
+    io.z = ctx->slots[slot].z;
+    io.out = ctx->outd;
+    run_pass(ctx, Op::LINESUMS, 1, io);
+    ctx->fwd += 1;
+    double s[9];
+    MVSK_CUDA(cudaMemcpyAsync(s, ctx->outd, 9 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+    double mud = 0.0;  // mu_f' d_f
+    for (long long j = 0; j < m; ++j) mud += ctx->mu[fm.active ? fm.idx[j] : j] * d[j];
+    const mvsk_coeffs& c = ctx->c;
+    // linesearch.hpp:72-78
+    out[0] = ctx->slots[slot].f;
+    out[1] = -c.c1 * mud + 2.0 * c.c2 * s[0] - 3.0 * c.c3 * s[1] + 4.0 * c.c4 * s[2];
+    out[2] = c.c2 * s[3] - 3.0 * c.c3 * s[4] + 6.0 * c.c4 * s[5];
+    out[3] = -c.c3 * s[6] + 4.0 * c.c4 * s[7];
+    out[4] = c.c4 * s[8];
+    for (int i = 0; i < 9; ++i) out[5 + i] = s[i];
+}
+
+void op_weighted_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, double* G) {
+    check_slot(ctx, slot);
+    const long long n = ctx->n;
+    if (!ctx->gram) MVSK_CUDA(cudaMalloc(&ctx->gram, (size_t)n * n * sizeof(double)));
+    run_psi2(ctx, ctx->slots[slot].z, ctx->tvec, ctx->T_local);
+    run_weighted_gram(ctx, ctx->tvec, ctx->gram, 1.0 / (double)ctx->T_global);
+    std::vector<double> full((size_t)n * n);
+    MVSK_CUDA(cudaMemcpyAsync(full.data(), ctx->gram, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+    const long long m = fm.m;
+    for (long long i = 0; i < m; ++i) {
+        const long long gi = fm.active ? fm.idx[i] : i;
+        for (long long j = 0; j < m; ++j) G[i * m + j] = full[gi * n + (fm.active ? fm.idx[j] : j)];
+    }
+}
+
+void op_third_trace_rows(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* P, double* out) {
+    check_slot(ctx, slot);
+    const long long ld = ctx->ld, m = fm.m;
+    if ((size_t)16 * ld * sizeof(double) > ctx->max_smem)
+        throw ApiError(MVSK_DIMENSION_ERROR, "direct tangent mode supports n <= " +
+                                                 std::to_string(ctx->max_smem / (16 * sizeof(double))));
+    if (!ctx->pmat) MVSK_CUDA(cudaMalloc(&ctx->pmat, (size_t)ld * ld * sizeof(double)));
+    ensure_tvec2(ctx);
+    std::vector<double> Pf((size_t)ld * ld, 0.0);
+    for (long long i = 0; i < m; ++i) {
+        const long long gi = fm.active ? fm.idx[i] : i;
+        for (long long j = 0; j < m; ++j) Pf[gi * ld + (fm.active ? fm.idx[j] : j)] = P[i * m + j];
+    }
+    MVSK_CUDA(cudaMemcpyAsync(ctx->pmat, Pf.data(), Pf.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    run_quadform(ctx, ctx->pmat, ctx->tvec2);
+    run_third_weights(ctx, ctx->slots[slot].z, ctx->tvec2, ctx->tvec);
+    PassIO io;
+    io.tw = ctx->tvec;
+    io.out = ctx->outd;
+    io.ldo = ctx->ld;
+    run_pass(ctx, Op::XTW, 1, io);
+    fetch_out(ctx, fm, ctx->outd, 1, ctx->ld, out);
+    // the sync above keeps Pf alive until the async H2D has completed
+}
+
+}  // namespace mvsk_b200

@@ -1,0 +1,394 @@
+// Launch planning, dispatch and epilogues for the streaming oracle kernels.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "oracle_ops.cuh"
+
+namespace mvsk_b200 {
+
+namespace {
+
+constexpr int kMaxTeam = 512;       // threads per CTA (launch bound)
+constexpr size_t kStageTarget = 32 * 1024;
+constexpr size_t kRingTarget = 160 * 1024;
+
+struct Plan {
+    int Q = 1, P = 32, G = 1, RG = 1, S = 2;
+    size_t smem = 0;
+    int nb = 1;
+    const void* fn = nullptr;
+};
+
+template <Op OP, int K, int Q, int RG>
+const void* kfn() {
+    return reinterpret_cast<const void*>(&stream_kernel<OP, K, Q, RG>);
+}
+
+// (Q, RG) pairs instantiated for every op: RG * Q <= 8 keeps the staged row
+// slice within 16 fp64 registers per thread.
+#define MVSK_QRG(OP, K)                                                         \
+    if (Q == 1 && RG == 1) return kfn<OP, K, 1, 1>();                           \
+    if (Q == 1 && RG == 2) return kfn<OP, K, 1, 2>();                           \
+    if (Q == 1 && RG == 4) return kfn<OP, K, 1, 4>();                           \
+    if (Q == 2 && RG == 1) return kfn<OP, K, 2, 1>();                           \
+    if (Q == 2 && RG == 2) return kfn<OP, K, 2, 2>();                           \
+    if (Q == 2 && RG == 4) return kfn<OP, K, 2, 4>();                           \
+    if (Q == 4 && RG == 1) return kfn<OP, K, 4, 1>();                           \
+    if (Q == 4 && RG == 2) return kfn<OP, K, 4, 2>();
+
+const void* select_kernel(Op op, int K, int Q, int RG) {
+    switch (op) {
+    case Op::FGRAD:
+        MVSK_QRG(Op::FGRAD, 1)
+        if (Q == 8 && RG == 1) return kfn<Op::FGRAD, 1, 8, 1>();
+        break;
+    case Op::LINESUMS:
+        MVSK_QRG(Op::LINESUMS, 1)
+        if (Q == 8 && RG == 1) return kfn<Op::LINESUMS, 1, 8, 1>();
+        break;
+    case Op::XTW:
+        MVSK_QRG(Op::XTW, 1)
+        if (Q == 8 && RG == 1) return kfn<Op::XTW, 1, 8, 1>();
+        break;
+    case Op::HVP:
+        if (K == 1) {
+            MVSK_QRG(Op::HVP, 1)
+            if (Q == 8 && RG == 1) return kfn<Op::HVP, 1, 8, 1>();
+        } else if (K == 2) {
+            MVSK_QRG(Op::HVP, 2)
+        } else if (K == 4) {
+            if (Q == 1 && RG == 1) return kfn<Op::HVP, 4, 1, 1>();
+            if (Q == 1 && RG == 2) return kfn<Op::HVP, 4, 1, 2>();
+            if (Q == 2 && RG == 1) return kfn<Op::HVP, 4, 2, 1>();
+        }
+        break;
+    case Op::THIRD:
+        if (K == 1) {
+            MVSK_QRG(Op::THIRD, 1)
+        }
+        break;
+    }
+    return nullptr;
+}
+#undef MVSK_QRG
+
+// largest Q allowed per (op, K) given register budgets
+int max_q(Op op, int K) {
+    if (op == Op::HVP) return K == 1 ? 8 : K == 2 ? 4 : 2;
+    if (op == Op::THIRD) return 4;
+    return 8;
+}
+
+int round_team(int need) {
+    if (need <= 32) {
+        int p = 1;
+        while (p < need) p <<= 1;
+        return std::max(p, 2);
+    }
+    return (need + 31) / 32 * 32;
+}
+
+bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
+    const long long npairs = ctx->ld / 2;
+    const int qmax = max_q(op, K);
+    int Q = -1;
+    for (int q = 1; q <= qmax; q <<= 1) {
+        if ((npairs + q - 1) / q <= 256) {
+            Q = q;
+            break;
+        }
+    }
+    if (Q < 0)
+        for (int q = 1; q <= qmax; q <<= 1)
+            if ((npairs + q - 1) / q <= kMaxTeam) {
+                Q = q;
+                break;
+            }
+    if (Q < 0) return false;
+    const int P = round_team((int)((npairs + Q - 1) / Q));
+    int G = std::max(1, kMaxTeam / P);
+    const size_t row_bytes = (size_t)ctx->ld * sizeof(double);
+    // rows per stage ~ kStageTarget; RG * Q <= 8 and RG in {1,2,4}
+    long long want_rows = std::max<long long>(1, (long long)(kStageTarget / row_bytes));
+    // fewer teams when a stage would hold more rows than wanted
+    while (G > 1 && G > want_rows) G >>= 1;
+    int RG = 1;
+    while (RG < 4 && RG * 2 * Q <= 8 && (long long)G * RG * 2 <= want_rows) RG <<= 1;
+    if (op == Op::HVP && K == 4 && Q == 2) RG = 1;
+    if (op == Op::THIRD && Q == 4) RG = std::min(RG, 2);
+    const long long R = (long long)G * RG;
+    const size_t stage_bytes = ((size_t)R * row_bytes + 127) & ~(size_t)127;
+    const int nst_total = (int)std::max<long long>(1, (ctx->T_local + R - 1) / R);
+    int S = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, kRingTarget / stage_bytes));
+    S = std::min(S, std::max(2, nst_total));
+    // team-combine and scalar scratch live in the ring after the last stage
+    const int nacc = (op == Op::HVP || op == Op::THIRD) ? K : (op == Op::LINESUMS ? 0 : 1);
+    const int ndot = (op == Op::FGRAD || op == Op::LINESUMS) ? 1 : (op == Op::THIRD ? 2 * K : (op == Op::XTW ? 0 : K));
+    const int nwp = P >= 32 ? P / 32 : 1;
+    const size_t red_bytes = (((size_t)2 * R * std::max(ndot, 1) * nwp * sizeof(double)) + 127) & ~(size_t)127;
+    size_t ring = (size_t)S * stage_bytes;
+    const size_t combine = ((size_t)G * std::max(nacc, 1) * ctx->ld + 16 + (size_t)G * 16) * sizeof(double);
+    ring = std::max(ring, combine);
+    pl.smem = 128 + red_bytes + ring;
+    if (pl.smem > ctx->max_smem) {
+        // shrink the ring first
+        while (S > 2 && 128 + red_bytes + std::max((size_t)S * stage_bytes, combine) > ctx->max_smem) --S;
+        ring = std::max((size_t)S * stage_bytes, combine);
+        pl.smem = 128 + red_bytes + ring;
+        if (pl.smem > ctx->max_smem) return false;
+    }
+    pl.Q = Q;
+    pl.P = P;
+    pl.G = G;
+    pl.RG = RG;
+    pl.S = S;
+    pl.fn = select_kernel(op, K, Q, RG);
+    if (!pl.fn) return false;
+    const int occ = std::max<int>(1, (int)std::min<size_t>(4, (ctx->max_smem + 1024) / (pl.smem + 1024)));
+    const long long want_blocks = std::max<long long>(1, (ctx->T_local + R - 1) / R);
+    pl.nb = (int)std::min<long long>((long long)ctx->nsm * occ, want_blocks);
+    return true;
+}
+
+struct FinishArgs {
+    int op;
+    int k;
+    int ld, n;
+    long long ldo;
+    int nb;
+    int do_reduce, do_epi;
+    const double* part_acc;
+    const double* part_sc;
+    double* red;  // [k*ld + kNumScalars]
+    // epilogue
+    double* out;
+    double* g;          // FGRAD gradient
+    double* sc;         // FGRAD scalars
+    const double* mu;   // ld
+    const double* x;    // ld (FGRAD mu'x)
+    double c1, c2, c3, c4, T, value_offset;
+};
+
+__global__ void finish_kernel(const FinishArgs f) {
+    const int nacc = (f.op == (int)Op::LINESUMS) ? 0 : f.k;
+    const int tot = nacc * f.ld;
+    const int nsc = f.op == (int)Op::FGRAD ? 3 : (f.op == (int)Op::LINESUMS ? 9 : 0);
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gstride = gridDim.x * blockDim.x;
+    // 1) fixed-order reduction over CTA partials
+    if (f.do_reduce) {
+        for (int i = gtid; i < tot; i += gstride) {
+            double v = 0.0;
+            for (int b = 0; b < f.nb; ++b) v += f.part_acc[(size_t)b * tot + i];
+            f.red[i] = v;
+        }
+        if (blockIdx.x == 0 && threadIdx.x < nsc) {
+            double v = 0.0;
+            for (int b = 0; b < f.nb; ++b) v += f.part_sc[(size_t)b * kNumScalars + threadIdx.x];
+            f.red[tot + threadIdx.x] = v;
+        }
+    }
+    if (!f.do_epi) return;
+    if (f.do_reduce) {
+        // the scalar sums are produced by block 0 only; a grid-wide dependency
+        // exists only for FGRAD/LINESUMS scalars, handled by block 0 below
+    }
+    // 2) epilogue
+    if (f.op == (int)Op::FGRAD) {
+        for (int i = gtid; i < f.ld; i += gstride) {
+            const double v = f.red[i];
+            f.g[i] = i < f.n ? (-f.c1 * f.mu[i] + v) : 0.0;
+        }
+        if (blockIdx.x == 0) {
+            __shared__ double sh[256];
+            double s = 0.0;
+            for (int i = threadIdx.x; i < f.n; i += blockDim.x) s += f.mu[i] * f.x[i];
+            sh[threadIdx.x] = s;
+            __syncthreads();
+            for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+                if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) {
+                const double mux = sh[0];
+                const double s2 = f.red[tot], s3 = f.red[tot + 1], s4 = f.red[tot + 2];
+                // oracle.hpp:62-64
+                f.sc[0] = f.value_offset - f.c1 * mux + (f.c2 * s2 - f.c3 * s3 + f.c4 * s4) / f.T;
+                f.sc[1] = mux;
+                f.sc[2] = s2 / f.T;
+                f.sc[3] = s3 / f.T;
+                f.sc[4] = s4 / f.T;
+            }
+        }
+    } else if (f.op == (int)Op::LINESUMS) {
+        if (blockIdx.x == 0 && threadIdx.x < 9) f.out[threadIdx.x] = f.red[tot + threadIdx.x] / f.T;
+    } else {
+        for (int i = gtid; i < tot; i += gstride) {
+            const int k = i / f.ld, c = i - k * f.ld;
+            if (c < f.n) f.out[(size_t)k * f.ldo + c] = f.red[i];
+        }
+    }
+}
+
+__global__ void psi2_kernel(const double* z, double* out, long long T, double c2, double c3, double c4) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < T; t += (long long)gridDim.x * blockDim.x) {
+        const double zt = z[t];
+        out[t] = 2.0 * c2 - 6.0 * c3 * zt + 12.0 * c4 * (zt * zt);  // oracle.hpp:116-119
+    }
+}
+
+std::mutex g_attr_mu;
+
+void set_smem_attr(const void* fn, size_t smem) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+void ensure_part(mvsk_gpu_ctx* ctx, size_t elems) {
+    if (ctx->part_acc_elems >= elems) return;
+    if (ctx->part_acc) MVSK_CUDA(cudaFree(ctx->part_acc));
+    ctx->part_acc = nullptr;
+    MVSK_CUDA(cudaMalloc(&ctx->part_acc, elems * sizeof(double)));
+    ctx->part_acc_elems = elems;
+}
+
+}  // namespace
+
+void ensure_host_staging(mvsk_gpu_ctx* ctx, size_t elems) {
+    if (ctx->h_elems >= elems) return;
+    if (ctx->h_in) cudaFreeHost(ctx->h_in);
+    if (ctx->h_out) cudaFreeHost(ctx->h_out);
+    ctx->h_in = ctx->h_out = nullptr;
+    MVSK_CUDA(cudaMallocHost(&ctx->h_in, elems * sizeof(double)));
+    MVSK_CUDA(cudaMallocHost(&ctx->h_out, elems * sizeof(double)));
+    ctx->h_elems = elems;
+}
+
+static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io);
+
+void run_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
+    if (op == Op::HVP && k > 1) {
+        // widest supported RHS block per pass (4, 2, 1), chunked over k
+        int done = 0;
+        while (done < k) {
+            int kk = (k - done) >= 4 ? 4 : ((k - done) >= 2 ? 2 : 1);
+            Plan tmp;
+            while (kk > 1 && !make_plan(ctx, op, kk, tmp)) kk >>= 1;
+            PassIO sub = io;
+            sub.vin = io.vin + (size_t)done * ctx->ld;
+            sub.out = io.out + (size_t)done * io.ldo;
+            run_single(ctx, op, kk, sub);
+            done += kk;
+        }
+        return;
+    }
+    if (op == Op::THIRD && k > 1) {
+        for (int i = 0; i < k; ++i) {
+            PassIO sub = io;
+            sub.vin = io.vin + (size_t)i * ctx->ld;
+            sub.vin2 = io.vin2 + (size_t)i * ctx->ld;
+            sub.out = io.out + (size_t)i * io.ldo;
+            run_single(ctx, op, 1, sub);
+        }
+        return;
+    }
+    run_single(ctx, op, k, io);
+}
+
+static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
+    Plan pl;
+    if (!make_plan(ctx, op, k, pl))
+        throw ApiError(MVSK_DIMENSION_ERROR, "no streaming-kernel plan for n=" + std::to_string(ctx->n) +
+                                                 " (this build supports n <= 8192)");
+    const int nacc = (op == Op::HVP || op == Op::THIRD) ? k : (op == Op::LINESUMS ? 0 : 1);
+    ensure_part(ctx, (size_t)pl.nb * std::max(nacc, 1) * ctx->ld);
+    set_smem_attr(pl.fn, pl.smem);
+
+    StreamArgs a{};
+    a.X = ctx->X;
+    a.T = ctx->T_local;
+    a.ld = (int)ctx->ld;
+    a.npairs = (int)(ctx->ld / 2);
+    a.P = pl.P;
+    a.G = pl.G;
+    a.RG = pl.RG;
+    a.S = pl.S;
+    a.evict_first = (size_t)ctx->T_local * ctx->ld * sizeof(double) > (size_t)96 * 1024 * 1024;
+    a.vin = io.vin;
+    a.vin2 = io.vin2;
+    a.z = (op == Op::FGRAD) ? ctx->zoff_dev : io.z;
+    a.tw = io.tw;
+    a.part_acc = ctx->part_acc;
+    a.part_sc = ctx->part_sc;
+    a.c2 = ctx->c.c2;
+    a.c3 = ctx->c.c3;
+    a.c4 = ctx->c.c4;
+    a.Tglob = (double)ctx->T_global;
+    Slot* slot = nullptr;
+    if (op == Op::FGRAD) {
+        slot = &ctx->slots[io.slot];
+        a.zout = slot->z;
+    } else {
+        a.zout = io.zout;
+    }
+    if (ctx->T_local > 0) {
+        void* args[] = {&a};
+        MVSK_CUDA(cudaLaunchKernel(pl.fn, dim3(pl.nb), dim3(pl.G * pl.P), args, pl.smem, ctx->stream));
+    }
+    ctx->phys += 1;
+
+    FinishArgs f{};
+    f.op = (int)op;
+    f.k = op == Op::LINESUMS ? 0 : std::max(nacc, 1);
+    f.ld = (int)ctx->ld;
+    f.n = (int)ctx->n;
+    f.ldo = io.ldo;
+    f.nb = ctx->T_local > 0 ? pl.nb : 0;
+    f.part_acc = ctx->part_acc;
+    f.part_sc = ctx->part_sc;
+    f.red = ctx->red;
+    f.out = io.out;
+    f.mu = ctx->mu_dev;
+    f.x = io.x_for_mux;
+    f.c1 = ctx->c.c1;
+    f.c2 = ctx->c.c2;
+    f.c3 = ctx->c.c3;
+    f.c4 = ctx->c.c4;
+    f.T = (double)ctx->T_global;
+    f.value_offset = ctx->value_offset;
+    if (slot) {
+        f.g = slot->g;
+        f.sc = slot->sc;
+    }
+    const int tot = std::max(f.k, 1) * f.ld;
+    const int fb = std::max(1, std::min(4 * ctx->nsm, (tot + 255) / 256));
+    if (ctx->nranks == 1) {
+        f.do_reduce = 1;
+        f.do_epi = 1;
+        // scalars are reduced by block 0 and consumed by block 0 only
+        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
+        MVSK_CUDA(cudaGetLastError());
+    } else {
+        f.do_reduce = 1;
+        f.do_epi = 0;
+        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
+        MVSK_CUDA(cudaGetLastError());
+        const int nsc = op == Op::FGRAD ? 3 : (op == Op::LINESUMS ? 9 : 0);
+        const size_t cnt = (size_t)(op == Op::LINESUMS ? 0 : tot) + nsc;
+        MVSK_NCCL(ncclAllReduce(ctx->red, ctx->red, cnt, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+        f.do_reduce = 0;
+        f.do_epi = 1;
+        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
+        MVSK_CUDA(cudaGetLastError());
+    }
+}
+
+void run_psi2(mvsk_gpu_ctx* ctx, const double* z, double* out, long long T) {
+    if (T <= 0) return;
+    const int nb = (int)std::min<long long>(4 * ctx->nsm, (T + 255) / 256);
+    psi2_kernel<<<nb, 256, 0, ctx->stream>>>(z, out, T, ctx->c.c2, ctx->c.c3, ctx->c.c4);
+    MVSK_CUDA(cudaGetLastError());
+}
+
+}  // namespace mvsk_b200

@@ -1,0 +1,44 @@
+// Host-side launch layer for the streaming kernels (shared by the C-ABI and
+// the C++ direction / solve driver).
+#pragma once
+#include "context.cuh"
+
+namespace mvsk_b200 {
+
+// One fused pass of `op` over this rank's rows, then the deterministic cross-CTA
+// reduction, the optional allreduce over the row-shard group, and the op
+// epilogue. Inputs are device vectors of stride ld (zero padded). Outputs:
+//   FGRAD:    slot z, slot g (ld), slot sc
+//   HVP/THIRD: out (k x ldo)
+//   LINESUMS: out[0..9) = s_rs / T ; zout (optional) = A d
+//   XTW:      out (ld) = X^T tw (raw sum, no scaling)
+struct PassIO {
+    const double* vin = nullptr;
+    const double* vin2 = nullptr;
+    const double* z = nullptr;
+    const double* tw = nullptr;
+    double* zout = nullptr;
+    double* out = nullptr;
+    long long ldo = 0;    // output stride for HVP/THIRD/XTW
+    int slot = -1;        // FGRAD target slot
+    const double* x_for_mux = nullptr;  // FGRAD: x (ld) for mu'x
+};
+
+void run_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io);
+
+// psi''(z) elementwise (hessian_diag_weights)
+void run_psi2(mvsk_gpu_ctx* ctx, const double* z, double* out, long long T);
+
+// Weighted Gram G = X^T diag(w) X / T over the full panel (n x n, row-major,
+// symmetric, both triangles written); allreduced across the shard group.
+void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, double scale);
+
+// q_t = x_t^T P x_t (P: ld x ld, zero outside the face) for this rank's rows
+void run_quadform(mvsk_gpu_ctx* ctx, const double* P_dev, double* q_dev);
+// tw_t = psi3(z_t) q_t / T with psi3 the third derivative weight
+void run_third_weights(mvsk_gpu_ctx* ctx, const double* z, const double* q, double* tw);
+
+// device scratch sizing (grows workspaces on demand)
+void ensure_host_staging(mvsk_gpu_ctx* ctx, size_t elems);
+
+}  // namespace mvsk_b200

@@ -1,0 +1,86 @@
+"""CPU-side checks of the drop-in boundary: libmvsk_b200.so loads, exports
+every symbol include/mvsk_gpu.h declares, the ctypes struct layouts match the
+C layouts, and with no GPU the product fails loudly (no CPU fallback)."""
+import ctypes as C
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2604_25378_b200 import _abi
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "mvsk_gpu.h"
+
+
+def _declared():
+    txt = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(mvsk_gpu_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _abi.load_library()
+    names = _declared()
+    assert len(names) >= 30
+    missing = [s for s in names if not hasattr(lib, s)]
+    assert not missing, missing
+    # and the ctypes table covers exactly the header
+    assert sorted(n for n, _, _ in _abi.SIGNATURES) == names
+
+
+def test_struct_layouts_match_c(tmp_path):
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "mvsk_gpu.h"\nint main(){printf("%zu %zu %zu %zu %zu %zu %zu\\n",'
+                   ' sizeof(mvsk_coeffs), sizeof(mvsk_tangent_config), sizeof(mvsk_direction_diag),'
+                   ' sizeof(mvsk_solver_config), sizeof(mvsk_solve_report), offsetof(mvsk_solver_config, tangent),'
+                   ' offsetof(mvsk_solve_report, status)); return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    want = [C.sizeof(_abi.mvsk_coeffs), C.sizeof(_abi.mvsk_tangent_config), C.sizeof(_abi.mvsk_direction_diag),
+            C.sizeof(_abi.mvsk_solver_config), C.sizeof(_abi.mvsk_solve_report),
+            _abi.mvsk_solver_config.tangent.offset, _abi.mvsk_solve_report.status.offset]
+    assert got == want
+
+
+def test_status_strings_and_presets_without_gpu():
+    lib = _abi.load_library()
+    assert lib.mvsk_gpu_status_string(4) == b"numeric_error"
+    from paper_2604_25378_b200.gpu_oracle import DomainError, preset
+    s, l = preset("small"), preset("large")
+    assert s.max_iter == 300 and s.tangent.mode == 0 and s.tangent.lambda_ == 0.0
+    assert l.max_iter == 40 and l.tangent.mode == 1 and l.tangent.lambda_ == 1e-4
+    assert l.stall_restarts == 1 and l.identification_pass == 1 and l.max_elapsed_seconds == 60.0
+    with pytest.raises(DomainError):
+        preset("medium")
+
+
+def test_presets_match_oracle_restatement():
+    from oracle import pyoracle as po
+    from paper_2604_25378_b200.gpu_oracle import preset
+    for name in ("small", "large"):
+        a, b = bytes(preset(name)), bytes(po.preset(name))
+        assert a == b, name
+
+
+def test_no_cpu_fallback_without_device():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2604_25378_b200.gpu_oracle import CudaError, GpuOracle
+    with pytest.raises(CudaError):
+        GpuOracle(np.zeros((4, 2)), np.zeros(2), [1, 1, 1, 1])
+
+
+def test_crra_and_centering_mirror():
+    from oracle import pyoracle as po
+    from paper_2604_25378_b200.gpu_oracle import center_panel, crra_coefficients
+    for g in (1.0, 2.0, 5.0, 10.0, 20.0):
+        assert np.array_equal(crra_coefficients(g), po.crra(g))
+    R = np.random.default_rng(0).uniform(-0.1, 0.4, (50, 7))
+    A, mu = center_panel(R)
+    A2, mu2 = po.center_panel(R)
+    np.testing.assert_allclose(A, A2, atol=1e-16)
+    np.testing.assert_allclose(mu, mu2, rtol=1e-15)

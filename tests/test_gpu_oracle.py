@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs. Mirrors the reference's oracle tests (test_oracle.cpp,
+test_linesearch.cpp) with the CPU restatement as the independent reference.
+
+Tolerance (north_star): objective, gradient and HVP to 1e-11 relative. We use
+  |gpu - cpu|_inf <= 1e-11 * max(|cpu|_inf, scale)
+where `scale` is the magnitude of the summed terms (|A|^T |w| for the A^T w
+products); the two sides sum the same terms in different orders, so that is
+the floating-point error scale of the reference's own arithmetic."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from tests import refhelpers as rh
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-11
+
+
+def _close(gpu, cpu, scale=0.0, rel=REL):
+    gpu, cpu = np.asarray(gpu), np.asarray(cpu)
+    ref = max(float(np.max(np.abs(cpu))) if cpu.size else 0.0, float(scale))
+    err = float(np.max(np.abs(gpu - cpu))) if cpu.size else 0.0
+    assert err <= rel * ref + 1e-300, f"err {err:.3e} > {rel:g} * {ref:.3e}"
+
+
+def _gpu(A, mu, c, **kw):
+    from paper_2604_25378_b200.gpu_oracle import GpuOracle
+    return GpuOracle(A, mu, c, **kw)
+
+
+def _absscale(A, w):
+    return float(np.max(np.abs(A).T @ np.abs(w)))
+
+
+PANELS = [(4, 15, 0), (5, 30, 3), (7, 33, 5), (9, 64, 11), (2, 40, 1), (1, 6, 2), (33, 257, 4), (130, 700, 6)]
+
+
+@pytest.mark.parametrize("n,T,seed", PANELS)
+@pytest.mark.parametrize("prof", [0, 1, 2, 3])
+def test_value_gradient_moments(n, T, seed, prof):
+    c = [np.array([10, 1, 10, 1.0]), np.array([1, 10, 1, 10.0]), np.array([10, 10, 10, 10.0]), rh.crra(6.0)][prof]
+    A, mu = rh.lcg_panel(n, T, seed)
+    x = rh.simplex_point(n, seed + 100)
+    cpu = po.CpuOracle(A, mu, c)
+    gpu = _gpu(A, mu, c)
+    cc, gc = cpu.make_cache(x), gpu.make_cache(x)
+    _close(gpu.value(gc), cpu.value(cc))
+    np.testing.assert_allclose(gpu.moments(gc), cpu.moments(cc), rtol=1e-11, atol=1e-300)
+    z = A @ x
+    w = (2 * c[1] * z - 3 * c[2] * z * z + 4 * c[3] * z ** 3) / T
+    _close(gpu.gradient(gc), cpu.gradient(cc), _absscale(A, w))
+    assert abs(gpu.value(gc) - rh.ref_value(A, mu, c, x)) <= 1e-13 * (1 + abs(rh.ref_value(A, mu, c, x)))
+
+
+@pytest.mark.parametrize("n,T,seed", PANELS)
+def test_hvp_third_weights_direction(n, T, seed):
+    c = rh.crra(6.0)
+    A, mu = rh.lcg_panel(n, T, seed)
+    x = rh.simplex_point(n, seed)
+    cpu, gpu = po.CpuOracle(A, mu, c), _gpu(A, mu, c)
+    cc, gc = cpu.make_cache(x), gpu.make_cache(x)
+    rng = np.random.default_rng(seed)
+    V = rng.standard_normal((8, n))
+    z = A @ x
+    psi2 = 2 * c[1] - 6 * c[2] * z + 12 * c[3] * z * z
+    for k in (1, 2, 3, 4, 8):
+        H = gpu.hvp(gc, V[:k])
+        for i in range(k):
+            ref = cpu.hvp(cc, V[i])
+            _close(H[i], ref, _absscale(A, psi2 * (A @ V[i]) / T))
+    U = rng.standard_normal((3, n))
+    T3 = gpu.third_action(gc, U, V[:3])
+    psi3 = -6 * c[2] + 24 * c[3] * z
+    for i in range(3):
+        _close(T3[i], cpu.third_action(cc, U[i], V[i]), _absscale(A, psi3 * (A @ U[i]) * (A @ V[i]) / T))
+    np.testing.assert_allclose(gpu.hessian_diag_weights(gc), cpu.hessian_diag_weights(cc), rtol=1e-13, atol=1e-15)
+    d = V[0]
+    _close(gpu.sample_direction(d), cpu.sample_direction(d), float(np.max(np.abs(A) @ np.abs(d))))
+
+
+@pytest.mark.parametrize("n,T,seed", PANELS[:6])
+def test_line_model(n, T, seed):
+    if n < 2:
+        pytest.skip("needs a tangent direction")
+    c = rh.crra(6.0) if seed % 2 else np.array([10, 10, 10, 10.0])
+    A, mu = rh.lcg_panel(n, T, seed)
+    x = rh.simplex_point(n, seed + 30, 1e-3)
+    d = po.splitmix(seed + 200, "uniform", n, -1.0, 1.0)
+    d -= d.mean()
+    cpu, gpu = po.CpuOracle(A, mu, c), _gpu(A, mu, c)
+    cc, gc = cpu.make_cache(x), gpu.make_cache(x)
+    cap = po.alpha_max(x, d, 0.0)
+    mc = cpu.line_model(cc, d, cap)
+    mg = gpu.line_model(gc, d, cap)
+    got = np.array([mg.a0, mg.a1, mg.a2, mg.a3, mg.a4, *mg.sums])
+    np.testing.assert_allclose(got, mc, rtol=1e-11, atol=1e-14 * np.max(np.abs(mc)))
+    assert mg.a1 == pytest.approx(gpu.gradient(gc) @ d, rel=1e-11)
+    from paper_2604_25378_b200.gpu_oracle import DomainError
+    with pytest.raises(DomainError):
+        gpu.line_model(gc, np.ones(n), 1.0)
+    with pytest.raises(DomainError):
+        gpu.line_model(gc, np.zeros(n), 1.0)
+
+
+def test_pass_count_contract():  # test_oracle.cpp:126-154
+    A, mu = rh.lcg_panel(6, 18, 5)
+    gpu = _gpu(A, mu, rh.crra(4.0))
+    x, v = rh.simplex_point(6, 2), rh.simplex_point(6, 3)
+    cache = gpu.make_cache(x)
+    assert gpu.passes()[:2] == (1, 0)
+    gpu.gradient(cache)
+    assert gpu.passes()[:2] == (1, 1)
+    gpu.gradient(cache)
+    assert sum(gpu.passes()[:2]) == 2
+    gpu.reset_passes()
+    gpu.hvp(cache, v)
+    assert sum(gpu.passes()[:2]) == 2 and gpu.passes()[2] == 1  # one physical pass
+    gpu.reset_passes()
+    gpu.third_action(cache, v, x)
+    assert sum(gpu.passes()[:2]) == 3 and gpu.passes()[2] == 1
+
+
+def test_face_view_matches_restricted_oracle():  # test_oracle.cpp:156-186
+    tau = 1e-8
+    A, mu = rh.lcg_panel(6, 20, 9)
+    c = rh.crra(6.0)
+    x = np.array([0.3, tau, 0.25, 0.2, tau, 0.25 - 2 * tau])
+    idx, zoff, mu_pin, _ = po.restrict_to_face(A, mu, x, tau)
+    face_cpu = po.CpuOracle(A[:, idx], mu[idx], c, zoff=zoff, value_offset=-c[0] * mu_pin)
+    cr = face_cpu.make_cache(x[idx])
+    gpu = _gpu(A, mu, c)
+    gpu.set_face(idx, tau)
+    gc = gpu.make_cache(x[idx])
+    assert abs(gpu.value(gc) - face_cpu.value(cr)) <= 1e-12 * (1 + abs(face_cpu.value(cr)))
+    np.testing.assert_allclose(gpu.gradient(gc), face_cpu.gradient(cr), rtol=1e-12)
+    v = np.array([0.5, -0.2, 0.1, -0.4])
+    np.testing.assert_allclose(gpu.hvp(gc, v), face_cpu.hvp(cr, v), rtol=1e-11)
+    # the explicit zoff/value_offset constructor form (oracle.hpp:31-33)
+    g2 = _gpu(A[:, idx], mu[idx], c)
+    g2.set_offset(zoff, -c[0] * mu_pin)
+    c2 = g2.make_cache(x[idx])
+    assert abs(g2.value(c2) - face_cpu.value(cr)) <= 1e-13 * (1 + abs(face_cpu.value(cr)))
+    np.testing.assert_allclose(g2.gradient(c2), face_cpu.gradient(cr), rtol=1e-12)
+
+
+def test_typed_errors():  # test_oracle.cpp:208-225
+    from paper_2604_25378_b200.gpu_oracle import DimensionError, NumericError
+    A, mu = rh.lcg_panel(4, 10, 1)
+    c = rh.crra(2.0)
+    with pytest.raises(DimensionError):
+        _gpu(A, np.zeros(3), c)
+    g = _gpu(A, mu, c)
+    with pytest.raises(DimensionError):
+        g.make_cache(np.zeros(5))
+    wild = _gpu(np.full((4, 2), 1e200), np.zeros(2), c)
+    with pytest.raises(NumericError):
+        wild.make_cache(np.array([1.0, 0.0]))
+
+
+def test_weighted_gram_dmma():
+    for (n, T, seed) in [(20, 500, 1), (100, 1000, 2), (131, 777, 3), (300, 2000, 4)]:
+        A, mu = rh.lcg_panel(n, T, seed) if n <= 33 else (np.random.default_rng(seed).uniform(-0.1, 0.4, (T, n)), None)
+        if mu is None:
+            A = A - A.mean(axis=0)
+            mu = np.zeros(n)
+        c = rh.crra(10.0)
+        gpu = _gpu(A, mu, c)
+        x = rh.simplex_point(n, seed)
+        gc = gpu.make_cache(x)
+        z = A @ x
+        psi2 = 2 * c[1] - 6 * c[2] * z + 12 * c[3] * z * z
+        ref = (A * psi2[:, None]).T @ A / T
+        G = gpu.weighted_gram(gc)
+        scale = float(np.max((np.abs(A) * np.abs(psi2)[:, None]).T @ np.abs(A) / T))
+        _close(G, ref, scale)
+        assert np.array_equal(G, G.T)
+
+
+def test_datagen_configs_parity():
+    from paper_2604_25378_b200.datagen import make_panel, random_simplex_point, random_tangents
+    for name in ("C1", "C2", "C3"):
+        A, mu, c = make_panel(name, seed=1)
+        T, n = A.shape
+        x = random_simplex_point(n, 3)
+        V = random_tangents(n, 4, 3)
+        cpu, gpu = po.CpuOracle(A, mu, c), _gpu(A, mu, c)
+        cc, gc = cpu.make_cache(x), gpu.make_cache(x)
+        _close(gpu.value(gc), cpu.value(cc))
+        z = A @ x
+        _close(gpu.gradient(gc), cpu.gradient(cc),
+               _absscale(A, (2 * c[1] * z - 3 * c[2] * z * z + 4 * c[3] * z ** 3) / T))
+        H = gpu.hvp(gc, V)
+        psi2 = 2 * c[1] - 6 * c[2] * z + 12 * c[3] * z * z
+        for i in range(4):
+            _close(H[i], cpu.hvp(cc, V[i]), _absscale(A, psi2 * (A @ V[i]) / T))
+
+
+def test_device_path_matches_host_path():
+    torch = pytest.importorskip("torch")
+    from paper_2604_25378_b200.datagen import make_panel, random_simplex_point, random_tangents
+    A, mu, c = make_panel("C2", seed=2)
+    T, n = A.shape
+    Xd = torch.from_numpy(A).cuda()
+    gpu = _gpu(None, mu, c, device_panel=(Xd.data_ptr(), n, T, n))
+    host = _gpu(A, mu, c)
+    x = random_simplex_point(n, 1)
+    V = random_tangents(n, 8, 1)
+    xd = torch.from_numpy(x).cuda()
+    Vd = torch.from_numpy(V).cuda()
+    out = torch.empty_like(Vd)
+    gpu.make_cache_device(0, xd.data_ptr())
+    gpu.hvp_device(0, Vd.data_ptr(), 8, out.data_ptr())
+    sums = torch.empty(9, dtype=torch.float64, device="cuda")
+    gpu.line_sums_device(0, Vd[0].data_ptr(), sums.data_ptr())
+    gpu.synchronize()
+    hc = host.make_cache(x)
+    np.testing.assert_array_equal(out.cpu().numpy(), host.hvp(hc, V))
+    lm = host.line_model(hc, V[0], 1.0)
+    np.testing.assert_array_equal(sums.cpu().numpy(), lm.sums)
+    z, g, s = gpu.slot_pointers(0)
+    assert z and g and s
