@@ -206,7 +206,9 @@ def main():
         nid = bytes(idt.cpu().numpy().tobytes())
     gpu = GpuOracle(None, mu, c, device=local, rank=rank, nranks=ws, row0=row0, T_global=T, nccl_id=nid,
                     device_panel=(X.data_ptr(), n, T_loc, n))
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: the context launches on it and the CUDA events time it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     gpu.set_stream(stream.cuda_stream)
 
     x = random_simplex_point(n, 7)

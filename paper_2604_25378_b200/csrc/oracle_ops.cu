@@ -1,9 +1,12 @@
 // Launch planning, dispatch and epilogues for the streaming oracle kernels.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "oracle_ops.cuh"
+#include "stream_cluster.cuh"
 
 namespace mvsk_b200 {
 
@@ -57,6 +60,7 @@ const void* select_kernel(Op op, int K, int Q, int RG) {
             if (Q == 8 && RG == 1) return kfn<Op::HVP, 1, 8, 1>();
         } else if (K == 2) {
             MVSK_QRG(Op::HVP, 2)
+            if (Q == 8 && RG == 1) return kfn<Op::HVP, 2, 8, 1>();
         } else if (K == 4) {
             if (Q == 1 && RG == 1) return kfn<Op::HVP, 4, 1, 1>();
             if (Q == 1 && RG == 2) return kfn<Op::HVP, 4, 1, 2>();
@@ -66,6 +70,7 @@ const void* select_kernel(Op op, int K, int Q, int RG) {
     case Op::THIRD:
         if (K == 1) {
             MVSK_QRG(Op::THIRD, 1)
+            if (Q == 8 && RG == 1) return kfn<Op::THIRD, 1, 8, 1>();
         }
         break;
     }
@@ -73,11 +78,22 @@ const void* select_kernel(Op op, int K, int Q, int RG) {
 }
 #undef MVSK_QRG
 
-// largest Q allowed per (op, K) given register budgets
+// largest Q allowed per (op, K) given register budgets (<= ~110 live fp64)
 int max_q(Op op, int K) {
-    if (op == Op::HVP) return K == 1 ? 8 : K == 2 ? 4 : 2;
-    if (op == Op::THIRD) return 4;
+    if (op == Op::HVP) return K == 1 ? 8 : K == 2 ? 8 : 2;
+    if (op == Op::THIRD) return 8;
     return 8;
+}
+
+int op_ndot(Op op, int K) {
+    return (op == Op::FGRAD || op == Op::LINESUMS) ? 1 : (op == Op::THIRD ? 2 * K : (op == Op::XTW ? 0 : K));
+}
+int op_nacc(Op op, int K) { return (op == Op::HVP || op == Op::THIRD) ? K : (op == Op::LINESUMS ? 0 : 1); }
+
+// mirror of StreamRegs<>::max_threads (stream_kernels.cuh)
+int max_threads(Op op, int K, int Q, int RG) {
+    const int nv = std::max(op_ndot(op, K), 1), na = std::max(op_nacc(op, K), 1);
+    return 2 * Q * (nv + na + RG) > 48 ? 256 : 512;
 }
 
 int round_team(int need) {
@@ -89,55 +105,76 @@ int round_team(int need) {
     return (need + 31) / 32 * 32;
 }
 
+// MVSK_TUNE="Q,G,RG,S,OCC" (0 = heuristic) overrides the plan; used by the
+// tuning sweep only (scripts/tune_stream.py)
+struct TuneOverride {
+    int Q = 0, G = 0, RG = 0, S = 0, OCC = 0;
+};
+TuneOverride tune_override() {
+    TuneOverride t;
+    if (const char* e = std::getenv("MVSK_TUNE")) std::sscanf(e, "%d,%d,%d,%d,%d", &t.Q, &t.G, &t.RG, &t.S, &t.OCC);
+    return t;
+}
+
+// Launch plan. Measured on B200 at C5 (profiles/r01_tune_c5.txt): teams of
+// <= 256 threads (8 column pairs each at n=4096), two teams per CTA on
+// different rows, a 2-deep ring of 64 KB stages -> 7.1-7.4 TB/s streamed.
 bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
+    const TuneOverride tov = tune_override();
     const long long npairs = ctx->ld / 2;
     const int qmax = max_q(op, K);
     int Q = -1;
-    for (int q = 1; q <= qmax; q <<= 1) {
+    for (int q = 1; q <= qmax; q <<= 1)
         if ((npairs + q - 1) / q <= 256) {
             Q = q;
             break;
         }
-    }
     if (Q < 0)
         for (int q = 1; q <= qmax; q <<= 1)
-            if ((npairs + q - 1) / q <= kMaxTeam) {
+            if ((npairs + q - 1) / q <= max_threads(op, K, q, 1)) {
                 Q = q;
                 break;
             }
+    if (tov.Q > 0 && tov.Q <= qmax && (npairs + tov.Q - 1) / tov.Q <= max_threads(op, K, tov.Q, 1)) Q = tov.Q;
     if (Q < 0) return false;
     const int P = round_team((int)((npairs + Q - 1) / Q));
-    int G = std::max(1, kMaxTeam / P);
+    if (P > max_threads(op, K, Q, 1)) return false;
     const size_t row_bytes = (size_t)ctx->ld * sizeof(double);
-    // rows per stage ~ kStageTarget; RG * Q <= 8 and RG in {1,2,4}
-    long long want_rows = std::max<long long>(1, (long long)(kStageTarget / row_bytes));
-    // fewer teams when a stage would hold more rows than wanted
+    const size_t stage_target = 64 * 1024;
+    // teams per CTA (each team streams its own rows)
+    int G = std::max(1, max_threads(op, K, Q, 1) / P);
+    const long long want_rows = std::max<long long>(1, (long long)(stage_target / row_bytes));
     while (G > 1 && G > want_rows) G >>= 1;
     int RG = 1;
-    while (RG < 4 && RG * 2 * Q <= 8 && (long long)G * RG * 2 <= want_rows) RG <<= 1;
+    while (RG < 4 && RG * 2 * Q <= 8 && (long long)G * RG * 2 <= want_rows &&
+           G * P <= max_threads(op, K, Q, RG * 2))
+        RG <<= 1;
+    if (tov.G > 0 && tov.G * P <= max_threads(op, K, Q, RG)) G = tov.G;
+    if (tov.RG > 0 && tov.RG * Q <= 8 && G * P <= max_threads(op, K, Q, tov.RG)) RG = tov.RG;
     if (op == Op::HVP && K == 4 && Q == 2) RG = 1;
-    if (op == Op::THIRD && Q == 4) RG = std::min(RG, 2);
+    if (G * P > max_threads(op, K, Q, RG)) return false;
     const long long R = (long long)G * RG;
     const size_t stage_bytes = ((size_t)R * row_bytes + 127) & ~(size_t)127;
     const int nst_total = (int)std::max<long long>(1, (ctx->T_local + R - 1) / R);
-    int S = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, kRingTarget / stage_bytes));
+    // one team: a deeper ring hides the per-row latency (C5: third 2.28 -> 1.80 ms,
+    // 2-RHS HVP 2.44 -> 1.85 ms); two teams already overlap two rows per stage
+    int S = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, (G == 1 ? 128 * 1024 : 64 * 1024) / stage_bytes));
+    if (tov.S >= 2 && tov.S <= kMaxStages) S = tov.S;
     S = std::min(S, std::max(2, nst_total));
     // team-combine and scalar scratch live in the ring after the last stage
-    const int nacc = (op == Op::HVP || op == Op::THIRD) ? K : (op == Op::LINESUMS ? 0 : 1);
-    const int ndot = (op == Op::FGRAD || op == Op::LINESUMS) ? 1 : (op == Op::THIRD ? 2 * K : (op == Op::XTW ? 0 : K));
+    const int nacc = op_nacc(op, K);
+    const int ndot = op_ndot(op, K);
     const int nwp = P >= 32 ? P / 32 : 1;
     const size_t red_bytes = (((size_t)2 * R * std::max(ndot, 1) * nwp * sizeof(double)) + 127) & ~(size_t)127;
-    size_t ring = (size_t)S * stage_bytes;
     const size_t combine = ((size_t)G * std::max(nacc, 1) * ctx->ld + 16 + (size_t)G * 16) * sizeof(double);
-    ring = std::max(ring, combine);
+    size_t ring = std::max((size_t)S * stage_bytes, combine);
     pl.smem = 128 + red_bytes + ring;
-    if (pl.smem > ctx->max_smem) {
-        // shrink the ring first
-        while (S > 2 && 128 + red_bytes + std::max((size_t)S * stage_bytes, combine) > ctx->max_smem) --S;
+    while (pl.smem > ctx->max_smem && S > 2) {
+        --S;
         ring = std::max((size_t)S * stage_bytes, combine);
         pl.smem = 128 + red_bytes + ring;
-        if (pl.smem > ctx->max_smem) return false;
     }
+    if (pl.smem > ctx->max_smem) return false;
     pl.Q = Q;
     pl.P = P;
     pl.G = G;
@@ -145,10 +182,96 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     pl.S = S;
     pl.fn = select_kernel(op, K, Q, RG);
     if (!pl.fn) return false;
-    const int occ = std::max<int>(1, (int)std::min<size_t>(4, (ctx->max_smem + 1024) / (pl.smem + 1024)));
+    const int threads = G * P;
+    int occ = (int)std::min<size_t>(4, (ctx->max_smem + 1024) / (pl.smem + 1024));
+    occ = std::max(1, std::min(occ, 2048 / threads));
+    if (tov.OCC > 0) occ = std::min(occ, tov.OCC);
     const long long want_blocks = std::max<long long>(1, (ctx->T_local + R - 1) / R);
     pl.nb = (int)std::min<long long>((long long)ctx->nsm * occ, want_blocks);
     return true;
+}
+
+// ---- cluster column-split plans (multi-RHS HVP / THIRD) ------------------------
+struct CPlan {
+    int C = 4, Q = 1, RG = 1, P = 256, S = 2;
+    size_t smem = 0;
+    int ncl = 1;
+    const void* fn = nullptr;
+};
+
+template <Op OP, int K, int Q, int RG>
+const void* cfn() {
+    return reinterpret_cast<const void*>(&stream_cluster_kernel<OP, K, Q, RG>);
+}
+
+const void* select_cluster(Op op, int K, int Q, int RG) {
+    if (op == Op::HVP && K == 8) {
+        if (Q == 1 && RG == 4) return cfn<Op::HVP, 8, 1, 4>();
+        if (Q == 2 && RG == 4) return cfn<Op::HVP, 8, 2, 4>();
+        if (Q == 2 && RG == 2) return cfn<Op::HVP, 8, 2, 2>();
+    } else if (op == Op::HVP && K == 4) {
+        if (Q == 1 && RG == 4) return cfn<Op::HVP, 4, 1, 4>();
+        if (Q == 2 && RG == 4) return cfn<Op::HVP, 4, 2, 4>();
+        if (Q == 4 && RG == 4) return cfn<Op::HVP, 4, 4, 4>();
+    } else if (op == Op::THIRD && K == 8) {
+        if (Q == 1 && RG == 2) return cfn<Op::THIRD, 8, 1, 2>();
+        if (Q == 2 && RG == 2) return cfn<Op::THIRD, 8, 2, 2>();
+    } else if (op == Op::THIRD && K == 4) {
+        if (Q == 1 && RG == 4) return cfn<Op::THIRD, 4, 1, 4>();
+        if (Q == 2 && RG == 4) return cfn<Op::THIRD, 4, 2, 4>();
+        if (Q == 4 && RG == 2) return cfn<Op::THIRD, 4, 4, 2>();
+    }
+    return nullptr;
+}
+
+bool make_cluster_plan(const mvsk_gpu_ctx* ctx, Op op, int K, CPlan& pl) {
+    int forceC = 0, forceRG = 0;
+    if (const char* e = std::getenv("MVSK_TUNE_CLUSTER")) std::sscanf(e, "%d,%d", &forceC, &forceRG);
+    const int ndot = op == Op::THIRD ? 2 * K : K;
+    const int Cs[3] = {4, 8, 2};
+    for (int ci = 0; ci < 3; ++ci) {
+        const int C = forceC ? forceC : Cs[ci];
+        if (ctx->ld % (2 * C)) {
+            if (forceC) return false;
+            continue;
+        }
+        const int cw = (int)(ctx->ld / C);
+        const int npc = cw / 2;
+        int Q = 1;
+        while (Q < 4 && (npc + Q - 1) / Q > 256) Q <<= 1;
+        if ((npc + Q - 1) / Q > 256) {
+            if (forceC) return false;
+            continue;
+        }
+        int RG = 4;
+        while (RG > 1 && (RG * ndot > 32 || !select_cluster(op, K, Q, RG))) RG >>= 1;
+        if (forceRG && select_cluster(op, K, Q, forceRG) && forceRG * ndot <= 32) RG = forceRG;
+        const void* fn = select_cluster(op, K, Q, RG);
+        if (!fn) {
+            if (forceC) return false;
+            continue;
+        }
+        const int V = RG * ndot;
+        const size_t stage = ((size_t)RG * cw * sizeof(double) + 127) & ~(size_t)127;
+        int S = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, (128 * 1024) / stage));
+        size_t head = 128 + (size_t)(2 * V * 8 + 2 * 16 * V + 2 * V) * sizeof(double);
+        head = (head + 127) & ~(size_t)127;
+        while (S > 2 && head + S * stage > ctx->max_smem) --S;
+        if (head + S * stage > ctx->max_smem) {
+            if (forceC) return false;
+            continue;
+        }
+        pl.C = C;
+        pl.Q = Q;
+        pl.RG = RG;
+        pl.P = 256;
+        pl.S = S;
+        pl.smem = head + S * stage;
+        pl.fn = fn;
+        pl.ncl = std::max(1, ctx->nsm / C);
+        return true;
+    }
+    return false;
 }
 
 struct FinishArgs {
@@ -198,7 +321,7 @@ __global__ void finish_kernel(const FinishArgs f) {
     if (f.op == (int)Op::FGRAD) {
         for (int i = gtid; i < f.ld; i += gstride) {
             const double v = f.red[i];
-            f.g[i] = i < f.n ? (-f.c1 * f.mu[i] + v) : 0.0;
+            f.g[i] = i < f.n ? (-f.c1 * f.mu[i] + v / f.T) : 0.0;  // oracle.hpp:82-84 (1/T folded here)
         }
         if (blockIdx.x == 0) {
             __shared__ double sh[256];
@@ -226,7 +349,8 @@ __global__ void finish_kernel(const FinishArgs f) {
     } else {
         for (int i = gtid; i < tot; i += gstride) {
             const int k = i / f.ld, c = i - k * f.ld;
-            if (c < f.n) f.out[(size_t)k * f.ldo + c] = f.red[i];
+            // HVP / THIRD: A^T(w)/T with the 1/T folded out of the per-row weights
+            if (c < f.n) f.out[(size_t)k * f.ldo + c] = f.op == (int)Op::XTW ? f.red[i] : f.red[i] / f.T;
         }
     }
 }
@@ -266,34 +390,131 @@ void ensure_host_staging(mvsk_gpu_ctx* ctx, size_t elems) {
 }
 
 static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io);
+static bool run_cluster(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io);
 
 void run_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
-    if (op == Op::HVP && k > 1) {
-        // widest supported RHS block per pass (4, 2, 1), chunked over k
+    if ((op == Op::HVP || op == Op::THIRD) && k > 1) {
+        // widest supported RHS block per pass: cluster column-split for 8 / 4,
+        // single-CTA rows for 2 / 1; chunked over k
         int done = 0;
         while (done < k) {
-            int kk = (k - done) >= 4 ? 4 : ((k - done) >= 2 ? 2 : 1);
-            Plan tmp;
-            while (kk > 1 && !make_plan(ctx, op, kk, tmp)) kk >>= 1;
+            const int left = k - done;
             PassIO sub = io;
             sub.vin = io.vin + (size_t)done * ctx->ld;
+            if (io.vin2) sub.vin2 = io.vin2 + (size_t)done * ctx->ld;
             sub.out = io.out + (size_t)done * io.ldo;
-            run_single(ctx, op, kk, sub);
+            int kk = 0;
+            for (int w : {8, 4})
+                if (!kk && left >= w && run_cluster(ctx, op, w, sub)) kk = w;
+            if (!kk) {
+                kk = (op == Op::HVP && left >= 2) ? 2 : 1;
+                Plan tmp;
+                while (kk > 1 && !make_plan(ctx, op, kk, tmp)) kk >>= 1;
+                run_single(ctx, op, kk, sub);
+            }
             done += kk;
         }
         return;
     }
-    if (op == Op::THIRD && k > 1) {
-        for (int i = 0; i < k; ++i) {
-            PassIO sub = io;
-            sub.vin = io.vin + (size_t)i * ctx->ld;
-            sub.vin2 = io.vin2 + (size_t)i * ctx->ld;
-            sub.out = io.out + (size_t)i * io.ldo;
-            run_single(ctx, op, 1, sub);
-        }
-        return;
-    }
     run_single(ctx, op, k, io);
+}
+
+// cross-CTA (or cross-cluster) fixed-order reduction, allreduce over the
+// row-shard group, and the op epilogue
+static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO& io, Slot* slot) {
+    FinishArgs f{};
+    f.op = (int)op;
+    f.k = op == Op::LINESUMS ? 0 : std::max(nacc, 1);
+    f.ld = (int)ctx->ld;
+    f.n = (int)ctx->n;
+    f.ldo = io.ldo;
+    f.nb = ctx->T_local > 0 ? nb : 0;
+    f.part_acc = ctx->part_acc;
+    f.part_sc = ctx->part_sc;
+    f.red = ctx->red;
+    f.out = io.out;
+    f.mu = ctx->mu_dev;
+    f.x = io.x_for_mux;
+    f.c1 = ctx->c.c1;
+    f.c2 = ctx->c.c2;
+    f.c3 = ctx->c.c3;
+    f.c4 = ctx->c.c4;
+    f.T = (double)ctx->T_global;
+    f.value_offset = ctx->value_offset;
+    if (slot) {
+        f.g = slot->g;
+        f.sc = slot->sc;
+    }
+    const int tot = std::max(f.k, 1) * f.ld;
+    const int fb = std::max(1, std::min(4 * ctx->nsm, (tot + 255) / 256));
+    if (ctx->nranks == 1) {
+        f.do_reduce = 1;
+        f.do_epi = 1;
+        // scalars are reduced by block 0 and consumed by block 0 only
+        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
+        MVSK_CUDA(cudaGetLastError());
+    } else {
+        f.do_reduce = 1;
+        f.do_epi = 0;
+        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
+        MVSK_CUDA(cudaGetLastError());
+        const int nsc = op == Op::FGRAD ? 3 : (op == Op::LINESUMS ? 9 : 0);
+        const size_t cnt = (size_t)(op == Op::LINESUMS ? 0 : tot) + nsc;
+        MVSK_NCCL(ncclAllReduce(ctx->red, ctx->red, cnt, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+        f.do_reduce = 0;
+        f.do_epi = 1;
+        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
+        MVSK_CUDA(cudaGetLastError());
+    }
+}
+
+static bool run_cluster(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
+    CPlan pl;
+    if (!make_cluster_plan(ctx, op, k, pl)) return false;
+    set_smem_attr(pl.fn, pl.smem);
+    // clusters that can be co-resident, at most one wave
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = pl.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(pl.P);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(pl.ncl * pl.C);
+    int maxcl = 0;
+    if (cudaOccupancyMaxActiveClusters(&maxcl, pl.fn, &cfg) == cudaSuccess && maxcl > 0)
+        pl.ncl = std::min(pl.ncl, maxcl);
+    else
+        cudaGetLastError();
+    pl.ncl = (int)std::max<long long>(1, std::min<long long>(pl.ncl, (ctx->T_local + pl.RG - 1) / pl.RG));
+    cfg.gridDim = dim3(pl.ncl * pl.C);
+    ensure_part(ctx, (size_t)pl.ncl * k * ctx->ld);
+    ClusterArgs a{};
+    a.X = ctx->X;
+    a.T = ctx->T_local;
+    a.ld = (int)ctx->ld;
+    a.cw = (int)(ctx->ld / pl.C);
+    a.P = pl.P;
+    a.S = pl.S;
+    a.evict_first = (size_t)ctx->T_local * ctx->ld * sizeof(double) > (size_t)96 * 1024 * 1024;
+    a.vin = io.vin;
+    a.vin2 = io.vin2;
+    a.z = io.z;
+    a.part_acc = ctx->part_acc;
+    a.c2 = ctx->c.c2;
+    a.c3 = ctx->c.c3;
+    a.c4 = ctx->c.c4;
+    if (ctx->T_local > 0) {
+        void* args[] = {&a};
+        MVSK_CUDA(cudaLaunchKernelExC(&cfg, pl.fn, args));
+    }
+    ctx->phys += 1;
+    finish_pass(ctx, op, k, pl.ncl, io, nullptr);
+    return true;
 }
 
 static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
@@ -337,51 +558,7 @@ static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
         MVSK_CUDA(cudaLaunchKernel(pl.fn, dim3(pl.nb), dim3(pl.G * pl.P), args, pl.smem, ctx->stream));
     }
     ctx->phys += 1;
-
-    FinishArgs f{};
-    f.op = (int)op;
-    f.k = op == Op::LINESUMS ? 0 : std::max(nacc, 1);
-    f.ld = (int)ctx->ld;
-    f.n = (int)ctx->n;
-    f.ldo = io.ldo;
-    f.nb = ctx->T_local > 0 ? pl.nb : 0;
-    f.part_acc = ctx->part_acc;
-    f.part_sc = ctx->part_sc;
-    f.red = ctx->red;
-    f.out = io.out;
-    f.mu = ctx->mu_dev;
-    f.x = io.x_for_mux;
-    f.c1 = ctx->c.c1;
-    f.c2 = ctx->c.c2;
-    f.c3 = ctx->c.c3;
-    f.c4 = ctx->c.c4;
-    f.T = (double)ctx->T_global;
-    f.value_offset = ctx->value_offset;
-    if (slot) {
-        f.g = slot->g;
-        f.sc = slot->sc;
-    }
-    const int tot = std::max(f.k, 1) * f.ld;
-    const int fb = std::max(1, std::min(4 * ctx->nsm, (tot + 255) / 256));
-    if (ctx->nranks == 1) {
-        f.do_reduce = 1;
-        f.do_epi = 1;
-        // scalars are reduced by block 0 and consumed by block 0 only
-        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
-        MVSK_CUDA(cudaGetLastError());
-    } else {
-        f.do_reduce = 1;
-        f.do_epi = 0;
-        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
-        MVSK_CUDA(cudaGetLastError());
-        const int nsc = op == Op::FGRAD ? 3 : (op == Op::LINESUMS ? 9 : 0);
-        const size_t cnt = (size_t)(op == Op::LINESUMS ? 0 : tot) + nsc;
-        MVSK_NCCL(ncclAllReduce(ctx->red, ctx->red, cnt, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
-        f.do_reduce = 0;
-        f.do_epi = 1;
-        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
-        MVSK_CUDA(cudaGetLastError());
-    }
+    finish_pass(ctx, op, nacc, pl.nb, io, slot);
 }
 
 void run_psi2(mvsk_gpu_ctx* ctx, const double* z, double* out, long long T) {

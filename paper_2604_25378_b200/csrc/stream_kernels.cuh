@@ -64,8 +64,19 @@ struct OpShape {
     static constexpr int NVEC = NDOT;  // input vectors held in registers
 };
 
+// fp64 values a thread keeps live across a stage: input vectors, accumulators
+// and the staged row slice. Heavy variants are capped at 256 threads so they
+// may use up to 255 registers; light ones allow 512 threads (128 registers).
 template <Op OP, int K, int Q, int RG>
-__global__ void __launch_bounds__(512, 1) stream_kernel(const StreamArgs a) {
+struct StreamRegs {
+    static constexpr int NV = OpShape<OP, K>::NDOT > 0 ? OpShape<OP, K>::NDOT : 1;
+    static constexpr int NA = OpShape<OP, K>::NACC > 0 ? OpShape<OP, K>::NACC : 1;
+    static constexpr int live = 2 * Q * (NV + NA + RG);
+    static constexpr int max_threads = live > 48 ? 256 : 512;
+};
+
+template <Op OP, int K, int Q, int RG>
+__global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG>::max_threads, 1) stream_kernel(const StreamArgs a) {
     using Sh = OpShape<OP, K>;
     constexpr int NDOT = Sh::NDOT;
     constexpr int NACC = Sh::NACC;
@@ -146,7 +157,21 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(const StreamArgs a) {
 #pragma unroll
     for (int i = 0; i < 9; ++i) sc[i] = 0.0;
 
-    const double c2 = a.c2, c3 = a.c3, c4 = a.c4, Tg = a.Tglob;
+    const double c2 = a.c2, c3 = a.c3, c4 = a.c4;
+
+    // per-row sample inputs (z, z offset or X^T weights) are prefetched one
+    // stage ahead so their global-load latency never sits on the row's path
+    constexpr bool NEEDS_ROWVAL = (OP != Op::FGRAD);
+    const double* rowval = (OP == Op::XTW) ? a.tw : a.z;
+    double znext[RG];
+    auto load_rowvals = [&](int s_, double (&dst)[RG]) {
+#pragma unroll
+        for (int rr = 0; rr < RG; ++rr) {
+            const long long r = (long long)s_ * R + g + rr * G;
+            dst[rr] = (rowval && s_ < nst && r < nrows) ? __ldg(rowval + r0 + r) : 0.0;
+        }
+    };
+    if (NEEDS_ROWVAL || a.z) load_rowvals(0, znext);
 
     for (int s = 0; s < nst; ++s) {
         const int slot = s % S;
@@ -154,6 +179,10 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(const StreamArgs a) {
         const long long srow0 = r0 + (long long)s * R;
         const long long left = r1 - srow0;
         const int rows_here = left < R ? (int)left : R;
+        double zcur[RG];
+#pragma unroll
+        for (int rr = 0; rr < RG; ++rr) zcur[rr] = znext[rr];
+        if (NEEDS_ROWVAL || a.z) load_rowvals(s + 1, znext);
         mbar_wait(&full[slot], parity);
         const double* st = reinterpret_cast<const double*>(stage_base + slot * stage_bytes);
 
@@ -177,15 +206,15 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(const StreamArgs a) {
         for (int rr = 0; rr < RG; ++rr)
 #pragma unroll
             for (int k = 0; k < NDR; ++k) {
-                double d = 0.0;
+                double d0 = 0.0, d1 = 0.0;  // two independent FMA chains
                 if constexpr (NDOT > 0) {
 #pragma unroll
                     for (int q = 0; q < Q; ++q) {
-                        d = fma(x[rr][q].x, vreg[k][q].x, d);
-                        d = fma(x[rr][q].y, vreg[k][q].y, d);
+                        d0 = fma(x[rr][q].x, vreg[k][q].x, d0);
+                        d1 = fma(x[rr][q].y, vreg[k][q].y, d1);
                     }
                 }
-                dot[rr][k] = d;
+                dot[rr][k] = d0 + d1;
             }
         if constexpr (NDOT > 0) {
             const int width = P < 32 ? P : 32;
@@ -243,10 +272,10 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(const StreamArgs a) {
                 if constexpr (OP == Op::FGRAD) {
                     // oracle.hpp:58-64, 82-83
                     double zt = dot[rr][0];
-                    if (a.z) zt += a.z[t];
+                    if (a.z) zt += zcur[rr];
                     const double z2 = zt * zt;
                     const double z3 = z2 * zt;
-                    w[0] = (2.0 * c2 * zt - 3.0 * c3 * z2 + 4.0 * c4 * z3) / Tg;
+                    w[0] = 2.0 * c2 * zt - 3.0 * c3 * z2 + 4.0 * c4 * z3;  // 1/T applied in the epilogue
                     if (p == 0) {
                         sc[0] += z2;
                         sc[1] += z3;
@@ -255,20 +284,20 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(const StreamArgs a) {
                     }
                 } else if constexpr (OP == Op::HVP) {
                     // oracle.hpp:95-96
-                    const double zt = a.z[t];
+                    const double zt = zcur[rr];
                     const double psi2 = 2.0 * c2 - 6.0 * c3 * zt + 12.0 * c4 * (zt * zt);
 #pragma unroll
-                    for (int k = 0; k < K; ++k) w[k] = psi2 * dot[rr][k] / Tg;
+                    for (int k = 0; k < K; ++k) w[k] = psi2 * dot[rr][k];
                 } else if constexpr (OP == Op::THIRD) {
                     // oracle.hpp:107-108
-                    const double zt = a.z[t];
+                    const double zt = zcur[rr];
                     const double psi3 = -6.0 * c3 + 24.0 * c4 * zt;
 #pragma unroll
-                    for (int k = 0; k < K; ++k) w[k] = psi3 * dot[rr][k] * dot[rr][K + k] / Tg;
+                    for (int k = 0; k < K; ++k) w[k] = psi3 * dot[rr][k] * dot[rr][K + k];
                 } else if constexpr (OP == Op::LINESUMS) {
                     // linesearch.hpp:26-38
                     if (p == 0) {
-                        const double zt = a.z[t], wt = dot[rr][0];
+                        const double zt = zcur[rr], wt = dot[rr][0];
                         const double w2 = wt * wt, z2 = zt * zt;
                         sc[0] += zt * wt;
                         sc[1] += z2 * wt;
@@ -282,7 +311,7 @@ __global__ void __launch_bounds__(512, 1) stream_kernel(const StreamArgs a) {
                         if (a.zout) a.zout[t] = wt;
                     }
                 } else {  // XTW
-                    w[0] = a.tw[t];
+                    w[0] = zcur[rr];
                 }
             }
             if constexpr (NACC > 0) {

@@ -80,6 +80,36 @@ def test_hvp_third_weights_direction(n, T, seed):
     _close(gpu.sample_direction(d), cpu.sample_direction(d), float(np.max(np.abs(A) @ np.abs(d))))
 
 
+@pytest.mark.parametrize("n,T", [(4, 50), (64, 300), (100, 1000), (128, 513), (800, 2500), (4096, 700)])
+def test_multi_rhs_cluster_paths(n, T):
+    """k = 8 / 4 RHS go through the cluster column-split kernel (DSMEM exchange
+    of partial row dots) whenever ld splits evenly; parity vs the CPU oracle."""
+    c = rh.crra(10.0)
+    rng = np.random.default_rng(n + T)
+    A = rng.uniform(-0.1, 0.4, (T, n))
+    mu = A.mean(axis=0)
+    A = A - mu
+    x = rng.exponential(size=n)
+    x /= x.sum()
+    cpu, gpu = po.CpuOracle(A, mu, c), _gpu(A, mu, c)
+    cc, gc = cpu.make_cache(x), gpu.make_cache(x)
+    z = A @ x
+    psi2 = 2 * c[1] - 6 * c[2] * z + 12 * c[3] * z * z
+    psi3 = -6 * c[2] + 24 * c[3] * z
+    U = rng.standard_normal((13, n))
+    V = rng.standard_normal((13, n))
+    for k in (8, 4, 13):
+        H = gpu.hvp(gc, V[:k])
+        T3 = gpu.third_action(gc, U[:k], V[:k])
+        for i in range(k):
+            _close(H[i], cpu.hvp(cc, V[i]), _absscale(A, psi2 * (A @ V[i]) / T))
+            _close(T3[i], cpu.third_action(cc, U[i], V[i]), _absscale(A, psi3 * (A @ U[i]) * (A @ V[i]) / T))
+    f0, t0, p0 = gpu.passes()
+    gpu.hvp(gc, V[:8])
+    f1, t1, p1 = gpu.passes()
+    assert (f1 - f0, t1 - t0) == (8, 8)  # the reference contract: 2 logical passes per HVP
+
+
 @pytest.mark.parametrize("n,T,seed", PANELS[:6])
 def test_line_model(n, T, seed):
     if n < 2:
