@@ -204,22 +204,27 @@ const void* cfn() {
     return reinterpret_cast<const void*>(&stream_cluster_kernel<OP, K, Q, RG>);
 }
 
+// instantiated (K, Q, RG): the pipelined kernel keeps two copies of the staged
+// row slice, so the register budget (<= 255) bounds Q * RG per K
 const void* select_cluster(Op op, int K, int Q, int RG) {
     if (op == Op::HVP && K == 8) {
         if (Q == 1 && RG == 4) return cfn<Op::HVP, 8, 1, 4>();
-        if (Q == 2 && RG == 4) return cfn<Op::HVP, 8, 2, 4>();
+        if (Q == 1 && RG == 2) return cfn<Op::HVP, 8, 1, 2>();
         if (Q == 2 && RG == 2) return cfn<Op::HVP, 8, 2, 2>();
+        if (Q == 2 && RG == 1) return cfn<Op::HVP, 8, 2, 1>();
     } else if (op == Op::HVP && K == 4) {
         if (Q == 1 && RG == 4) return cfn<Op::HVP, 4, 1, 4>();
         if (Q == 2 && RG == 4) return cfn<Op::HVP, 4, 2, 4>();
-        if (Q == 4 && RG == 4) return cfn<Op::HVP, 4, 4, 4>();
+        if (Q == 2 && RG == 2) return cfn<Op::HVP, 4, 2, 2>();
+        if (Q == 4 && RG == 2) return cfn<Op::HVP, 4, 4, 2>();
+        if (Q == 4 && RG == 1) return cfn<Op::HVP, 4, 4, 1>();
     } else if (op == Op::THIRD && K == 8) {
         if (Q == 1 && RG == 2) return cfn<Op::THIRD, 8, 1, 2>();
-        if (Q == 2 && RG == 2) return cfn<Op::THIRD, 8, 2, 2>();
+        if (Q == 1 && RG == 1) return cfn<Op::THIRD, 8, 1, 1>();
     } else if (op == Op::THIRD && K == 4) {
         if (Q == 1 && RG == 4) return cfn<Op::THIRD, 4, 1, 4>();
-        if (Q == 2 && RG == 4) return cfn<Op::THIRD, 4, 2, 4>();
-        if (Q == 4 && RG == 2) return cfn<Op::THIRD, 4, 4, 2>();
+        if (Q == 2 && RG == 2) return cfn<Op::THIRD, 4, 2, 2>();
+        if (Q == 2 && RG == 1) return cfn<Op::THIRD, 4, 2, 1>();
     }
     return nullptr;
 }
@@ -254,7 +259,7 @@ bool make_cluster_plan(const mvsk_gpu_ctx* ctx, Op op, int K, CPlan& pl) {
         const int V = RG * ndot;
         const size_t stage = ((size_t)RG * cw * sizeof(double) + 127) & ~(size_t)127;
         int S = (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, (128 * 1024) / stage));
-        size_t head = 128 + (size_t)(2 * V * 8 + 2 * 16 * V + 2 * V) * sizeof(double);
+        size_t head = 256 + (size_t)(2 * V * 8 + kXSlots * 16 * V + 2 * V) * sizeof(double);
         head = (head + 127) & ~(size_t)127;
         while (S > 2 && head + S * stage > ctx->max_smem) --S;
         if (head + S * stage > ctx->max_smem) {
@@ -293,41 +298,47 @@ struct FinishArgs {
     double c1, c2, c3, c4, T, value_offset;
 };
 
-__global__ void finish_kernel(const FinishArgs f) {
+// Block = 64 output columns x 4 partial-range groups; each thread sums its
+// quarter of the CTA partials with 4 independent accumulators, the quarters are
+// combined in a fixed order (deterministic), then the op epilogue is applied.
+constexpr int kFinCols = 64;
+__global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
     const int nacc = (f.op == (int)Op::LINESUMS) ? 0 : f.k;
     const int tot = nacc * f.ld;
     const int nsc = f.op == (int)Op::FGRAD ? 3 : (f.op == (int)Op::LINESUMS ? 9 : 0);
-    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int gstride = gridDim.x * blockDim.x;
+    const int cl = threadIdx.x & (kFinCols - 1), grp = threadIdx.x / kFinCols;
+    const int i = blockIdx.x * kFinCols + cl;
+    __shared__ double part[4][kFinCols];
+    auto qsum = [&](const double* base, size_t stride, int lo, int hi) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int b = lo;
+        for (; b + 3 < hi; b += 4) {
+            a0 += base[(size_t)b * stride];
+            a1 += base[(size_t)(b + 1) * stride];
+            a2 += base[(size_t)(b + 2) * stride];
+            a3 += base[(size_t)(b + 3) * stride];
+        }
+        for (; b < hi; ++b) a0 += base[(size_t)b * stride];
+        return (a0 + a1) + (a2 + a3);
+    };
     // 1) fixed-order reduction over CTA partials
     if (f.do_reduce) {
-        for (int i = gtid; i < tot; i += gstride) {
-            double v = 0.0;
-            for (int b = 0; b < f.nb; ++b) v += f.part_acc[(size_t)b * tot + i];
-            f.red[i] = v;
-        }
-        if (blockIdx.x == 0 && threadIdx.x < nsc) {
-            double v = 0.0;
-            for (int b = 0; b < f.nb; ++b) v += f.part_sc[(size_t)b * kNumScalars + threadIdx.x];
-            f.red[tot + threadIdx.x] = v;
-        }
+        if (i < tot) part[grp][cl] = qsum(f.part_acc + i, (size_t)tot, f.nb * grp / 4, f.nb * (grp + 1) / 4);
+        if (blockIdx.x == 0 && threadIdx.x < nsc)
+            f.red[tot + threadIdx.x] = qsum(f.part_sc + threadIdx.x, kNumScalars, 0, f.nb);
+        __syncthreads();
+        if (grp == 0 && i < tot) f.red[i] = ((part[0][cl] + part[1][cl]) + part[2][cl]) + part[3][cl];
+        __syncthreads();
     }
     if (!f.do_epi) return;
-    if (f.do_reduce) {
-        // the scalar sums are produced by block 0 only; a grid-wide dependency
-        // exists only for FGRAD/LINESUMS scalars, handled by block 0 below
-    }
-    // 2) epilogue
+    // 2) epilogue (each element by the thread that reduced it; scalars by block 0)
     if (f.op == (int)Op::FGRAD) {
-        for (int i = gtid; i < f.ld; i += gstride) {
-            const double v = f.red[i];
-            f.g[i] = i < f.n ? (-f.c1 * f.mu[i] + v / f.T) : 0.0;  // oracle.hpp:82-84 (1/T folded here)
-        }
+        if (grp == 0 && i < f.ld) f.g[i] = i < f.n ? (-f.c1 * f.mu[i] + f.red[i] / f.T) : 0.0;  // oracle.hpp:82-84
         if (blockIdx.x == 0) {
             __shared__ double sh[256];
-            double s = 0.0;
-            for (int i = threadIdx.x; i < f.n; i += blockDim.x) s += f.mu[i] * f.x[i];
-            sh[threadIdx.x] = s;
+            double sacc = 0.0;
+            for (int j = threadIdx.x; j < f.n; j += blockDim.x) sacc += f.mu[j] * f.x[j];
+            sh[threadIdx.x] = sacc;
             __syncthreads();
             for (int w = blockDim.x / 2; w > 0; w >>= 1) {
                 if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
@@ -346,12 +357,10 @@ __global__ void finish_kernel(const FinishArgs f) {
         }
     } else if (f.op == (int)Op::LINESUMS) {
         if (blockIdx.x == 0 && threadIdx.x < 9) f.out[threadIdx.x] = f.red[tot + threadIdx.x] / f.T;
-    } else {
-        for (int i = gtid; i < tot; i += gstride) {
-            const int k = i / f.ld, c = i - k * f.ld;
-            // HVP / THIRD: A^T(w)/T with the 1/T folded out of the per-row weights
-            if (c < f.n) f.out[(size_t)k * f.ldo + c] = f.op == (int)Op::XTW ? f.red[i] : f.red[i] / f.T;
-        }
+    } else if (grp == 0 && i < tot) {
+        const int k = i / f.ld, c = i - k * f.ld;
+        // HVP / THIRD: A^T(w)/T with the 1/T folded out of the per-row weights
+        if (c < f.n) f.out[(size_t)k * f.ldo + c] = f.op == (int)Op::XTW ? f.red[i] : f.red[i] / f.T;
     }
 }
 
@@ -446,7 +455,7 @@ static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO
         f.sc = slot->sc;
     }
     const int tot = std::max(f.k, 1) * f.ld;
-    const int fb = std::max(1, std::min(4 * ctx->nsm, (tot + 255) / 256));
+    const int fb = std::max(1, (tot + kFinCols - 1) / kFinCols);
     if (ctx->nranks == 1) {
         f.do_reduce = 1;
         f.do_epi = 1;

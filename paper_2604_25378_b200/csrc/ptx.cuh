@@ -64,3 +64,45 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 
 }  // namespace mvsk_b200
+
+namespace mvsk_b200 {
+
+// ---- distributed shared memory (cluster) helpers --------------------------
+// shared::cluster address of `local_smem` in the CTA of rank `rank`
+__device__ __forceinline__ uint32_t mapa_u32(const void* local_smem, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local_smem)), "r"(rank));
+    return r;
+}
+
+// remote 8-byte store into a peer CTA's smem, completing 8 tx-bytes on the
+// peer's mbarrier (both addresses are shared::cluster addresses from mapa)
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+
+// release-arrive on a (possibly remote) mbarrier at cluster scope
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t rbar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait_cluster(bar, parity)) {
+    }
+}
+
+}  // namespace mvsk_b200
