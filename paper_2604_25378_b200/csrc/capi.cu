@@ -283,8 +283,7 @@ int32_t mvsk_gpu_make_cache(mvsk_gpu_ctx* ctx, int32_t slot, const double* x, do
 
 int32_t mvsk_gpu_value(mvsk_gpu_ctx* ctx, int32_t slot, double* f_out) {
     return guard(ctx, [&] {
-        check_slot(ctx, slot);
-        *f_out = ctx->slots[slot].f;
+        *f_out = op_value(ctx, slot);
     });
 }
 
@@ -379,6 +378,8 @@ int32_t mvsk_gpu_make_cache_device(mvsk_gpu_ctx* ctx, int32_t slot, const double
         run_pass(ctx, Op::FGRAD, 1, io);
         ctx->fwd += 1;
         ctx->slots[slot].valid = true;  // scalars stay on device (slot sc)
+        ctx->slots[slot].g_host_valid = false;
+        ctx->slots[slot].scalars_host_valid = false;
         ctx->slots[slot].grad_counted = false;
     });
 }

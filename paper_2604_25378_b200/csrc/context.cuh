@@ -44,6 +44,9 @@ struct Slot {
     double f = 0.0;
     double mom[4] = {0, 0, 0, 0};
     std::vector<double> x_full;  // host copy of the cached point (full coordinates)
+    std::vector<double> g_host;  // host copy of the gradient (full coordinates, ld)
+    bool g_host_valid = false;
+    bool scalars_host_valid = false;  // f / mom mirror the device scalars
 };
 
 // Face view over the resident panel (replaces the column-gathered face panel of

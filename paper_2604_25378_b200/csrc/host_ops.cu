@@ -77,6 +77,7 @@ double op_make_cache(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const doubl
     check_slot(ctx, slot, false);
     Slot& s = ctx->slots[slot];
     s.valid = false;
+    s.g_host_valid = false;
     stage_in(ctx, fm, x, 1, fm.tau, 0);
     s.x_full.assign(ctx->h_in, ctx->h_in + ctx->ld);
     PassIO io;
@@ -85,19 +86,45 @@ double op_make_cache(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const doubl
     io.x_for_mux = ctx->vin;
     run_pass(ctx, Op::FGRAD, 1, io);
     ctx->fwd += 1;  // oracle.hpp:127
-    double h[5];
+    // scalars and the gradient come back in the same round trip (the gradient
+    // is almost always requested next: oracle.hpp:79, solver.hpp:378-379)
+    ensure_host_staging(ctx, (size_t)ctx->ld + 8);
+    double* h = ctx->h_out;
     MVSK_CUDA(cudaMemcpyAsync(h, s.sc, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    MVSK_CUDA(cudaMemcpyAsync(h + 8, s.g, ctx->ld * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
     s.f = h[0];
     for (int i = 0; i < 4; ++i) s.mom[i] = h[1 + i];
+    s.g_host.assign(h + 8, h + 8 + ctx->ld);
+    s.g_host_valid = true;
+    s.scalars_host_valid = true;
     s.grad_counted = false;
     if (!std::isfinite(s.f)) throw ApiError(MVSK_NUMERIC_ERROR, "oracle: non-finite objective value");  // :66-67
     s.valid = true;
     return s.f;
 }
 
-void op_moments(const mvsk_gpu_ctx* ctx, int slot, double out[4]) {
+// host mirror of a slot's device scalars (caches built by the device path)
+static void sync_scalars(mvsk_gpu_ctx* ctx, int slot) {
+    Slot& s = ctx->slots[slot];
+    if (s.scalars_host_valid) return;
+    double h[5];
+    MVSK_CUDA(cudaMemcpyAsync(h, s.sc, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+    s.f = h[0];
+    for (int i = 0; i < 4; ++i) s.mom[i] = h[1 + i];
+    s.scalars_host_valid = true;
+}
+
+double op_value(mvsk_gpu_ctx* ctx, int slot) {
     check_slot(ctx, slot);
+    sync_scalars(ctx, slot);
+    return ctx->slots[slot].f;
+}
+
+void op_moments(mvsk_gpu_ctx* ctx, int slot, double out[4]) {
+    check_slot(ctx, slot);
+    sync_scalars(ctx, slot);
     for (int i = 0; i < 4; ++i) out[i] = ctx->slots[slot].mom[i];
 }
 
@@ -110,7 +137,10 @@ void op_gradient(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, double* g) {
         ctx->tr += 1;
         s.grad_counted = true;
     }
-    fetch_out(ctx, fm, s.g, 1, ctx->ld, g);
+    if (s.g_host_valid)
+        from_full(ctx, fm, s.g_host.data(), g);
+    else
+        fetch_out(ctx, fm, s.g, 1, ctx->ld, g);
     if (!finite(g, fm.m)) throw ApiError(MVSK_NUMERIC_ERROR, "oracle: non-finite gradient");  // :85-86
 }
 
@@ -195,7 +225,7 @@ void op_line_model(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double*
     for (long long j = 0; j < m; ++j) mud += ctx->mu[fm.active ? fm.idx[j] : j] * d[j];
     const mvsk_coeffs& c = ctx->c;
     // linesearch.hpp:72-78
-    out[0] = ctx->slots[slot].f;
+    out[0] = op_value(ctx, slot);
     out[1] = -c.c1 * mud + 2.0 * c.c2 * s[0] - 3.0 * c.c3 * s[1] + 4.0 * c.c4 * s[2];
     out[2] = c.c2 * s[3] - 3.0 * c.c3 * s[4] + 6.0 * c.c4 * s[5];
     out[3] = -c.c3 * s[6] + 4.0 * c.c4 * s[7];

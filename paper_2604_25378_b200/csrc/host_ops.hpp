@@ -16,8 +16,9 @@ void check_slot(const mvsk_gpu_ctx* ctx, int slot, bool need_valid = true);
 
 // make_cache: returns f; throws numeric_error on a non-finite value
 double op_make_cache(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* x);
-// moments (mu'x, E z^2, E z^3, E z^4) of a valid slot
-void op_moments(const mvsk_gpu_ctx* ctx, int slot, double out[4]);
+// value / moments (mu'x, E z^2, E z^3, E z^4) of a valid slot
+double op_value(mvsk_gpu_ctx* ctx, int slot);
+void op_moments(mvsk_gpu_ctx* ctx, int slot, double out[4]);
 void op_gradient(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, double* g);
 void op_hvp(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* V, int k, double* HV);
 void op_third(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* U, const double* V, int k, double* out);

@@ -4,9 +4,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "oracle_ops.cuh"
 #include "stream_cluster.cuh"
+#include "stream_dmma.cuh"
 
 namespace mvsk_b200 {
 
@@ -93,7 +95,8 @@ int op_nacc(Op op, int K) { return (op == Op::HVP || op == Op::THIRD) ? K : (op 
 // mirror of StreamRegs<>::max_threads (stream_kernels.cuh)
 int max_threads(Op op, int K, int Q, int RG) {
     const int nv = std::max(op_ndot(op, K), 1), na = std::max(op_nacc(op, K), 1);
-    return 2 * Q * (nv + na + RG) > 48 ? 256 : 512;
+    const int live = 2 * Q * (nv + na + RG);
+    return live <= 48 ? 512 : (live <= 64 ? 384 : 256);
 }
 
 int round_team(int need) {
@@ -279,6 +282,79 @@ bool make_cluster_plan(const mvsk_gpu_ctx* ctx, Op op, int K, CPlan& pl) {
     return false;
 }
 
+// ---- DMMA cluster plans (multi-RHS HVP / THIRD on the fp64 tensor cores) -------
+struct DPlan {
+    int C = 4, WC = 128, S = 3;
+    size_t smem = 0;
+    int ncl = 1;
+    const void* fn = nullptr;
+};
+
+template <Op OP, int K, int WC>
+const void* dfn() {
+    return reinterpret_cast<const void*>(&stream_dmma_kernel<OP, K, WC>);
+}
+
+const void* select_dmma(Op op, int K, int WC) {
+#define MVSK_DWC(OP, K)                                    \
+    if (WC == 32) return dfn<OP, K, 32>();                  \
+    if (WC == 64) return dfn<OP, K, 64>();                  \
+    if (WC == 128) return dfn<OP, K, 128>();
+    if (op == Op::HVP && K == 8) { MVSK_DWC(Op::HVP, 8) }
+    if (op == Op::HVP && K == 4) { MVSK_DWC(Op::HVP, 4) }
+    if (op == Op::THIRD && K == 4) { MVSK_DWC(Op::THIRD, 4) }
+    if (op == Op::THIRD && K == 8) {
+        if (WC == 32) return dfn<Op::THIRD, 8, 32>();
+        if (WC == 64) return dfn<Op::THIRD, 8, 64>();
+    }
+#undef MVSK_DWC
+    return nullptr;
+}
+
+bool make_dmma_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
+    if (std::getenv("MVSK_NO_DMMA")) return false;
+    int forceC = 0;
+    if (const char* e = std::getenv("MVSK_TUNE_DMMA")) std::sscanf(e, "%d", &forceC);
+    const int ndot = op == Op::THIRD ? 2 * K : K;
+    const int V = 8 * ndot;
+    const int Cs[4] = {4, 8, 2, 1};
+    for (int i = 0; i < 4; ++i) {
+        const int C = forceC ? forceC : Cs[i];
+        if (ctx->ld % (2 * C)) {
+            if (forceC) return false;
+            continue;
+        }
+        const int cw = (int)(ctx->ld / C);
+        int WC = 32;
+        while (WC < 128 && 8 * WC < cw) WC <<= 1;
+        if (8 * WC < cw) {
+            if (forceC) return false;
+            continue;
+        }
+        const void* fn = select_dmma(op, K, WC);
+        if (!fn) {
+            if (forceC) return false;
+            continue;
+        }
+        const size_t stage = (size_t)8 * (8 * WC + 4) * sizeof(double);
+        size_t head = 256 + (size_t)(8 * V + kXSlots * C * V + 2 * V) * sizeof(double);
+        head = (head + 127) & ~(size_t)127;
+        int S = (int)std::min<size_t>(6, (ctx->max_smem - head) / stage);
+        if (S < 3) {
+            if (forceC) return false;
+            continue;
+        }
+        pl.C = C;
+        pl.WC = WC;
+        pl.S = S;
+        pl.smem = head + (size_t)S * stage;
+        pl.fn = fn;
+        pl.ncl = std::max(1, ctx->nsm / C);
+        return true;
+    }
+    return false;
+}
+
 struct FinishArgs {
     int op;
     int k;
@@ -373,9 +449,19 @@ __global__ void psi2_kernel(const double* z, double* out, long long T, double c2
 
 std::mutex g_attr_mu;
 
+// cudaFuncSetAttribute once per (kernel, size): it is a driver call, not free
 void set_smem_attr(const void* fn, size_t smem) {
+    static std::vector<std::pair<const void*, size_t>> done;
     std::lock_guard<std::mutex> lk(g_attr_mu);
+    for (auto& d : done)
+        if (d.first == fn) {
+            if (d.second >= smem) return;
+            MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            d.second = smem;
+            return;
+        }
     MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done.emplace_back(fn, smem);
 }
 
 void ensure_part(mvsk_gpu_ctx* ctx, size_t elems) {
@@ -400,6 +486,7 @@ void ensure_host_staging(mvsk_gpu_ctx* ctx, size_t elems) {
 
 static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io);
 static bool run_cluster(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io);
+static bool run_dmma(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io);
 
 void run_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     if ((op == Op::HVP || op == Op::THIRD) && k > 1) {
@@ -413,6 +500,8 @@ void run_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
             if (io.vin2) sub.vin2 = io.vin2 + (size_t)done * ctx->ld;
             sub.out = io.out + (size_t)done * io.ldo;
             int kk = 0;
+            for (int w : {8, 4})
+                if (!kk && left >= w && run_dmma(ctx, op, w, sub)) kk = w;
             for (int w : {8, 4})
                 if (!kk && left >= w && run_cluster(ctx, op, w, sub)) kk = w;
             if (!kk) {
@@ -508,6 +597,53 @@ static bool run_cluster(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     a.ld = (int)ctx->ld;
     a.cw = (int)(ctx->ld / pl.C);
     a.P = pl.P;
+    a.S = pl.S;
+    a.evict_first = (size_t)ctx->T_local * ctx->ld * sizeof(double) > (size_t)96 * 1024 * 1024;
+    a.vin = io.vin;
+    a.vin2 = io.vin2;
+    a.z = io.z;
+    a.part_acc = ctx->part_acc;
+    a.c2 = ctx->c.c2;
+    a.c3 = ctx->c.c3;
+    a.c4 = ctx->c.c4;
+    if (ctx->T_local > 0) {
+        void* args[] = {&a};
+        MVSK_CUDA(cudaLaunchKernelExC(&cfg, pl.fn, args));
+    }
+    ctx->phys += 1;
+    finish_pass(ctx, op, k, pl.ncl, io, nullptr);
+    return true;
+}
+
+static bool run_dmma(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
+    DPlan pl;
+    if (!make_dmma_plan(ctx, op, k, pl)) return false;
+    set_smem_attr(pl.fn, pl.smem);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = pl.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(pl.ncl * pl.C);
+    int maxcl = 0;
+    if (cudaOccupancyMaxActiveClusters(&maxcl, pl.fn, &cfg) == cudaSuccess && maxcl > 0)
+        pl.ncl = std::min(pl.ncl, maxcl);
+    else
+        cudaGetLastError();
+    pl.ncl = (int)std::max<long long>(1, std::min<long long>(pl.ncl, (ctx->T_local + 7) / 8));
+    cfg.gridDim = dim3(pl.ncl * pl.C);
+    ensure_part(ctx, (size_t)pl.ncl * k * ctx->ld);
+    DmmaArgs a{};
+    a.X = ctx->X;
+    a.T = ctx->T_local;
+    a.ld = (int)ctx->ld;
+    a.cw = (int)(ctx->ld / pl.C);
     a.S = pl.S;
     a.evict_first = (size_t)ctx->T_local * ctx->ld * sizeof(double) > (size_t)96 * 1024 * 1024;
     a.vin = io.vin;

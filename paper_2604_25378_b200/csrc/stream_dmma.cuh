@@ -1,0 +1,247 @@
+// Multi-RHS fused passes on the fp64 tensor cores (DMMA.8x8x4) with a
+// thread-block-cluster column split.
+//
+// A stage is 8 sample rows. For k right-hand sides both halves of the fused
+// op are small dense products:
+//   phase 1  Y (8 x k)  = X_s (8 x cw) . V (cw x k)        row dots
+//   phase 2  G (cw x k) += X_s^T (cw x 8) . W (8 x k)      X^T accumulation
+// with W = psi''(z) o Y (HVP) or psi'''(z) o Y_u o Y_v (THIRD). Both run as
+// mma.sync.m8n8k4.f64 on the staged tile in shared memory: one warp
+// instruction does 256 FMAs instead of 32, which is what lets 8 right-hand
+// sides ride one HBM pass. The cw columns of a CTA are split over its 8 warps
+// (WC each); the per-warp phase-1 partials are summed in a fixed order, the C
+// CTA partials of the cluster are exchanged through DSMEM (st.async +
+// mbarrier complete_tx, as in stream_cluster.cuh) and summed in rank order,
+// so every CTA holds bit-identical Y. X is read from HBM once.
+//
+// Reference: oracle.hpp:92-101 (hvp), :103-113 (third_action).
+#pragma once
+#include <cooperative_groups.h>
+
+#include "stream_cluster.cuh"
+
+namespace mvsk_b200 {
+
+struct DmmaArgs {
+    const double* X;  // T_local x ld
+    long long T;
+    int ld;
+    int cw;   // columns owned by a CTA (even)
+    int S;    // ring depth (>= 3)
+    int evict_first;
+    const double* vin;   // HVP: K vectors; THIRD: K u-vectors (stride ld)
+    const double* vin2;  // THIRD: K v-vectors
+    const double* z;
+    double* part_acc;    // [ncluster][K][ld]
+    double c2, c3, c4;
+};
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+template <Op OP, int K>
+struct DmmaShape {
+    static constexpr int NDOT = OP == Op::THIRD ? 2 * K : K;  // phase-1 columns
+    static constexpr int NT1 = (NDOT + 7) / 8;                // phase-1 n-tiles
+    static constexpr int V = 8 * NDOT;                        // partial dots per stage
+};
+
+template <Op OP, int K, int WC>
+__global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
+    using Sh = DmmaShape<OP, K>;
+    constexpr int NDOT = Sh::NDOT, NT1 = Sh::NT1, V = Sh::V;
+    constexpr int KS1 = WC / 4;  // phase-1 k-steps per warp
+    constexpr int MT = WC / 8;   // phase-2 m-tiles per warp
+    constexpr int E = kXSlots;
+    constexpr int RS = 8 * WC + 4;  // smem row stride (doubles): conflict-free fragment loads
+    static_assert(K <= 8, "phase 2 uses one n-tile");
+    cg::cluster_group cluster = cg::this_cluster();
+    const int C = (int)cluster.num_blocks();
+    const int crank = (int)cluster.block_rank();
+    const int ncl = gridDim.x / C;
+    const int ci = blockIdx.x / C;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g4 = lane >> 2, t4 = lane & 3;  // fragment coordinates
+    const int cw = a.cw, S = a.S;
+    const long long ld = a.ld;
+    const int col0 = crank * cw;
+    const int wcol = warp * WC;  // warp's first column inside the CTA slice
+
+    // smem: [full S | xfull E] mbarriers (256 B) [red 8 x V][xchg E x C x V][fdot 2 x V][ring S x 8 x RS]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t* xfull = full + 8;
+    double* red = reinterpret_cast<double*>(smem_raw + 256);
+    double* xchg = red + 8 * V;
+    double* fdot = xchg + E * C * V;
+    size_t off = 256 + (size_t)(8 * V + E * C * V + 2 * V) * sizeof(double);
+    off = (off + 127) & ~(size_t)127;
+    constexpr size_t stage_elems = (size_t)8 * RS;
+    double* ring = reinterpret_cast<double*>(smem_raw + off);
+
+    const long long T = a.T;
+    const long long r0 = T * ci / ncl, r1 = T * (ci + 1) / ncl;
+    const long long nrows = r1 - r0;
+    const int nst = (int)((nrows + 7) / 8);
+
+    // zero the whole ring once: the pad columns [cw, RS) are never written by
+    // the TMA, and the rows past the block end of a partial last stage keep
+    // finite (stale or zero) values, so 0-weighted products stay 0
+    for (size_t i = tid; i < (size_t)S * stage_elems; i += 256) ring[i] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes before the async-proxy fills
+    uint64_t policy = 0;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+        for (int e = 0; e < E; ++e) mbar_init(&xfull[e], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int s) {
+        const int slot = s % S;
+        const long long rows = (nrows - (long long)s * 8) < 8 ? (nrows - (long long)s * 8) : 8;
+        mbar_arrive_expect_tx(&full[slot], (uint32_t)(rows * cw * sizeof(double)));
+        for (int r = 0; r < rows; ++r)
+            bulk_g2s(ring + slot * stage_elems + (size_t)r * RS, a.X + (r0 + (long long)s * 8 + r) * ld + col0,
+                     (uint32_t)(cw * sizeof(double)), &full[slot], policy);
+    };
+    if (tid == 0) {
+        policy = a.evict_first ? policy_evict_first() : policy_evict_last();
+        const int pre = nst < S ? nst : S;
+        for (int s = 0; s < pre; ++s) issue(s);
+    }
+    cluster.sync();  // peers' barriers initialised before any push
+
+    // phase-1 B fragments: B[k = t4][n = g4] of every k-step = V[col][j]
+    double vb[NT1][KS1];
+#pragma unroll
+    for (int nt = 0; nt < NT1; ++nt)
+#pragma unroll
+        for (int ks = 0; ks < KS1; ++ks) {
+            const int c = wcol + ks * 4 + t4;
+            const int j = nt * 8 + g4;
+            double v = 0.0;
+            if (c < cw && j < NDOT) {
+                const double* src = (OP == Op::THIRD && j >= K) ? a.vin2 + (long long)(j - K) * ld
+                                                                 : a.vin + (long long)j * ld;
+                v = src[col0 + c];
+            }
+            vb[nt][ks] = v;
+        }
+    double acc[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+    const double c2 = a.c2, c3 = a.c3, c4 = a.c4;
+
+    // ---- produce(s): wait for the tile, phase 1, warp partials, push the CTA partial
+    auto produce = [&](int s, double (&zr)[2]) {
+        const int slot = s % S;
+        const long long srow0 = r0 + (long long)s * 8;
+        zr[0] = (srow0 + t4 < r1) ? __ldg(a.z + srow0 + t4) : 0.0;
+        zr[1] = (srow0 + 4 + t4 < r1) ? __ldg(a.z + srow0 + 4 + t4) : 0.0;
+        mbar_wait(&full[slot], (uint32_t)((s / S) & 1));
+        const double* X = ring + slot * stage_elems;  // rows past the block end: finite stale data,
+                                                      // their dots are never used (zero weights)
+        double cfr[2][NT1][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int nt = 0; nt < NT1; ++nt) cfr[h][nt][0] = cfr[h][nt][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS1; ++ks) {
+            const double av = X[g4 * RS + wcol + ks * 4 + t4];
+#pragma unroll
+            for (int nt = 0; nt < NT1; ++nt) dmma884(cfr[ks & 1][nt], av, vb[nt][ks]);
+        }
+        // Y partial: C[row = g4][j = nt*8 + 2*t4 + i]
+        double* rb = red + warp * V;
+#pragma unroll
+        for (int nt = 0; nt < NT1; ++nt)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int j = nt * 8 + 2 * t4 + i;
+                if (j < NDOT) rb[g4 * NDOT + j] = cfr[0][nt][i] + cfr[1][nt][i];
+            }
+        __syncthreads();  // (A) warp partials published; all consumes up to s-2 done
+        if (tid == 0 && s >= 2 && s - 2 + S < nst) issue(s - 2 + S);
+        if (tid < V) {
+            double sum = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) sum += red[w * V + tid];
+            const int e = s % E;
+            double* slotp = xchg + ((size_t)e * C + crank) * V + tid;
+            for (int r = 0; r < C; ++r) st_async_f64(mapa_u32(slotp, r), sum, mapa_u32(&xfull[e], r));
+        }
+    };
+
+    // ---- consume(s): full dots, weights, phase 2
+    auto consume = [&](int s, const double (&zr)[2]) {
+        const int slot = s % S;
+        const int e = s % E;
+        const long long srow0 = r0 + (long long)s * 8;
+        double* fb = fdot + (s & 1) * V;
+        if (tid == 0) mbar_arrive_expect_tx(&xfull[e], (uint32_t)(C * V * sizeof(double)));
+        if (tid < V) {
+            mbar_wait_cluster(&xfull[e], (uint32_t)((s / E) & 1));
+            const double* xb = xchg + (size_t)e * C * V;
+            double sum = 0.0;
+            for (int r = 0; r < C; ++r) sum += xb[r * V + tid];
+            fb[tid] = sum;
+        }
+        __syncthreads();  // (B) full dots visible
+        // W fragments: B2[k = row = kh*4 + t4][n = g4]
+        double wf[2];
+#pragma unroll
+        for (int kh = 0; kh < 2; ++kh) {
+            const int r = kh * 4 + t4;
+            const bool valid = (srow0 + r < r1) && g4 < K;
+            double w = 0.0;
+            if (valid) {
+                const double zt = zr[kh];
+                if constexpr (OP == Op::HVP) {
+                    const double psi2 = 2.0 * c2 - 6.0 * c3 * zt + 12.0 * c4 * (zt * zt);
+                    w = psi2 * fb[r * NDOT + g4];
+                } else {
+                    const double psi3 = -6.0 * c3 + 24.0 * c4 * zt;
+                    w = psi3 * fb[r * NDOT + g4] * fb[r * NDOT + K + g4];
+                }
+            }
+            wf[kh] = w;
+        }
+        const double* X = ring + slot * stage_elems;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh) {
+                const double av = X[(kh * 4 + t4) * RS + wcol + mt * 8 + g4];
+                dmma884(acc[mt], av, wf[kh]);
+            }
+    };
+
+    double za[2], zb[2];
+    if (nst > 0) produce(0, za);
+    int s = 0;
+    for (; s + 1 < nst; s += 2) {
+        produce(s + 1, zb);
+        consume(s, za);
+        if (s + 2 < nst) produce(s + 2, za);
+        consume(s + 1, zb);
+    }
+    if (s < nst) consume(s, za);
+
+    // G fragment: D[m = col = g4][n = k = 2*t4 + i]
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int c = wcol + mt * 8 + g4;
+            const int k = 2 * t4 + i;
+            if (c < cw && k < K) a.part_acc[((size_t)ci * K + k) * ld + col0 + c] = acc[mt][i];
+        }
+    cluster.sync();  // no CTA exits while a peer may still push into it
+}
+
+}  // namespace mvsk_b200

@@ -65,14 +65,14 @@ struct OpShape {
 };
 
 // fp64 values a thread keeps live across a stage: input vectors, accumulators
-// and the staged row slice. Heavy variants are capped at 256 threads so they
-// may use up to 255 registers; light ones allow 512 threads (128 registers).
+// and the staged row slice. Heavy variants are capped at 384 / 256 threads so
+// they may use up to 168 / 255 registers; light ones allow 512 (128 registers).
 template <Op OP, int K, int Q, int RG>
 struct StreamRegs {
     static constexpr int NV = OpShape<OP, K>::NDOT > 0 ? OpShape<OP, K>::NDOT : 1;
     static constexpr int NA = OpShape<OP, K>::NACC > 0 ? OpShape<OP, K>::NACC : 1;
     static constexpr int live = 2 * Q * (NV + NA + RG);
-    static constexpr int max_threads = live > 48 ? 256 : 512;
+    static constexpr int max_threads = live <= 48 ? 512 : (live <= 64 ? 384 : 256);
 };
 
 template <Op OP, int K, int Q, int RG>

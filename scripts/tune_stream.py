@@ -56,8 +56,13 @@ def timeit(fn, reps=10):
 
 grid = [os.environ.get("MVSK_TUNE_GRID")] if os.environ.get("MVSK_TUNE_GRID") else None
 for op in [o for o in ops if o in ("hvp8", "third8", "hvp4")]:
-    for cl in ["0,0", "2,0", "4,0", "8,0", "4,1", "4,2", "4,4", "8,1", "8,2", "8,4", "2,1", "2,2"]:
-        os.environ["MVSK_TUNE_CLUSTER"] = cl
+    for cl in ["dmma0", "dmma2", "dmma4", "dmma8", "0,0", "2,0", "4,0", "8,0", "2,2", "4,4"]:
+        if cl.startswith("dmma"):
+            os.environ.pop("MVSK_NO_DMMA", None)
+            os.environ["MVSK_TUNE_DMMA"] = cl[4:]
+        else:
+            os.environ["MVSK_NO_DMMA"] = "1"
+            os.environ["MVSK_TUNE_CLUSTER"] = cl
         try:
             ms = timeit(FN[op])
         except Exception as e:  # noqa
@@ -67,6 +72,8 @@ for op in [o for o in ops if o in ("hvp8", "third8", "hvp4")]:
         print(f"{cfg} {op} cluster C,RG={cl}: {ms:.4f} ms  {alg / ms / 1e6:.0f} GB/s  {k * 1000 / ms:.0f} per s",
               flush=True)
     os.environ.pop("MVSK_TUNE_CLUSTER", None)
+    os.environ.pop("MVSK_TUNE_DMMA", None)
+    os.environ.pop("MVSK_NO_DMMA", None)
 ops = [o for o in ops if o not in ("hvp8", "third8", "hvp4")]
 for op in ops:
     os.environ.pop("MVSK_TUNE", None)
