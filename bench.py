@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--seed", type=int, default=5000)
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary ops")
+    ap.add_argument("--no-solve", action="store_true", help="skip the full-solve leg")
     return ap.parse_args()
 
 
@@ -122,6 +123,46 @@ def cpu_hvp_rate(A_sample: np.ndarray, mu, c, T_full: int, threads: int, reps: i
     t = ts[(len(ts) - 1) // 2]
     po.set_threads(1)
     return (Ts / T_full) / t, t
+
+
+def solve_leg():
+    """Full YAND solves (solver.hpp:195) through the C-ABI on BASELINE configs
+    2-4, GPU wall time (lower median of 3 after a warm-up; C4: 1 run) next to the
+    CPU oracle restatement (1 thread, C2-C3 only: C4 exceeds a minute on the
+    CPU). max_elapsed is disabled on both sides so both do the same work."""
+    from oracle import pyoracle as po
+    from paper_2604_25378_b200.datagen import crra, make_panel
+    from paper_2604_25378_b200.gpu_oracle import GpuOracle, preset
+    out = []
+    for name, kappa, mode, gamma, reps, cpu in (("C2", 1.0, "small", None, 3, True), ("C2", 1.0, "large", None, 3, True),
+                                                ("C3", 1.0, "large", 5.0, 3, True), ("C3", 1.0, "large", 20.0, 3, True),
+                                                ("C4", 1.0, "large", None, 1, False)):
+        A, mu, c = make_panel(name, seed=11, kappa=kappa)
+        if gamma is not None:
+            c = crra(gamma)
+        g = GpuOracle(A, mu, c)
+        cfg = preset(mode)
+        cfg.has_max_elapsed = 0
+        g.solve(cfg)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            x, rep = g.solve(cfg)
+            ts.append(time.perf_counter() - t0)
+        ts.sort()
+        row = {"config": name, "n": A.shape[1], "T": A.shape[0], "preset": mode, "gamma": gamma or 10.0,
+               "gpu_s": ts[(len(ts) - 1) // 2], "status": int(rep.status), "iterations": rep.iterations,
+               "kkt": rep.kkt_residual, "physical_passes": int(rep.physical_passes),
+               "logical_passes": int(rep.oracle_passes)}
+        if cpu:
+            cc = po.preset(mode)
+            cc.has_max_elapsed = 0
+            t0 = time.perf_counter()
+            xc, rc = po.solve(A, mu, c, cc)
+            row.update(cpu_s=time.perf_counter() - t0, cpu_status=int(rc.status), df=abs(rc.f_star - rep.f_star))
+        g.close()
+        out.append(row)
+    return out
 
 
 def run_reference(args):
@@ -317,6 +358,11 @@ def main():
                     "sample": f"one HVP on rows 0..{Ts} of the same panel (2 reference passes), "
                               f"{t_s:.3f} s each, lower median of 3 after 1 warm-up, scaled by T/{Ts}"}
 
+    # ---- YAND full-solve wall time (the metric's second half), rank 0 at N=1
+    solves = None
+    if rank == 0 and ws == 1 and not args.no_solve:
+        solves = solve_leg()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -330,6 +376,8 @@ def main():
         }
         if cpu_base is not None:
             line["cpu_baseline"] = cpu_base
+        if solves is not None:
+            line["solve"] = solves
         print(json.dumps(line), flush=True)
     gpu.close()
     if ws > 1:

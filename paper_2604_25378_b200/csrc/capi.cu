@@ -108,7 +108,9 @@ mvsk_gpu_ctx* make_ctx(long long T_local, long long row0, long long T_global, lo
         ctx->c = *c;
         ctx->nranks = nranks;
         ctx->rank = rank;
-        if (nranks > 1) {
+        // a communicator is created whenever an id is given (also for a 1-rank
+        // group, which runs the same allreduce path on one GPU)
+        if (nranks > 1 || id) {
             if (!id) throw ApiError(MVSK_DOMAIN_ERROR, "nccl unique id required for nranks > 1");
             ncclUniqueId uid;
             std::memcpy(&uid, id, sizeof(uid));

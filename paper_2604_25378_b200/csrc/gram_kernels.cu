@@ -246,7 +246,7 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
     gram_finish_kernel<<<npairs, 256, 0, ctx->stream>>>(ctx->gram_part, npairs, nsplit, n, scale, G_dev, n);
     MVSK_CUDA(cudaGetLastError());
     ctx->phys += 1;
-    if (ctx->nranks > 1)
+    if (ctx->comm)
         MVSK_NCCL(ncclAllReduce(G_dev, G_dev, (size_t)n * n, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
 }
 

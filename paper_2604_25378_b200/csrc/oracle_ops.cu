@@ -126,8 +126,18 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     const TuneOverride tov = tune_override();
     const long long npairs = ctx->ld / 2;
     const int qmax = max_q(op, K);
+    // small panels (< 64 rows per SM) are latency-bound: favour short teams and
+    // several teams per CTA so more rows are in flight (C3: 63 -> 34 us / HVP)
+    const bool small = ctx->T_local < 64LL * ctx->nsm;
     int Q = -1;
-    for (int q = 1; q <= qmax; q <<= 1)
+    if (small) {
+        for (int q = qmax; q >= 1; q >>= 1)
+            if ((npairs + q - 1) / q >= 32 && (npairs + q - 1) / q <= max_threads(op, K, q, 1)) {
+                Q = q;
+                break;
+            }
+    }
+    for (int q = 1; Q < 0 && q <= qmax; q <<= 1)
         if ((npairs + q - 1) / q <= 256) {
             Q = q;
             break;
@@ -145,11 +155,11 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     const size_t row_bytes = (size_t)ctx->ld * sizeof(double);
     const size_t stage_target = 64 * 1024;
     // teams per CTA (each team streams its own rows)
-    int G = std::max(1, max_threads(op, K, Q, 1) / P);
+    int G = std::max(1, (small ? std::min(256, max_threads(op, K, Q, 1)) : max_threads(op, K, Q, 1)) / P);
     const long long want_rows = std::max<long long>(1, (long long)(stage_target / row_bytes));
     while (G > 1 && G > want_rows) G >>= 1;
     int RG = 1;
-    while (RG < 4 && RG * 2 * Q <= 8 && (long long)G * RG * 2 <= want_rows &&
+    while (!small && RG < 4 && RG * 2 * Q <= 8 && (long long)G * RG * 2 <= want_rows &&
            G * P <= max_threads(op, K, Q, RG * 2))
         RG <<= 1;
     if (tov.G > 0 && tov.G * P <= max_threads(op, K, Q, RG)) G = tov.G;
@@ -545,7 +555,7 @@ static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO
     }
     const int tot = std::max(f.k, 1) * f.ld;
     const int fb = std::max(1, (tot + kFinCols - 1) / kFinCols);
-    if (ctx->nranks == 1) {
+    if (!ctx->comm) {
         f.do_reduce = 1;
         f.do_epi = 1;
         // scalars are reduced by block 0 and consumed by block 0 only

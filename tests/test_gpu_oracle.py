@@ -251,3 +251,31 @@ def test_device_path_matches_host_path():
     np.testing.assert_array_equal(sums.cpu().numpy(), lm.sums)
     z, g, s = gpu.slot_pointers(0)
     assert z and g and s
+
+
+def test_nccl_single_rank_group_path():
+    """With an NCCL unique id the context builds a communicator (here a 1-rank
+    group) and every op runs the multi-GPU finish path: fixed-order partial
+    reduction -> ncclAllReduce(sum, fp64) -> epilogue. Results must equal the
+    single-GPU path bit for bit (an allreduce over one rank is a copy)."""
+    from paper_2604_25378_b200.gpu_oracle import nccl_unique_id
+    A, mu = rh.lcg_panel(64, 777, 5)
+    c = rh.crra(10.0)
+    T = A.shape[0]
+    plain = _gpu(A, mu, c)
+    group = _gpu(A, mu, c, rank=0, nranks=1, row0=0, T_global=T, nccl_id=nccl_unique_id())
+    x = rh.simplex_point(64, 3)
+    V = np.random.default_rng(1).standard_normal((8, 64))
+    cp, cg = plain.make_cache(x), group.make_cache(x)
+    assert plain.value(cp) == group.value(cg)
+    np.testing.assert_array_equal(plain.gradient(cp), group.gradient(cg))
+    np.testing.assert_array_equal(plain.hvp(cp, V), group.hvp(cg, V))
+    np.testing.assert_array_equal(plain.third_action(cp, V[:3], V[3:6]), group.third_action(cg, V[:3], V[3:6]))
+    d = V[0] - V[0].mean()
+    lp, lg = plain.line_model(cp, d, 1.0), group.line_model(cg, d, 1.0)
+    np.testing.assert_array_equal(lp.sums, lg.sums)
+    np.testing.assert_array_equal(plain.weighted_gram(cp), group.weighted_gram(cg))
+    from paper_2604_25378_b200.gpu_oracle import preset
+    xs1, r1 = plain.solve(preset("large"))
+    xs2, r2 = group.solve(preset("large"))
+    np.testing.assert_array_equal(xs1, xs2)
