@@ -175,7 +175,7 @@ def run_reference(args):
     from paper_2604_25378_b200.datagen import CONFIGS, raw_returns
     spec = CONFIGS[args.config]
     cores = os.cpu_count() or 1
-    Ts = min(spec.T, 65536)
+    Ts = min(spec.T, 32768)
     R = raw_returns(spec, args.seed, rows=(0, Ts)).numpy()
     mu = R.sum(axis=0) / Ts
     A = R - mu

@@ -143,6 +143,17 @@ int32_t mvsk_gpu_create_from_device(const double* A_dev, int64_t ld, int64_t T_l
                                     const double* mu, const mvsk_coeffs* c, int32_t device,
                                     int32_t nranks, int32_t rank, const void* nccl_unique_id,
                                     mvsk_gpu_ctx** out);
+/* load_returns_binary + center_panel + Oracle (panel_io.hpp:121-141, panel.hpp:32-44,
+ * oracle.hpp:43-45): reads this rank's row block of a binary panel file ("MVSK",
+ * u32 T, u32 n, row-major LE f64 raw returns) straight into device memory and
+ * centres it with the global column means (allreduced across the group).
+ * Malformed files / non-finite entries -> MVSK_DATA_ERROR. */
+int32_t mvsk_gpu_create_from_binary(const char* path, const mvsk_coeffs* c, int32_t device, int32_t nranks,
+                                    int32_t rank, const void* nccl_unique_id, mvsk_gpu_ctx** out);
+/* header of a binary panel file (no device needed): T, n */
+int32_t mvsk_gpu_binary_dims(const char* path, int64_t* T, int64_t* n);
+/* column means mu (n) of the context's panel */
+int32_t mvsk_gpu_mu(const mvsk_gpu_ctx* ctx, double* mu_out);
 int32_t mvsk_gpu_destroy(mvsk_gpu_ctx* ctx);
 const char* mvsk_gpu_last_error(const mvsk_gpu_ctx* ctx);
 /* Run all device work on this cudaStream_t (NULL = the context's own stream). */

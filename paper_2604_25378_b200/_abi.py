@@ -118,6 +118,9 @@ SIGNATURES = [
      [_D, _I64, _I64, _I64, _I64, _D, C.POINTER(mvsk_coeffs), _I32, _I32, _I32, _P, C.POINTER(_P)]),
     ("mvsk_gpu_create_from_device", _I32,
      [_P, _I64, _I64, _I64, _I64, _I64, _D, C.POINTER(mvsk_coeffs), _I32, _I32, _I32, _P, C.POINTER(_P)]),
+    ("mvsk_gpu_create_from_binary", _I32, [C.c_char_p, C.POINTER(mvsk_coeffs), _I32, _I32, _I32, _P, C.POINTER(_P)]),
+    ("mvsk_gpu_binary_dims", _I32, [C.c_char_p, C.POINTER(_I64), C.POINTER(_I64)]),
+    ("mvsk_gpu_mu", _I32, [_P, _D]),
     ("mvsk_gpu_destroy", _I32, [_P]),
     ("mvsk_gpu_last_error", C.c_char_p, [_P]),
     ("mvsk_gpu_set_stream", _I32, [_P, _P]),

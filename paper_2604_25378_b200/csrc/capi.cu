@@ -212,6 +212,55 @@ int32_t mvsk_gpu_create_from_device(const double* A_dev, int64_t ld, int64_t T_l
     });
 }
 
+}  // extern "C"
+
+namespace mvsk_b200 {
+struct BinaryHeader {
+    long long T = 0, n = 0;
+};
+BinaryHeader read_binary_header(const char* path);
+void ingest_binary(mvsk_gpu_ctx* ctx, const char* path);
+}  // namespace mvsk_b200
+
+extern "C" {
+
+int32_t mvsk_gpu_binary_dims(const char* path, int64_t* T, int64_t* n) {
+    return guard(nullptr, [&] {
+        const auto h = read_binary_header(path);
+        if (T) *T = h.T;
+        if (n) *n = h.n;
+    });
+}
+
+int32_t mvsk_gpu_create_from_binary(const char* path, const mvsk_coeffs* c, int32_t device, int32_t nranks,
+                                    int32_t rank, const void* nccl_unique_id, mvsk_gpu_ctx** out) {
+    return guard(nullptr, [&] {
+        if (!out) throw ApiError(MVSK_DOMAIN_ERROR, "null out");
+        *out = nullptr;
+        const auto h = read_binary_header(path);
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw ApiError(MVSK_DOMAIN_ERROR, "bad rank / nranks");
+        const long long row0 = h.T * rank / nranks, T_loc = h.T * (rank + 1) / nranks - row0;
+        std::vector<double> mu0((size_t)h.n, 0.0);
+        mvsk_gpu_ctx* ctx = make_ctx(T_loc, row0, h.T, h.n, mu0.data(), c, device, nranks, rank, nccl_unique_id);
+        try {
+            const size_t bytes = (size_t)std::max<long long>(1, ctx->T_local) * ctx->ld * sizeof(double);
+            MVSK_CUDA(cudaMalloc(&ctx->X, bytes));
+            ctx->owns_X = true;
+            alloc_workspaces(ctx);
+            ingest_binary(ctx, path);
+        } catch (...) {
+            free_all(ctx);
+            throw;
+        }
+        *out = ctx;
+    });
+}
+
+int32_t mvsk_gpu_mu(const mvsk_gpu_ctx* ctx, double* mu_out) {
+    std::memcpy(mu_out, ctx->mu.data(), ctx->mu.size() * sizeof(double));
+    return MVSK_OK;
+}
+
 int32_t mvsk_gpu_destroy(mvsk_gpu_ctx* ctx) {
     free_all(ctx);
     return MVSK_OK;

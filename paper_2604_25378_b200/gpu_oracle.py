@@ -150,6 +150,30 @@ class GpuOracle:
         self._m = self.n
         self._next_slot = 0
 
+    @classmethod
+    def from_binary(cls, path, coeffs, device: int = 0, *, rank: int = 0, nranks: int = 1,
+                    nccl_id: bytes | None = None) -> "GpuOracle":
+        """load_returns_binary + center_panel + Oracle (panel_io.hpp:121-141):
+        this rank's rows of a binary panel file go straight to device memory."""
+        self = cls.__new__(cls)
+        self.lib = _abi.load_library()
+        self._ctx = C.c_void_p()
+        self.c = _vec(coeffs, 4)
+        cf = mvsk_coeffs(*self.c)
+        idb = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        code = self.lib.mvsk_gpu_create_from_binary(str(path).encode(), C.byref(cf), device, nranks, rank, idb,
+                                                    C.byref(self._ctx))
+        if code != 0:
+            raise _ERR.get(code, MvskError)(self.lib.mvsk_gpu_last_error(None).decode())
+        Tg, Tl, n = C.c_int64(), C.c_int64(), C.c_int64()
+        self.lib.mvsk_gpu_dims(self._ctx, C.byref(Tg), C.byref(Tl), C.byref(n))
+        self.T, self.T_local, self.n = Tg.value, Tl.value, n.value
+        self.mu = np.empty(self.n)
+        self.lib.mvsk_gpu_mu(self._ctx, _p(self.mu))
+        self._m = self.n
+        self._next_slot = 0
+        return self
+
     # ---- lifecycle --------------------------------------------------------
     def close(self):
         if getattr(self, "_ctx", None) and self._ctx.value:
@@ -349,3 +373,23 @@ def shard_rows(T: int, nranks: int, rank: int):
     lo = T * rank // nranks
     hi = T * (rank + 1) // nranks
     return lo, hi - lo
+
+
+def binary_dims(path) -> tuple[int, int]:
+    """Header of a binary panel file (panel_io.hpp:123-134): (T, n); raises DataError."""
+    lib = _abi.load_library()
+    T, n = C.c_int64(), C.c_int64()
+    code = lib.mvsk_gpu_binary_dims(str(path).encode(), C.byref(T), C.byref(n))
+    if code != 0:
+        raise _ERR.get(code, MvskError)(lib.mvsk_gpu_last_error(None).decode())
+    return T.value, n.value
+
+
+def save_returns_binary(path, R: np.ndarray) -> None:
+    """Writer of the reference's binary panel format (panel_io.hpp:143-154)."""
+    R = np.ascontiguousarray(R, dtype="<f8")
+    T, n = R.shape
+    with open(path, "wb") as f:
+        f.write(b"MVSK")
+        f.write(np.array([T, n], dtype="<u4").tobytes())
+        f.write(R.tobytes())

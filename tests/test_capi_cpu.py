@@ -84,3 +84,26 @@ def test_crra_and_centering_mirror():
     A2, mu2 = po.center_panel(R)
     np.testing.assert_allclose(A, A2, atol=1e-16)
     np.testing.assert_allclose(mu, mu2, rtol=1e-15)
+
+
+def test_binary_panel_header_validation(tmp_path):
+    """panel_io.hpp:123-141 error behaviour, checked host-side (no device)."""
+    from paper_2604_25378_b200.gpu_oracle import DataError, binary_dims, save_returns_binary
+    R = np.random.default_rng(0).uniform(-0.1, 0.4, (7, 3))
+    p = tmp_path / "ok.bin"
+    save_returns_binary(p, R)
+    assert binary_dims(p) == (7, 3)
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"NOPE" + p.read_bytes()[4:])
+    with pytest.raises(DataError):
+        binary_dims(bad)
+    short = tmp_path / "short.bin"
+    short.write_bytes(p.read_bytes()[:-8])
+    with pytest.raises(DataError):
+        binary_dims(short)
+    degen = tmp_path / "degen.bin"
+    degen.write_bytes(b"MVSK" + np.array([1, 3], dtype="<u4").tobytes() + np.zeros(3).tobytes())
+    with pytest.raises(DataError):
+        binary_dims(degen)
+    with pytest.raises(DataError):
+        binary_dims(tmp_path / "missing.bin")

@@ -279,3 +279,26 @@ def test_nccl_single_rank_group_path():
     xs1, r1 = plain.solve(preset("large"))
     xs2, r2 = group.solve(preset("large"))
     np.testing.assert_array_equal(xs1, xs2)
+
+
+def test_binary_ingest_matches_host_centering(tmp_path):
+    """mvsk_gpu_create_from_binary: raw returns file -> device rows -> centred
+    on the device; oracle outputs match the CPU oracle on the host-centred panel,
+    and a non-finite entry raises DataError (center_panel, panel.hpp:38-39)."""
+    from paper_2604_25378_b200.gpu_oracle import DataError, GpuOracle, save_returns_binary
+    R = rh.lcg_panel_raw(37, 400, 8)
+    path = tmp_path / "panel.bin"
+    save_returns_binary(path, R)
+    c = rh.crra(10.0)
+    g = GpuOracle.from_binary(path, c)
+    A, mu = po.center_panel(R)
+    np.testing.assert_allclose(g.mu, mu, rtol=1e-14, atol=1e-17)
+    cpu = po.CpuOracle(A, mu, c)
+    x = rh.simplex_point(37, 5)
+    gc, cc = g.make_cache(x), cpu.make_cache(x)
+    assert abs(g.value(gc) - cpu.value(cc)) <= 1e-12 * (1 + abs(cpu.value(cc)))
+    np.testing.assert_allclose(g.gradient(gc), cpu.gradient(cc), rtol=1e-10, atol=1e-13)
+    R[3, 4] = np.nan
+    save_returns_binary(path, R)
+    with pytest.raises(DataError):
+        GpuOracle.from_binary(path, c)
