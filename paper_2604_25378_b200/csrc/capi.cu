@@ -6,6 +6,7 @@
 #include <cstring>
 
 #include "host_ops.hpp"
+#include "pcg_device.hpp"
 
 using namespace mvsk_b200;
 
@@ -72,6 +73,7 @@ void free_all(mvsk_gpu_ctx* ctx) {
     if (ctx->h_in) cudaFreeHost(ctx->h_in);
     if (ctx->h_out) cudaFreeHost(ctx->h_out);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
+    pcg_workspace_free(ctx);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
@@ -102,7 +104,10 @@ mvsk_gpu_ctx* make_ctx(long long T_local, long long row0, long long T_global, lo
         ctx->T_global = T_global;
         ctx->row0 = row0;
         ctx->n = n;
-        ctx->ld = (n + 1) / 2 * 2;
+        // row pitch: 16-byte rows for the bulk-copy engine; for n >= 512 a
+        // multiple of 16 doubles so the tensor-core multi-RHS kernel can split
+        // rows over 8-CTA clusters (<= 3 % padding, zero-filled)
+        ctx->ld = n >= 512 ? (n + 15) / 16 * 16 : (n + 1) / 2 * 2;
         ctx->pub_face.m = n;
         ctx->mu.assign(mu, mu + n);
         ctx->c = *c;

@@ -14,6 +14,8 @@
 
 namespace mvsk_b200 {
 
+struct PcgWorkspace;
+
 struct ApiError : std::runtime_error {
     int code;
     ApiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
@@ -94,6 +96,7 @@ struct mvsk_gpu_ctx {
     double* gram = nullptr;  // n x n (lazy)
     double* tvec2 = nullptr; // T_local scratch (lazy)
     double* pmat = nullptr;  // ld x ld (lazy)
+    mvsk_b200::PcgWorkspace* pcg = nullptr;  // device-resident PCG buffers (lazy)
     double* gram_part = nullptr;
     size_t gram_part_elems = 0;
     // pinned host staging

@@ -22,6 +22,7 @@
 #include <optional>
 
 #include "host_ops.hpp"
+#include "pcg_device.hpp"
 
 namespace mvsk_b200 {
 namespace {
@@ -548,8 +549,53 @@ Vec yand_direction(const View& O, int slot, const TangentCfg& cfg, uint64_t it_s
             u = solve_with(std::max(cfg.lambda, 1e-4));
             if (!all_finite(u)) throw ApiError(MVSK_NUMERIC_ERROR, "yand_direction: tangent solve failed");
         }
+    } else if (!std::getenv("MVSK_HOST_PCG")) {
+        // ---- matrix-free PCG branch (:189-242), Krylov loops resident on the device
+        PcgInput in;
+        in.m = n;
+        in.vU = basis.v;
+        in.bU = basis.beta;
+        in.vQ = frame.v;
+        in.bQ = frame.beta;
+        in.nu = frame.nu;
+        in.gn = gn;
+        in.lambda = cfg.lambda;
+        in.tol = cfg.tol;
+        in.maxit = cfg.maxit;
+        in.probe_cap = cfg.exact_trace ? cfg.maxit : cfg.probe_maxit;
+        in.hutchinson_probes = cfg.probes;
+        in.exact_trace = cfg.exact_trace;
+        in.has_third = has_third;
+        if (cfg.jacobi) {  // :197-209 probe stream
+            SplitMix64 rng(0x0d1a6ULL ^ it_seed);
+            for (int p = 0; p < 8; ++p) {
+                Vec r((size_t)mm);
+                for (long long i = 0; i < mm; ++i) r[(size_t)i] = rng.next_sign();
+                in.jacobi_probes.push_back(std::move(r));
+            }
+        }
+        if (has_third) {
+            if (cfg.exact_trace) {  // :217-226
+                for (long long k = 0; k < mm; ++k) {
+                    Vec e((size_t)mm, 0.0);
+                    e[(size_t)k] = 1.0;
+                    in.probes.push_back(std::move(e));
+                }
+            } else {  // :227-237
+                SplitMix64 rng(0x5eedULL ^ it_seed);
+                for (int pr = 0; pr < cfg.probes; ++pr) {
+                    Vec r((size_t)mm);
+                    for (long long i = 0; i < mm; ++i) r[(size_t)i] = rng.next_sign();
+                    in.probes.push_back(std::move(r));
+                }
+            }
+        }
+        PcgOutput po = pcg_direction_device(ctx, slot, O.fm, in);
+        u = std::move(po.u);
+        diag.krylov_iters += po.iters;
+        if (po.breakdown) diag.pcg_breakdown = 1;
     } else {
-        // ---- matrix-free PCG branch (:189-242)
+        // ---- matrix-free PCG branch (:189-242), host-driven Krylov loops
         const HopBatch Hop = [&](const std::vector<Vec>& E) {
             std::vector<Vec> amb;
             for (const Vec& e : E) amb.push_back(basis.apply(frame.apply_Q(e)));

@@ -309,6 +309,7 @@ const void* select_dmma(Op op, int K, int WC) {
 #define MVSK_DWC(OP, K)                                    \
     if (WC == 32) return dfn<OP, K, 32>();                  \
     if (WC == 64) return dfn<OP, K, 64>();                  \
+    if (WC == 80) return dfn<OP, K, 80>();                  \
     if (WC == 128) return dfn<OP, K, 128>();
     if (op == Op::HVP && K == 8) { MVSK_DWC(Op::HVP, 8) }
     if (op == Op::HVP && K == 4) { MVSK_DWC(Op::HVP, 4) }
@@ -316,6 +317,7 @@ const void* select_dmma(Op op, int K, int WC) {
     if (op == Op::THIRD && K == 8) {
         if (WC == 32) return dfn<Op::THIRD, 8, 32>();
         if (WC == 64) return dfn<Op::THIRD, 8, 64>();
+        if (WC == 80) return dfn<Op::THIRD, 8, 80>();
     }
 #undef MVSK_DWC
     return nullptr;
@@ -335,9 +337,10 @@ bool make_dmma_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
             continue;
         }
         const int cw = (int)(ctx->ld / C);
-        int WC = 32;
-        while (WC < 128 && 8 * WC < cw) WC <<= 1;
-        if (8 * WC < cw) {
+        int WC = 0;
+        for (int w : {32, 64, 80, 128})
+            if (!WC && 8 * w >= cw) WC = w;
+        if (!WC) {
             if (forceC) return false;
             continue;
         }
@@ -382,6 +385,8 @@ struct FinishArgs {
     const double* mu;   // ld
     const double* x;    // ld (FGRAD mu'x)
     double c1, c2, c3, c4, T, value_offset;
+    const int* skip;
+    int nskip;
 };
 
 // Block = 64 output columns x 4 partial-range groups; each thread sums its
@@ -389,6 +394,7 @@ struct FinishArgs {
 // combined in a fixed order (deterministic), then the op epilogue is applied.
 constexpr int kFinCols = 64;
 __global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
+    if (pass_skipped(f.skip, f.nskip)) return;
     const int nacc = (f.op == (int)Op::LINESUMS) ? 0 : f.k;
     const int tot = nacc * f.ld;
     const int nsc = f.op == (int)Op::FGRAD ? 3 : (f.op == (int)Op::LINESUMS ? 9 : 0);
@@ -549,6 +555,8 @@ static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO
     f.c4 = ctx->c.c4;
     f.T = (double)ctx->T_global;
     f.value_offset = ctx->value_offset;
+    f.skip = io.skip;
+    f.nskip = io.nskip;
     if (slot) {
         f.g = slot->g;
         f.sc = slot->sc;
@@ -613,6 +621,8 @@ static bool run_cluster(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     a.vin2 = io.vin2;
     a.z = io.z;
     a.part_acc = ctx->part_acc;
+    a.skip = io.skip;
+    a.nskip = io.nskip;
     a.c2 = ctx->c.c2;
     a.c3 = ctx->c.c3;
     a.c4 = ctx->c.c4;
@@ -660,6 +670,8 @@ static bool run_dmma(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     a.vin2 = io.vin2;
     a.z = io.z;
     a.part_acc = ctx->part_acc;
+    a.skip = io.skip;
+    a.nskip = io.nskip;
     a.c2 = ctx->c.c2;
     a.c3 = ctx->c.c3;
     a.c4 = ctx->c.c4;
@@ -697,6 +709,8 @@ static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     a.tw = io.tw;
     a.part_acc = ctx->part_acc;
     a.part_sc = ctx->part_sc;
+    a.skip = io.skip;
+    a.nskip = io.nskip;
     a.c2 = ctx->c.c2;
     a.c3 = ctx->c.c3;
     a.c4 = ctx->c.c4;

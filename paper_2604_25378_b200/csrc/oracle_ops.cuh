@@ -20,6 +20,8 @@ struct PassIO {
     double* zout = nullptr;
     double* out = nullptr;
     long long ldo = 0;    // output stride for HVP/THIRD/XTW
+    const int* skip = nullptr;  // device flags: the whole pass is a no-op if all nskip are 0
+    int nskip = 0;
     int slot = -1;        // FGRAD target slot
     const double* x_for_mux = nullptr;  // FGRAD: x (ld) for mu'x
 };

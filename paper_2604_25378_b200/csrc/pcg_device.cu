@@ -1,0 +1,454 @@
+// Device-resident PCG for the YAND direction (affine_normal.hpp:189-242).
+//
+// The reduced tangent operator H e = Q^T U^T grad2 f (U Q e) + lambda e is
+// applied without leaving the device: a "lift" kernel applies the two
+// Householder reflectors (U: simplex.hpp:63-70, Q: affine_normal.hpp:28-33) to
+// every CG column and scatters it into the HVP input rows (face -> full
+// coordinates), one fused k-RHS HVP pass runs, and an "update" kernel gathers,
+// applies Q^T U^T (:36-39, simplex.hpp:73-78) and performs the capped-CG step
+// of every column (cg_capped, affine_normal.hpp:85-113: per-column alpha/beta,
+// nonpositive curvature -> breakdown, ||r|| <= tol ||rhs|| or the cap -> stop).
+// The host only reads back a k-int activity mask per CG step (and the
+// solution at the end); no n-vector crosses PCIe inside the Krylov loops.
+// One CTA owns one CG column; every reduction has a fixed order.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "host_ops.hpp"
+#include "pcg_device.hpp"
+
+namespace mvsk_b200 {
+namespace {
+
+constexpr int kPT = 512;  // threads per column CTA
+
+__device__ double block_sum(double v, double* sh) {
+    // fixed-order tree: warp shuffles then a 16-way smem combine
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sh[i];
+    return s;
+}
+
+struct Geo {
+    const double* vU;  // m
+    double bU;
+    const double* vQ;  // m - 1
+    double bQ;
+    const long long* idx;  // m face -> full index (null: identity)
+    int m;
+    int ld;
+};
+
+// q = Q e (e: m-2) in smem (m-1), then y = U q (m) scattered to a full row
+__device__ void lift_col(const Geo& g, const double* e, bool apply_q, double* row, double* q, double* sh) {
+    const int m = g.m, m1 = m - 1;
+    // q: pad (0, e) and reflect with Q, or take e (length m-1) as is
+    double part = 0.0;
+    for (int i = threadIdx.x; i < m1; i += blockDim.x) {
+        const double v = apply_q ? (i == 0 ? 0.0 : e[i - 1]) : e[i];
+        q[i] = v;
+        part += g.vQ[i] * v;
+    }
+    if (apply_q) {
+        const double s = g.bQ * block_sum(part, sh);
+        for (int i = threadIdx.x; i < m1; i += blockDim.x) q[i] -= s * g.vQ[i];
+    }
+    __syncthreads();
+    double part2 = 0.0;
+    for (int i = threadIdx.x + 1; i < m; i += blockDim.x) part2 += g.vU[i] * q[i - 1];
+    const double s2 = g.bU * block_sum(part2, sh);
+    for (int i = threadIdx.x; i < g.ld; i += blockDim.x) row[i] = 0.0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const double y = (i == 0 ? 0.0 : q[i - 1]) - s2 * g.vU[i];
+        row[g.idx ? (int)g.idx[i] : i] = y;
+    }
+}
+
+// Q^T U^T h (h gathered from a full row): returns a pointer into `t` (2m doubles
+// of smem) holding m-2 values (apply_q) or m-1 values (U^T only)
+__device__ const double* reduce_col(const Geo& g, const double* row, bool apply_q, double* t, double* sh) {
+    const int m = g.m, m1 = m - 1;
+    double part = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) part += g.vU[i] * row[g.idx ? (int)g.idx[i] : i];
+    const double s = g.bU * block_sum(part, sh);
+    double part2 = 0.0;
+    for (int i = threadIdx.x; i < m1; i += blockDim.x) {
+        const int fi = g.idx ? (int)g.idx[i + 1] : i + 1;
+        const double v = row[fi] - s * g.vU[i + 1];
+        t[i] = v;
+        part2 += g.vQ[i] * v;
+    }
+    if (!apply_q) {
+        __syncthreads();
+        return t;
+    }
+    const double s2 = g.bQ * block_sum(part2, sh);  // (its barriers also publish t)
+    double* r = t + m;
+    for (int i = threadIdx.x; i < m1 - 1; i += blockDim.x) r[i] = t[i + 1] - s2 * g.vQ[i + 1];
+    __syncthreads();
+    return r;
+}
+
+struct CGState {
+    double* X;  // [k][mm]
+    double* R;
+    double* Z;
+    double* P;
+    double* rz;      // [k]
+    double* target;  // [k]
+    int* active;     // [k]
+    int* iters;      // [k]
+    int* breakdown;  // [k]
+    const double* jd;  // mm or null
+    int mm;
+    int cap;
+    double tol;
+};
+
+__global__ void __launch_bounds__(kPT) cg_init_kernel(CGState s, const double* rhs) {
+    __shared__ double sh[32];
+    const int c = blockIdx.x, mm = s.mm;
+    const double* b = rhs + (size_t)c * mm;
+    double* X = s.X + (size_t)c * mm;
+    double* R = s.R + (size_t)c * mm;
+    double* Z = s.Z + (size_t)c * mm;
+    double* P = s.P + (size_t)c * mm;
+    double prz = 0.0, pbb = 0.0;
+    for (int i = threadIdx.x; i < mm; i += blockDim.x) {
+        const double r = b[i];
+        const double z = s.jd ? r / s.jd[i] : r;
+        X[i] = 0.0;
+        R[i] = r;
+        Z[i] = z;
+        P[i] = z;
+        prz += r * z;
+        pbb += r * r;
+    }
+    const double rz = block_sum(prz, sh);
+    const double bb = block_sum(pbb, sh);
+    if (threadIdx.x == 0) {
+        s.rz[c] = rz;
+        s.target[c] = s.tol * sqrt(bb);
+        s.iters[c] = 0;
+        s.breakdown[c] = 0;
+        s.active[c] = (s.cap > 0 && sqrt(bb) > s.target[c]) ? 1 : 0;  // :94 loop test at it = 0
+    }
+}
+
+// lift P (or an arbitrary source block) of the active columns into HVP input rows
+__global__ void __launch_bounds__(kPT) lift_kernel(Geo g, const double* E, int ldE, bool apply_q, const int* active,
+                                                   double* vin) {
+    extern __shared__ double q[];
+    __shared__ double sh[32];
+    const int c = blockIdx.x;
+    double* row = vin + (size_t)c * g.ld;
+    if (active && !active[c]) {
+        for (int i = threadIdx.x; i < g.ld; i += blockDim.x) row[i] = 0.0;
+        return;
+    }
+    lift_col(g, E + (size_t)c * ldE, apply_q, row, q, sh);
+}
+
+// one capped-CG step per active column, from the HVP rows H (full coordinates)
+__global__ void __launch_bounds__(kPT) cg_step_kernel(Geo g, CGState s, const double* H, double lambda) {
+    extern __shared__ double t[];
+    __shared__ double sh[32];
+    const int c = blockIdx.x, mm = s.mm;
+    if (!s.active[c]) return;
+    // thread 0 rewrites rz only after every thread passed the barriers below
+    const double rz_old = s.rz[c];
+    double* hp_ = const_cast<double*>(reduce_col(g, H + (size_t)c * g.ld, true, t, sh));  // Q^T U^T H p
+    double* X = s.X + (size_t)c * mm;
+    double* R = s.R + (size_t)c * mm;
+    double* Z = s.Z + (size_t)c * mm;
+    double* P = s.P + (size_t)c * mm;
+    double pp = 0.0;
+    for (int i = threadIdx.x; i < mm; i += blockDim.x) {
+        const double hp = hp_[i] + lambda * P[i];  // Hop: red + lambda e (:194)
+        hp_[i] = hp;
+        pp += P[i] * hp;
+    }
+    const double pHp = block_sum(pp, sh);
+    if (pHp <= 0.0) {  // :97-100
+        if (threadIdx.x == 0) {
+            s.breakdown[c] = 1;
+            s.active[c] = 0;
+        }
+        return;
+    }
+    const double alpha = rz_old / pHp;
+    double prz = 0.0, prr = 0.0;
+    for (int i = threadIdx.x; i < mm; i += blockDim.x) {
+        X[i] += alpha * P[i];
+        const double r = R[i] - alpha * hp_[i];
+        R[i] = r;
+        const double z = s.jd ? r / s.jd[i] : r;
+        Z[i] = z;
+        prz += r * z;
+        prr += r * r;
+    }
+    const double rz2 = block_sum(prz, sh);
+    const double rr = block_sum(prr, sh);
+    const double beta = rz2 / rz_old;
+    for (int i = threadIdx.x; i < mm; i += blockDim.x) P[i] = Z[i] + beta * P[i];
+    if (threadIdx.x == 0) {
+        s.rz[c] = rz2;
+        const int it = s.iters[c] + 1;
+        s.iters[c] = it;
+        s.active[c] = (it < s.cap && sqrt(rr) > s.target[c]) ? 1 : 0;  // :94
+    }
+}
+
+// out = Q^T U^T H (+ lambda e) per column, or a += sum_c Q^T U^T H_c (in column order)
+__global__ void __launch_bounds__(kPT) reduce_kernel(Geo g, const double* H, int k, bool apply_q, double* out,
+                                                     int ldo) {
+    extern __shared__ double t[];
+    __shared__ double sh[32];
+    const int c = blockIdx.x;
+    const double* r = reduce_col(g, H + (size_t)c * g.ld, apply_q, t, sh);
+    const int len = apply_q ? g.m - 2 : g.m - 1;
+    for (int i = threadIdx.x; i < len; i += blockDim.x) out[(size_t)c * ldo + i] = r[i];
+}
+
+template <class T>
+T* carve(unsigned char*& cur, size_t count) {
+    T* p = reinterpret_cast<T*>(cur);
+    cur += ((count * sizeof(T) + 255) / 256) * 256;
+    return p;
+}
+
+}  // namespace
+
+struct PcgWorkspace {
+    size_t bytes = 0;
+    unsigned char* dev = nullptr;
+    int* host_flags = nullptr;  // pinned [4 * kPcgMaxCols]
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+
+void pcg_workspace_free(mvsk_gpu_ctx* ctx) {
+    if (!ctx->pcg) return;
+    if (ctx->pcg->dev) cudaFree(ctx->pcg->dev);
+    if (ctx->pcg->host_flags) cudaFreeHost(ctx->pcg->host_flags);
+    for (cudaEvent_t e : ctx->pcg->ev)
+        if (e) cudaEventDestroy(e);
+    delete ctx->pcg;
+    ctx->pcg = nullptr;
+}
+
+PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const PcgInput& in) {
+    const int m = (int)in.m, m1 = m - 1, mm = m - 2;
+    const int K = kPcgMaxCols;
+    const size_t ld = (size_t)ctx->ld;
+    // ---- workspace
+    const size_t need = 256 * 32 + sizeof(double) * ((size_t)m + m1 + m1 + 6 * (size_t)K * mm + 4 * mm + 4 * K) +
+                        sizeof(long long) * m + sizeof(int) * 4 * K;
+    if (!ctx->pcg) ctx->pcg = new PcgWorkspace();
+    PcgWorkspace& ws = *ctx->pcg;
+    if (ws.bytes < need) {
+        if (ws.dev) MVSK_CUDA(cudaFree(ws.dev));
+        ws.dev = nullptr;
+        MVSK_CUDA(cudaMalloc(&ws.dev, need));
+        ws.bytes = need;
+    }
+    if (!ws.host_flags) MVSK_CUDA(cudaMallocHost(&ws.host_flags, sizeof(int) * 4 * K));
+    for (cudaEvent_t& e : ws.ev)
+        if (!e) MVSK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    unsigned char* cur = ws.dev;
+    double* vU = carve<double>(cur, m);
+    double* vQ = carve<double>(cur, m1);
+    double* nu = carve<double>(cur, m1);
+    double* X = carve<double>(cur, (size_t)K * mm);
+    double* Rm = carve<double>(cur, (size_t)K * mm);
+    double* Z = carve<double>(cur, (size_t)K * mm);
+    double* P = carve<double>(cur, (size_t)K * mm);
+    double* src = carve<double>(cur, (size_t)K * mm);  // rhs / probes
+    double* rows = carve<double>(cur, (size_t)K * mm);  // reduced outputs
+    double* jd = carve<double>(cur, mm);
+    double* hvec = carve<double>(cur, mm);
+    double* avec = carve<double>(cur, mm);
+    double* rz = carve<double>(cur, K);
+    double* target = carve<double>(cur, K);
+    long long* idx = carve<long long>(cur, m);
+    int* active = carve<int>(cur, K);
+    int* iters = carve<int>(cur, K);
+    int* bdown = carve<int>(cur, K);
+    cudaStream_t st = ctx->stream;
+
+    MVSK_CUDA(cudaMemcpyAsync(vU, in.vU.data(), m * sizeof(double), cudaMemcpyHostToDevice, st));
+    MVSK_CUDA(cudaMemcpyAsync(vQ, in.vQ.data(), m1 * sizeof(double), cudaMemcpyHostToDevice, st));
+    MVSK_CUDA(cudaMemcpyAsync(nu, in.nu.data(), m1 * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (fm.active) MVSK_CUDA(cudaMemcpyAsync(idx, fm.idx.data(), m * sizeof(long long), cudaMemcpyHostToDevice, st));
+    Geo g{vU, in.bU, vQ, in.bQ, fm.active ? idx : nullptr, m, (int)ld};
+    const size_t dsm = (size_t)2 * std::max(m, 1) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        for (const void* fn : {(const void*)lift_kernel, (const void*)cg_step_kernel, (const void*)reduce_kernel})
+            MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024 * 2));
+        attr = true;
+    }
+    const Slot& sl = ctx->slots[slot];
+    double* vin = ctx->vin;
+    double* vin2 = ctx->vin + (size_t)MVSK_GPU_MAX_RHS * ld;
+    double* H = ctx->outd;
+
+    PcgOutput out;
+    auto hvp_rows = [&](int k, int logical) {
+        PassIO io;
+        io.vin = vin;
+        io.z = sl.z;
+        io.out = H;
+        io.ldo = (long long)ld;
+        run_pass(ctx, Op::HVP, k, io);
+        ctx->fwd += logical;  // reference contract: 2 passes per (active) HVP
+        ctx->tr += logical;
+    };
+    // capped CG on k columns in lock-step (the columns' arithmetic is
+    // cg_capped's). Steps are enqueued one ahead of the host's look at the
+    // activity flags: step s+1 is already queued while the host reads the flags
+    // that gate step s, and a step whose flags are all 0 is a device-side no-op
+    // (every kernel of the step, including the HVP pass, exits on entry). So
+    // the GPU never idles on a host round trip inside the Krylov loop.
+    auto cg = [&](int k, int cap, const double* jdp) {
+        CGState s{X, Rm, Z, P, rz, target, active, iters, bdown, jdp, mm, cap, in.tol};
+        cg_init_kernel<<<k, kPT, 0, st>>>(s, src);
+        MVSK_CUDA(cudaGetLastError());
+        int* hf = ws.host_flags;  // [2][K] flag snapshots + [2K..) iters / breakdown
+        MVSK_CUDA(cudaMemcpyAsync(hf, active, k * sizeof(int), cudaMemcpyDeviceToHost, st));
+        MVSK_CUDA(cudaEventRecord(ws.ev[0], st));
+        for (int step = 0; step < cap; ++step) {
+            lift_kernel<<<k, kPT, dsm, st>>>(g, P, mm, true, active, vin);
+            MVSK_CUDA(cudaGetLastError());
+            PassIO io;
+            io.vin = vin;
+            io.z = sl.z;
+            io.out = H;
+            io.ldo = (long long)ld;
+            io.skip = active;
+            io.nskip = k;
+            run_pass(ctx, Op::HVP, k, io);
+            cg_step_kernel<<<k, kPT, dsm, st>>>(g, s, H, in.lambda);
+            MVSK_CUDA(cudaGetLastError());
+            const int nb = (step + 1) & 1;
+            MVSK_CUDA(cudaMemcpyAsync(hf + nb * K, active, k * sizeof(int), cudaMemcpyDeviceToHost, st));
+            MVSK_CUDA(cudaEventRecord(ws.ev[nb], st));
+            // flags that gated this step
+            MVSK_CUDA(cudaEventSynchronize(ws.ev[step & 1]));
+            int nact = 0;
+            for (int c = 0; c < k; ++c) nact += hf[(step & 1) * K + c];
+            if (!nact) {
+                ctx->phys -= 1;  // the step ran as a no-op
+                break;
+            }
+            ctx->fwd += nact;  // reference contract: 2 passes per (active) HVP
+            ctx->tr += nact;
+        }
+        MVSK_CUDA(cudaMemcpyAsync(hf + 2 * K, iters, k * sizeof(int), cudaMemcpyDeviceToHost, st));
+        MVSK_CUDA(cudaMemcpyAsync(hf + 3 * K, bdown, k * sizeof(int), cudaMemcpyDeviceToHost, st));
+        MVSK_CUDA(cudaStreamSynchronize(st));
+        for (int c = 0; c < k; ++c) {
+            out.iters += hf[2 * K + c];
+            if (hf[3 * K + c]) out.breakdown = true;
+        }
+    };
+
+    // ---- Jacobi diagonal (:197-209): 8 probes through Hop in one batch
+    const double* jdp = nullptr;
+    if (!in.jacobi_probes.empty()) {
+        const int k = (int)in.jacobi_probes.size();
+        std::vector<double> buf((size_t)k * mm);
+        for (int p = 0; p < k; ++p) std::copy(in.jacobi_probes[p].begin(), in.jacobi_probes[p].end(), buf.begin() + (size_t)p * mm);
+        MVSK_CUDA(cudaMemcpyAsync(src, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        lift_kernel<<<k, kPT, dsm, st>>>(g, src, mm, true, nullptr, vin);
+        MVSK_CUDA(cudaGetLastError());
+        hvp_rows(k, k);
+        reduce_kernel<<<k, kPT, dsm, st>>>(g, H, k, true, rows, mm);
+        MVSK_CUDA(cudaGetLastError());
+        // + lambda r (Hop), then the mean of r o Hop(r)
+        std::vector<double> hr(buf.size());
+        MVSK_CUDA(cudaMemcpyAsync(hr.data(), rows, hr.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+        MVSK_CUDA(cudaStreamSynchronize(st));
+        for (size_t i = 0; i < hr.size(); ++i) hr[i] += in.lambda * buf[i];
+        std::vector<double> dg((size_t)mm, 0.0);
+        for (int p = 0; p < k; ++p)
+            for (int i = 0; i < mm; ++i) dg[(size_t)i] += buf[(size_t)p * mm + i] * hr[(size_t)p * mm + i];
+        const double fl = std::max(1e-12, in.lambda);
+        for (double& v : dg) {
+            v /= (double)k;
+            v = std::max(v, fl);
+        }
+        MVSK_CUDA(cudaMemcpyAsync(jd, dg.data(), mm * sizeof(double), cudaMemcpyHostToDevice, st));
+        MVSK_CUDA(cudaStreamSynchronize(st));
+        jdp = jd;
+    }
+
+    // ---- h = Q^T U^T grad2 f (U nu)  (:212-213)
+    lift_kernel<<<1, kPT, dsm, st>>>(g, nu, m1, false, nullptr, vin);
+    MVSK_CUDA(cudaGetLastError());
+    hvp_rows(1, 1);
+    reduce_kernel<<<1, kPT, dsm, st>>>(g, H, 1, true, hvec, mm);
+    MVSK_CUDA(cudaGetLastError());
+
+    // ---- a: Hutchinson probes or exact trace (:215-237), blocks of K columns
+    int nprobe_total = 0;
+    MVSK_CUDA(cudaMemsetAsync(avec, 0, mm * sizeof(double), st));
+    std::vector<double> a_host((size_t)mm, 0.0);
+    if (in.has_third) {
+        const int P_all = (int)in.probes.size();
+        nprobe_total = P_all;
+        for (int b0 = 0; b0 < P_all; b0 += K) {
+            const int k = std::min(K, P_all - b0);
+            std::vector<double> buf((size_t)k * mm);
+            for (int p = 0; p < k; ++p)
+                std::copy(in.probes[b0 + p].begin(), in.probes[b0 + p].end(), buf.begin() + (size_t)p * mm);
+            MVSK_CUDA(cudaMemcpyAsync(src, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+            cg(k, in.probe_cap, jdp);
+            // third_action(U Q s_p, U Q r_p) for the block, one fused pass
+            lift_kernel<<<k, kPT, dsm, st>>>(g, X, mm, true, nullptr, vin);
+            lift_kernel<<<k, kPT, dsm, st>>>(g, src, mm, true, nullptr, vin2);
+            MVSK_CUDA(cudaGetLastError());
+            PassIO io;
+            io.vin = vin;
+            io.vin2 = vin2;
+            io.z = sl.z;
+            io.out = H;
+            io.ldo = (long long)ld;
+            run_pass(ctx, Op::THIRD, k, io);
+            ctx->fwd += 2 * k;
+            ctx->tr += k;
+            reduce_kernel<<<k, kPT, dsm, st>>>(g, H, k, true, rows, mm);
+            MVSK_CUDA(cudaGetLastError());
+            // accumulate in probe order on the host (a is an mm-vector)
+            std::vector<double> t3((size_t)k * mm);
+            MVSK_CUDA(cudaMemcpyAsync(t3.data(), rows, t3.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+            MVSK_CUDA(cudaStreamSynchronize(st));
+            for (int p = 0; p < k; ++p)
+                for (int i = 0; i < mm; ++i) a_host[(size_t)i] += t3[(size_t)p * mm + i];
+        }
+        if (!in.exact_trace)
+            for (double& v : a_host) v /= (double)in.hutchinson_probes;
+    }
+    // rhs = h - (||gbar|| / n) a  (:239)
+    std::vector<double> h_host((size_t)mm);
+    MVSK_CUDA(cudaMemcpyAsync(h_host.data(), hvec, mm * sizeof(double), cudaMemcpyDeviceToHost, st));
+    MVSK_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> r_host((size_t)mm);
+    for (int i = 0; i < mm; ++i) r_host[(size_t)i] = h_host[(size_t)i] - (in.gn / (double)m) * a_host[(size_t)i];
+    MVSK_CUDA(cudaMemcpyAsync(src, r_host.data(), mm * sizeof(double), cudaMemcpyHostToDevice, st));
+    // main CG (:240-241)
+    cg(1, in.maxit, jdp);
+    out.u.resize((size_t)mm);
+    MVSK_CUDA(cudaMemcpyAsync(out.u.data(), X, mm * sizeof(double), cudaMemcpyDeviceToHost, st));
+    MVSK_CUDA(cudaStreamSynchronize(st));
+    (void)nprobe_total;
+    return out;
+}
+
+}  // namespace mvsk_b200

@@ -49,6 +49,8 @@ struct ClusterArgs {
     const double* z;     // cached z
     double* part_acc;    // [ncluster][K][ld]
     double c2, c3, c4;
+    const int* skip;
+    int nskip;
 };
 
 // Butterfly reduce-scatter of V <= 32 values over the 32 lanes of a warp.
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(256, 1) stream_cluster_kernel(const ClusterArg
     constexpr int V = Sh::V;
     constexpr int E = kXSlots;
     static_assert(V <= 32, "partial dots per stage must fit one warp");
+    if (pass_skipped(a.skip, a.nskip)) return;  // uniform over the whole grid
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.num_blocks();
     const int crank = (int)cluster.block_rank();

@@ -34,6 +34,8 @@ struct DmmaArgs {
     const double* z;
     double* part_acc;    // [ncluster][K][ld]
     double c2, c3, c4;
+    const int* skip;
+    int nskip;
 };
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
@@ -58,6 +60,7 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
     constexpr int E = kXSlots;
     constexpr int RS = 8 * WC + 4;  // smem row stride (doubles): conflict-free fragment loads
     static_assert(K <= 8, "phase 2 uses one n-tile");
+    if (pass_skipped(a.skip, a.nskip)) return;  // uniform over the whole grid
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.num_blocks();
     const int crank = (int)cluster.block_rank();

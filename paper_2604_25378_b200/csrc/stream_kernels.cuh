@@ -46,7 +46,18 @@ struct StreamArgs {
     double* part_sc;     // [gridDim][kNumScalars]
     double c2, c3, c4;
     double Tglob;        // global T (the reference divides by T = A.rows())
+    const int* skip;     // optional: skip the pass when all nskip flags are 0
+    int nskip;
 };
+
+// Device-side early exit for speculatively enqueued Krylov steps: the pass is a
+// no-op when no CG column is still active (pcg_device.cu).
+__device__ __forceinline__ bool pass_skipped(const int* skip, int nskip) {
+    if (!skip) return false;
+    int any = 0;
+    for (int i = 0; i < nskip; ++i) any |= skip[i];
+    return any == 0;
+}
 
 template <int K>
 struct OpWidth {
@@ -84,6 +95,7 @@ __global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG>::max_threads, 1) stre
     constexpr int NA = NACC > 0 ? NACC : 1;
     constexpr int NDR = NDOT > 0 ? NDOT : 1;
 
+    if (pass_skipped(a.skip, a.nskip)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int P = a.P, G = a.G, S = a.S;

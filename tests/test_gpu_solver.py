@@ -186,3 +186,55 @@ def test_config_solve_parity(name, kappa, mode):
     xc, rc, env, _ = _cpu_envelope(A, mu, c, cfg_c)
     xg, rg = _gpu(A, mu, c).solve(cfg_g)
     _same_solution(xg, rg, xc, rc, cfg_g.tau, envelope=env)
+
+
+def test_device_pcg_matches_host_pcg(monkeypatch):
+    """The device-resident Krylov loops (pcg_device.cu) against the host-driven
+    ones and the CPU oracle, including faces, Jacobi and exact trace. The bar
+    is the reference's own reorder envelope: the restated CPU direction under a
+    different summation order (2 threads) moves by ~5e-9 (plain PCG) but by
+    ~5e-2 with the probe-estimated Jacobi preconditioner (clamped estimates make
+    the preconditioned recurrence ill-conditioned), so each case is checked
+    against max(1e-8 relative, 10 x that envelope)."""
+    from paper_2604_25378_b200.datagen import make_panel
+    from paper_2604_25378_b200.gpu_oracle import GpuOracle, tangent_config
+    A, mu, c = make_panel("C2", seed=4, kappa=10.0)
+    n = A.shape[1]
+    x = rh.simplex_point(n, 3, 1e-6)
+    cpu = po.CpuOracle(A, mu, c)
+    g = GpuOracle(A, mu, c)
+    for kw in (dict(lam=1e-4), dict(lam=1e-4, jacobi=True), dict(lam=1e-4, probes=16),
+               dict(lam=0.0, krylov_tol=1e-12, krylov_maxit=200, exact_trace=True)):
+        gc = g.make_cache(x)
+        dd, dg_diag = g.yand_direction(gc, tangent_config("pcg", **kw), 7)
+        monkeypatch.setenv("MVSK_HOST_PCG", "1")
+        gc = g.make_cache(x)
+        dh, dh_diag = g.yand_direction(gc, tangent_config("pcg", **kw), 7)
+        monkeypatch.delenv("MVSK_HOST_PCG")
+        dc, dc_diag = cpu.yand_direction(cpu.make_cache(x), po.tangent_config("pcg", **kw), 7)
+        po.set_threads(2)
+        try:
+            dc2, _ = cpu.yand_direction(cpu.make_cache(x), po.tangent_config("pcg", **kw), 7)
+        finally:
+            po.set_threads(1)
+        env = float(np.max(np.abs(dc - dc2)))
+        scale = 1 + float(np.max(np.abs(dc)))
+        tol = max(1e-8 * scale, 10 * env)
+        if not kw.get("exact_trace"):  # capped truncated CG: identical iteration counts
+            assert dg_diag.krylov_iters == dh_diag.krylov_iters == dc_diag.krylov_iters
+        assert np.max(np.abs(dd - dc)) <= tol, (kw, np.max(np.abs(dd - dc)), env)
+        assert np.max(np.abs(dh - dc)) <= tol, (kw, np.max(np.abs(dh - dc)), env)
+    # on a face
+    tau = 1e-8
+    xf = x.copy()
+    xf[[3, 17, 40]] = tau
+    xf /= xf.sum()
+    xf[[3, 17, 40]] = tau
+    idx = np.array([i for i in range(n) if i not in (3, 17, 40)])
+    g.set_face(idx, tau)
+    gc = g.make_cache(xf[idx])
+    dd, _ = g.yand_direction(gc, tangent_config("pcg", lam=1e-4), 3)
+    monkeypatch.setenv("MVSK_HOST_PCG", "1")
+    gc = g.make_cache(xf[idx])
+    dh, _ = g.yand_direction(gc, tangent_config("pcg", lam=1e-4), 3)
+    assert np.max(np.abs(dd - dh)) <= 1e-8 * (1 + np.max(np.abs(dh)))
