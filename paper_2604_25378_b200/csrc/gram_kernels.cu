@@ -16,7 +16,8 @@ namespace mvsk_b200 {
 namespace {
 
 constexpr int GBM = 128;            // output tile (square)
-constexpr int GBK = 16;             // sample rows per chunk
+constexpr int GBK = 32;             // sample rows per chunk
+constexpr int GST = 3;              // cp.async ring depth
 constexpr int GPAD = 4;             // smem row pad (doubles): conflict-free fragment loads
 constexpr int GLDS = GBM + GPAD;    // smem row stride
 constexpr int GTHREADS = 256;       // 8 warps: 4 (m) x 2 (n), warp tile 32 x 64
@@ -58,9 +59,9 @@ __device__ __forceinline__ void pair_of(int p, int& ti, int& tj) {
 
 __global__ void __launch_bounds__(GTHREADS, 1) syrk_dmma_kernel(const GramArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* sA = reinterpret_cast<double*>(smem_raw);           // [2][GBK][GLDS]
-    double* sB = sA + 2 * GBK * GLDS;                            // [2][GBK][GLDS]
-    double* sw = sB + 2 * GBK * GLDS;                            // [2][GBK]
+    double* sA = reinterpret_cast<double*>(smem_raw);           // [GST][GBK][GLDS]
+    double* sB = sA + GST * GBK * GLDS;                          // [GST][GBK][GLDS]
+    double* sw = sB + GST * GBK * GLDS;                          // [GST][GBK]
     int ti, tj;
     pair_of(blockIdx.x, ti, tj);
     const int i0 = ti * GBM, j0 = tj * GBM;
@@ -96,14 +97,17 @@ __global__ void __launch_bounds__(GTHREADS, 1) syrk_dmma_kernel(const GramArgs a
 #pragma unroll
         for (int fn = 0; fn < 8; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
 
-    if (nchunk > 0) load_chunk(0, 0);
-    cp_async_commit();
-    for (int c = 0; c < nchunk; ++c) {
-        const int buf = c & 1;
-        if (c + 1 < nchunk) load_chunk(c + 1, buf ^ 1);
+    // GST-deep cp.async ring: one commit group per chunk (possibly empty)
+    for (int c = 0; c < GST - 1; ++c) {
+        if (c < nchunk) load_chunk(c, c);
         cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
+    }
+    for (int c = 0; c < nchunk; ++c) {
+        const int buf = c % GST;
+        cp_async_wait<GST - 2>();  // chunk c landed
+        __syncthreads();           // ... for every thread; chunk c-1's buffer is free
+        if (c + GST - 1 < nchunk) load_chunk(c + GST - 1, (c + GST - 1) % GST);
+        cp_async_commit();
         const double* A = sA + buf * GBK * GLDS;
         const double* B = sB + buf * GBK * GLDS;
         const double* W = sw + buf * GBK;
@@ -121,7 +125,6 @@ __global__ void __launch_bounds__(GTHREADS, 1) syrk_dmma_kernel(const GramArgs a
 #pragma unroll
                 for (int fn = 0; fn < 8; ++fn) dmma_8x8x4(acc[fm][fn], af[fm], bf[fn]);
         }
-        __syncthreads();
     }
     // partial tile out (row-major 128 x 128)
     double* out = a.part + ((size_t)split * gridDim.x + blockIdx.x) * (GBM * GBM);
@@ -235,7 +238,7 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
     a.ntile = ntile;
     a.nsplit = nsplit;
     a.part = ctx->gram_part;
-    const size_t smem = (size_t)(4 * GBK * GLDS + 2 * GBK) * sizeof(double);
+    const size_t smem = (size_t)(2 * GST * GBK * GLDS + GST * GBK) * sizeof(double);
     static bool attr = false;
     if (!attr) {
         MVSK_CUDA(cudaFuncSetAttribute(syrk_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
