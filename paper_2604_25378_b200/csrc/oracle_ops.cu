@@ -300,24 +300,26 @@ struct DPlan {
     const void* fn = nullptr;
 };
 
-template <Op OP, int K, int WC>
+template <Op OP, int K, int WC, int D>
 const void* dfn() {
-    return reinterpret_cast<const void*>(&stream_dmma_kernel<OP, K, WC>);
+    return reinterpret_cast<const void*>(&stream_dmma_kernel<OP, K, WC, D>);
 }
 
-const void* select_dmma(Op op, int K, int WC) {
-#define MVSK_DWC(OP, K)                                    \
-    if (WC == 32) return dfn<OP, K, 32>();                  \
-    if (WC == 64) return dfn<OP, K, 64>();                  \
-    if (WC == 80) return dfn<OP, K, 80>();                  \
-    if (WC == 128) return dfn<OP, K, 128>();
-    if (op == Op::HVP && K == 8) { MVSK_DWC(Op::HVP, 8) }
-    if (op == Op::HVP && K == 4) { MVSK_DWC(Op::HVP, 4) }
-    if (op == Op::THIRD && K == 4) { MVSK_DWC(Op::THIRD, 4) }
-    if (op == Op::THIRD && K == 8) {
-        if (WC == 32) return dfn<Op::THIRD, 8, 32>();
-        if (WC == 64) return dfn<Op::THIRD, 8, 64>();
-        if (WC == 80) return dfn<Op::THIRD, 8, 80>();
+const void* select_dmma(Op op, int K, int WC, int D) {
+#define MVSK_DWC(OP, K, D)                                 \
+    if (WC == 32) return dfn<OP, K, 32, D>();               \
+    if (WC == 64) return dfn<OP, K, 64, D>();               \
+    if (WC == 80) return dfn<OP, K, 80, D>();               \
+    if (WC == 128) return dfn<OP, K, 128, D>();
+    if (D == 1) {
+        if (op == Op::HVP && K == 8) { MVSK_DWC(Op::HVP, 8, 1) }
+        if (op == Op::HVP && K == 4) { MVSK_DWC(Op::HVP, 4, 1) }
+        if (op == Op::THIRD && K == 4) { MVSK_DWC(Op::THIRD, 4, 1) }
+        if (op == Op::THIRD && K == 8) {
+            if (WC == 32) return dfn<Op::THIRD, 8, 32, 1>();
+            if (WC == 64) return dfn<Op::THIRD, 8, 64, 1>();
+            if (WC == 80) return dfn<Op::THIRD, 8, 80, 1>();
+        }
     }
 #undef MVSK_DWC
     return nullptr;
@@ -325,8 +327,8 @@ const void* select_dmma(Op op, int K, int WC) {
 
 bool make_dmma_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
     if (std::getenv("MVSK_NO_DMMA")) return false;
-    int forceC = 0;
-    if (const char* e = std::getenv("MVSK_TUNE_DMMA")) std::sscanf(e, "%d", &forceC);
+    int forceC = 0, forceD = 0;
+    if (const char* e = std::getenv("MVSK_TUNE_DMMA")) std::sscanf(e, "%d,%d", &forceC, &forceD);
     const int ndot = op == Op::THIRD ? 2 * K : K;
     const int V = 8 * ndot;
     const int Cs[4] = {4, 8, 2, 1};
@@ -344,19 +346,31 @@ bool make_dmma_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
             if (forceC) return false;
             continue;
         }
-        const void* fn = select_dmma(op, K, WC);
+        const size_t stage = (size_t)8 * (8 * WC + 4) * sizeof(double);
+        // exchange depth (D = 2 measured no faster than 1 at C5: the per-stage
+        // chain, not the DSMEM latency, bounds it; only D = 1 is instantiated)
+        int D = 0;
+        const void* fn = nullptr;
+        int S = 0;
+        size_t head = 0;
+        for (int d : {1}) {
+            if (fn || (forceD && d != forceD)) continue;
+            const void* f = select_dmma(op, K, WC, d);
+            if (!f) continue;
+            size_t h = 256 + (size_t)(8 * V + (2 * d + 2) * C * V + 2 * V) * sizeof(double);
+            h = (h + 127) & ~(size_t)127;
+            const int s = (int)std::min<size_t>(6, (ctx->max_smem - h) / stage);
+            if (s < d + 2) continue;
+            fn = f;
+            D = d;
+            S = s;
+            head = h;
+        }
         if (!fn) {
             if (forceC) return false;
             continue;
         }
-        const size_t stage = (size_t)8 * (8 * WC + 4) * sizeof(double);
-        size_t head = 256 + (size_t)(8 * V + kXSlots * C * V + 2 * V) * sizeof(double);
-        head = (head + 127) & ~(size_t)127;
-        int S = (int)std::min<size_t>(6, (ctx->max_smem - head) / stage);
-        if (S < 3) {
-            if (forceC) return false;
-            continue;
-        }
+        (void)D;
         pl.C = C;
         pl.WC = WC;
         pl.S = S;

@@ -51,13 +51,16 @@ struct DmmaShape {
     static constexpr int V = 8 * NDOT;                        // partial dots per stage
 };
 
-template <Op OP, int K, int WC>
+// D = exchange pipelining depth: produce(s + D) is issued before consume(s),
+// so D stages of DSMEM exchange are in flight (needs a TMA ring S >= D + 2 and
+// E = 2D + 2 exchange slots, see the slot-reuse argument in stream_cluster.cuh).
+template <Op OP, int K, int WC, int D>
 __global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
     using Sh = DmmaShape<OP, K>;
     constexpr int NDOT = Sh::NDOT, NT1 = Sh::NT1, V = Sh::V;
     constexpr int KS1 = WC / 4;  // phase-1 k-steps per warp
     constexpr int MT = WC / 8;   // phase-2 m-tiles per warp
-    constexpr int E = kXSlots;
+    constexpr int E = 2 * D + 2;
     constexpr int RS = 8 * WC + 4;  // smem row stride (doubles): conflict-free fragment loads
     static_assert(K <= 8, "phase 2 uses one n-tile");
     if (pass_skipped(a.skip, a.nskip)) return;  // uniform over the whole grid
@@ -168,8 +171,8 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
                 const int j = nt * 8 + 2 * t4 + i;
                 if (j < NDOT) rb[g4 * NDOT + j] = cfr[0][nt][i] + cfr[1][nt][i];
             }
-        __syncthreads();  // (A) warp partials published; all consumes up to s-2 done
-        if (tid == 0 && s >= 2 && s - 2 + S < nst) issue(s - 2 + S);
+        __syncthreads();  // (A) warp partials published; all consumes up to s-D-1 done
+        if (tid == 0 && s >= D + 1 && s - D - 1 + S < nst) issue(s - D - 1 + S);
         if (tid < V) {
             double sum = 0.0;
 #pragma unroll
@@ -224,16 +227,20 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
             }
     };
 
-    double za[2], zb[2];
-    if (nst > 0) produce(0, za);
-    int s = 0;
-    for (; s + 1 < nst; s += 2) {
-        produce(s + 1, zb);
-        consume(s, za);
-        if (s + 2 < nst) produce(s + 2, za);
-        consume(s + 1, zb);
+    double zr[D + 1][2];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        if (i < nst) produce(i, zr[i]);
+    for (int s0 = 0; s0 < nst; s0 += D + 1) {
+#pragma unroll
+        for (int j = 0; j <= D; ++j) {
+            const int s = s0 + j;
+            if (s < nst) {
+                if (s + D < nst) produce(s + D, zr[(j + D) % (D + 1)]);
+                consume(s, zr[j]);
+            }
+        }
     }
-    if (s < nst) consume(s, za);
 
     // G fragment: D[m = col = g4][n = k = 2*t4 + i]
 #pragma unroll

@@ -56,7 +56,7 @@ def timeit(fn, reps=10):
 
 grid = [os.environ.get("MVSK_TUNE_GRID")] if os.environ.get("MVSK_TUNE_GRID") else None
 for op in [o for o in ops if o in ("hvp8", "third8", "hvp4")]:
-    for cl in ["dmma0", "dmma2", "dmma4", "dmma8", "0,0", "2,0", "4,0", "8,0", "2,2", "4,4"]:
+    for cl in ["dmma0", "dmma4,1", "dmma8,1", "dmma8,2", "dmma2,1", "0,0"]:
         if cl.startswith("dmma"):
             os.environ.pop("MVSK_NO_DMMA", None)
             os.environ["MVSK_TUNE_DMMA"] = cl[4:]
