@@ -310,8 +310,16 @@ def main():
     alg_bytes = 8.0 * T_loc * n + 8.0 * T_loc + 16.0 * n  # one read of the shard + z + v/out
     peak, peak_kind = hbm_peak()
     achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    try:  # dram read+write per launch from the committed ncu --set full capture of this workload
+        tr = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        if ws == 1 and args.config == "C5":
+            traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "peak_kind": peak_kind,
+                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write, profiles/ncu_traffic.json)",
+                "algorithmic_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
                 "note": "achieved = (8*T_local*n + 8*T_local + 16*n) B per HVP / mean per-call time of the "
                         "fused stream kernel + its reduction kernel, CUDA events on the launching stream"}
 
