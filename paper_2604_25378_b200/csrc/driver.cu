@@ -15,6 +15,7 @@
 // Host geometry (O(n) Householder applies, projections) stays on the host.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -26,6 +27,22 @@
 
 namespace mvsk_b200 {
 namespace {
+
+// ---- optional host-side profile of a solve (MVSK_PROFILE=1 -> stderr) --------
+struct Prof {
+    bool on = false;
+    double proj = 0, dir = 0, cache = 0, grad = 0, line = 0, total = 0;
+    long nproj = 0, ndir = 0, ncache = 0, nline = 0;
+};
+Prof g_prof;
+struct Tick {
+    double& acc;
+    std::chrono::steady_clock::time_point t0;
+    explicit Tick(double& a) : acc(a), t0(std::chrono::steady_clock::now()) {}
+    ~Tick() {
+        if (g_prof.on) acc += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
 
 // ---- small dense helpers -----------------------------------------------------
 double dot(const Vec& a, const Vec& b) {
@@ -181,6 +198,8 @@ double alpha_max(const Vec& x, const Vec& d, double tau) {
 }
 
 Vec project_slice(const Vec& v, double tau, double mass = 1.0) {
+    Tick tk(g_prof.proj);
+    ++g_prof.nproj;
     const size_t n = v.size();
     const double s = mass - (double)n * tau;
     if (!(tau >= 0.0) || !(s > 0.0)) throw ApiError(MVSK_DOMAIN_ERROR, "project_slice: need 0 <= tau < mass/n");
@@ -304,8 +323,13 @@ struct View {
     mvsk_gpu_ctx* ctx;
     FaceMap fm;
     long long m() const { return fm.m; }
-    double make_cache(int slot, const Vec& x) const { return op_make_cache(ctx, slot, fm, x.data()); }
+    double make_cache(int slot, const Vec& x) const {
+        Tick tk(g_prof.cache);
+        ++g_prof.ncache;
+        return op_make_cache(ctx, slot, fm, x.data());
+    }
     Vec gradient(int slot) const {
+        Tick tk(g_prof.grad);
         Vec g((size_t)fm.m);
         op_gradient(ctx, slot, fm, g.data());
         return g;
@@ -340,6 +364,8 @@ struct View {
         return out;
     }
     LineModel line_model(int slot, const Vec& d, double cap) const {
+        Tick tk(g_prof.line);
+        ++g_prof.nline;
         double o[14];
         op_line_model(ctx, slot, fm, d.data(), o);
         LineModel lm;
@@ -948,7 +974,12 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
             // the face cache is rebuilt by the residual checks above (shared
             // tmp slot only); kSlotFace still holds the face point
             mvsk_direction_diag dd{};
-            const Vec d = yand_direction(face, kSlotFace, config.tangent, (uint64_t)it_total, dd);
+            Vec d;
+            {
+                Tick tk(g_prof.dir);
+                ++g_prof.ndir;
+                d = yand_direction(face, kSlotFace, config.tangent, (uint64_t)it_total, dd);
+            }
             rep.krylov += dd.krylov_iters;
             const double amax = alpha_max(xf, d, tau);
             bool moved = false;
@@ -1243,8 +1274,17 @@ int32_t mvsk_gpu_solve(mvsk_gpu_ctx* ctx, const mvsk_solver_config* cfg, const d
             obs = [&](int it, double f, const Vec& x) { observer(observer_user, it, f, x.data(), (int64_t)x.size()); };
         const Vec xs = x0 ? Vec(x0, x0 + ctx->n) : Vec();
         const FaceMap saved = ctx->pub_face;
+        g_prof = Prof();
+        g_prof.on = std::getenv("MVSK_PROFILE") != nullptr;
         Report r = solve(ctx, sc, xs, obs);
         ctx->pub_face = saved;
+        if (g_prof.on)
+            std::fprintf(stderr,
+                         "[mvsk profile] total %.3f ms | make_cache %.3f ms (%ld) | gradient %.3f ms | direction %.3f "
+                         "ms (%ld) | line_model %.3f ms (%ld) | project_slice %.3f ms (%ld)\n",
+                         1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
+                         1e3 * g_prof.cache, g_prof.ncache, 1e3 * g_prof.grad, 1e3 * g_prof.dir, g_prof.ndir,
+                         1e3 * g_prof.line, g_prof.nline, 1e3 * g_prof.proj, g_prof.nproj);
         std::copy(r.x.begin(), r.x.end(), x_star);
         std::memset(report, 0, sizeof(*report));
         report->f_star = r.f;
