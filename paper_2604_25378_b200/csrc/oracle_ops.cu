@@ -130,9 +130,9 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     // several teams per CTA so more rows are in flight (C3: 63 -> 34 us / HVP)
     const bool small = ctx->T_local < 64LL * ctx->nsm;
     int Q = -1;
-    if (small) {
-        for (int q = qmax; q >= 1; q >>= 1)
-            if ((npairs + q - 1) / q >= 32 && (npairs + q - 1) / q <= max_threads(op, K, q, 1)) {
+    if (small) {  // teams of <= 128 threads (C2/C3 sweeps, profiles/r01_tune_C*.txt)
+        for (int q = 1; q <= qmax; q <<= 1)
+            if ((npairs + q - 1) / q <= 128 && (npairs + q - 1) / q <= max_threads(op, K, q, 1)) {
                 Q = q;
                 break;
             }
@@ -155,7 +155,7 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     const size_t row_bytes = (size_t)ctx->ld * sizeof(double);
     const size_t stage_target = 64 * 1024;
     // teams per CTA (each team streams its own rows)
-    int G = std::max(1, (small ? std::min(256, max_threads(op, K, Q, 1)) : max_threads(op, K, Q, 1)) / P);
+    int G = small ? std::max(1, std::min(4, max_threads(op, K, Q, 1) / P)) : std::max(1, max_threads(op, K, Q, 1) / P);
     const long long want_rows = std::max<long long>(1, (long long)(stage_target / row_bytes));
     while (G > 1 && G > want_rows) G >>= 1;
     int RG = 1;
@@ -198,6 +198,7 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     const int threads = G * P;
     int occ = (int)std::min<size_t>(4, (ctx->max_smem + 1024) / (pl.smem + 1024));
     occ = std::max(1, std::min(occ, 2048 / threads));
+    if (small) occ = 1;  // fewer CTA partials: the cross-CTA reduction dominates small panels
     if (tov.OCC > 0) occ = std::min(occ, tov.OCC);
     const long long want_blocks = std::max<long long>(1, (ctx->T_local + R - 1) / R);
     pl.nb = (int)std::min<long long>((long long)ctx->nsm * occ, want_blocks);
@@ -406,15 +407,19 @@ struct FinishArgs {
 // Block = 64 output columns x 4 partial-range groups; each thread sums its
 // quarter of the CTA partials with 4 independent accumulators, the quarters are
 // combined in a fixed order (deterministic), then the op epilogue is applied.
-constexpr int kFinCols = 64;
-__global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
+// Block = cols x ng threads (cols * ng = 256): ng groups split the CTA partials
+// (ng grows with the partial count so small panels with many CTAs do not
+// serialise on one thread per column); groups combine in a fixed order.
+constexpr int kFinThreads = 256;
+__global__ void __launch_bounds__(kFinThreads) finish_kernel(const FinishArgs f, int ng) {
     if (pass_skipped(f.skip, f.nskip)) return;
     const int nacc = (f.op == (int)Op::LINESUMS) ? 0 : f.k;
     const int tot = nacc * f.ld;
     const int nsc = f.op == (int)Op::FGRAD ? 3 : (f.op == (int)Op::LINESUMS ? 9 : 0);
-    const int cl = threadIdx.x & (kFinCols - 1), grp = threadIdx.x / kFinCols;
-    const int i = blockIdx.x * kFinCols + cl;
-    __shared__ double part[4][kFinCols];
+    const int cols = kFinThreads / ng;
+    const int cl = threadIdx.x % cols, grp = threadIdx.x / cols;
+    const int i = blockIdx.x * cols + cl;
+    __shared__ double part[kFinThreads];  // [ng][cols]
     auto qsum = [&](const double* base, size_t stride, int lo, int hi) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int b = lo;
@@ -429,11 +434,22 @@ __global__ void __launch_bounds__(256) finish_kernel(const FinishArgs f) {
     };
     // 1) fixed-order reduction over CTA partials
     if (f.do_reduce) {
-        if (i < tot) part[grp][cl] = qsum(f.part_acc + i, (size_t)tot, f.nb * grp / 4, f.nb * (grp + 1) / 4);
-        if (blockIdx.x == 0 && threadIdx.x < nsc)
-            f.red[tot + threadIdx.x] = qsum(f.part_sc + threadIdx.x, kNumScalars, 0, f.nb);
+        if (i < tot) part[grp * cols + cl] = qsum(f.part_acc + i, (size_t)tot, f.nb * grp / ng, f.nb * (grp + 1) / ng);
+        if (blockIdx.x == 0) {  // each scalar by one warp: lanes split the CTAs, fixed-order combine
+            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+            for (int sidx = w; sidx < nsc; sidx += kFinThreads / 32) {
+                double v = 0.0;
+                for (int b = lane; b < f.nb; b += 32) v += f.part_sc[(size_t)b * kNumScalars + sidx];
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) f.red[tot + sidx] = v;
+            }
+        }
         __syncthreads();
-        if (grp == 0 && i < tot) f.red[i] = ((part[0][cl] + part[1][cl]) + part[2][cl]) + part[3][cl];
+        if (grp == 0 && i < tot) {
+            double v = part[cl];
+            for (int q = 1; q < ng; ++q) v += part[q * cols + cl];
+            f.red[i] = v;
+        }
         __syncthreads();
     }
     if (!f.do_epi) return;
@@ -576,24 +592,25 @@ static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO
         f.sc = slot->sc;
     }
     const int tot = std::max(f.k, 1) * f.ld;
-    const int fb = std::max(1, (tot + kFinCols - 1) / kFinCols);
+    const int ng = nb >= 512 ? 32 : nb >= 128 ? 8 : 4;
+    const int fb = std::max(1, (tot + kFinThreads / ng - 1) / (kFinThreads / ng));
     if (!ctx->comm) {
         f.do_reduce = 1;
         f.do_epi = 1;
         // scalars are reduced by block 0 and consumed by block 0 only
-        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
+        finish_kernel<<<fb, kFinThreads, 0, ctx->stream>>>(f, ng);
         MVSK_CUDA(cudaGetLastError());
     } else {
         f.do_reduce = 1;
         f.do_epi = 0;
-        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
+        finish_kernel<<<fb, kFinThreads, 0, ctx->stream>>>(f, ng);
         MVSK_CUDA(cudaGetLastError());
         const int nsc = op == Op::FGRAD ? 3 : (op == Op::LINESUMS ? 9 : 0);
         const size_t cnt = (size_t)(op == Op::LINESUMS ? 0 : tot) + nsc;
         MVSK_NCCL(ncclAllReduce(ctx->red, ctx->red, cnt, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
         f.do_reduce = 0;
         f.do_epi = 1;
-        finish_kernel<<<fb, 256, 0, ctx->stream>>>(f);
+        finish_kernel<<<fb, kFinThreads, 0, ctx->stream>>>(f, ng);
         MVSK_CUDA(cudaGetLastError());
     }
 }
