@@ -155,7 +155,8 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     const size_t row_bytes = (size_t)ctx->ld * sizeof(double);
     const size_t stage_target = 64 * 1024;
     // teams per CTA (each team streams its own rows)
-    int G = small ? std::max(1, std::min(4, max_threads(op, K, Q, 1) / P)) : std::max(1, max_threads(op, K, Q, 1) / P);
+    int G = small ? std::max(1, std::min(std::max(4, 32 / P), max_threads(op, K, Q, 1) / P))
+                  : std::max(1, max_threads(op, K, Q, 1) / P);
     const long long want_rows = std::max<long long>(1, (long long)(stage_target / row_bytes));
     while (G > 1 && G > want_rows) G >>= 1;
     int RG = 1;

@@ -377,10 +377,10 @@ __global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG>::max_threads, 1) stre
 #pragma unroll
             for (int i = 0; i < NS; ++i) scb[g * NS + i] = sc[i];
         __syncthreads();
-        if (tid < NS) {
+        for (int i = tid; i < NS; i += blockDim.x) {  // tiny CTAs may have < NS threads
             double v = 0.0;
-            for (int gg = 0; gg < G; ++gg) v += scb[gg * NS + tid];
-            a.part_sc[(size_t)blockIdx.x * kNumScalars + tid] = v;
+            for (int gg = 0; gg < G; ++gg) v += scb[gg * NS + i];
+            a.part_sc[(size_t)blockIdx.x * kNumScalars + i] = v;
         }
     }
 }
