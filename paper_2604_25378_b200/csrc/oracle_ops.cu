@@ -14,9 +14,6 @@ namespace mvsk_b200 {
 
 namespace {
 
-constexpr int kMaxTeam = 512;       // threads per CTA (launch bound)
-constexpr size_t kStageTarget = 32 * 1024;
-constexpr size_t kRingTarget = 160 * 1024;
 
 struct Plan {
     int Q = 1, P = 32, G = 1, RG = 1, S = 2;

@@ -59,11 +59,6 @@ __device__ __forceinline__ bool pass_skipped(const int* skip, int nskip) {
     return any == 0;
 }
 
-template <int K>
-struct OpWidth {
-    static constexpr int value = K;
-};
-
 // number of dot products per row and accumulator sets per op
 template <Op OP, int K>
 struct OpShape {
@@ -72,7 +67,6 @@ struct OpShape {
                                 : (OP == Op::XTW)                       ? 0
                                                                         : K;
     static constexpr int NACC = (OP == Op::LINESUMS) ? 0 : (OP == Op::HVP || OP == Op::THIRD) ? K : 1;
-    static constexpr int NVEC = NDOT;  // input vectors held in registers
 };
 
 // fp64 values a thread keeps live across a stage: input vectors, accumulators
