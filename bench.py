@@ -339,6 +339,15 @@ def main():
         gram_ms = timed(lambda: gpu.weighted_gram_device(0, G.data_ptr()), 1, 1)
         extra["gram_ms"] = gram_ms
         extra["gram_tflops"] = (T * n * (n + 1.0)) / (gram_ms * 1e-3) / 1e12
+        try:  # fp64 tensor-pipe peak measured on this pool (profiles/r01_fp64_peak.json)
+            pk = json.loads((ROOT / "profiles" / "r01_fp64_peak.json").read_text())["dmma_tflops"]
+            extra["gram_roofline"] = {"bound": "tensor", "achieved": extra["gram_tflops"], "peak": pk,
+                                      "unit": "TFLOP/s", "frac": extra["gram_tflops"] / pk,
+                                      "flops_per_launch": T * n * (n + 1.0)}
+        except Exception:
+            pass
+        # 8-RHS HVP: 4*T*n*k flop on the fp64 tensor pipe vs one HBM read of X
+        extra["hvp8_tflops"] = 4.0 * T * n * 8 / (extra["hvp8_ms"] * 1e-3) / 1e12
         del G
 
     # ---- e2e through the host-pointer C-ABI (pinned staging inside), per step: H2D v, D2H Hv
