@@ -107,3 +107,16 @@ def test_binary_panel_header_validation(tmp_path):
         binary_dims(degen)
     with pytest.raises(DataError):
         binary_dims(tmp_path / "missing.bin")
+
+
+def test_cpp_host_example_builds_and_validates_arguments():
+    """examples/mvsk_gpu_solve: a C++ host linked only against the C-ABI."""
+    exe = ROOT / "examples" / "_bin" / "mvsk_gpu_solve"
+    if not exe.exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT / "examples")], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 2 and "usage" in r.stderr
+    r = subprocess.run([str(exe), "/nonexistent.bin", "--gamma", "5"], capture_output=True, text=True)
+    assert r.returncode == 1 and "cannot open" in r.stderr  # data_error -> exit 1 (mvsk_main.cpp:213-219)
+    r = subprocess.run([str(exe), "x.bin", "--preset", "medium"], capture_output=True, text=True)
+    assert r.returncode == 2

@@ -238,3 +238,33 @@ def test_device_pcg_matches_host_pcg(monkeypatch):
     gc = g.make_cache(xf[idx])
     dh, _ = g.yand_direction(gc, tangent_config("pcg", lam=1e-4), 3)
     assert np.max(np.abs(dd - dh)) <= 1e-8 * (1 + np.max(np.abs(dh)))
+
+
+def test_cpp_host_solves_a_binary_panel(tmp_path):
+    """examples/mvsk_gpu_solve (C++ over the C-ABI only) on a raw-returns panel
+    file: same status / objective / active set as the CPU oracle solve."""
+    import json
+    import subprocess
+    from pathlib import Path
+    from paper_2604_25378_b200.datagen import CONFIGS, crra, raw_returns
+    from paper_2604_25378_b200.gpu_oracle import save_returns_binary
+    root = Path(__file__).resolve().parent.parent
+    exe = root / "examples" / "_bin" / "mvsk_gpu_solve"
+    R = raw_returns(CONFIGS["C2"], 21).numpy()
+    path = tmp_path / "c2.bin"
+    save_returns_binary(path, R)
+    r = subprocess.run([str(exe), str(path), "--gamma", "10", "--preset", "large", "--epsilon", "1e-10",
+                        "--no-max-elapsed"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    rep = json.loads(r.stdout)
+    assert rep["status"] == "converged" and rep["config"] == "large" and len(rep["x_star"]) == 100
+    A, mu = po.center_panel(R)
+    cfg = po.preset("large")
+    cfg.has_max_elapsed = 0
+    cfg.epsilon = 1e-10
+    xc, rc = po.solve(A, mu, crra(10.0), cfg)
+    xg = np.array(rep["x_star"])
+    assert rc.status == 0
+    assert abs(rep["f_star"] - rc.f_star) <= 1e-12 * (1 + abs(rc.f_star))
+    assert _active(xg, 1e-8) == _active(xc, 1e-8)
+    assert np.max(np.abs(xg - xc)) <= 1e-7
