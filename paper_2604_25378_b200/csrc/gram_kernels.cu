@@ -239,11 +239,7 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
     a.nsplit = nsplit;
     a.part = ctx->gram_part;
     const size_t smem = (size_t)(2 * GST * GBK * GLDS + GST * GBK) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        MVSK_CUDA(cudaFuncSetAttribute(syrk_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    set_smem_attr(reinterpret_cast<const void*>(&syrk_dmma_kernel), smem);
     syrk_dmma_kernel<<<dim3(npairs, nsplit), GTHREADS, smem, ctx->stream>>>(a);
     MVSK_CUDA(cudaGetLastError());
     gram_finish_kernel<<<npairs, 256, 0, ctx->stream>>>(ctx->gram_part, npairs, nsplit, n, scale, G_dev, n);
@@ -259,8 +255,7 @@ void run_quadform(mvsk_gpu_ctx* ctx, const double* P_dev, double* q_dev) {
     if (T <= 0) return;
     const int nb = (int)((T + RB - 1) / RB);
     const size_t smem = (size_t)RB * ctx->ld * sizeof(double);
-    if (smem > 48 * 1024)
-        MVSK_CUDA(cudaFuncSetAttribute(quadform_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(&quadform_kernel<RB>), smem);
     quadform_kernel<RB><<<nb, 256, smem, ctx->stream>>>(ctx->X, T, (int)ctx->ld, P_dev, q_dev);
     MVSK_CUDA(cudaGetLastError());
 }

@@ -491,23 +491,6 @@ __global__ void psi2_kernel(const double* z, double* out, long long T, double c2
     }
 }
 
-std::mutex g_attr_mu;
-
-// cudaFuncSetAttribute once per (kernel, size): it is a driver call, not free
-void set_smem_attr(const void* fn, size_t smem) {
-    static std::vector<std::pair<const void*, size_t>> done;
-    std::lock_guard<std::mutex> lk(g_attr_mu);
-    for (auto& d : done)
-        if (d.first == fn) {
-            if (d.second >= smem) return;
-            MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            d.second = smem;
-            return;
-        }
-    MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    done.emplace_back(fn, smem);
-}
-
 void ensure_part(mvsk_gpu_ctx* ctx, size_t elems) {
     if (ctx->part_acc_elems >= elems) return;
     if (ctx->part_acc) MVSK_CUDA(cudaFree(ctx->part_acc));
@@ -517,6 +500,33 @@ void ensure_part(mvsk_gpu_ctx* ctx, size_t elems) {
 }
 
 }  // namespace
+
+namespace {
+std::mutex g_attr_mu;
+}
+
+// cudaFuncSetAttribute once per (device, kernel, size): a driver call, not free,
+// and per-device (one process may drive several GPUs)
+void set_smem_attr(const void* fn, size_t smem) {
+    struct Entry {
+        int dev;
+        const void* fn;
+        size_t smem;
+    };
+    static std::vector<Entry> done;
+    int dev = 0;
+    MVSK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    for (auto& d : done)
+        if (d.dev == dev && d.fn == fn) {
+            if (d.smem >= smem) return;
+            MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            d.smem = smem;
+            return;
+        }
+    MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done.push_back({dev, fn, smem});
+}
 
 void ensure_host_staging(mvsk_gpu_ctx* ctx, size_t elems) {
     if (ctx->h_elems >= elems) return;

@@ -40,6 +40,9 @@ void run_quadform(mvsk_gpu_ctx* ctx, const double* P_dev, double* q_dev);
 // tw_t = psi3(z_t) q_t / T with psi3 the third derivative weight
 void run_third_weights(mvsk_gpu_ctx* ctx, const double* z, const double* q, double* tw);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size)
+void set_smem_attr(const void* fn, size_t smem);
+
 // device scratch sizing (grows workspaces on demand)
 void ensure_host_staging(mvsk_gpu_ctx* ctx, size_t elems);
 

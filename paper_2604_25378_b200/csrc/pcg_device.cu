@@ -288,12 +288,8 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     if (fm.active) MVSK_CUDA(cudaMemcpyAsync(idx, fm.idx.data(), m * sizeof(long long), cudaMemcpyHostToDevice, st));
     Geo g{vU, in.bU, vQ, in.bQ, fm.active ? idx : nullptr, m, (int)ld};
     const size_t dsm = (size_t)2 * std::max(m, 1) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        for (const void* fn : {(const void*)lift_kernel, (const void*)cg_step_kernel, (const void*)reduce_kernel})
-            MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024 * 2));
-        attr = true;
-    }
+    for (const void* fn : {(const void*)lift_kernel, (const void*)cg_step_kernel, (const void*)reduce_kernel})
+        set_smem_attr(fn, dsm);
     const Slot& sl = ctx->slots[slot];
     double* vin = ctx->vin;
     double* vin2 = ctx->vin + (size_t)MVSK_GPU_MAX_RHS * ld;

@@ -302,3 +302,51 @@ def test_binary_ingest_matches_host_centering(tmp_path):
     save_returns_binary(path, R)
     with pytest.raises(DataError):
         GpuOracle.from_binary(path, c)
+
+
+@pytest.mark.parametrize("n,T", [(8192, 64), (8190, 3), (2, 2), (3, 1000), (1, 2)])
+def test_edge_shapes(n, T):
+    """Widest supported rows (n = 8192), odd n, the minimum T = 2, a tall-thin
+    panel and n = 1: parity with the CPU oracle for f, g and a 3-RHS HVP."""
+    rng = np.random.default_rng(n * 7 + T)
+    A = rng.uniform(-0.1, 0.4, (T, n))
+    A -= A.mean(axis=0)
+    mu = rng.uniform(0, 5e-4, n)
+    c = rh.crra(10.0)
+    x = rng.exponential(size=n)
+    x /= x.sum()
+    V = rng.standard_normal((3, n))
+    cpu, gpu = po.CpuOracle(A, mu, c), _gpu(A, mu, c)
+    cc, gc = cpu.make_cache(x), gpu.make_cache(x)
+    _close(gpu.value(gc), cpu.value(cc))
+    z = A @ x
+    _close(gpu.gradient(gc), cpu.gradient(cc), _absscale(A, (2 * c[1] * z - 3 * c[2] * z * z + 4 * c[3] * z ** 3) / T))
+    H = gpu.hvp(gc, V)
+    psi2 = 2 * c[1] - 6 * c[2] * z + 12 * c[3] * z * z
+    for i in range(3):
+        _close(H[i], cpu.hvp(cc, V[i]), _absscale(A, psi2 * (A @ V[i]) / T))
+
+
+def test_contract_violations():
+    """Typed errors at the boundary: too-wide rows, RHS count, slots, faces."""
+    from paper_2604_25378_b200.gpu_oracle import DimensionError, DomainError
+    A, mu = rh.lcg_panel(6, 20, 3)
+    g = _gpu(A, mu, rh.crra(4.0))
+    cache = g.make_cache(rh.simplex_point(6, 1))
+    with pytest.raises(DimensionError):
+        g.hvp(cache, np.ones((17, 6)))  # > MVSK_GPU_MAX_RHS
+    with pytest.raises(DomainError):
+        g.make_cache(rh.simplex_point(6, 1), slot=8)
+    with pytest.raises(DomainError):
+        g.set_face(np.array([3, 1]), 1e-8)  # not increasing
+    with pytest.raises(DomainError):
+        g.set_face(np.array([], dtype=np.int64), 1e-8)  # degenerate face
+    g.set_face(np.array([0, 2, 5]), 1e-8)
+    with pytest.raises(DomainError):  # slots were invalidated by the face change
+        g.gradient(cache)
+    wide = np.zeros((2, 8200))
+    with pytest.raises(DimensionError):
+        gw = _gpu(wide, np.zeros(8200), rh.crra(2.0))
+        gw.make_cache(np.full(8200, 1 / 8200))
+    H16 = g.hvp(g.make_cache(np.array([0.4, 0.3, 0.3])), np.ones((16, 3)) * np.array([1.0, -1.0, 0.0]))
+    assert H16.shape == (16, 3) and np.all(H16 == H16[0])
