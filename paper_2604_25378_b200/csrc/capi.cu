@@ -72,6 +72,8 @@ void free_all(mvsk_gpu_ctx* ctx) {
     }
     if (ctx->h_in) cudaFreeHost(ctx->h_in);
     if (ctx->h_out) cudaFreeHost(ctx->h_out);
+    for (auto& g : ctx->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     pcg_workspace_free(ctx);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -304,6 +306,7 @@ int32_t mvsk_gpu_set_offset(mvsk_gpu_ctx* ctx, const double* zoff, double value_
             ctx->zoff_dev = nullptr;
         }
         ctx->value_offset = value_offset;
+        ++ctx->epoch;  // the z offset pointer / value offset are baked into captured passes
         for (auto& s : ctx->slots) s.valid = false;
     });
 }

@@ -109,4 +109,16 @@ struct mvsk_gpu_ctx {
 
     uint64_t fwd = 0, tr = 0, phys = 0;
     std::string err;
+
+    // host-API ops replayed as CUDA graphs (host_ops.cu); entries are dropped
+    // whenever a captured device/pinned buffer may have moved (epoch)
+    struct GraphEntry {
+        int op, k, slot;
+        uint64_t epoch;
+        cudaGraphExec_t exec;
+        uint64_t phys;  // physical passes one replay performs
+        bool ok;
+    };
+    std::vector<GraphEntry> graphs;
+    uint64_t epoch = 0;
 };

@@ -229,6 +229,7 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
         ctx->gram_part = nullptr;
         MVSK_CUDA(cudaMalloc(&ctx->gram_part, need * sizeof(double)));
         ctx->gram_part_elems = need;
+        ++ctx->epoch;
     }
     GramArgs a{};
     a.X = ctx->X;

@@ -6,7 +6,9 @@
 // counted by run_pass.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 
 #include "host_ops.hpp"
 
@@ -59,12 +61,93 @@ void stage_in(mvsk_gpu_ctx* ctx, const FaceMap& fm, const double* V, int k, doub
                               cudaMemcpyHostToDevice, ctx->stream));
 }
 
+// split form of stage_in / fetch_out for graph capture: the host-side scatter /
+// gather stays outside the graph, the pinned<->device copies go inside
+void stage_host(mvsk_gpu_ctx* ctx, const FaceMap& fm, const double* V, int k, double fill, size_t base) {
+    const size_t ld = (size_t)ctx->ld;
+    for (int i = 0; i < k; ++i) to_full(ctx, fm, V + (size_t)i * fm.m, fill, ctx->h_in + (base + i) * ld);
+}
+void copy_in(mvsk_gpu_ctx* ctx, int k, size_t base) {
+    const size_t ld = (size_t)ctx->ld;
+    MVSK_CUDA(cudaMemcpyAsync(ctx->vin + base * ld, ctx->h_in + base * ld, (size_t)k * ld * sizeof(double),
+                              cudaMemcpyHostToDevice, ctx->stream));
+}
+void copy_out(mvsk_gpu_ctx* ctx, const double* dev, int k, long long stride_dev) {
+    MVSK_CUDA(cudaMemcpyAsync(ctx->h_out, dev, (size_t)k * stride_dev * sizeof(double), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+}
+void finish_out(mvsk_gpu_ctx* ctx, const FaceMap& fm, int k, long long stride_dev, double* out) {
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < k; ++i) from_full(ctx, fm, ctx->h_out + (size_t)i * stride_dev, out + (size_t)i * fm.m);
+}
+
 void fetch_out(mvsk_gpu_ctx* ctx, const FaceMap& fm, const double* dev, int k, long long stride_dev, double* out) {
     ensure_host_staging(ctx, (size_t)k * stride_dev);
     MVSK_CUDA(cudaMemcpyAsync(ctx->h_out, dev, (size_t)k * stride_dev * sizeof(double), cudaMemcpyDeviceToHost,
                               ctx->stream));
     MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int i = 0; i < k; ++i) from_full(ctx, fm, ctx->h_out + (size_t)i * stride_dev, out + (size_t)i * fm.m);
+}
+
+// Runs the device part of a host-API op (H2D of the staged inputs, the fused
+// pass(es), reduction/epilogue, D2H of the results) as ONE CUDA graph launch.
+// The first call of a (op, k, slot) key runs eagerly (it also sizes every
+// workspace); the second captures the same enqueue sequence; later calls replay
+// it. A replay is valid while no captured buffer moved (ctx->epoch). Plans are
+// deterministic functions of the shapes, so replays compute the same bits as
+// eager launches.
+void run_graphed(mvsk_gpu_ctx* ctx, int op, int k, int slot, const std::function<void()>& enqueue) {
+    static const bool disabled = std::getenv("MVSK_NO_GRAPHS") != nullptr;
+    mvsk_gpu_ctx::GraphEntry* e = nullptr;
+    for (auto& g : ctx->graphs)
+        if (g.op == op && g.k == k && g.slot == slot) e = &g;
+    if (disabled || !e) {
+        enqueue();
+        if (!disabled) ctx->graphs.push_back({op, k, slot, ctx->epoch, nullptr, 0, true});
+        return;
+    }
+    if (e->exec && e->epoch == ctx->epoch) {
+        MVSK_CUDA(cudaGraphLaunch(e->exec, ctx->stream));
+        ctx->phys += e->phys;
+        return;
+    }
+    if (!e->ok || e->epoch != ctx->epoch) {  // buffers moved since: run eagerly once more
+        if (e->exec) cudaGraphExecDestroy(e->exec);
+        e->exec = nullptr;
+        e->ok = true;
+        e->epoch = ctx->epoch;
+        enqueue();
+        return;
+    }
+    // capture
+    const uint64_t p0 = ctx->phys;
+    const uint64_t ep0 = ctx->epoch;
+    cudaGraph_t graph = nullptr;
+    MVSK_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    bool threw = false;
+    try {
+        enqueue();
+    } catch (...) {
+        threw = true;
+    }
+    const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+    cudaGetLastError();
+    cudaGraphExec_t exec = nullptr;
+    if (!threw && ce == cudaSuccess && graph && ctx->epoch == ep0 &&
+        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+        e->exec = exec;
+        e->phys = ctx->phys - p0;
+        ctx->phys = p0;
+        if (graph) cudaGraphDestroy(graph);
+        MVSK_CUDA(cudaGraphLaunch(exec, ctx->stream));
+        ctx->phys += e->phys;
+        return;
+    }
+    cudaGetLastError();
+    if (graph) cudaGraphDestroy(graph);
+    ctx->phys = p0;
+    e->ok = false;  // not capturable here: stay eager
+    enqueue();
 }
 
 void ensure_tvec2(mvsk_gpu_ctx* ctx) {
@@ -78,20 +161,23 @@ double op_make_cache(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const doubl
     Slot& s = ctx->slots[slot];
     s.valid = false;
     s.g_host_valid = false;
-    stage_in(ctx, fm, x, 1, fm.tau, 0);
+    ensure_host_staging(ctx, std::max<size_t>((size_t)ctx->ld + 8, (size_t)MVSK_GPU_MAX_RHS * 2 * ctx->ld));
+    stage_host(ctx, fm, x, 1, fm.tau, 0);
     s.x_full.assign(ctx->h_in, ctx->h_in + ctx->ld);
-    PassIO io;
-    io.vin = ctx->vin;
-    io.slot = slot;
-    io.x_for_mux = ctx->vin;
-    run_pass(ctx, Op::FGRAD, 1, io);
-    ctx->fwd += 1;  // oracle.hpp:127
-    // scalars and the gradient come back in the same round trip (the gradient
-    // is almost always requested next: oracle.hpp:79, solver.hpp:378-379)
-    ensure_host_staging(ctx, (size_t)ctx->ld + 8);
     double* h = ctx->h_out;
-    MVSK_CUDA(cudaMemcpyAsync(h, s.sc, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    MVSK_CUDA(cudaMemcpyAsync(h + 8, s.g, ctx->ld * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    run_graphed(ctx, (int)Op::FGRAD, 1, slot, [&] {
+        copy_in(ctx, 1, 0);
+        PassIO io;
+        io.vin = ctx->vin;
+        io.slot = slot;
+        io.x_for_mux = ctx->vin;
+        run_pass(ctx, Op::FGRAD, 1, io);
+        // scalars and the gradient come back in the same round trip (the gradient
+        // is almost always requested next: oracle.hpp:79, solver.hpp:378-379)
+        MVSK_CUDA(cudaMemcpyAsync(h, s.sc, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        MVSK_CUDA(cudaMemcpyAsync(h + 8, s.g, ctx->ld * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    });
+    ctx->fwd += 1;  // oracle.hpp:127
     MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
     s.f = h[0];
     for (int i = 0; i < 4; ++i) s.mom[i] = h[1 + i];
@@ -147,34 +233,45 @@ void op_gradient(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, double* g) {
 void op_hvp(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* V, int k, double* HV) {
     check_slot(ctx, slot);
     if (k < 1 || k > MVSK_GPU_MAX_RHS) throw ApiError(MVSK_DIMENSION_ERROR, "hvp: k out of range");
-    stage_in(ctx, fm, V, k, 0.0, 0);
-    PassIO io;
-    io.vin = ctx->vin;
-    io.z = ctx->slots[slot].z;
-    io.out = ctx->outd;
-    io.ldo = ctx->ld;
-    run_pass(ctx, Op::HVP, k, io);
+    ensure_host_staging(ctx, (size_t)MVSK_GPU_MAX_RHS * 2 * ctx->ld);
+    stage_host(ctx, fm, V, k, 0.0, 0);
+    run_graphed(ctx, (int)Op::HVP, k, slot, [&] {
+        copy_in(ctx, k, 0);
+        PassIO io;
+        io.vin = ctx->vin;
+        io.z = ctx->slots[slot].z;
+        io.out = ctx->outd;
+        io.ldo = ctx->ld;
+        run_pass(ctx, Op::HVP, k, io);
+        copy_out(ctx, ctx->outd, k, ctx->ld);
+    });
     ctx->fwd += k;  // oracle.hpp:134
     ctx->tr += k;   // oracle.hpp:138
-    fetch_out(ctx, fm, ctx->outd, k, ctx->ld, HV);
+    finish_out(ctx, fm, k, ctx->ld, HV);
     if (!finite(HV, (long long)k * fm.m)) throw ApiError(MVSK_NUMERIC_ERROR, "oracle: non-finite Hessian product");
 }
 
 void op_third(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* U, const double* V, int k, double* out) {
     check_slot(ctx, slot);
     if (k < 1 || k > MVSK_GPU_MAX_RHS) throw ApiError(MVSK_DIMENSION_ERROR, "third_action: k out of range");
-    stage_in(ctx, fm, U, k, 0.0, 0);
-    stage_in(ctx, fm, V, k, 0.0, MVSK_GPU_MAX_RHS);
-    PassIO io;
-    io.vin = ctx->vin;
-    io.vin2 = ctx->vin + (size_t)MVSK_GPU_MAX_RHS * ctx->ld;
-    io.z = ctx->slots[slot].z;
-    io.out = ctx->outd;
-    io.ldo = ctx->ld;
-    run_pass(ctx, Op::THIRD, k, io);
+    ensure_host_staging(ctx, (size_t)MVSK_GPU_MAX_RHS * 2 * ctx->ld);
+    stage_host(ctx, fm, U, k, 0.0, 0);
+    stage_host(ctx, fm, V, k, 0.0, MVSK_GPU_MAX_RHS);
+    run_graphed(ctx, (int)Op::THIRD, k, slot, [&] {
+        copy_in(ctx, k, 0);
+        copy_in(ctx, k, MVSK_GPU_MAX_RHS);
+        PassIO io;
+        io.vin = ctx->vin;
+        io.vin2 = ctx->vin + (size_t)MVSK_GPU_MAX_RHS * ctx->ld;
+        io.z = ctx->slots[slot].z;
+        io.out = ctx->outd;
+        io.ldo = ctx->ld;
+        run_pass(ctx, Op::THIRD, k, io);
+        copy_out(ctx, ctx->outd, k, ctx->ld);
+    });
     ctx->fwd += 2 * k;
     ctx->tr += k;
-    fetch_out(ctx, fm, ctx->outd, k, ctx->ld, out);
+    finish_out(ctx, fm, k, ctx->ld, out);
     if (!finite(out, (long long)k * fm.m)) throw ApiError(MVSK_NUMERIC_ERROR, "oracle: non-finite third-order action");
 }
 
@@ -211,16 +308,21 @@ void op_line_model(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double*
     const double dn = std::sqrt(dn2);
     if (!(dn > 0)) throw ApiError(MVSK_DOMAIN_ERROR, "line_model: zero direction");
     if (std::abs(dsum) > 1e-10 * dn) throw ApiError(MVSK_DOMAIN_ERROR, "line_model: direction is not tangent to the simplex");
-    stage_in(ctx, fm, d, 1, 0.0, 0);
-    PassIO io;
-    io.vin = ctx->vin;
-    io.z = ctx->slots[slot].z;
-    io.out = ctx->outd;
-    run_pass(ctx, Op::LINESUMS, 1, io);
+    ensure_host_staging(ctx, (size_t)MVSK_GPU_MAX_RHS * 2 * ctx->ld);
+    stage_host(ctx, fm, d, 1, 0.0, 0);
+    run_graphed(ctx, (int)Op::LINESUMS, 1, slot, [&] {
+        copy_in(ctx, 1, 0);
+        PassIO io;
+        io.vin = ctx->vin;
+        io.z = ctx->slots[slot].z;
+        io.out = ctx->outd;
+        run_pass(ctx, Op::LINESUMS, 1, io);
+        copy_out(ctx, ctx->outd, 1, 9);
+    });
     ctx->fwd += 1;
-    double s[9];
-    MVSK_CUDA(cudaMemcpyAsync(s, ctx->outd, 9 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+    double s[9];
+    std::memcpy(s, ctx->h_out, sizeof(s));
     double mud = 0.0;  // mu_f' d_f
     for (long long j = 0; j < m; ++j) mud += ctx->mu[fm.active ? fm.idx[j] : j] * d[j];
     const mvsk_coeffs& c = ctx->c;

@@ -60,6 +60,7 @@ const void* select_kernel(Op op, int K, int Q, int RG) {
         } else if (K == 2) {
             MVSK_QRG(Op::HVP, 2)
             if (Q == 8 && RG == 1) return kfn<Op::HVP, 2, 8, 1>();
+            if (Q == 8 && RG == 2) return kfn<Op::HVP, 2, 8, 2>();
         } else if (K == 4) {
             if (Q == 1 && RG == 1) return kfn<Op::HVP, 4, 1, 1>();
             if (Q == 1 && RG == 2) return kfn<Op::HVP, 4, 1, 2>();
@@ -70,6 +71,7 @@ const void* select_kernel(Op op, int K, int Q, int RG) {
         if (K == 1) {
             MVSK_QRG(Op::THIRD, 1)
             if (Q == 8 && RG == 1) return kfn<Op::THIRD, 1, 8, 1>();
+            if (Q == 8 && RG == 2) return kfn<Op::THIRD, 1, 8, 2>();
         }
         break;
     }
@@ -160,8 +162,16 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     while (!small && RG < 4 && RG * 2 * Q <= 8 && (long long)G * RG * 2 <= want_rows &&
            G * P <= max_threads(op, K, Q, RG * 2))
         RG <<= 1;
+    // a heavy op whose team fills the CTA (THIRD, 2-RHS HVP at n=4096) would
+    // otherwise keep one row in flight per CTA and expose the per-row reduction
+    // latency (C5 third: 8 warps/SM, 'wait' + short-scoreboard stalls); two rows
+    // per team interleave two independent chains
+    if (!small && G == 1 && RG == 1 && Q == 8 && P <= max_threads(op, K, Q, 2) &&
+        select_kernel(op, K, Q, 2) != nullptr && want_rows >= 2)
+        RG = 2;
     if (tov.G > 0 && tov.G * P <= max_threads(op, K, Q, RG)) G = tov.G;
-    if (tov.RG > 0 && tov.RG * Q <= 8 && G * P <= max_threads(op, K, Q, tov.RG)) RG = tov.RG;
+    if (tov.RG > 0 && (tov.RG * Q <= 8 || select_kernel(op, K, Q, tov.RG)) && G * P <= max_threads(op, K, Q, tov.RG))
+        RG = tov.RG;
     if (op == Op::HVP && K == 4 && Q == 2) RG = 1;
     if (G * P > max_threads(op, K, Q, RG)) return false;
     const long long R = (long long)G * RG;
@@ -497,6 +507,7 @@ void ensure_part(mvsk_gpu_ctx* ctx, size_t elems) {
     ctx->part_acc = nullptr;
     MVSK_CUDA(cudaMalloc(&ctx->part_acc, elems * sizeof(double)));
     ctx->part_acc_elems = elems;
+    ++ctx->epoch;
 }
 
 }  // namespace
@@ -536,6 +547,7 @@ void ensure_host_staging(mvsk_gpu_ctx* ctx, size_t elems) {
     MVSK_CUDA(cudaMallocHost(&ctx->h_in, elems * sizeof(double)));
     MVSK_CUDA(cudaMallocHost(&ctx->h_out, elems * sizeof(double)));
     ctx->h_elems = elems;
+    ++ctx->epoch;
 }
 
 static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io);

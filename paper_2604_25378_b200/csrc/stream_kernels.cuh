@@ -223,15 +223,24 @@ __global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG>::max_threads, 1) stre
                 dot[rr][k] = d0 + d1;
             }
         if constexpr (NDOT > 0) {
-            const int width = P < 32 ? P : 32;
+            if (P >= 32) {
+                // full-warp butterfly, unrolled so the RG x NDOT chains interleave
 #pragma unroll
-            for (int rr = 0; rr < RG; ++rr)
+                for (int o = 16; o >= 1; o >>= 1)
 #pragma unroll
-                for (int k = 0; k < NDOT; ++k) {
-                    double d = dot[rr][k];
-                    for (int o = width >> 1; o >= 1; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o, width);
-                    dot[rr][k] = d;
-                }
+                    for (int rr = 0; rr < RG; ++rr)
+#pragma unroll
+                        for (int k = 0; k < NDOT; ++k) dot[rr][k] += __shfl_xor_sync(0xffffffffu, dot[rr][k], o);
+            } else {
+#pragma unroll
+                for (int rr = 0; rr < RG; ++rr)
+#pragma unroll
+                    for (int k = 0; k < NDOT; ++k) {
+                        double d = dot[rr][k];
+                        for (int o = P >> 1; o >= 1; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o, P);
+                        dot[rr][k] = d;
+                    }
+            }
             if (P > 32 && lane == 0) {
                 double* rb = red + (size_t)(s & 1) * R * NDOT * nwp;
 #pragma unroll
@@ -257,10 +266,17 @@ __global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG>::max_threads, 1) stre
                 for (int rr = 0; rr < RG; ++rr)
 #pragma unroll
                     for (int k = 0; k < NDOT; ++k) {
+                        // fixed-order pairwise combine of the team's warp partials
+                        // (two independent chains instead of one serial one)
                         const double* src = rb + ((g * RG + rr) * NDOT + k) * nwp;
-                        double d = 0.0;
-                        for (int w = 0; w < nwp; ++w) d += src[w];
-                        dot[rr][k] = d;
+                        double d0 = 0.0, d1 = 0.0;
+                        int w = 0;
+                        for (; w + 1 < nwp; w += 2) {
+                            d0 += src[w];
+                            d1 += src[w + 1];
+                        }
+                        if (w < nwp) d0 += src[w];
+                        dot[rr][k] = d0 + d1;
                     }
             }
         }

@@ -28,6 +28,7 @@ fn = {
     "hvp4": lambda: gpu.hvp_device(0, Vd.data_ptr(), 4, out.data_ptr()),
     "hvp8": lambda: gpu.hvp_device(0, Vd.data_ptr(), 8, out.data_ptr()),
     "third8": lambda: gpu.third_action_device(0, Vd.data_ptr(), Vd.data_ptr(), 8, out.data_ptr()),
+    "third": lambda: gpu.third_action_device(0, Vd.data_ptr(), Vd[1:].data_ptr(), 1, out.data_ptr()),
     "gram": lambda: gpu.weighted_gram_device(0, G.data_ptr()),
 }[op]
 for _ in range(reps):

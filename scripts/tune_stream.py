@@ -79,8 +79,10 @@ for op in ops:
     os.environ.pop("MVSK_TUNE", None)
     base = timeit(FN[op])
     print(f"{cfg} {op} default: {base:.4f} ms  {alg / base / 1e6:.0f} GB/s", flush=True)
+    if os.environ.get("TUNE_DEFAULT_ONLY"):
+        continue
     for Q, G, RG, S, OCC in itertools.product([2, 4, 8], [1, 2, 4], [1, 2, 4], [2, 3, 4, 6], [1, 2]):
-        if RG * Q > 8:
+        if RG * Q > 8 and not (Q == 8 and RG == 2 and G == 1):
             continue
         os.environ["MVSK_TUNE"] = f"{Q},{G},{RG},{S},{OCC}"
         try:

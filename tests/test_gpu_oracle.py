@@ -350,3 +350,43 @@ def test_contract_violations():
         gw.make_cache(np.full(8200, 1 / 8200))
     H16 = g.hvp(g.make_cache(np.array([0.4, 0.3, 0.3])), np.ones((16, 3)) * np.array([1.0, -1.0, 0.0]))
     assert H16.shape == (16, 3) and np.all(H16 == H16[0])
+
+
+def test_graph_replay_tracks_inputs_and_offsets():
+    """Host-API ops are replayed as CUDA graphs from their third call on
+    (host_ops.cu run_graphed). Every replay must see the new inputs, and a
+    set_offset (which moves/changes buffers baked into the graph) must
+    invalidate the captured graphs."""
+    A, mu = rh.lcg_panel(24, 300, 17)
+    c = rh.crra(8.0)
+    T, n = A.shape
+    cpu = po.CpuOracle(A, mu, c)
+    gpu = _gpu(A, mu, c)
+    rng = np.random.default_rng(3)
+    for it in range(6):
+        x = rng.dirichlet(np.ones(n))
+        gc, cc = gpu.make_cache(x), cpu.make_cache(x)
+        assert abs(gpu.value(gc) - cpu.value(cc)) <= 1e-12 * (1 + abs(cpu.value(cc)))
+        _close(gpu.gradient(gc), cpu.gradient(cc))
+        V = rng.standard_normal((3, n))
+        H = gpu.hvp(gc, V)
+        for i in range(3):
+            _close(H[i], cpu.hvp(cc, V[i]))
+        d = rng.standard_normal(n)
+        d -= d.mean()
+        cap = po.alpha_max(x, d, 0.0)
+        mg, mc = gpu.line_model(gc, d, cap), cpu.line_model(cc, d, cap)
+        got = np.array([mg.a0, mg.a1, mg.a2, mg.a3, mg.a4, *mg.sums])
+        np.testing.assert_allclose(got, mc, rtol=1e-11, atol=1e-14 * np.max(np.abs(mc)))
+    zoff = rng.standard_normal(T) * 1e-3
+    for it in range(4):
+        gpu.set_offset(zoff * (it + 1), 1e-4 * it)
+        off = po.CpuOracle(A, mu, c, zoff=zoff * (it + 1), value_offset=1e-4 * it)
+        x = rng.dirichlet(np.ones(n))
+        gc, cc = gpu.make_cache(x), off.make_cache(x)
+        assert abs(gpu.value(gc) - off.value(cc)) <= 1e-12 * (1 + abs(off.value(cc)))
+        _close(gpu.gradient(gc), off.gradient(cc))
+        v = rng.standard_normal(n)
+        _close(gpu.hvp(gc, v), off.hvp(cc, v))
+    assert gpu.passes()[2] > 0
+    gpu.close()
