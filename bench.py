@@ -160,6 +160,14 @@ def solve_leg():
             t0 = time.perf_counter()
             xc, rc = po.solve(A, mu, c, cc)
             row.update(cpu_s=time.perf_counter() - t0, cpu_status=int(rc.status), df=abs(rc.f_star - rep.f_star))
+        if name == "C4":
+            # BASELINE config 4's return-floor sweep: 5 floors between the
+            # min-variance and max-mean means, c1 calibrated per floor
+            t0 = time.perf_counter()
+            sw = g.floor_sweep(cfg, nfloors=5)
+            row["floor_sweep"] = {
+                "wall_s": time.perf_counter() - t0, "solves": sw.total_solves, "m_mv": sw.m_mv, "m_max": sw.m_max,
+                "points": [{k: p[k] for k in ("floor", "c1", "mean", "status", "solves")} for p in sw.points]}
         g.close()
         out.append(row)
     return out

@@ -214,6 +214,36 @@ int32_t mvsk_gpu_solve(mvsk_gpu_ctx* ctx, const mvsk_solver_config* cfg, const d
                        double* x_star, mvsk_solve_report* report, mvsk_observer_fn observer,
                        void* observer_user);
 
+/* Replace the preference coefficients (c1..c4) of a live context; invalidates
+ * every cache slot (their f / gradient depend on c). */
+int32_t mvsk_gpu_set_coeffs(mvsk_gpu_ctx* ctx, const mvsk_coeffs* c);
+
+/* Return-floor sweep (BASELINE config 4). Not in the reference code: the paper's
+ * calibration of the mean coefficient so that the optimum's
+ * in-sample mean mu'x* lies as close as possible to a return floor, c2..c4 held
+ * at the context's values. floors may be NULL: then nfloors interior points
+ * r_k = m_mv + k/(nfloors+1) (m_max - m_mv), m_mv the mean of the
+ * minimum-variance optimum (c = (0, c2, 0, 0)), m_max = max_j mu_j. */
+typedef struct {
+    double mean_tol;    /* stop when |mu'x* - r| <= mean_tol * (m_max - m_mv); default 1e-3 */
+    int32_t max_solves; /* solve budget per floor; default 16 */
+    int32_t warm_start; /* start each solve from the evaluated optimum nearest in c1 */
+} mvsk_sweep_config;
+typedef struct {
+    double floor;  /* target in-sample mean r */
+    double c1;     /* calibrated mean coefficient */
+    double mean;   /* mu'x* at c1 */
+    double f_star;
+    double kkt_residual;
+    int32_t status; /* SolveStatus of that solve */
+    int32_t solves; /* solves this floor added */
+} mvsk_floor_point;
+/* x_out: nfloors x n (row k = optimum for floor k), may be NULL. sw may be NULL
+ * (defaults). The context's coefficients are restored on return. */
+int32_t mvsk_gpu_floor_sweep(mvsk_gpu_ctx* ctx, const mvsk_solver_config* cfg, const mvsk_sweep_config* sw,
+                             int32_t nfloors, const double* floors, double* x_out, mvsk_floor_point* points,
+                             double* m_mv, double* m_max, int32_t* total_solves);
+
 /* ---- device-resident fast path (inputs/outputs already in HBM) --------------
  * Same math as above, full coordinates (length n, no face), asynchronous on the
  * context stream, no host synchronisation; used for HBM-roofline measurement and

@@ -49,6 +49,22 @@ class mvsk_tangent_config(C.Structure):
     ]
 
 
+class mvsk_sweep_config(C.Structure):
+    _fields_ = [("mean_tol", C.c_double), ("max_solves", C.c_int32), ("warm_start", C.c_int32)]
+
+
+class mvsk_floor_point(C.Structure):
+    _fields_ = [
+        ("floor", C.c_double),
+        ("c1", C.c_double),
+        ("mean", C.c_double),
+        ("f_star", C.c_double),
+        ("kkt_residual", C.c_double),
+        ("status", C.c_int32),
+        ("solves", C.c_int32),
+    ]
+
+
 class mvsk_direction_diag(C.Structure):
     _fields_ = [
         ("reduced_grad_norm", C.c_double),
@@ -144,6 +160,10 @@ SIGNATURES = [
      [_P, _I32, C.POINTER(mvsk_tangent_config), C.c_uint64, _D, C.POINTER(mvsk_direction_diag)]),
     ("mvsk_gpu_solve", _I32,
      [_P, C.POINTER(mvsk_solver_config), _D, _D, C.POINTER(mvsk_solve_report), OBSERVER_FN, _P]),
+    ("mvsk_gpu_set_coeffs", _I32, [_P, C.POINTER(mvsk_coeffs)]),
+    ("mvsk_gpu_floor_sweep", _I32,
+     [_P, C.POINTER(mvsk_solver_config), C.POINTER(mvsk_sweep_config), _I32, _D, _D, C.POINTER(mvsk_floor_point),
+      _D, _D, C.POINTER(_I32)]),
     ("mvsk_gpu_make_cache_device", _I32, [_P, _I32, _P]),
     ("mvsk_gpu_hvp_device", _I32, [_P, _I32, _P, _I32, _P]),
     ("mvsk_gpu_third_action_device", _I32, [_P, _I32, _P, _P, _I32, _P]),

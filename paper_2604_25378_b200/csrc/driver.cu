@@ -1177,6 +1177,156 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
     return finish(best.x, status, rb);
 }
 
+SolveCfg solve_cfg_of(const mvsk_solver_config* cfg) {
+    SolveCfg sc;
+    sc.eps = cfg->epsilon;
+    sc.tau = cfg->tau;
+    sc.max_iter = cfg->max_iter;
+    if (cfg->has_max_elapsed) sc.max_elapsed = cfg->max_elapsed_seconds;
+    sc.trial = cfg->projected_trial_step;
+    sc.restarts.assign(cfg->restart_trial_steps,
+                       cfg->restart_trial_steps + std::max(0, std::min(4, cfg->n_restart_trial_steps)));
+    sc.restart_max_iter = cfg->restart_max_iter;
+    sc.tangent = tangent_of(cfg->tangent);
+    sc.armijo = cfg->line_search == 1;
+    sc.stall_restarts = cfg->stall_restarts != 0;
+    sc.identification = cfg->identification_pass != 0;
+    return sc;
+}
+
+// coefficients are baked into captured graphs and every cached slot's f / g
+void set_coeffs(mvsk_gpu_ctx* ctx, const mvsk_coeffs& c) {
+    ctx->c = c;
+    ++ctx->epoch;
+    for (auto& s : ctx->slots) {
+        s.valid = false;
+        s.g_host_valid = false;
+        s.scalars_host_valid = false;
+    }
+}
+
+// ---- return-floor sweep (BASELINE config 4) -------------------------------------
+// Not part of the reference code: the paper's calibration of the mean
+// coefficient (PAPER.md:757 — "calibrate the mean coefficient so that the
+// resulting MVSK portfolio lies as close as possible to the same in-sample
+// return floor"), with c2..c4 held at the context's values. For each floor r the
+// in-sample mean m(c1) = mu'x*(c1) of the optimum, nondecreasing in c1, is
+// bracketed (c1 = 0, then doubling from the context's c1) and bisected until
+// |m - r| <= mean_tol * (m_max - m_mv) or the per-floor solve budget is spent;
+// every solve is cached and shared between floors. Default floors are the
+// interior points r_k = m_mv + k/(K+1) (m_max - m_mv): m_mv is the mean of the
+// minimum-variance optimum (c = (0, c2, 0, 0)), m_max = max_j mu_j (the
+// max-mean vertex).
+struct FloorEval {
+    double c1, mean, f, kkt;
+    int status;
+    Vec x;
+};
+
+struct SweepOut {
+    std::vector<FloorEval> best;
+    std::vector<int> solves;
+    std::vector<double> floors;
+    double m_mv = 0, m_max = 0;
+    int total = 0;
+};
+
+SweepOut floor_sweep(mvsk_gpu_ctx* ctx, const SolveCfg& sc, const mvsk_sweep_config& sw, const std::vector<double>& user_floors,
+                     int nfloors) {
+    const mvsk_coeffs c0 = ctx->c;
+    const Vec& mu = ctx->mu;
+    auto mean_of = [&](const Vec& x) {
+        double m = 0.0;
+        for (size_t i = 0; i < x.size(); ++i) m += mu[i] * x[i];
+        return m;
+    };
+    SweepOut out;
+    std::vector<FloorEval> cache;
+    auto run = [&](const mvsk_coeffs& c, const Vec& x0) {
+        set_coeffs(ctx, c);
+        Report r = solve(ctx, sc, x0, nullptr);
+        ++out.total;
+        return FloorEval{c.c1, mean_of(r.x), r.f, r.kkt, r.status, r.x};
+    };
+    try {
+        const FloorEval mv = run(mvsk_coeffs{0.0, c0.c2, 0.0, 0.0}, Vec());
+        out.m_mv = mv.mean;
+        out.m_max = *std::max_element(mu.begin(), mu.end());
+        const double span = out.m_max - out.m_mv;
+        if (!user_floors.empty()) {
+            out.floors = user_floors;
+        } else {
+            for (int k = 1; k <= nfloors; ++k) out.floors.push_back(out.m_mv + span * k / (double)(nfloors + 1));
+        }
+        const double tol = (sw.mean_tol > 0 ? sw.mean_tol : 1e-3) * std::max(std::fabs(span), 1e-300);
+        const int budget = sw.max_solves > 0 ? sw.max_solves : 16;
+        // E(c1): cached solve, warm-started from the evaluated optimum nearest in c1
+        auto eval = [&](double c1, int& used) -> const FloorEval& {
+            for (const FloorEval& e : cache)
+                if (e.c1 == c1) return e;
+            Vec x0;
+            if (sw.warm_start && !cache.empty()) {
+                const FloorEval* nb = &cache[0];
+                for (const FloorEval& e : cache)
+                    if (std::fabs(e.c1 - c1) < std::fabs(nb->c1 - c1)) nb = &e;
+                x0 = nb->x;
+            }
+            cache.push_back(run(mvsk_coeffs{c1, c0.c2, c0.c3, c0.c4}, x0));
+            ++used;
+            return cache.back();
+        };
+        const double c1_start = c0.c1 > 0 ? c0.c1 : 1.0;
+        for (const double r : out.floors) {
+            int used = 0;
+            eval(0.0, used);
+            auto closest = [&]() {
+                const FloorEval* b = nullptr;
+                for (const FloorEval& e : cache)
+                    if (!b || std::fabs(e.mean - r) < std::fabs(b->mean - r) ||
+                        (std::fabs(e.mean - r) == std::fabs(b->mean - r) && e.c1 < b->c1))
+                        b = &e;
+                return *b;
+            };
+            auto bracket = [&](double& lo, double& hi, bool& have_hi) {
+                lo = 0.0;
+                have_hi = false;
+                hi = 0.0;
+                for (const FloorEval& e : cache) {
+                    if (e.mean < r && e.c1 > lo) lo = e.c1;
+                    if (e.mean >= r && (!have_hi || e.c1 < hi)) {
+                        hi = e.c1;
+                        have_hi = true;
+                    }
+                }
+            };
+            double lo, hi;
+            bool have_hi;
+            bracket(lo, hi, have_hi);
+            // grow the upper end until the optimum's mean reaches the floor
+            double probe = c1_start;
+            for (const FloorEval& e : cache) probe = std::max(probe, e.c1);
+            while (!have_hi && used < budget && probe < 1e15) {
+                const FloorEval& e = eval(probe, used);
+                if (e.mean >= r) break;
+                probe *= 2.0;
+                bracket(lo, hi, have_hi);
+            }
+            bracket(lo, hi, have_hi);
+            while (have_hi && used < budget && std::fabs(closest().mean - r) > tol && hi - lo > 1e-12 * hi) {
+                eval(0.5 * (lo + hi), used);
+                bracket(lo, hi, have_hi);
+            }
+            out.best.push_back(closest());
+            out.solves.push_back(used);
+        }
+    } catch (...) {
+        set_coeffs(ctx, c0);
+        throw;
+    }
+    set_coeffs(ctx, c0);
+    return out;
+}
+
 thread_local std::string g_err2;
 
 template <class F>
@@ -1255,19 +1405,7 @@ int32_t mvsk_gpu_solve(mvsk_gpu_ctx* ctx, const mvsk_solver_config* cfg, const d
     return guard(ctx, [&] {
         MVSK_CUDA(cudaSetDevice(ctx->device));
         const auto t0 = std::chrono::steady_clock::now();
-        SolveCfg sc;
-        sc.eps = cfg->epsilon;
-        sc.tau = cfg->tau;
-        sc.max_iter = cfg->max_iter;
-        if (cfg->has_max_elapsed) sc.max_elapsed = cfg->max_elapsed_seconds;
-        sc.trial = cfg->projected_trial_step;
-        sc.restarts.assign(cfg->restart_trial_steps,
-                           cfg->restart_trial_steps + std::max(0, std::min(4, cfg->n_restart_trial_steps)));
-        sc.restart_max_iter = cfg->restart_max_iter;
-        sc.tangent = tangent_of(cfg->tangent);
-        sc.armijo = cfg->line_search == 1;
-        sc.stall_restarts = cfg->stall_restarts != 0;
-        sc.identification = cfg->identification_pass != 0;
+        const SolveCfg sc = solve_cfg_of(cfg);
         const uint64_t f0 = ctx->fwd, t0p = ctx->tr, p0 = ctx->phys;
         std::function<void(int, double, const Vec&)> obs;
         if (observer)
@@ -1300,6 +1438,55 @@ int32_t mvsk_gpu_solve(mvsk_gpu_ctx* ctx, const mvsk_solver_config* cfg, const d
         report->status = r.status;
         report->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         std::strncpy(report->config_label, cfg->label, sizeof(report->config_label) - 1);
+    });
+}
+
+int32_t mvsk_gpu_set_coeffs(mvsk_gpu_ctx* ctx, const mvsk_coeffs* c) {
+    return guard(ctx, [&] {
+        if (!c) throw ApiError(MVSK_DOMAIN_ERROR, "set_coeffs: null coefficients");
+        if (!std::isfinite(c->c1) || !std::isfinite(c->c2) || !std::isfinite(c->c3) || !std::isfinite(c->c4))
+            throw ApiError(MVSK_DOMAIN_ERROR, "set_coeffs: non-finite coefficient");
+        set_coeffs(ctx, *c);
+    });
+}
+
+int32_t mvsk_gpu_floor_sweep(mvsk_gpu_ctx* ctx, const mvsk_solver_config* cfg, const mvsk_sweep_config* sw,
+                             int32_t nfloors, const double* floors, double* x_out, mvsk_floor_point* points,
+                             double* m_mv, double* m_max, int32_t* total_solves) {
+    return guard(ctx, [&] {
+        MVSK_CUDA(cudaSetDevice(ctx->device));
+        if (!cfg || nfloors < 1) throw ApiError(MVSK_DOMAIN_ERROR, "floor_sweep: need a solver config and nfloors >= 1");
+        mvsk_sweep_config d{};
+        d.mean_tol = 1e-3;
+        d.max_solves = 16;
+        d.warm_start = 1;
+        const mvsk_sweep_config& s = sw ? *sw : d;
+        std::vector<double> fl;
+        if (floors) {
+            fl.assign(floors, floors + nfloors);
+            for (double v : fl)
+                if (!std::isfinite(v)) throw ApiError(MVSK_DOMAIN_ERROR, "floor_sweep: non-finite floor");
+        }
+        const FaceMap saved = ctx->pub_face;
+        const SweepOut o = floor_sweep(ctx, solve_cfg_of(cfg), s, fl, nfloors);
+        ctx->pub_face = saved;
+        for (int k = 0; k < nfloors; ++k) {
+            const FloorEval& e = o.best[(size_t)k];
+            if (x_out) std::copy(e.x.begin(), e.x.end(), x_out + (size_t)k * ctx->n);
+            if (points) {
+                mvsk_floor_point& p = points[k];
+                p.floor = o.floors[(size_t)k];
+                p.c1 = e.c1;
+                p.mean = e.mean;
+                p.f_star = e.f;
+                p.kkt_residual = e.kkt;
+                p.status = e.status;
+                p.solves = o.solves[(size_t)k];
+            }
+        }
+        if (m_mv) *m_mv = o.m_mv;
+        if (m_max) *m_max = o.m_max;
+        if (total_solves) *total_solves = o.total;
     });
 }
 

@@ -220,9 +220,11 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
     const int n = (int)ctx->n;
     const int ntile = (n + GBM - 1) / GBM;
     const int npairs = ntile * (ntile + 1) / 2;
-    // split the sample range so that >= 1 wave of CTAs is busy, min 256 rows / split
+    // split the sample range so that >= 1 wave of CTAs is busy, min 64 rows
+    // (2 chunks) per split: a single-tile Gram (n <= 128, C1/C2) otherwise runs
+    // on one or a few SMs (C1: one CTA over 500 rows, ~65 us per direction)
     int nsplit = std::max(1, ctx->nsm / npairs);
-    nsplit = (int)std::max<long long>(1, std::min<long long>(nsplit, ctx->T_local / 256));
+    nsplit = (int)std::max<long long>(1, std::min<long long>(nsplit, ctx->T_local / 64));
     const size_t need = (size_t)nsplit * npairs * GBM * GBM;
     if (ctx->gram_part_elems < need) {
         if (ctx->gram_part) MVSK_CUDA(cudaFree(ctx->gram_part));

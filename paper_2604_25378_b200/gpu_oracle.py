@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _abi
-from ._abi import (OBSERVER_FN, mvsk_coeffs, mvsk_direction_diag, mvsk_solve_report, mvsk_solver_config,
+from ._abi import (OBSERVER_FN, mvsk_coeffs, mvsk_direction_diag, mvsk_floor_point, mvsk_solve_report,
+                   mvsk_solver_config, mvsk_sweep_config,
                    mvsk_tangent_config)
 
 
@@ -112,6 +113,16 @@ class LineModel:
 
     def eval(self, alpha):
         return self.a0 + alpha * (self.a1 + alpha * (self.a2 + alpha * (self.a3 + alpha * self.a4)))
+
+
+@dataclass
+class FloorSweep:
+    """Result of GpuOracle.floor_sweep: one calibrated optimum per return floor."""
+    points: list  # of dicts: floor, c1, mean, f_star, kkt_residual, status, solves
+    X: np.ndarray  # nfloors x n optima
+    m_mv: float  # in-sample mean of the minimum-variance optimum
+    m_max: float  # max_j mu_j (max-mean vertex)
+    total_solves: int
 
 
 class GpuOracle:
@@ -309,6 +320,28 @@ class GpuOracle:
             cb = OBSERVER_FN()
         self._chk(self.lib.mvsk_gpu_solve(self._ctx, C.byref(cfg), _p(x0a), _p(xs), C.byref(rep), cb, None))
         return xs, rep
+
+    def set_coeffs(self, coeffs):
+        """Replace c1..c4 on the live context (the panel stays resident)."""
+        self.c = _vec(coeffs, 4)
+        self._chk(self.lib.mvsk_gpu_set_coeffs(self._ctx, C.byref(mvsk_coeffs(*self.c))))
+
+    def floor_sweep(self, cfg: mvsk_solver_config, nfloors: int = 5, floors=None, mean_tol: float = 1e-3,
+                    max_solves: int = 16, warm_start: bool = True) -> FloorSweep:
+        """Return-floor sweep (BASELINE config 4; c1 calibration of PAPER.md:757,
+        not part of the reference code): for each floor, the c1 >= 0 whose
+        optimum's in-sample mean is closest to it, c2..c4 fixed."""
+        fl = None if floors is None else _vec(floors)
+        if fl is not None:
+            nfloors = fl.size
+        X = np.empty((nfloors, self.n))
+        pts = (mvsk_floor_point * nfloors)()
+        sw = mvsk_sweep_config(mean_tol, max_solves, 1 if warm_start else 0)
+        mmv, mmax, tot = C.c_double(), C.c_double(), C.c_int32()
+        self._chk(self.lib.mvsk_gpu_floor_sweep(self._ctx, C.byref(cfg), C.byref(sw), nfloors, _p(fl), _p(X), pts,
+                                                C.byref(mmv), C.byref(mmax), C.byref(tot)))
+        points = [{k: getattr(p, k) for k, _ in mvsk_floor_point._fields_} for p in pts]
+        return FloorSweep(points, X, mmv.value, mmax.value, tot.value)
 
     # ---- device-resident path (pointers into HBM, async on the context stream)
     def make_cache_device(self, slot: int, x_ptr: int):

@@ -145,3 +145,79 @@ def dominated_panel(T: int):
 
 def crra(gamma):
     return np.array([1.0, gamma / 2, gamma * (gamma + 1) / 6, gamma * (gamma + 1) * (gamma + 2) / 24])
+
+
+def floor_sweep_ref(solve_fn, mu, c, nfloors=5, floors=None, mean_tol=1e-3, max_solves=16, warm_start=True):
+    """Python mirror of the return-floor sweep (driver.cu floor_sweep; the
+    paper's c1 calibration, PAPER.md:757 — not part of the reference code),
+    driven by any solve_fn(coeffs, x0) -> x. Used to check the device sweep's
+    decisions against CPU-oracle solves."""
+    mu = np.asarray(mu, dtype=np.float64)
+    c = np.asarray(c, dtype=np.float64)
+    total = [0]
+
+    def run(coeffs, x0):
+        x = solve_fn(np.asarray(coeffs, dtype=np.float64), x0)
+        total[0] += 1
+        return {"c1": float(coeffs[0]), "mean": float(mu @ x), "x": x}
+
+    mv = run([0.0, c[1], 0.0, 0.0], None)
+    m_mv, m_max = mv["mean"], float(np.max(mu))
+    span = m_max - m_mv
+    fl = list(floors) if floors is not None else [m_mv + span * k / (nfloors + 1) for k in range(1, nfloors + 1)]
+    tol = mean_tol * max(abs(span), 1e-300)
+    cache = []
+
+    def ev(c1, used):
+        for e in cache:
+            if e["c1"] == c1:
+                return e
+        x0 = None
+        if warm_start and cache:
+            nb = cache[0]
+            for e in cache:
+                if abs(e["c1"] - c1) < abs(nb["c1"] - c1):
+                    nb = e
+            x0 = nb["x"]
+        cache.append(run([c1, c[1], c[2], c[3]], x0))
+        used[0] += 1
+        return cache[-1]
+
+    c1_start = c[0] if c[0] > 0 else 1.0
+    best, solves = [], []
+    for r in fl:
+        used = [0]
+        ev(0.0, used)
+
+        def closest():
+            b = None
+            for e in cache:
+                if b is None or abs(e["mean"] - r) < abs(b["mean"] - r) or (
+                        abs(e["mean"] - r) == abs(b["mean"] - r) and e["c1"] < b["c1"]):
+                    b = e
+            return b
+
+        def bracket():
+            lo, hi, have = 0.0, 0.0, False
+            for e in cache:
+                if e["mean"] < r and e["c1"] > lo:
+                    lo = e["c1"]
+                if e["mean"] >= r and (not have or e["c1"] < hi):
+                    hi, have = e["c1"], True
+            return lo, hi, have
+
+        lo, hi, have = bracket()
+        probe = max([c1_start] + [e["c1"] for e in cache])
+        while not have and used[0] < max_solves and probe < 1e15:
+            e = ev(probe, used)
+            if e["mean"] >= r:
+                break
+            probe *= 2.0
+            lo, hi, have = bracket()
+        lo, hi, have = bracket()
+        while have and used[0] < max_solves and abs(closest()["mean"] - r) > tol and hi - lo > 1e-12 * hi:
+            ev(0.5 * (lo + hi), used)
+            lo, hi, have = bracket()
+        best.append(closest())
+        solves.append(used[0])
+    return {"floors": fl, "best": best, "solves": solves, "m_mv": m_mv, "m_max": m_max, "total": total[0]}

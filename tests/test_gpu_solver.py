@@ -268,3 +268,35 @@ def test_cpp_host_solves_a_binary_panel(tmp_path):
     assert abs(rep["f_star"] - rc.f_star) <= 1e-12 * (1 + abs(rc.f_star))
     assert _active(xg, 1e-8) == _active(xc, 1e-8)
     assert np.max(np.abs(xg - xc)) <= 1e-7
+
+
+@pytest.mark.parametrize("name,mode", [("C1", "small"), ("C2", "large")])
+def test_floor_sweep_matches_cpu_mirror(name, mode):
+    """Return-floor sweep (BASELINE config 4, c1 calibration of PAPER.md:757):
+    the device sweep (driver.cu floor_sweep over GPU solves) takes the same
+    bracketing/bisection decisions as the Python mirror over CPU-oracle solves,
+    so the calibrated c1 agree exactly and the optima to the solve bar."""
+    from paper_2604_25378_b200.datagen import make_panel
+    from paper_2604_25378_b200.gpu_oracle import preset
+    A, mu, c = make_panel(name, seed=5)
+    cfg_c, cfg_g = po.preset(mode), preset(mode)
+    for cfg in (cfg_c, cfg_g):
+        cfg.has_max_elapsed = 0
+        cfg.epsilon = 1e-10
+    ref = rh.floor_sweep_ref(lambda cc, x0: po.solve(A, mu, cc, cfg_c, x0)[0], mu, c, nfloors=3)
+    g = _gpu(A, mu, c)
+    out = g.floor_sweep(cfg_g, nfloors=3)
+    assert out.total_solves == ref["total"]
+    assert out.m_max == ref["m_max"]
+    assert abs(out.m_mv - ref["m_mv"]) <= 1e-9 * abs(ref["m_max"] - ref["m_mv"])
+    span = ref["m_max"] - ref["m_mv"]
+    for k, p in enumerate(out.points):
+        b = ref["best"][k]
+        assert p["c1"] == b["c1"], (k, p["c1"], b["c1"])
+        assert abs(p["mean"] - b["mean"]) <= 1e-8 * span
+        assert abs(p["mean"] - p["floor"]) <= 1e-3 * span or p["solves"] >= 16
+        assert float(np.max(np.abs(out.X[k] - b["x"]))) <= 1e-6
+    # coefficients restored
+    x = rh.simplex_point(A.shape[1], 3, 1e-3)
+    cc = po.CpuOracle(A, mu, c).make_cache(x)
+    assert abs(g.value(g.make_cache(x)) - po.CpuOracle(A, mu, c).value(cc)) <= 1e-12 * (1 + abs(po.CpuOracle(A, mu, c).value(cc)))
