@@ -320,6 +320,13 @@ const void* select_dmma(Op op, int K, int WC, int D) {
     if (WC == 64) return dfn<OP, K, 64, D>();               \
     if (WC == 80) return dfn<OP, K, 80, D>();               \
     if (WC == 128) return dfn<OP, K, 128, D>();
+    if (D == 0) {
+        if (op == Op::HVP && K == 8) { MVSK_DWC(Op::HVP, 8, 0) }
+        if (op == Op::THIRD && K == 8) {
+            if (WC == 64) return dfn<Op::THIRD, 8, 64, 0>();
+            if (WC == 80) return dfn<Op::THIRD, 8, 80, 0>();
+        }
+    }
     if (D == 1) {
         if (op == Op::HVP && K == 8) { MVSK_DWC(Op::HVP, 8, 1) }
         if (op == Op::HVP && K == 4) { MVSK_DWC(Op::HVP, 4, 1) }
@@ -356,14 +363,16 @@ bool make_dmma_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
             continue;
         }
         const size_t stage = (size_t)8 * (8 * WC + 4) * sizeof(double);
-        // exchange depth (D = 2 measured no faster than 1 at C5: the per-stage
-        // chain, not the DSMEM latency, bounds it; only D = 1 is instantiated)
+        // exchange depth D: produce(s + D) runs before consume(s). D = 0 frees a
+        // ring slot one phase earlier (two fills in flight with S = 3 at cw = 1024)
+        // and measured 1-4 % faster than D = 1 (C5 hvp8 2.30 vs 2.39 ms, C4 third8
+        // 0.120 vs 0.124 ms, profiles/r01_tune_dmma_depth.txt); D = 2 was no faster
         int D = 0;
         const void* fn = nullptr;
         int S = 0;
         size_t head = 0;
-        for (int d : {1}) {
-            if (fn || (forceD && d != forceD)) continue;
+        for (int d : {0, 1}) {
+            if (fn || (forceD > 0 && d != forceD) || (forceD < 0 && d != 0)) continue;  // -1 forces D = 0
             const void* f = select_dmma(op, K, WC, d);
             if (!f) continue;
             size_t h = 256 + (size_t)(8 * V + (2 * d + 2) * C * V + 2 * V) * sizeof(double);

@@ -39,7 +39,9 @@ struct DmmaArgs {
 };
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+    // not volatile: a pure function of its operands, so ptxas may interleave
+    // independent accumulator chains
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                  : "+d"(d[0]), "+d"(d[1])
                  : "d"(a), "d"(b));
 }
@@ -151,17 +153,26 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
         mbar_wait(&full[slot], (uint32_t)((s / S) & 1));
         const double* X = ring + slot * stage_elems;  // rows past the block end: finite stale data,
                                                       // their dots are never used (zero weights)
-        double cfr[2][NT1][2];
+        // NCH independent accumulator chains per n-tile hide the DMMA latency
+        constexpr int NCH = NT1 >= 2 ? 2 : 4;
+        double cfr[NCH][NT1][2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < NCH; ++h)
 #pragma unroll
             for (int nt = 0; nt < NT1; ++nt) cfr[h][nt][0] = cfr[h][nt][1] = 0.0;
 #pragma unroll
         for (int ks = 0; ks < KS1; ++ks) {
             const double av = X[g4 * RS + wcol + ks * 4 + t4];
 #pragma unroll
-            for (int nt = 0; nt < NT1; ++nt) dmma884(cfr[ks & 1][nt], av, vb[nt][ks]);
+            for (int nt = 0; nt < NT1; ++nt) dmma884(cfr[ks % NCH][nt], av, vb[nt][ks]);
         }
+#pragma unroll
+        for (int h = 1; h < NCH; ++h)
+#pragma unroll
+            for (int nt = 0; nt < NT1; ++nt) {
+                cfr[0][nt][0] += cfr[h][nt][0];
+                cfr[0][nt][1] += cfr[h][nt][1];
+            }
         // Y partial: C[row = g4][j = nt*8 + 2*t4 + i]
         double* rb = red + warp * V;
 #pragma unroll
@@ -169,7 +180,7 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 const int j = nt * 8 + 2 * t4 + i;
-                if (j < NDOT) rb[g4 * NDOT + j] = cfr[0][nt][i] + cfr[1][nt][i];
+                if (j < NDOT) rb[g4 * NDOT + j] = cfr[0][nt][i];
             }
         __syncthreads();  // (A) warp partials published; all consumes up to s-D-1 done
         if (tid == 0 && s >= D + 1 && s - D - 1 + S < nst) issue(s - D - 1 + S);
@@ -218,10 +229,11 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
             wf[kh] = w;
         }
         const double* X = ring + slot * stage_elems;
+        // k-half outer: the MT accumulators form independent chains
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
+        for (int kh = 0; kh < 2; ++kh)
 #pragma unroll
-            for (int kh = 0; kh < 2; ++kh) {
+            for (int mt = 0; mt < MT; ++mt) {
                 const double av = X[(kh * 4 + t4) * RS + wcol + mt * 8 + g4];
                 dmma884(acc[mt], av, wf[kh]);
             }

@@ -17,7 +17,12 @@ X = raw_returns(spec, 5000, device=dev)
 mu_t = X.sum(0) / spec.T
 X.sub_(mu_t)
 T, n = spec.T, spec.n
-gpu = GpuOracle(None, mu_t.cpu().numpy(), crra(spec.gamma), device_panel=(X.data_ptr(), n, T, n))
+ld = n if n < 512 else (n + 15) // 16 * 16  # the padded stride the host-upload path uses
+if ld != n:
+    Xp = torch.zeros((T, ld), dtype=X.dtype, device=dev)
+    Xp[:, :n] = X
+    X = Xp
+gpu = GpuOracle(None, mu_t.cpu().numpy(), crra(spec.gamma), device_panel=(X.data_ptr(), ld, T, n))
 xd = torch.from_numpy(random_simplex_point(n, 7)).to(dev)
 Vd = torch.from_numpy(random_tangents(n, 8, 7)).to(dev)
 out = torch.empty_like(Vd)

@@ -19,7 +19,12 @@ X = raw_returns(spec, 5000, device=dev)
 mu_t = X.sum(0) / spec.T
 X.sub_(mu_t)
 T, n = spec.T, spec.n
-gpu = GpuOracle(None, mu_t.cpu().numpy(), crra(spec.gamma), device_panel=(X.data_ptr(), n, T, n))
+ld = n if n < 512 else (n + 15) // 16 * 16  # the padded stride the host-upload path uses
+if ld != n:
+    Xp = torch.zeros((T, ld), dtype=X.dtype, device=dev)
+    Xp[:, :n] = X
+    X = Xp
+gpu = GpuOracle(None, mu_t.cpu().numpy(), crra(spec.gamma), device_panel=(X.data_ptr(), ld, T, n))
 st = torch.cuda.Stream(dev)
 torch.cuda.set_stream(st)
 gpu.set_stream(st.cuda_stream)
@@ -59,7 +64,7 @@ for op in [o for o in ops if o in ("hvp8", "third8", "hvp4")]:
     for cl in ["dmma0", "dmma4,1", "dmma8,1", "dmma8,2", "dmma2,1", "0,0"]:
         if cl.startswith("dmma"):
             os.environ.pop("MVSK_NO_DMMA", None)
-            os.environ["MVSK_TUNE_DMMA"] = cl[4:]
+            os.environ["MVSK_TUNE_DMMA"] = os.environ.get("MVSK_TUNE_DMMA_FIX") or cl[4:]
         else:
             os.environ["MVSK_NO_DMMA"] = "1"
             os.environ["MVSK_TUNE_CLUSTER"] = cl
