@@ -72,6 +72,7 @@ void free_all(mvsk_gpu_ctx* ctx) {
     }
     if (ctx->h_in) cudaFreeHost(ctx->h_in);
     if (ctx->h_out) cudaFreeHost(ctx->h_out);
+    if (ctx->h_mat) cudaFreeHost(ctx->h_mat);
     for (auto& g : ctx->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     if (ctx->comm) ncclCommDestroy(ctx->comm);

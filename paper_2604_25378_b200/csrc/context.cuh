@@ -103,6 +103,8 @@ struct mvsk_gpu_ctx {
     double* h_in = nullptr;
     double* h_out = nullptr;
     size_t h_elems = 0;
+    double* h_mat = nullptr;  // pinned n x n staging (direct branch: Gram out, P in)
+    size_t h_mat_elems = 0;
 
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;

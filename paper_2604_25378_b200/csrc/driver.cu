@@ -10,7 +10,7 @@
 //     arithmetic is exactly cg_capped's (:85-113);
 //   * the direct branch (:151-188) assembles G = A_F^T diag(psi'') A_F / T
 //     on the fp64 tensor cores and reduces M = (UQ)^T G (UQ) with the
-//     Householder structure on the host (O(n^2 mm)); h = (UQ)^T G U nu needs
+//     Householder structure on the host (O(n^2) + the mm^3 LU); h = (UQ)^T G U nu needs
 //     no extra pass; a = (UQ)^T A^T(psi''' o q) / T with q_t = a_t^T P a_t.
 // Host geometry (O(n) Householder applies, projections) stays on the host.
 #include <algorithm>
@@ -171,6 +171,32 @@ struct LU {
                 }
             }
         }
+    }
+    // A^-1, row-major. Row-oriented substitution on the permuted identity: every
+    // entry sees exactly the operation sequence of solve(e_j) (same bits), but
+    // the inner loops run along contiguous rows.
+    Vec inverse() const {
+        Vec Y((size_t)(n * n), 0.0);
+        for (long long i = 0; i < n; ++i) Y[(size_t)(i * n + perm[(size_t)i])] = 1.0;
+        for (long long i = 0; i < n; ++i) {
+            double* yi = &Y[(size_t)(i * n)];
+            for (long long c = 0; c < i; ++c) {
+                const double l = a[(size_t)(i * n + c)];
+                const double* yc = &Y[(size_t)(c * n)];
+                for (long long j = 0; j < n; ++j) yi[j] -= l * yc[j];
+            }
+        }
+        for (long long i = n - 1; i >= 0; --i) {
+            double* yi = &Y[(size_t)(i * n)];
+            for (long long c = i + 1; c < n; ++c) {
+                const double u = a[(size_t)(i * n + c)];
+                const double* yc = &Y[(size_t)(c * n)];
+                for (long long j = 0; j < n; ++j) yi[j] -= u * yc[j];
+            }
+            const double d = a[(size_t)(i * n + i)];
+            for (long long j = 0; j < n; ++j) yi[j] /= d;
+        }
+        return Y;
     }
     Vec solve(const Vec& b) const {
         Vec y((size_t)n);
@@ -459,6 +485,61 @@ TangentCfg tangent_of(const mvsk_tangent_config& c) {
 }
 
 // yand_direction (affine_normal.hpp:127-245) at the cache in `slot`
+// [H S H]_11 for symmetric S (k x k, row-major), H = I - beta v v^T: the
+// (k-1) x (k-1) block without row/col 0. S - beta v a^T - beta a v^T +
+// beta^2 (v^T a) v v^T with a = S v; evaluated on the lower triangle and
+// mirrored, so the result is exactly symmetric like S.
+Vec reflect_sym(const Vec& S, long long k, const Vec& v, double beta) {
+    Vec a((size_t)k, 0.0);
+    for (long long i = 0; i < k; ++i) {
+        double s = 0.0;
+        const double* sr = &S[(size_t)(i * k)];
+        for (long long j = 0; j < k; ++j) s += sr[j] * v[(size_t)j];
+        a[(size_t)i] = s;
+    }
+    const double c = beta * beta * dot(v, a);
+    const long long r = k - 1;
+    Vec o((size_t)(r * r));
+    for (long long i = 1; i < k; ++i)
+        for (long long j = 1; j <= i; ++j) {
+            const double val = S[(size_t)(i * k + j)] - (beta * v[(size_t)i] * a[(size_t)j] + beta * a[(size_t)i] * v[(size_t)j]) +
+                               c * v[(size_t)i] * v[(size_t)j];
+            o[(size_t)((i - 1) * r + (j - 1))] = val;
+            o[(size_t)((j - 1) * r + (i - 1))] = val;
+        }
+    return o;
+}
+
+// H [0 0; 0 D] H for a general D (r x r): the (r+1) x (r+1) lift that
+// P = (UQ) D (UQ)^T applies twice (D - beta v (v^T D) - beta (D v) v^T + beta^2
+// (v^T D v) v v^T on the zero-padded D)
+Vec unreflect(const Vec& D, long long r, const Vec& v, double beta) {
+    const long long k = r + 1;
+    Vec Dp((size_t)(k * k), 0.0);
+    for (long long i = 0; i < r; ++i)
+        for (long long j = 0; j < r; ++j) Dp[(size_t)((i + 1) * k + (j + 1))] = D[(size_t)(i * r + j)];
+    Vec dv((size_t)k, 0.0), vd((size_t)k, 0.0);  // D v and v^T D
+    for (long long i = 0; i < k; ++i) {
+        double s = 0.0;
+        const double* dr = &Dp[(size_t)(i * k)];
+        for (long long j = 0; j < k; ++j) s += dr[j] * v[(size_t)j];
+        dv[(size_t)i] = s;
+    }
+    for (long long i = 0; i < k; ++i) {
+        const double vi = v[(size_t)i];
+        if (vi == 0.0) continue;
+        const double* dr = &Dp[(size_t)(i * k)];
+        for (long long j = 0; j < k; ++j) vd[(size_t)j] += vi * dr[j];
+    }
+    const double c = beta * beta * dot(v, dv);
+    for (long long i = 0; i < k; ++i) {
+        double* pr = &Dp[(size_t)(i * k)];
+        const double bvi = beta * v[(size_t)i], bdvi = beta * dv[(size_t)i], cvi = c * v[(size_t)i];
+        for (long long j = 0; j < k; ++j) pr[j] += -(bvi * vd[(size_t)j] + bdvi * v[(size_t)j]) + cvi * v[(size_t)j];
+    }
+    return Dp;
+}
+
 Vec yand_direction(const View& O, int slot, const TangentCfg& cfg, uint64_t it_seed, mvsk_direction_diag& diag) {
     mvsk_gpu_ctx* ctx = O.ctx;
     const long long n = O.m();
@@ -482,49 +563,25 @@ Vec yand_direction(const View& O, int slot, const TangentCfg& cfg, uint64_t it_s
 
     if (!cfg.pcg) {
         // ---- direct branch via the weighted Gram (:151-188)
-        Vec UQ((size_t)(n * mm));  // n x mm, row-major
-        for (long long k = 0; k < mm; ++k) {
-            Vec e((size_t)mm, 0.0);
-            e[(size_t)k] = 1.0;
-            const Vec col = basis.apply(frame.apply_Q(e));
-            for (long long i = 0; i < n; ++i) UQ[(size_t)(i * mm + k)] = col[(size_t)i];
-        }
+        // W = A (UQ) never forms: with G = A^T diag(psi'') A / T from the DMMA
+        // kernel, M0 = (UQ)^T G (UQ) = [H_Q [H_U G H_U]_11 H_Q]_11 (two
+        // Householder similarity transforms, [.]_11 drops row/col 0), O(n^2)
+        // instead of the O(n^2 mm) dense products of :160-170.
         ctx->fwd += (uint64_t)mm + 1;  // the reference's W and t_nu passes (:159, :164)
         Vec G((size_t)(n * n));
         op_weighted_gram(ctx, slot, O.fm, G.data());
-        // GU = G (UQ)  (n x mm); M0 = (UQ)^T GU (mm x mm)
-        Vec GU((size_t)(n * mm), 0.0);
-        for (long long i = 0; i < n; ++i) {
-            double* gu = &GU[(size_t)(i * mm)];
-            for (long long j = 0; j < n; ++j) {
-                const double gij = G[(size_t)(i * n + j)];
-                if (gij == 0.0) continue;
-                const double* uq = &UQ[(size_t)(j * mm)];
-                for (long long k = 0; k < mm; ++k) gu[k] += gij * uq[k];
-            }
-        }
-        Vec M0((size_t)(mm * mm), 0.0);
-        for (long long i = 0; i < n; ++i) {
-            const double* uq = &UQ[(size_t)(i * mm)];
-            const double* gu = &GU[(size_t)(i * mm)];
-            for (long long a = 0; a < mm; ++a) {
-                const double ua = uq[a];
-                if (ua == 0.0) continue;
-                double* mr = &M0[(size_t)(a * mm)];
-                for (long long b = 0; b < mm; ++b) mr[b] += ua * gu[b];
-            }
-        }
+        const Vec B = reflect_sym(G, n, basis.v, basis.beta);   // H_U G H_U, then drop row/col 0
+        const Vec M0 = reflect_sym(B, m, frame.v, frame.beta);  // H_Q B H_Q, then drop row/col 0
         // h = (UQ)^T G (U nu)  (:165-166)
         const Vec unu = basis.apply(frame.nu);
         Vec Gu((size_t)n, 0.0);
         for (long long i = 0; i < n; ++i) {
             double s = 0.0;
-            for (long long j = 0; j < n; ++j) s += G[(size_t)(i * n + j)] * unu[(size_t)j];
+            const double* gr = &G[(size_t)(i * n)];
+            for (long long j = 0; j < n; ++j) s += gr[j] * unu[(size_t)j];
             Gu[(size_t)i] = s;
         }
-        Vec h((size_t)mm, 0.0);
-        for (long long i = 0; i < n; ++i)
-            for (long long k = 0; k < mm; ++k) h[(size_t)k] += UQ[(size_t)(i * mm + k)] * Gu[(size_t)i];
+        const Vec h = frame.apply_Qt(basis.apply_t(Gu));
 
         auto solve_with = [&](double lam) -> Vec {
             Vec M = M0;
@@ -532,24 +589,10 @@ Vec yand_direction(const View& O, int slot, const TangentCfg& cfg, uint64_t it_s
             const LU lu(M, mm);
             Vec a((size_t)mm, 0.0);
             if (has_third) {
-                // P = UQ M^-1 (UQ)^T  (n x n); S = M^-1 (UQ)^T column by column
-                Vec S((size_t)(mm * n));
-                Vec col((size_t)mm);
-                for (long long i = 0; i < n; ++i) {
-                    for (long long k = 0; k < mm; ++k) col[(size_t)k] = UQ[(size_t)(i * mm + k)];
-                    const Vec s = lu.solve(col);
-                    for (long long k = 0; k < mm; ++k) S[(size_t)(k * n + i)] = s[(size_t)k];
-                }
-                Vec P((size_t)(n * n), 0.0);
-                for (long long i = 0; i < n; ++i) {
-                    const double* uq = &UQ[(size_t)(i * mm)];
-                    double* pr = &P[(size_t)(i * n)];
-                    for (long long k = 0; k < mm; ++k) {
-                        const double uk = uq[k];
-                        const double* sk = &S[(size_t)(k * n)];
-                        for (long long j = 0; j < n; ++j) pr[j] += uk * sk[j];
-                    }
-                }
+                // P = UQ M^-1 (UQ)^T (n x n): the explicit inverse, then the two
+                // reflections back (pad row/col 0, H_Q . H_Q, pad, H_U . H_U)
+                const Vec Minv = lu.inverse();
+                const Vec P = unreflect(unreflect(Minv, mm, frame.v, frame.beta), m, basis.v, basis.beta);
                 bool fin = true;
                 for (double v : P)
                     if (!std::isfinite(v)) {
@@ -561,8 +604,7 @@ Vec yand_direction(const View& O, int slot, const TangentCfg& cfg, uint64_t it_s
                 } else {
                     Vec af((size_t)n);
                     op_third_trace_rows(ctx, slot, O.fm, P.data(), af.data());
-                    for (long long i = 0; i < n; ++i)
-                        for (long long k = 0; k < mm; ++k) a[(size_t)k] += UQ[(size_t)(i * mm + k)] * af[(size_t)i];
+                    a = frame.apply_Qt(basis.apply_t(af));
                 }
             }
             Vec rhs((size_t)mm);

@@ -96,6 +96,9 @@ void fetch_out(mvsk_gpu_ctx* ctx, const FaceMap& fm, const double* dev, int k, l
 // it. A replay is valid while no captured buffer moved (ctx->epoch). Plans are
 // deterministic functions of the shapes, so replays compute the same bits as
 // eager launches.
+// graph keys beyond the Op values
+constexpr int kGraphGram = 100, kGraphThirdTrace = 101;
+
 void run_graphed(mvsk_gpu_ctx* ctx, int op, int k, int slot, const std::function<void()>& enqueue) {
     static const bool disabled = std::getenv("MVSK_NO_GRAPHS") != nullptr;
     mvsk_gpu_ctx::GraphEntry* e = nullptr;
@@ -335,15 +338,28 @@ void op_line_model(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double*
     for (int i = 0; i < 9; ++i) out[5 + i] = s[i];
 }
 
+static void ensure_h_mat(mvsk_gpu_ctx* ctx, size_t elems) {
+    if (ctx->h_mat_elems >= elems) return;
+    if (ctx->h_mat) MVSK_CUDA(cudaFreeHost(ctx->h_mat));
+    ctx->h_mat = nullptr;
+    ctx->h_mat_elems = 0;
+    MVSK_CUDA(cudaMallocHost(&ctx->h_mat, elems * sizeof(double)));
+    ctx->h_mat_elems = elems;
+    ++ctx->epoch;
+}
+
 void op_weighted_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, double* G) {
     check_slot(ctx, slot);
     const long long n = ctx->n;
     if (!ctx->gram) MVSK_CUDA(cudaMalloc(&ctx->gram, (size_t)n * n * sizeof(double)));
-    run_psi2(ctx, ctx->slots[slot].z, ctx->tvec, ctx->T_local);
-    run_weighted_gram(ctx, ctx->tvec, ctx->gram, 1.0 / (double)ctx->T_global);
-    std::vector<double> full((size_t)n * n);
-    MVSK_CUDA(cudaMemcpyAsync(full.data(), ctx->gram, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToHost,
-                              ctx->stream));
+    ensure_h_mat(ctx, (size_t)ctx->ld * ctx->ld);
+    const double* full = ctx->h_mat;
+    run_graphed(ctx, kGraphGram, 1, slot, [&] {
+        run_psi2(ctx, ctx->slots[slot].z, ctx->tvec, ctx->T_local);
+        run_weighted_gram(ctx, ctx->tvec, ctx->gram, 1.0 / (double)ctx->T_global);
+        MVSK_CUDA(cudaMemcpyAsync(ctx->h_mat, ctx->gram, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    });
     MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
     const long long m = fm.m;
     for (long long i = 0; i < m; ++i) {
@@ -360,21 +376,26 @@ void op_third_trace_rows(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const d
                                                  std::to_string(ctx->max_smem / (16 * sizeof(double))));
     if (!ctx->pmat) MVSK_CUDA(cudaMalloc(&ctx->pmat, (size_t)ld * ld * sizeof(double)));
     ensure_tvec2(ctx);
-    std::vector<double> Pf((size_t)ld * ld, 0.0);
+    ensure_h_mat(ctx, (size_t)ld * ld);
+    ensure_host_staging(ctx, (size_t)MVSK_GPU_MAX_RHS * 2 * ld);
+    double* Pf = ctx->h_mat;  // pinned; the previous user (the Gram readback) has synchronised
+    std::fill(Pf, Pf + (size_t)ld * ld, 0.0);
     for (long long i = 0; i < m; ++i) {
         const long long gi = fm.active ? fm.idx[i] : i;
         for (long long j = 0; j < m; ++j) Pf[gi * ld + (fm.active ? fm.idx[j] : j)] = P[i * m + j];
     }
-    MVSK_CUDA(cudaMemcpyAsync(ctx->pmat, Pf.data(), Pf.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    run_quadform(ctx, ctx->pmat, ctx->tvec2);
-    run_third_weights(ctx, ctx->slots[slot].z, ctx->tvec2, ctx->tvec);
-    PassIO io;
-    io.tw = ctx->tvec;
-    io.out = ctx->outd;
-    io.ldo = ctx->ld;
-    run_pass(ctx, Op::XTW, 1, io);
-    fetch_out(ctx, fm, ctx->outd, 1, ctx->ld, out);
-    // the sync above keeps Pf alive until the async H2D has completed
+    run_graphed(ctx, kGraphThirdTrace, 1, slot, [&] {
+        MVSK_CUDA(cudaMemcpyAsync(ctx->pmat, Pf, (size_t)ld * ld * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        run_quadform(ctx, ctx->pmat, ctx->tvec2);
+        run_third_weights(ctx, ctx->slots[slot].z, ctx->tvec2, ctx->tvec);
+        PassIO io;
+        io.tw = ctx->tvec;
+        io.out = ctx->outd;
+        io.ldo = ctx->ld;
+        run_pass(ctx, Op::XTW, 1, io);
+        copy_out(ctx, ctx->outd, 1, ctx->ld);
+    });
+    finish_out(ctx, fm, 1, ctx->ld, out);
 }
 
 }  // namespace mvsk_b200

@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+bash scripts/gpu_tests.sh
+MVSK_PROFILE=1 timeout 900 python scripts/solve_bench.py --configs C1,C2 --cpu-max-n 0 --reps 1 2>&1 | grep -E "profile|config" | cut -c1-250 | awk 'NR%3!=1'
