@@ -321,7 +321,10 @@ const void* select_dmma(Op op, int K, int WC, int D) {
     if (WC == 80) return dfn<OP, K, 80, D>();               \
     if (WC == 128) return dfn<OP, K, 128, D>();
     if (D == 0) {
-        if (op == Op::HVP && K == 8) { MVSK_DWC(Op::HVP, 8, 0) }
+        if (op == Op::HVP && K == 8) {
+            MVSK_DWC(Op::HVP, 8, 0)
+            if (WC == 160) return dfn<Op::HVP, 8, 160, 0>();
+        }
         if (op == Op::THIRD && K == 8) {
             if (WC == 64) return dfn<Op::THIRD, 8, 64, 0>();
             if (WC == 80) return dfn<Op::THIRD, 8, 80, 0>();
@@ -356,8 +359,11 @@ bool make_dmma_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
         }
         const int cw = (int)(ctx->ld / C);
         int WC = 0;
-        for (int w : {32, 64, 80, 128})
-            if (!WC && 8 * w >= cw) WC = w;
+        for (int w : {32, 64, 80, 128, 160})
+            if (!WC && 8 * w >= cw && select_dmma(op, K, w, forceD < 0 ? 0 : (forceD > 0 ? forceD : 0))) WC = w;
+        if (!WC)
+            for (int w : {32, 64, 80, 128, 160})
+                if (!WC && 8 * w >= cw && select_dmma(op, K, w, 1)) WC = w;
         if (!WC) {
             if (forceC) return false;
             continue;

@@ -80,7 +80,8 @@ def test_hvp_third_weights_direction(n, T, seed):
     _close(gpu.sample_direction(d), cpu.sample_direction(d), float(np.max(np.abs(A) @ np.abs(d))))
 
 
-@pytest.mark.parametrize("n,T", [(4, 50), (64, 300), (100, 1000), (128, 513), (800, 2500), (4096, 700)])
+@pytest.mark.parametrize("n,T", [(4, 50), (64, 300), (100, 1000), (128, 513), (800, 2500), (4096, 700), (4500, 260),
+                                 (5000, 333)])
 def test_multi_rhs_cluster_paths(n, T):
     """k = 8 / 4 RHS go through the cluster column-split kernel (DSMEM exchange
     of partial row dots) whenever ld splits evenly; parity vs the CPU oracle."""
