@@ -188,11 +188,13 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     const int nwp = P >= 32 ? P / 32 : 1;
     const size_t red_bytes = (((size_t)2 * R * std::max(ndot, 1) * nwp * sizeof(double)) + 127) & ~(size_t)127;
     const size_t combine = ((size_t)G * std::max(nacc, 1) * ctx->ld + 16 + (size_t)G * 16) * sizeof(double);
-    size_t ring = std::max((size_t)S * stage_bytes, combine);
+    // the fused finish reuses the ring as a [threads] fp64 scratch
+    const size_t combine_all = std::max(combine, (size_t)(G * P) * sizeof(double));
+    size_t ring = std::max((size_t)S * stage_bytes, combine_all);
     pl.smem = 128 + red_bytes + ring;
     while (pl.smem > ctx->max_smem && S > 2) {
         --S;
-        ring = std::max((size_t)S * stage_bytes, combine);
+        ring = std::max((size_t)S * stage_bytes, combine_all);
         pl.smem = 128 + red_bytes + ring;
     }
     if (pl.smem > ctx->max_smem) return false;
@@ -406,107 +408,13 @@ bool make_dmma_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
     return false;
 }
 
-struct FinishArgs {
-    int op;
-    int k;
-    int ld, n;
-    long long ldo;
-    int nb;
-    int do_reduce, do_epi;
-    const double* part_acc;
-    const double* part_sc;
-    double* red;  // [k*ld + kNumScalars]
-    // epilogue
-    double* out;
-    double* g;          // FGRAD gradient
-    double* sc;         // FGRAD scalars
-    const double* mu;   // ld
-    const double* x;    // ld (FGRAD mu'x)
-    double c1, c2, c3, c4, T, value_offset;
-    const int* skip;
-    int nskip;
-};
 
-// Block = 64 output columns x 4 partial-range groups; each thread sums its
-// quarter of the CTA partials with 4 independent accumulators, the quarters are
-// combined in a fixed order (deterministic), then the op epilogue is applied.
-// Block = cols x ng threads (cols * ng = 256): ng groups split the CTA partials
-// (ng grows with the partial count so small panels with many CTAs do not
-// serialise on one thread per column); groups combine in a fixed order.
+
 constexpr int kFinThreads = 256;
 __global__ void __launch_bounds__(kFinThreads) finish_kernel(const FinishArgs f, int ng) {
     if (pass_skipped(f.skip, f.nskip)) return;
-    const int nacc = (f.op == (int)Op::LINESUMS) ? 0 : f.k;
-    const int tot = nacc * f.ld;
-    const int nsc = f.op == (int)Op::FGRAD ? 3 : (f.op == (int)Op::LINESUMS ? 9 : 0);
-    const int cols = kFinThreads / ng;
-    const int cl = threadIdx.x % cols, grp = threadIdx.x / cols;
-    const int i = blockIdx.x * cols + cl;
-    __shared__ double part[kFinThreads];  // [ng][cols]
-    auto qsum = [&](const double* base, size_t stride, int lo, int hi) {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int b = lo;
-        for (; b + 3 < hi; b += 4) {
-            a0 += base[(size_t)b * stride];
-            a1 += base[(size_t)(b + 1) * stride];
-            a2 += base[(size_t)(b + 2) * stride];
-            a3 += base[(size_t)(b + 3) * stride];
-        }
-        for (; b < hi; ++b) a0 += base[(size_t)b * stride];
-        return (a0 + a1) + (a2 + a3);
-    };
-    // 1) fixed-order reduction over CTA partials
-    if (f.do_reduce) {
-        if (i < tot) part[grp * cols + cl] = qsum(f.part_acc + i, (size_t)tot, f.nb * grp / ng, f.nb * (grp + 1) / ng);
-        if (blockIdx.x == 0) {  // each scalar by one warp: lanes split the CTAs, fixed-order combine
-            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-            for (int sidx = w; sidx < nsc; sidx += kFinThreads / 32) {
-                double v = 0.0;
-                for (int b = lane; b < f.nb; b += 32) v += f.part_sc[(size_t)b * kNumScalars + sidx];
-                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (lane == 0) f.red[tot + sidx] = v;
-            }
-        }
-        __syncthreads();
-        if (grp == 0 && i < tot) {
-            double v = part[cl];
-            for (int q = 1; q < ng; ++q) v += part[q * cols + cl];
-            f.red[i] = v;
-        }
-        __syncthreads();
-    }
-    if (!f.do_epi) return;
-    // 2) epilogue (each element by the thread that reduced it; scalars by block 0)
-    if (f.op == (int)Op::FGRAD) {
-        if (grp == 0 && i < f.ld) f.g[i] = i < f.n ? (-f.c1 * f.mu[i] + f.red[i] / f.T) : 0.0;  // oracle.hpp:82-84
-        if (blockIdx.x == 0) {
-            __shared__ double sh[256];
-            double sacc = 0.0;
-            for (int j = threadIdx.x; j < f.n; j += blockDim.x) sacc += f.mu[j] * f.x[j];
-            sh[threadIdx.x] = sacc;
-            __syncthreads();
-            for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-                if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-                __syncthreads();
-            }
-            if (threadIdx.x == 0) {
-                const double mux = sh[0];
-                const double s2 = f.red[tot], s3 = f.red[tot + 1], s4 = f.red[tot + 2];
-                // oracle.hpp:62-64
-                f.sc[0] = f.value_offset - f.c1 * mux + (f.c2 * s2 - f.c3 * s3 + f.c4 * s4) / f.T;
-                f.sc[1] = mux;
-                f.sc[2] = s2 / f.T;
-                f.sc[3] = s3 / f.T;
-                f.sc[4] = s4 / f.T;
-            }
-        }
-    } else if (f.op == (int)Op::LINESUMS) {
-        if (blockIdx.x == 0 && threadIdx.x < 9) f.out[threadIdx.x] = f.red[tot + threadIdx.x] / f.T;
-    } else if (grp == 0 && i < tot) {
-        const int k = i / f.ld, c = i - k * f.ld;
-        // HVP / THIRD: A^T(w)/T with the 1/T folded out of the per-row weights
-        if (c < f.n) f.out[(size_t)k * f.ldo + c] = f.op == (int)Op::XTW ? f.red[i] : f.red[i] / f.T;
-    }
+    __shared__ double part[kFinThreads];
+    finish_block(f, ng, blockIdx.x, threadIdx.x, kFinThreads, part);
 }
 
 __global__ void psi2_kernel(const double* z, double* out, long long T, double c2, double c3, double c4) {
@@ -600,7 +508,7 @@ void run_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
 
 // cross-CTA (or cross-cluster) fixed-order reduction, allreduce over the
 // row-shard group, and the op epilogue
-static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO& io, Slot* slot) {
+static FinishArgs finish_args(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO& io, Slot* slot) {
     FinishArgs f{};
     f.op = (int)op;
     f.k = op == Op::LINESUMS ? 0 : std::max(nacc, 1);
@@ -626,8 +534,15 @@ static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO
         f.g = slot->g;
         f.sc = slot->sc;
     }
+    return f;
+}
+
+static int finish_groups(int nb) { return nb >= 512 ? 32 : nb >= 128 ? 8 : 4; }
+
+static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO& io, Slot* slot) {
+    FinishArgs f = finish_args(ctx, op, nacc, nb, io, slot);
     const int tot = std::max(f.k, 1) * f.ld;
-    const int ng = nb >= 512 ? 32 : nb >= 128 ? 8 : 4;
+    const int ng = finish_groups(nb);
     const int fb = std::max(1, (tot + kFinThreads / ng - 1) / (kFinThreads / ng));
     if (!ctx->comm) {
         f.do_reduce = 1;
@@ -788,11 +703,41 @@ static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     } else {
         a.zout = io.zout;
     }
-    if (ctx->T_local > 0) {
-        void* args[] = {&a};
-        MVSK_CUDA(cudaLaunchKernel(pl.fn, dim3(pl.nb), dim3(pl.G * pl.P), args, pl.smem, ctx->stream));
-    }
     ctx->phys += 1;
+    if (ctx->T_local <= 0) {
+        finish_pass(ctx, op, nacc, pl.nb, io, slot);
+        return;
+    }
+    // single-rank passes finish inside the stream kernel: a cooperative launch
+    // (all CTAs co-resident by construction of the plan) lets the CTAs reduce
+    // each other's partials after one grid barrier, which saves the finish
+    // launch and its dependency gap (latency-bound small panels and Krylov
+    // steps). Multi-rank passes keep the separate finish around the allreduce.
+    const int threads = pl.G * pl.P;
+    static const bool no_fuse = std::getenv("MVSK_NO_FUSED_FINISH") != nullptr;
+    if (!ctx->comm && !no_fuse && threads % 32 == 0) {
+        a.fused = 1;
+        a.fin = finish_args(ctx, op, nacc, pl.nb, io, slot);
+        a.fin.do_reduce = 1;
+        a.fin.do_epi = 1;
+        int ng = finish_groups(pl.nb);
+        while (ng > 1 && threads / ng < 8) ng >>= 1;
+        a.fin_ng = ng;
+        const int cols = threads / ng;
+        const int tot = std::max(a.fin.k, 1) * a.fin.ld;
+        a.fin_nvb = std::max(1, (tot + cols - 1) / cols);
+        void* args[] = {&a};
+        const cudaError_t e =
+            cudaLaunchCooperativeKernel(pl.fn, dim3(pl.nb), dim3(threads), args, pl.smem, ctx->stream);
+        if (e == cudaSuccess) return;
+        if (e != cudaErrorCooperativeLaunchTooLarge) MVSK_CUDA(e);
+        cudaGetLastError();  // not co-resident with this plan: separate finish
+        a.fused = 0;
+    }
+    {
+        void* args[] = {&a};
+        MVSK_CUDA(cudaLaunchKernel(pl.fn, dim3(pl.nb), dim3(threads), args, pl.smem, ctx->stream));
+    }
     finish_pass(ctx, op, nacc, pl.nb, io, slot);
 }
 

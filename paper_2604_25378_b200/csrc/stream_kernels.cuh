@@ -19,16 +19,22 @@
 // :103-113 (third_action), linesearch.hpp:22-44 (power_sums), oracle.hpp:137-140
 // (transpose_apply).
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
 
 #include "ptx.cuh"
 
 namespace mvsk_b200 {
+namespace cg = cooperative_groups;
 
 enum class Op : int { FGRAD = 0, HVP = 1, THIRD = 2, LINESUMS = 3, XTW = 4 };
 
 constexpr int kMaxStages = 8;
 constexpr int kNumScalars = 16;  // per-CTA scalar partial slots
+
+}  // namespace mvsk_b200
+#include "finish.cuh"
+namespace mvsk_b200 {
 
 struct StreamArgs {
     const double* X;   // T_local x ld, row-major, 16-B aligned rows (ld even)
@@ -48,6 +54,11 @@ struct StreamArgs {
     double Tglob;        // global T (the reference divides by T = A.rows())
     const int* skip;     // optional: skip the pass when all nskip flags are 0
     int nskip;
+    // cooperative launch only: after the partials, a grid-wide barrier and the
+    // cross-CTA reduction + epilogue in the same kernel (no finish launch)
+    int fused;
+    int fin_ng, fin_nvb;
+    FinishArgs fin;
 };
 
 // Device-side early exit for speculatively enqueued Krylov steps: the pass is a
@@ -392,6 +403,14 @@ __global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG>::max_threads, 1) stre
             for (int gg = 0; gg < G; ++gg) v += scb[gg * NS + i];
             a.part_sc[(size_t)blockIdx.x * kNumScalars + i] = v;
         }
+    }
+    if (a.fused) {
+        // every CTA's partials are in global memory before any CTA reduces them
+        __threadfence();
+        cg::this_grid().sync();
+        double* part = reinterpret_cast<double*>(stage_base);  // the ring is free
+        for (int vb = blockIdx.x; vb < a.fin_nvb; vb += gridDim.x)
+            finish_block(a.fin, a.fin_ng, vb, tid, (int)blockDim.x, part);
     }
 }
 

@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+bash scripts/gpu_tests.sh
+TUNE_DEFAULT_ONLY=1 timeout 300 python scripts/tune_stream.py C5 hvp1,fgrad,lines,third 2>&1 | grep default
+TUNE_DEFAULT_ONLY=1 timeout 300 python scripts/tune_stream.py C4 hvp1,fgrad 2>&1 | grep default
+TUNE_DEFAULT_ONLY=1 timeout 300 python scripts/tune_stream.py C2 hvp1,fgrad 2>&1 | grep default
+timeout 900 python scripts/solve_bench.py --configs C1,C2,C3,C4 --cpu-max-n 0 --reps 3 2>&1 | cut -c1-200
