@@ -112,7 +112,8 @@ struct CGState {
     double tol;
 };
 
-__global__ void __launch_bounds__(kPT) cg_init_kernel(CGState s, const double* rhs) {
+__global__ void __launch_bounds__(kPT) cg_init_kernel(Geo g, CGState s, const double* rhs, double* vin) {
+    extern __shared__ double q[];
     __shared__ double sh[32];
     const int c = blockIdx.x, mm = s.mm;
     const double* b = rhs + (size_t)c * mm;
@@ -140,6 +141,9 @@ __global__ void __launch_bounds__(kPT) cg_init_kernel(CGState s, const double* r
         s.breakdown[c] = 0;
         s.active[c] = (s.cap > 0 && sqrt(bb) > s.target[c]) ? 1 : 0;  // :94 loop test at it = 0
     }
+    // lift the first search direction into the HVP input row (fused lift_kernel)
+    __syncthreads();
+    lift_col(g, P, true, vin + (size_t)c * g.ld, q, sh);
 }
 
 // lift P (or an arbitrary source block) of the active columns into HVP input rows
@@ -157,7 +161,7 @@ __global__ void __launch_bounds__(kPT) lift_kernel(Geo g, const double* E, int l
 }
 
 // one capped-CG step per active column, from the HVP rows H (full coordinates)
-__global__ void __launch_bounds__(kPT) cg_step_kernel(Geo g, CGState s, const double* H, double lambda) {
+__global__ void __launch_bounds__(kPT) cg_step_kernel(Geo g, CGState s, const double* H, double lambda, double* vin) {
     extern __shared__ double t[];
     __shared__ double sh[32];
     const int c = blockIdx.x, mm = s.mm;
@@ -198,12 +202,17 @@ __global__ void __launch_bounds__(kPT) cg_step_kernel(Geo g, CGState s, const do
     const double rr = block_sum(prr, sh);
     const double beta = rz2 / rz_old;
     for (int i = threadIdx.x; i < mm; i += blockDim.x) P[i] = Z[i] + beta * P[i];
+    const int it = s.iters[c] + 1;
+    const bool still = it < s.cap && sqrt(rr) > s.target[c];  // :94
+    __syncthreads();  // every thread has read iters/target and written its P slice
     if (threadIdx.x == 0) {
         s.rz[c] = rz2;
-        const int it = s.iters[c] + 1;
         s.iters[c] = it;
-        s.active[c] = (it < s.cap && sqrt(rr) > s.target[c]) ? 1 : 0;  // :94
+        s.active[c] = still ? 1 : 0;
     }
+    // lift the next search direction into the HVP input row (fused lift_kernel;
+    // t's reduced-H values are dead here, so it holds q)
+    if (still) lift_col(g, P, true, vin + (size_t)c * g.ld, t, sh);
 }
 
 // out = Q^T U^T H (+ lambda e) per column, or a += sum_c Q^T U^T H_c (in column order)
@@ -288,7 +297,8 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     if (fm.active) MVSK_CUDA(cudaMemcpyAsync(idx, fm.idx.data(), m * sizeof(long long), cudaMemcpyHostToDevice, st));
     Geo g{vU, in.bU, vQ, in.bQ, fm.active ? idx : nullptr, m, (int)ld};
     const size_t dsm = (size_t)2 * std::max(m, 1) * sizeof(double);
-    for (const void* fn : {(const void*)lift_kernel, (const void*)cg_step_kernel, (const void*)reduce_kernel})
+    for (const void* fn : {(const void*)lift_kernel, (const void*)cg_step_kernel, (const void*)reduce_kernel,
+                           (const void*)cg_init_kernel})
         set_smem_attr(fn, dsm);
     const Slot& sl = ctx->slots[slot];
     double* vin = ctx->vin;
@@ -314,14 +324,15 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     // the GPU never idles on a host round trip inside the Krylov loop.
     auto cg = [&](int k, int cap, const double* jdp) {
         CGState s{X, Rm, Z, P, rz, target, active, iters, bdown, jdp, mm, cap, in.tol};
-        cg_init_kernel<<<k, kPT, 0, st>>>(s, src);
+        cg_init_kernel<<<k, kPT, dsm, st>>>(g, s, src, vin);
         MVSK_CUDA(cudaGetLastError());
         int* hf = ws.host_flags;  // [2][K] flag snapshots + [2K..) iters / breakdown
         MVSK_CUDA(cudaMemcpyAsync(hf, active, k * sizeof(int), cudaMemcpyDeviceToHost, st));
         MVSK_CUDA(cudaEventRecord(ws.ev[0], st));
         for (int step = 0; step < cap; ++step) {
-            lift_kernel<<<k, kPT, dsm, st>>>(g, P, mm, true, active, vin);
-            MVSK_CUDA(cudaGetLastError());
+            // vin holds the lifted direction of every active column (cg_init /
+            // the previous cg_step); inactive columns' rows are stale but finite
+            // and their HVP results are ignored
             PassIO io;
             io.vin = vin;
             io.z = sl.z;
@@ -330,7 +341,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
             io.skip = active;
             io.nskip = k;
             run_pass(ctx, Op::HVP, k, io);
-            cg_step_kernel<<<k, kPT, dsm, st>>>(g, s, H, in.lambda);
+            cg_step_kernel<<<k, kPT, dsm, st>>>(g, s, H, in.lambda, vin);
             MVSK_CUDA(cudaGetLastError());
             const int nb = (step + 1) & 1;
             MVSK_CUDA(cudaMemcpyAsync(hf + nb * K, active, k * sizeof(int), cudaMemcpyDeviceToHost, st));
