@@ -656,6 +656,8 @@ static bool run_dmma(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     a.c2 = ctx->c.c2;
     a.c3 = ctx->c.c3;
     a.c4 = ctx->c.c4;
+    a.early_refill = 1;
+    if (const char* e = std::getenv("MVSK_DMMA_EARLY")) a.early_refill = std::atoi(e);
     if (ctx->T_local > 0) {
         void* args[] = {&a};
         MVSK_CUDA(cudaLaunchKernelExC(&cfg, pl.fn, args));

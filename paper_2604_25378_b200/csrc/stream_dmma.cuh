@@ -36,6 +36,7 @@ struct DmmaArgs {
     double c2, c3, c4;
     const int* skip;
     int nskip;
+    int early_refill;  // barrier at the top of produce() and refill there
 };
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
@@ -150,6 +151,12 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
         const long long srow0 = r0 + (long long)s * 8;
         zr[0] = (srow0 + t4 < r1) ? __ldg(a.z + srow0 + t4) : 0.0;
         zr[1] = (srow0 + 4 + t4 < r1) ? __ldg(a.z + srow0 + 4 + t4) : 0.0;
+        if (a.early_refill) {
+            // every warp is past its last read of the slot consumed one stage
+            // earlier: refill it now rather than after this stage's phase 1
+            __syncthreads();
+            if (tid == 0 && s >= D + 1 && s - D - 1 + S < nst) issue(s - D - 1 + S);
+        }
         mbar_wait(&full[slot], (uint32_t)((s / S) & 1));
         const double* X = ring + slot * stage_elems;  // rows past the block end: finite stale data,
                                                       // their dots are never used (zero weights)
@@ -183,7 +190,7 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
                 if (j < NDOT) rb[g4 * NDOT + j] = cfr[0][nt][i];
             }
         __syncthreads();  // (A) warp partials published; all consumes up to s-D-1 done
-        if (tid == 0 && s >= D + 1 && s - D - 1 + S < nst) issue(s - D - 1 + S);
+        if (!a.early_refill && tid == 0 && s >= D + 1 && s - D - 1 + S < nst) issue(s - D - 1 + S);
         if (tid < V) {
             double sum = 0.0;
 #pragma unroll
