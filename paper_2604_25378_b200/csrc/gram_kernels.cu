@@ -8,6 +8,7 @@
 // fp64 has no tcgen05 kind on sm_100a (CUDA 12.9 exposes f16/tf32/f8f6f4/i8/
 // mxf4 only), so DMMA through mma.sync is the tensor-core path for fp64.
 #include <algorithm>
+#include <cmath>
 
 #include "oracle_ops.cuh"
 
@@ -225,6 +226,21 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
     // on one or a few SMs (C1: one CTA over 500 rows, ~65 us per direction)
     int nsplit = std::max(1, ctx->nsm / npairs);
     nsplit = (int)std::max<long long>(1, std::min<long long>(nsplit, ctx->T_local / 64));
+    if (npairs >= ctx->nsm) {
+        // one CTA per SM: pick the split whose (tiles x splits) work items fill
+        // the last wave best (C5: 528 tiles = 3.57 waves -> 7 splits = 24.97
+        // waves); the split partials cost one extra 128 KB write + read per item
+        double best = 0.0;
+        for (int s = 1; s <= 16; ++s) {
+            if (ctx->T_local / s < 64LL * GBK) break;
+            const double w = (double)npairs * s / ctx->nsm;
+            const double eff = w / std::ceil(w);
+            if (eff > best + 0.005) {
+                best = eff;
+                nsplit = s;
+            }
+        }
+    }
     const size_t need = (size_t)nsplit * npairs * GBM * GBM;
     if (ctx->gram_part_elems < need) {
         if (ctx->gram_part) MVSK_CUDA(cudaFree(ctx->gram_part));
