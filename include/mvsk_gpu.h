@@ -199,6 +199,8 @@ int32_t mvsk_gpu_line_model(mvsk_gpu_ctx* ctx, int32_t slot, const double* d, do
 int32_t mvsk_gpu_passes(const mvsk_gpu_ctx* ctx, uint64_t* forward, uint64_t* transpose,
                         uint64_t* physical);
 int32_t mvsk_gpu_reset_passes(mvsk_gpu_ctx* ctx);
+/* kernels this context has enqueued so far (CUDA-graph replays included) */
+int32_t mvsk_gpu_launch_count(const mvsk_gpu_ctx* ctx, uint64_t* launches);
 
 /* ---- direction / solve -------------------------------------------------- */
 /* Weighted Gram G = A_F^T diag(psi''(z)) A_F / T over the current face (nf x nf,

@@ -155,6 +155,7 @@ SIGNATURES = [
     ("mvsk_gpu_line_model", _I32, [_P, _I32, _D, C.c_double, _D]),
     ("mvsk_gpu_passes", _I32, [_P, _U64P, _U64P, _U64P]),
     ("mvsk_gpu_reset_passes", _I32, [_P]),
+    ("mvsk_gpu_launch_count", _I32, [_P, _U64P]),
     ("mvsk_gpu_weighted_gram", _I32, [_P, _I32, _D]),
     ("mvsk_gpu_yand_direction", _I32,
      [_P, _I32, C.POINTER(mvsk_tangent_config), C.c_uint64, _D, C.POINTER(mvsk_direction_diag)]),

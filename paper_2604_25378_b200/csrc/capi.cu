@@ -269,6 +269,12 @@ int32_t mvsk_gpu_mu(const mvsk_gpu_ctx* ctx, double* mu_out) {
     return MVSK_OK;
 }
 
+int32_t mvsk_gpu_launch_count(const mvsk_gpu_ctx* ctx, uint64_t* launches) {
+    if (!ctx || !launches) return MVSK_DOMAIN_ERROR;
+    *launches = ctx->launches;
+    return MVSK_OK;
+}
+
 int32_t mvsk_gpu_destroy(mvsk_gpu_ctx* ctx) {
     free_all(ctx);
     return MVSK_OK;

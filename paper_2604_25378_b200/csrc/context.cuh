@@ -110,6 +110,7 @@ struct mvsk_gpu_ctx {
     int nranks = 1, rank = 0;
 
     uint64_t fwd = 0, tr = 0, phys = 0;
+    uint64_t launches = 0;  // kernels this context enqueued (graph replays included)
     std::string err;
 
     // host-API ops replayed as CUDA graphs (host_ops.cu); entries are dropped
@@ -119,6 +120,7 @@ struct mvsk_gpu_ctx {
         uint64_t epoch;
         cudaGraphExec_t exec;
         uint64_t phys;  // physical passes one replay performs
+        uint64_t launches;  // kernels one replay launches
         bool ok;
     };
     std::vector<GraphEntry> graphs;

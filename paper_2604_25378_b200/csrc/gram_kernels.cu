@@ -259,8 +259,10 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
     a.part = ctx->gram_part;
     const size_t smem = (size_t)(2 * GST * GBK * GLDS + GST * GBK) * sizeof(double);
     set_smem_attr(reinterpret_cast<const void*>(&syrk_dmma_kernel), smem);
+    ++ctx->launches;
     syrk_dmma_kernel<<<dim3(npairs, nsplit), GTHREADS, smem, ctx->stream>>>(a);
     MVSK_CUDA(cudaGetLastError());
+    ++ctx->launches;
     gram_finish_kernel<<<npairs, 256, 0, ctx->stream>>>(ctx->gram_part, npairs, nsplit, n, scale, G_dev, n);
     MVSK_CUDA(cudaGetLastError());
     ctx->phys += 1;
@@ -275,6 +277,7 @@ void run_quadform(mvsk_gpu_ctx* ctx, const double* P_dev, double* q_dev) {
     const int nb = (int)((T + RB - 1) / RB);
     const size_t smem = (size_t)RB * ctx->ld * sizeof(double);
     if (smem > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(&quadform_kernel<RB>), smem);
+    ++ctx->launches;
     quadform_kernel<RB><<<nb, 256, smem, ctx->stream>>>(ctx->X, T, (int)ctx->ld, P_dev, q_dev);
     MVSK_CUDA(cudaGetLastError());
 }
@@ -283,6 +286,7 @@ void run_third_weights(mvsk_gpu_ctx* ctx, const double* z, const double* q, doub
     const long long T = ctx->T_local;
     if (T <= 0) return;
     const int nb = (int)std::min<long long>(4 * ctx->nsm, (T + 255) / 256);
+    ++ctx->launches;
     third_weights_kernel<<<nb, 256, 0, ctx->stream>>>(z, q, tw, T, ctx->c.c3, ctx->c.c4, (double)ctx->T_global);
     MVSK_CUDA(cudaGetLastError());
 }

@@ -106,12 +106,13 @@ void run_graphed(mvsk_gpu_ctx* ctx, int op, int k, int slot, const std::function
         if (g.op == op && g.k == k && g.slot == slot) e = &g;
     if (disabled || !e) {
         enqueue();
-        if (!disabled) ctx->graphs.push_back({op, k, slot, ctx->epoch, nullptr, 0, true});
+        if (!disabled) ctx->graphs.push_back({op, k, slot, ctx->epoch, nullptr, 0, 0, true});
         return;
     }
     if (e->exec && e->epoch == ctx->epoch) {
         MVSK_CUDA(cudaGraphLaunch(e->exec, ctx->stream));
         ctx->phys += e->phys;
+        ctx->launches += e->launches;
         return;
     }
     if (!e->ok || e->epoch != ctx->epoch) {  // buffers moved since: run eagerly once more
@@ -123,7 +124,7 @@ void run_graphed(mvsk_gpu_ctx* ctx, int op, int k, int slot, const std::function
         return;
     }
     // capture
-    const uint64_t p0 = ctx->phys;
+    const uint64_t p0 = ctx->phys, l0 = ctx->launches;
     const uint64_t ep0 = ctx->epoch;
     cudaGraph_t graph = nullptr;
     MVSK_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
@@ -140,15 +141,19 @@ void run_graphed(mvsk_gpu_ctx* ctx, int op, int k, int slot, const std::function
         cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
         e->exec = exec;
         e->phys = ctx->phys - p0;
+        e->launches = ctx->launches - l0;
         ctx->phys = p0;
+        ctx->launches = l0;
         if (graph) cudaGraphDestroy(graph);
         MVSK_CUDA(cudaGraphLaunch(exec, ctx->stream));
         ctx->phys += e->phys;
+        ctx->launches += e->launches;
         return;
     }
     cudaGetLastError();
     if (graph) cudaGraphDestroy(graph);
     ctx->phys = p0;
+    ctx->launches = l0;
     e->ok = false;  // not capturable here: stay eager
     enqueue();
 }

@@ -107,6 +107,7 @@ void ingest_binary(mvsk_gpu_ctx* ctx, const char* path) {
         MVSK_CUDA(cudaMalloc(&sums, (n + 1) * sizeof(double)));
         MVSK_CUDA(cudaMalloc(&bad, sizeof(int)));
         MVSK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+        ++ctx->launches;
         colsum_kernel<<<(int)((n + 127) / 128), 128, 0, ctx->stream>>>(ctx->X, T_loc, (int)ld, (int)n, sums, bad);
         MVSK_CUDA(cudaGetLastError());
         int hbad = 0;
@@ -127,6 +128,7 @@ void ingest_binary(mvsk_gpu_ctx* ctx, const char* path) {
         ctx->mu.resize((size_t)n);
         for (long long j = 0; j < n; ++j) ctx->mu[(size_t)j] = hs[(size_t)j] / (double)ctx->T_global;
         MVSK_CUDA(cudaMemcpyAsync(sums, ctx->mu.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        ++ctx->launches;
         center_kernel<<<4 * ctx->nsm, 256, 0, ctx->stream>>>(ctx->X, T_loc, (int)ld, (int)n, sums);
         MVSK_CUDA(cudaGetLastError());
         MVSK_CUDA(cudaMemcpyAsync(ctx->mu_dev, ctx->mu.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));

@@ -548,11 +548,13 @@ static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO
         f.do_reduce = 1;
         f.do_epi = 1;
         // scalars are reduced by block 0 and consumed by block 0 only
+        ++ctx->launches;
         finish_kernel<<<fb, kFinThreads, 0, ctx->stream>>>(f, ng);
         MVSK_CUDA(cudaGetLastError());
     } else {
         f.do_reduce = 1;
         f.do_epi = 0;
+        ++ctx->launches;
         finish_kernel<<<fb, kFinThreads, 0, ctx->stream>>>(f, ng);
         MVSK_CUDA(cudaGetLastError());
         const int nsc = op == Op::FGRAD ? 3 : (op == Op::LINESUMS ? 9 : 0);
@@ -560,6 +562,7 @@ static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO
         MVSK_NCCL(ncclAllReduce(ctx->red, ctx->red, cnt, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
         f.do_reduce = 0;
         f.do_epi = 1;
+        ++ctx->launches;
         finish_kernel<<<fb, kFinThreads, 0, ctx->stream>>>(f, ng);
         MVSK_CUDA(cudaGetLastError());
     }
@@ -609,6 +612,7 @@ static bool run_cluster(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     a.c4 = ctx->c.c4;
     if (ctx->T_local > 0) {
         void* args[] = {&a};
+        ++ctx->launches;
         MVSK_CUDA(cudaLaunchKernelExC(&cfg, pl.fn, args));
     }
     ctx->phys += 1;
@@ -660,6 +664,7 @@ static bool run_dmma(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     if (const char* e = std::getenv("MVSK_DMMA_EARLY")) a.early_refill = std::atoi(e);
     if (ctx->T_local > 0) {
         void* args[] = {&a};
+        ++ctx->launches;
         MVSK_CUDA(cudaLaunchKernelExC(&cfg, pl.fn, args));
     }
     ctx->phys += 1;
@@ -731,13 +736,17 @@ static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
         void* args[] = {&a};
         const cudaError_t e =
             cudaLaunchCooperativeKernel(pl.fn, dim3(pl.nb), dim3(threads), args, pl.smem, ctx->stream);
-        if (e == cudaSuccess) return;
+        if (e == cudaSuccess) {
+            ++ctx->launches;
+            return;
+        }
         if (e != cudaErrorCooperativeLaunchTooLarge) MVSK_CUDA(e);
         cudaGetLastError();  // not co-resident with this plan: separate finish
         a.fused = 0;
     }
     {
         void* args[] = {&a};
+        ++ctx->launches;
         MVSK_CUDA(cudaLaunchKernel(pl.fn, dim3(pl.nb), dim3(threads), args, pl.smem, ctx->stream));
     }
     finish_pass(ctx, op, nacc, pl.nb, io, slot);
@@ -746,6 +755,7 @@ static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
 void run_psi2(mvsk_gpu_ctx* ctx, const double* z, double* out, long long T) {
     if (T <= 0) return;
     const int nb = (int)std::min<long long>(4 * ctx->nsm, (T + 255) / 256);
+    ++ctx->launches;
     psi2_kernel<<<nb, 256, 0, ctx->stream>>>(z, out, T, ctx->c.c2, ctx->c.c3, ctx->c.c4);
     MVSK_CUDA(cudaGetLastError());
 }

@@ -324,6 +324,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     // the GPU never idles on a host round trip inside the Krylov loop.
     auto cg = [&](int k, int cap, const double* jdp) {
         CGState s{X, Rm, Z, P, rz, target, active, iters, bdown, jdp, mm, cap, in.tol};
+        ++ctx->launches;
         cg_init_kernel<<<k, kPT, dsm, st>>>(g, s, src, vin);
         MVSK_CUDA(cudaGetLastError());
         int* hf = ws.host_flags;  // [2][K] flag snapshots + [2K..) iters / breakdown
@@ -341,6 +342,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
             io.skip = active;
             io.nskip = k;
             run_pass(ctx, Op::HVP, k, io);
+            ++ctx->launches;
             cg_step_kernel<<<k, kPT, dsm, st>>>(g, s, H, in.lambda, vin);
             MVSK_CUDA(cudaGetLastError());
             const int nb = (step + 1) & 1;
@@ -373,9 +375,11 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         std::vector<double> buf((size_t)k * mm);
         for (int p = 0; p < k; ++p) std::copy(in.jacobi_probes[p].begin(), in.jacobi_probes[p].end(), buf.begin() + (size_t)p * mm);
         MVSK_CUDA(cudaMemcpyAsync(src, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        ++ctx->launches;
         lift_kernel<<<k, kPT, dsm, st>>>(g, src, mm, true, nullptr, vin);
         MVSK_CUDA(cudaGetLastError());
         hvp_rows(k, k);
+        ++ctx->launches;
         reduce_kernel<<<k, kPT, dsm, st>>>(g, H, k, true, rows, mm);
         MVSK_CUDA(cudaGetLastError());
         // + lambda r (Hop), then the mean of r o Hop(r)
@@ -397,9 +401,11 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     }
 
     // ---- h = Q^T U^T grad2 f (U nu)  (:212-213)
+    ++ctx->launches;
     lift_kernel<<<1, kPT, dsm, st>>>(g, nu, m1, false, nullptr, vin);
     MVSK_CUDA(cudaGetLastError());
     hvp_rows(1, 1);
+    ++ctx->launches;
     reduce_kernel<<<1, kPT, dsm, st>>>(g, H, 1, true, hvec, mm);
     MVSK_CUDA(cudaGetLastError());
 
@@ -418,7 +424,9 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
             MVSK_CUDA(cudaMemcpyAsync(src, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice, st));
             cg(k, in.probe_cap, jdp);
             // third_action(U Q s_p, U Q r_p) for the block, one fused pass
+            ++ctx->launches;
             lift_kernel<<<k, kPT, dsm, st>>>(g, X, mm, true, nullptr, vin);
+            ++ctx->launches;
             lift_kernel<<<k, kPT, dsm, st>>>(g, src, mm, true, nullptr, vin2);
             MVSK_CUDA(cudaGetLastError());
             PassIO io;
@@ -430,6 +438,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
             run_pass(ctx, Op::THIRD, k, io);
             ctx->fwd += 2 * k;
             ctx->tr += k;
+            ++ctx->launches;
             reduce_kernel<<<k, kPT, dsm, st>>>(g, H, k, true, rows, mm);
             MVSK_CUDA(cudaGetLastError());
             // accumulate in probe order on the host (a is an mm-vector)

@@ -293,6 +293,12 @@ class GpuOracle:
     def reset_passes(self):
         self.lib.mvsk_gpu_reset_passes(self._ctx)
 
+    def launch_count(self) -> int:
+        """Kernels this context has enqueued (graph replays included)."""
+        v = C.c_uint64()
+        self._chk(self.lib.mvsk_gpu_launch_count(self._ctx, C.byref(v)))
+        return v.value
+
     # ---- linesearch.hpp / affine_normal.hpp / solver.hpp ------------------
     def line_model(self, cache: OracleCache, d, cap: float) -> LineModel:
         d = _vec(d, self._m)
