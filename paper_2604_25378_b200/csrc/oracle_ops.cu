@@ -539,7 +539,10 @@ static FinishArgs finish_args(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const 
 
 static int finish_groups(int nb) { return nb >= 512 ? 32 : nb >= 128 ? 8 : 4; }
 
-static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO& io, Slot* slot) {
+// reduced: the CTA partials were already reduced into ctx->red inside the pass
+// (cooperative launch with do_epi = 0); only the allreduce and epilogue remain
+static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO& io, Slot* slot,
+                        bool reduced = false) {
     FinishArgs f = finish_args(ctx, op, nacc, nb, io, slot);
     const int tot = std::max(f.k, 1) * f.ld;
     const int ng = finish_groups(nb);
@@ -552,11 +555,13 @@ static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO
         finish_kernel<<<fb, kFinThreads, 0, ctx->stream>>>(f, ng);
         MVSK_CUDA(cudaGetLastError());
     } else {
-        f.do_reduce = 1;
-        f.do_epi = 0;
-        ++ctx->launches;
-        finish_kernel<<<fb, kFinThreads, 0, ctx->stream>>>(f, ng);
-        MVSK_CUDA(cudaGetLastError());
+        if (!reduced) {
+            f.do_reduce = 1;
+            f.do_epi = 0;
+            ++ctx->launches;
+            finish_kernel<<<fb, kFinThreads, 0, ctx->stream>>>(f, ng);
+            MVSK_CUDA(cudaGetLastError());
+        }
         const int nsc = op == Op::FGRAD ? 3 : (op == Op::LINESUMS ? 9 : 0);
         const size_t cnt = (size_t)(op == Op::LINESUMS ? 0 : tot) + nsc;
         MVSK_NCCL(ncclAllReduce(ctx->red, ctx->red, cnt, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
@@ -715,18 +720,19 @@ static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
         finish_pass(ctx, op, nacc, pl.nb, io, slot);
         return;
     }
-    // single-rank passes finish inside the stream kernel: a cooperative launch
-    // (all CTAs co-resident by construction of the plan) lets the CTAs reduce
-    // each other's partials after one grid barrier, which saves the finish
-    // launch and its dependency gap (latency-bound small panels and Krylov
-    // steps). Multi-rank passes keep the separate finish around the allreduce.
+    // the cross-CTA reduction runs inside the stream kernel: a cooperative
+    // launch (all CTAs co-resident by construction of the plan) lets the CTAs
+    // reduce each other's partials after one grid barrier, which saves the
+    // finish launch and its dependency gap (latency-bound small panels and
+    // Krylov steps). Single rank: the epilogue runs there too; row-sharded
+    // groups: the reduced buffer goes to the allreduce, then the epilogue kernel.
     const int threads = pl.G * pl.P;
     static const bool no_fuse = std::getenv("MVSK_NO_FUSED_FINISH") != nullptr;
-    if (!ctx->comm && !no_fuse && threads % 32 == 0) {
+    if (!no_fuse && threads % 32 == 0) {
         a.fused = 1;
         a.fin = finish_args(ctx, op, nacc, pl.nb, io, slot);
         a.fin.do_reduce = 1;
-        a.fin.do_epi = 1;
+        a.fin.do_epi = ctx->comm ? 0 : 1;
         int ng = finish_groups(pl.nb);
         while (ng > 1 && threads / ng < 8) ng >>= 1;
         a.fin_ng = ng;
@@ -738,6 +744,7 @@ static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
             cudaLaunchCooperativeKernel(pl.fn, dim3(pl.nb), dim3(threads), args, pl.smem, ctx->stream);
         if (e == cudaSuccess) {
             ++ctx->launches;
+            if (ctx->comm) finish_pass(ctx, op, nacc, pl.nb, io, slot, true);
             return;
         }
         if (e != cudaErrorCooperativeLaunchTooLarge) MVSK_CUDA(e);
