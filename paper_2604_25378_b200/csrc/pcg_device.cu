@@ -160,10 +160,21 @@ __global__ void __launch_bounds__(kPT) lift_kernel(Geo g, const double* E, int l
     lift_col(g, E + (size_t)c * ldE, apply_q, row, q, sh);
 }
 
+// step parameters live in device memory so one instantiated Krylov graph serves
+// every direction (the reflector scalars, face size, cap and tolerance change)
+struct StepParams {
+    Geo g;
+    CGState s;
+    double lambda;
+};
+
 // one capped-CG step per active column, from the HVP rows H (full coordinates)
-__global__ void __launch_bounds__(kPT) cg_step_kernel(Geo g, CGState s, const double* H, double lambda, double* vin) {
+__global__ void __launch_bounds__(kPT) cg_step_kernel(const StepParams* sp, const double* H, double* vin) {
     extern __shared__ double t[];
     __shared__ double sh[32];
+    const Geo g = sp->g;
+    const CGState s = sp->s;
+    const double lambda = sp->lambda;
     const int c = blockIdx.x, mm = s.mm;
     if (!s.active[c]) return;
     // thread 0 rewrites rz only after every thread passed the barriers below
@@ -226,6 +237,16 @@ __global__ void __launch_bounds__(kPT) reduce_kernel(Geo g, const double* H, int
     for (int i = threadIdx.x; i < len; i += blockDim.x) out[(size_t)c * ldo + i] = r[i];
 }
 
+// while-loop condition of the device Krylov graph: another step iff any column
+// is still active (each column's own test already includes the cap, :94)
+__global__ void cg_decide_kernel(const int* active, int k, cudaGraphConditionalHandle h) {
+    if (threadIdx.x == 0) {
+        int any = 0;
+        for (int c = 0; c < k; ++c) any |= active[c];
+        cudaGraphSetConditional(h, any ? 1u : 0u);
+    }
+}
+
 template <class T>
 T* carve(unsigned char*& cur, size_t count) {
     T* p = reinterpret_cast<T*>(cur);
@@ -239,11 +260,25 @@ struct PcgWorkspace {
     size_t bytes = 0;
     unsigned char* dev = nullptr;
     int* host_flags = nullptr;  // pinned [4 * kPcgMaxCols]
+    StepParams* host_params = nullptr;  // pinned staging of the device StepParams
     cudaEvent_t ev[2] = {nullptr, nullptr};
+    // device-resident Krylov loops: a conditional-while graph per (k, slot)
+    struct LoopGraph {
+        int k, slot;
+        uint64_t epoch;
+        cudaGraphExec_t exec;
+        uint64_t phys_per_step, launches_per_step;
+    };
+    std::vector<LoopGraph> graphs;
+    std::vector<std::pair<int, int>> seen;  // (k, slot) keys that ran once (sized every workspace)
+    bool graphs_broken = false;
 };
 
 void pcg_workspace_free(mvsk_gpu_ctx* ctx) {
     if (!ctx->pcg) return;
+    for (auto& lg : ctx->pcg->graphs)
+        if (lg.exec) cudaGraphExecDestroy(lg.exec);
+    if (ctx->pcg->host_params) cudaFreeHost(ctx->pcg->host_params);
     if (ctx->pcg->dev) cudaFree(ctx->pcg->dev);
     if (ctx->pcg->host_flags) cudaFreeHost(ctx->pcg->host_flags);
     for (cudaEvent_t e : ctx->pcg->ev)
@@ -256,9 +291,11 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     const int m = (int)in.m, m1 = m - 1, mm = m - 2;
     const int K = kPcgMaxCols;
     const size_t ld = (size_t)ctx->ld;
-    // ---- workspace
-    const size_t need = 256 * 32 + sizeof(double) * ((size_t)m + m1 + m1 + 6 * (size_t)K * mm + 4 * mm + 4 * K) +
-                        sizeof(long long) * m + sizeof(int) * 4 * K;
+    // ---- workspace, carved for the full n so its pointers do not move with the
+    // face size (they are baked into the instantiated Krylov graphs)
+    const long long N = ctx->n;
+    const size_t need = 256 * 32 + sizeof(double) * ((size_t)N + N + N + 6 * (size_t)K * N + 4 * N + 4 * K) +
+                        sizeof(long long) * N + sizeof(int) * 4 * K + sizeof(StepParams) + 256;
     if (!ctx->pcg) ctx->pcg = new PcgWorkspace();
     PcgWorkspace& ws = *ctx->pcg;
     if (ws.bytes < need) {
@@ -266,29 +303,32 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         ws.dev = nullptr;
         MVSK_CUDA(cudaMalloc(&ws.dev, need));
         ws.bytes = need;
+        ++ctx->epoch;
     }
     if (!ws.host_flags) MVSK_CUDA(cudaMallocHost(&ws.host_flags, sizeof(int) * 4 * K));
+    if (!ws.host_params) MVSK_CUDA(cudaMallocHost(&ws.host_params, sizeof(StepParams)));
     for (cudaEvent_t& e : ws.ev)
         if (!e) MVSK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     unsigned char* cur = ws.dev;
-    double* vU = carve<double>(cur, m);
-    double* vQ = carve<double>(cur, m1);
-    double* nu = carve<double>(cur, m1);
-    double* X = carve<double>(cur, (size_t)K * mm);
-    double* Rm = carve<double>(cur, (size_t)K * mm);
-    double* Z = carve<double>(cur, (size_t)K * mm);
-    double* P = carve<double>(cur, (size_t)K * mm);
-    double* src = carve<double>(cur, (size_t)K * mm);  // rhs / probes
-    double* rows = carve<double>(cur, (size_t)K * mm);  // reduced outputs
-    double* jd = carve<double>(cur, mm);
-    double* hvec = carve<double>(cur, mm);
-    double* avec = carve<double>(cur, mm);
+    double* vU = carve<double>(cur, N);
+    double* vQ = carve<double>(cur, N);
+    double* nu = carve<double>(cur, N);
+    double* X = carve<double>(cur, (size_t)K * N);  // [k][mm] blocks
+    double* Rm = carve<double>(cur, (size_t)K * N);
+    double* Z = carve<double>(cur, (size_t)K * N);
+    double* P = carve<double>(cur, (size_t)K * N);
+    double* src = carve<double>(cur, (size_t)K * N);  // rhs / probes
+    double* rows = carve<double>(cur, (size_t)K * N);  // reduced outputs
+    double* jd = carve<double>(cur, N);
+    double* hvec = carve<double>(cur, N);
+    double* avec = carve<double>(cur, N);
     double* rz = carve<double>(cur, K);
     double* target = carve<double>(cur, K);
-    long long* idx = carve<long long>(cur, m);
+    long long* idx = carve<long long>(cur, N);
     int* active = carve<int>(cur, K);
     int* iters = carve<int>(cur, K);
     int* bdown = carve<int>(cur, K);
+    StepParams* sp_dev = carve<StepParams>(cur, 1);
     cudaStream_t st = ctx->stream;
 
     MVSK_CUDA(cudaMemcpyAsync(vU, in.vU.data(), m * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -297,9 +337,10 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     if (fm.active) MVSK_CUDA(cudaMemcpyAsync(idx, fm.idx.data(), m * sizeof(long long), cudaMemcpyHostToDevice, st));
     Geo g{vU, in.bU, vQ, in.bQ, fm.active ? idx : nullptr, m, (int)ld};
     const size_t dsm = (size_t)2 * std::max(m, 1) * sizeof(double);
+    const size_t dsm_max = (size_t)2 * std::max<long long>(N, 1) * sizeof(double);  // cg_step (graph-baked)
     for (const void* fn : {(const void*)lift_kernel, (const void*)cg_step_kernel, (const void*)reduce_kernel,
                            (const void*)cg_init_kernel})
-        set_smem_attr(fn, dsm);
+        set_smem_attr(fn, dsm_max);
     const Slot& sl = ctx->slots[slot];
     double* vin = ctx->vin;
     double* vin2 = ctx->vin + (size_t)MVSK_GPU_MAX_RHS * ld;
@@ -322,11 +363,124 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     // that gate step s, and a step whose flags are all 0 is a device-side no-op
     // (every kernel of the step, including the HVP pass, exits on entry). So
     // the GPU never idles on a host round trip inside the Krylov loop.
+    // Capped CG on k columns in lock-step (the columns' arithmetic is
+    // cg_capped's). Preferred: the whole loop is ONE conditional-while CUDA graph
+    // (body = the k-RHS HVP pass, cg_step, and a 1-thread kernel that sets the
+    // loop condition from the columns' activity flags), so no host round trip
+    // happens inside the Krylov loop; the graph is instantiated once per
+    // (k, slot) and reused for every direction (its parameters live in device
+    // memory). Fallback: a host-driven loop that enqueues step s+1 before
+    // reading the flags that gate step s (a step whose flags are all 0 is a
+    // device-side no-op), so the GPU does not idle on the round trip either.
+    auto finish_counts = [&](int k, bool count_passes) {
+        int* hf = ws.host_flags;
+        MVSK_CUDA(cudaMemcpyAsync(hf + 2 * K, iters, k * sizeof(int), cudaMemcpyDeviceToHost, st));
+        MVSK_CUDA(cudaMemcpyAsync(hf + 3 * K, bdown, k * sizeof(int), cudaMemcpyDeviceToHost, st));
+        MVSK_CUDA(cudaStreamSynchronize(st));
+        int steps = 0;
+        for (int c = 0; c < k; ++c) {
+            const int col_steps = hf[2 * K + c] + (hf[3 * K + c] ? 1 : 0);  // HVPs column c consumed
+            out.iters += hf[2 * K + c];
+            if (hf[3 * K + c]) out.breakdown = true;
+            steps = std::max(steps, col_steps);
+            if (count_passes) {
+                ctx->fwd += col_steps;  // reference contract: 2 passes per (active) HVP
+                ctx->tr += col_steps;
+            }
+        }
+        return steps;
+    };
+    static const bool no_graph = std::getenv("MVSK_NO_CG_GRAPH") != nullptr;
+    auto cg_graph = [&](int k) -> PcgWorkspace::LoopGraph* {
+        if (no_graph || ws.graphs_broken) return nullptr;
+        // the first loop of a key runs host-driven: it sizes the pass workspaces,
+        // which must not be (re)allocated while a graph is being captured
+        if (std::find(ws.seen.begin(), ws.seen.end(), std::make_pair(k, slot)) == ws.seen.end()) {
+            ws.seen.emplace_back(k, slot);
+            return nullptr;
+        }
+        for (auto& lg : ws.graphs)
+            if (lg.k == k && lg.slot == slot) {
+                if (lg.epoch == ctx->epoch && lg.exec) return &lg;
+                if (lg.exec) cudaGraphExecDestroy(lg.exec);
+                lg.exec = nullptr;
+            }
+        cudaGraph_t gr = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        const uint64_t p0 = ctx->phys, l0 = ctx->launches;
+        bool ok = cudaGraphCreate(&gr, 0) == cudaSuccess;
+        cudaGraphConditionalHandle h{};
+        cudaGraphNode_t n0 = nullptr, wn = nullptr;
+        if (ok) ok = cudaGraphConditionalHandleCreate(&h, gr, 0, 0) == cudaSuccess;
+        if (ok) {  // initial condition: any column active after cg_init
+            int kk = k;
+            void* args[] = {&active, &kk, &h};
+            cudaKernelNodeParams kp{};
+            kp.func = reinterpret_cast<void*>(&cg_decide_kernel);
+            kp.gridDim = dim3(1);
+            kp.blockDim = dim3(32);
+            kp.kernelParams = args;
+            ok = cudaGraphAddKernelNode(&n0, gr, nullptr, 0, &kp) == cudaSuccess;
+        }
+        cudaGraph_t body = nullptr;
+        if (ok) {
+            cudaGraphNodeParams cp{};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            ok = cudaGraphAddNode(&wn, gr, &n0, 1, &cp) == cudaSuccess;
+            if (ok) body = cp.conditional.phGraph_out[0];
+        }
+        if (ok) ok = cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+                     cudaSuccess;
+        if (ok) {
+            bool threw = false;
+            try {
+                PassIO io;
+                io.vin = vin;
+                io.z = sl.z;
+                io.out = H;
+                io.ldo = (long long)ld;
+                run_pass(ctx, Op::HVP, k, io);
+                ++ctx->launches;
+                cg_step_kernel<<<k, kPT, dsm_max, st>>>(sp_dev, H, vin);
+                ++ctx->launches;
+                cg_decide_kernel<<<1, 32, 0, st>>>(active, k, h);
+            } catch (...) {
+                threw = true;
+            }
+            cudaGraph_t captured = nullptr;
+            ok = cudaStreamEndCapture(st, &captured) == cudaSuccess && !threw;
+        }
+        if (ok) ok = cudaGraphInstantiate(&exec, gr, 0) == cudaSuccess;
+        const uint64_t dp = ctx->phys - p0, dl = ctx->launches - l0;
+        ctx->phys = p0;
+        ctx->launches = l0;
+        if (gr) cudaGraphDestroy(gr);
+        cudaGetLastError();
+        if (!ok) {
+            if (exec) cudaGraphExecDestroy(exec);
+            ws.graphs_broken = true;  // e.g. a launch kind the conditional body rejects: host loop
+            return nullptr;
+        }
+        ws.graphs.push_back({k, slot, ctx->epoch, exec, dp, dl});
+        return &ws.graphs.back();
+    };
     auto cg = [&](int k, int cap, const double* jdp) {
         CGState s{X, Rm, Z, P, rz, target, active, iters, bdown, jdp, mm, cap, in.tol};
+        *ws.host_params = StepParams{g, s, in.lambda};
+        MVSK_CUDA(cudaMemcpyAsync(sp_dev, ws.host_params, sizeof(StepParams), cudaMemcpyHostToDevice, st));
         ++ctx->launches;
         cg_init_kernel<<<k, kPT, dsm, st>>>(g, s, src, vin);
         MVSK_CUDA(cudaGetLastError());
+        if (PcgWorkspace::LoopGraph* lg = cg_graph(k)) {
+            MVSK_CUDA(cudaGraphLaunch(lg->exec, st));
+            const int steps = finish_counts(k, true);
+            ctx->phys += (uint64_t)steps * lg->phys_per_step;
+            ctx->launches += 1 + (uint64_t)steps * lg->launches_per_step;
+            return;
+        }
         int* hf = ws.host_flags;  // [2][K] flag snapshots + [2K..) iters / breakdown
         MVSK_CUDA(cudaMemcpyAsync(hf, active, k * sizeof(int), cudaMemcpyDeviceToHost, st));
         MVSK_CUDA(cudaEventRecord(ws.ev[0], st));
@@ -343,7 +497,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
             io.nskip = k;
             run_pass(ctx, Op::HVP, k, io);
             ++ctx->launches;
-            cg_step_kernel<<<k, kPT, dsm, st>>>(g, s, H, in.lambda, vin);
+            cg_step_kernel<<<k, kPT, dsm_max, st>>>(sp_dev, H, vin);
             MVSK_CUDA(cudaGetLastError());
             const int nb = (step + 1) & 1;
             MVSK_CUDA(cudaMemcpyAsync(hf + nb * K, active, k * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -356,16 +510,8 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
                 ctx->phys -= 1;  // the step ran as a no-op
                 break;
             }
-            ctx->fwd += nact;  // reference contract: 2 passes per (active) HVP
-            ctx->tr += nact;
         }
-        MVSK_CUDA(cudaMemcpyAsync(hf + 2 * K, iters, k * sizeof(int), cudaMemcpyDeviceToHost, st));
-        MVSK_CUDA(cudaMemcpyAsync(hf + 3 * K, bdown, k * sizeof(int), cudaMemcpyDeviceToHost, st));
-        MVSK_CUDA(cudaStreamSynchronize(st));
-        for (int c = 0; c < k; ++c) {
-            out.iters += hf[2 * K + c];
-            if (hf[3 * K + c]) out.breakdown = true;
-        }
+        finish_counts(k, true);
     };
 
     // ---- Jacobi diagonal (:197-209): 8 probes through Hop in one batch
