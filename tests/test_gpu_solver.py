@@ -300,3 +300,38 @@ def test_floor_sweep_matches_cpu_mirror(name, mode):
     x = rh.simplex_point(A.shape[1], 3, 1e-3)
     cc = po.CpuOracle(A, mu, c).make_cache(x)
     assert abs(g.value(g.make_cache(x)) - po.CpuOracle(A, mu, c).value(cc)) <= 1e-12 * (1 + abs(po.CpuOracle(A, mu, c).value(cc)))
+
+
+def test_krylov_graph_replays_bitwise():
+    """The first Krylov loop of a (k, slot) key runs host-driven, later ones as
+    the conditional-while CUDA graph (pcg_device.cu): same kernels in the same
+    order, so directions, iteration counts and the pass contract must be
+    bitwise identical across repeated calls, on the full panel and on faces of
+    different sizes (the graph is reused with new device-side parameters)."""
+    from paper_2604_25378_b200.datagen import make_panel
+    from paper_2604_25378_b200.gpu_oracle import GpuOracle, tangent_config
+    A, mu, c = make_panel("C2", seed=6, kappa=10.0)
+    n = A.shape[1]
+    g = GpuOracle(A, mu, c)
+    tau = 1e-8
+    cases = [(None, rh.simplex_point(n, 5, 1e-6))]
+    for drop in ([2, 9], [1, 4, 30, 77]):
+        x = rh.simplex_point(n, 8 + len(drop), 1e-6)
+        x[drop] = tau
+        idx = np.array([i for i in range(n) if i not in drop])
+        cases.append((idx, x[idx]))
+    for kw in (dict(lam=1e-4), dict(lam=1e-4, jacobi=True)):
+        for idx, xf in cases:
+            if idx is None:
+                g.set_face()
+            else:
+                g.set_face(idx, tau)
+            outs = []
+            for _ in range(3):
+                gc = g.make_cache(xf)
+                g.reset_passes()
+                d, diag = g.yand_direction(gc, tangent_config("pcg", **kw), 11)
+                outs.append((d, diag.krylov_iters, diag.pcg_breakdown, g.passes()[:2]))
+            for d, it, bd, ps in outs[1:]:
+                assert np.array_equal(d, outs[0][0])
+                assert (it, bd, ps) == outs[0][1:]
