@@ -643,12 +643,8 @@ Vec yand_direction(const View& O, int slot, const TangentCfg& cfg, uint64_t it_s
             }
         }
         if (has_third) {
-            if (cfg.exact_trace) {  // :217-226
-                for (long long k = 0; k < mm; ++k) {
-                    Vec e((size_t)mm, 0.0);
-                    e[(size_t)k] = 1.0;
-                    in.probes.push_back(std::move(e));
-                }
+            if (cfg.exact_trace) {  // :217-226, unit vectors generated on the device
+                in.unit_probes = true;
             } else {  // :227-237
                 SplitMix64 rng(0x5eedULL ^ it_seed);
                 for (int pr = 0; pr < cfg.probes; ++pr) {

@@ -22,6 +22,7 @@ namespace mvsk_b200 {
 namespace {
 
 constexpr int kPT = 512;  // threads per column CTA
+constexpr int kMaxDeferred = 64;  // Krylov loops per direction (probe blocks + main)
 
 __device__ double block_sum(double v, double* sh) {
     // fixed-order tree: warp shuffles then a 16-way smem combine
@@ -237,6 +238,47 @@ __global__ void __launch_bounds__(kPT) reduce_kernel(Geo g, const double* H, int
     for (int i = threadIdx.x; i < len; i += blockDim.x) out[(size_t)c * ldo + i] = r[i];
 }
 
+// Jacobi diagonal from the probe responses (:197-209): mean over probes of
+// r o (Qt Ut H U Q r + lambda r), floored at max(1e-12, lambda); probe order fixed
+__global__ void jacobi_diag_kernel(const double* probes, const double* rows, int k, int mm, double lambda, double fl,
+                                   double* jd) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mm; i += gridDim.x * blockDim.x) {
+        double v = 0.0;
+        for (int p = 0; p < k; ++p) {
+            const double r = probes[(size_t)p * mm + i];
+            v += r * (rows[(size_t)p * mm + i] + lambda * r);
+        }
+        v /= (double)k;
+        jd[i] = v > fl ? v : fl;
+    }
+}
+
+// exact-trace probes e_{b0}..e_{b0+k-1} (:217-226)
+__global__ void unit_probe_kernel(double* src, int k, int mm, int b0) {
+    const size_t tot = (size_t)k * mm;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+        const int p = (int)(e / mm), i = (int)(e - (size_t)p * mm);
+        src[e] = (i == b0 + p) ? 1.0 : 0.0;
+    }
+}
+
+// a += sum of the block's third-action rows, in probe order (:225, :235)
+__global__ void accum_rows_kernel(const double* rows, int k, int mm, double* a) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mm; i += gridDim.x * blockDim.x) {
+        double v = a[i];
+        for (int p = 0; p < k; ++p) v += rows[(size_t)p * mm + i];
+        a[i] = v;
+    }
+}
+
+// rhs = h - (||gbar|| / n) a, a averaged over the Hutchinson probes (:236, :239)
+__global__ void rhs_kernel(const double* h, const double* a, int mm, double adiv, double coef, double* rhs) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mm; i += gridDim.x * blockDim.x) {
+        const double ai = adiv > 0 ? a[i] / adiv : a[i];
+        rhs[i] = h[i] - coef * ai;
+    }
+}
+
 // while-loop condition of the device Krylov graph: another step iff any column
 // is still active (each column's own test already includes the cap, :94)
 __global__ void cg_decide_kernel(const int* active, int k, cudaGraphConditionalHandle h) {
@@ -260,7 +302,10 @@ struct PcgWorkspace {
     size_t bytes = 0;
     unsigned char* dev = nullptr;
     int* host_flags = nullptr;  // pinned [4 * kPcgMaxCols]
-    StepParams* host_params = nullptr;  // pinned staging of the device StepParams
+    StepParams* host_params = nullptr;  // pinned staging of the device StepParams [kMaxDeferred]
+    int* host_counts = nullptr;         // pinned [kMaxDeferred][2][K] iters / breakdown snapshots
+    double* host_stage = nullptr;       // pinned probe staging
+    size_t host_stage_elems = 0;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     // device-resident Krylov loops: a conditional-while graph per (k, slot)
     struct LoopGraph {
@@ -279,6 +324,8 @@ void pcg_workspace_free(mvsk_gpu_ctx* ctx) {
     for (auto& lg : ctx->pcg->graphs)
         if (lg.exec) cudaGraphExecDestroy(lg.exec);
     if (ctx->pcg->host_params) cudaFreeHost(ctx->pcg->host_params);
+    if (ctx->pcg->host_counts) cudaFreeHost(ctx->pcg->host_counts);
+    if (ctx->pcg->host_stage) cudaFreeHost(ctx->pcg->host_stage);
     if (ctx->pcg->dev) cudaFree(ctx->pcg->dev);
     if (ctx->pcg->host_flags) cudaFreeHost(ctx->pcg->host_flags);
     for (cudaEvent_t e : ctx->pcg->ev)
@@ -306,7 +353,20 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         ++ctx->epoch;
     }
     if (!ws.host_flags) MVSK_CUDA(cudaMallocHost(&ws.host_flags, sizeof(int) * 4 * K));
-    if (!ws.host_params) MVSK_CUDA(cudaMallocHost(&ws.host_params, sizeof(StepParams)));
+    // one pinned StepParams per Krylov loop of the direction: the H2D copies are
+    // asynchronous, so a later loop must not overwrite an earlier loop's staging
+    if (!ws.host_params) MVSK_CUDA(cudaMallocHost(&ws.host_params, sizeof(StepParams) * kMaxDeferred));
+    if (!ws.host_counts) MVSK_CUDA(cudaMallocHost(&ws.host_counts, sizeof(int) * kMaxDeferred * 2 * K));
+    // pinned probe staging: the Jacobi probes and every Hutchinson probe of this
+    // direction, copied asynchronously (no host round trip inside the direction)
+    const size_t stage_need = (in.jacobi_probes.size() + in.probes.size()) * (size_t)std::max(mm, 1);
+    if (ws.host_stage_elems < stage_need) {
+        if (ws.host_stage) MVSK_CUDA(cudaFreeHost(ws.host_stage));
+        ws.host_stage = nullptr;
+        ws.host_stage_elems = 0;
+        MVSK_CUDA(cudaMallocHost(&ws.host_stage, stage_need * sizeof(double)));
+        ws.host_stage_elems = stage_need;
+    }
     for (cudaEvent_t& e : ws.ev)
         if (!e) MVSK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     unsigned char* cur = ws.dev;
@@ -372,23 +432,40 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     // memory). Fallback: a host-driven loop that enqueues step s+1 before
     // reading the flags that gate step s (a step whose flags are all 0 is a
     // device-side no-op), so the GPU does not idle on the round trip either.
-    auto finish_counts = [&](int k, bool count_passes) {
-        int* hf = ws.host_flags;
-        MVSK_CUDA(cudaMemcpyAsync(hf + 2 * K, iters, k * sizeof(int), cudaMemcpyDeviceToHost, st));
-        MVSK_CUDA(cudaMemcpyAsync(hf + 3 * K, bdown, k * sizeof(int), cudaMemcpyDeviceToHost, st));
-        MVSK_CUDA(cudaStreamSynchronize(st));
-        int steps = 0;
-        for (int c = 0; c < k; ++c) {
-            const int col_steps = hf[2 * K + c] + (hf[3 * K + c] ? 1 : 0);  // HVPs column c consumed
-            out.iters += hf[2 * K + c];
-            if (hf[3 * K + c]) out.breakdown = true;
-            steps = std::max(steps, col_steps);
-            if (count_passes) {
+    // per-cg-call bookkeeping, settled after the direction's single final sync
+    struct Deferred {
+        int k;
+        int slot;  // pinned row of [iters | breakdown] snapshots
+        uint64_t pps, lps;  // passes / launches per step (graph loops); 0: counted already
+        bool graph;
+    };
+    std::vector<Deferred> deferred;
+    auto defer_counts = [&](int k, bool graph, uint64_t pps, uint64_t lps) {
+        const int row = (int)deferred.size();
+        if (row >= kMaxDeferred) throw ApiError(MVSK_INTERNAL_ERROR, "pcg: too many Krylov loops per direction");
+        int* hc = ws.host_counts + (size_t)row * 2 * K;
+        MVSK_CUDA(cudaMemcpyAsync(hc, iters, k * sizeof(int), cudaMemcpyDeviceToHost, st));
+        MVSK_CUDA(cudaMemcpyAsync(hc + K, bdown, k * sizeof(int), cudaMemcpyDeviceToHost, st));
+        deferred.push_back({k, row, pps, lps, graph});
+    };
+    auto settle_counts = [&]() {
+        for (const Deferred& d : deferred) {
+            const int* hc = ws.host_counts + (size_t)d.slot * 2 * K;
+            int steps = 0;
+            for (int c = 0; c < d.k; ++c) {
+                const int col_steps = hc[c] + (hc[K + c] ? 1 : 0);  // HVPs column c consumed
+                out.iters += hc[c];
+                if (hc[K + c]) out.breakdown = true;
+                steps = std::max(steps, col_steps);
                 ctx->fwd += col_steps;  // reference contract: 2 passes per (active) HVP
                 ctx->tr += col_steps;
             }
+            if (d.graph) {
+                ctx->phys += (uint64_t)steps * d.pps;
+                ctx->launches += 1 + (uint64_t)steps * d.lps;
+            }
         }
-        return steps;
+        deferred.clear();
     };
     static const bool no_graph = std::getenv("MVSK_NO_CG_GRAPH") != nullptr;
     auto cg_graph = [&](int k) -> PcgWorkspace::LoopGraph* {
@@ -469,16 +546,16 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     };
     auto cg = [&](int k, int cap, const double* jdp) {
         CGState s{X, Rm, Z, P, rz, target, active, iters, bdown, jdp, mm, cap, in.tol};
-        *ws.host_params = StepParams{g, s, in.lambda};
-        MVSK_CUDA(cudaMemcpyAsync(sp_dev, ws.host_params, sizeof(StepParams), cudaMemcpyHostToDevice, st));
+        if (deferred.size() >= (size_t)kMaxDeferred) throw ApiError(MVSK_INTERNAL_ERROR, "pcg: too many Krylov loops");
+        StepParams* hp = ws.host_params + deferred.size();
+        *hp = StepParams{g, s, in.lambda};
+        MVSK_CUDA(cudaMemcpyAsync(sp_dev, hp, sizeof(StepParams), cudaMemcpyHostToDevice, st));
         ++ctx->launches;
         cg_init_kernel<<<k, kPT, dsm, st>>>(g, s, src, vin);
         MVSK_CUDA(cudaGetLastError());
         if (PcgWorkspace::LoopGraph* lg = cg_graph(k)) {
             MVSK_CUDA(cudaGraphLaunch(lg->exec, st));
-            const int steps = finish_counts(k, true);
-            ctx->phys += (uint64_t)steps * lg->phys_per_step;
-            ctx->launches += 1 + (uint64_t)steps * lg->launches_per_step;
+            defer_counts(k, true, lg->phys_per_step, lg->launches_per_step);
             return;
         }
         int* hf = ws.host_flags;  // [2][K] flag snapshots + [2K..) iters / breakdown
@@ -511,38 +588,27 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
                 break;
             }
         }
-        finish_counts(k, true);
+        defer_counts(k, false, 0, 0);
     };
 
     // ---- Jacobi diagonal (:197-209): 8 probes through Hop in one batch
     const double* jdp = nullptr;
+    double* stage = ws.host_stage;
+    const int nb1 = (int)std::min<long long>(4LL * ctx->nsm, (mm + 255) / 256 + 1);
     if (!in.jacobi_probes.empty()) {
         const int k = (int)in.jacobi_probes.size();
-        std::vector<double> buf((size_t)k * mm);
-        for (int p = 0; p < k; ++p) std::copy(in.jacobi_probes[p].begin(), in.jacobi_probes[p].end(), buf.begin() + (size_t)p * mm);
-        MVSK_CUDA(cudaMemcpyAsync(src, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        for (int p = 0; p < k; ++p) std::copy(in.jacobi_probes[p].begin(), in.jacobi_probes[p].end(), stage + (size_t)p * mm);
+        MVSK_CUDA(cudaMemcpyAsync(src, stage, (size_t)k * mm * sizeof(double), cudaMemcpyHostToDevice, st));
+        stage += (size_t)k * mm;
         ++ctx->launches;
         lift_kernel<<<k, kPT, dsm, st>>>(g, src, mm, true, nullptr, vin);
         MVSK_CUDA(cudaGetLastError());
         hvp_rows(k, k);
         ++ctx->launches;
         reduce_kernel<<<k, kPT, dsm, st>>>(g, H, k, true, rows, mm);
+        ++ctx->launches;
+        jacobi_diag_kernel<<<nb1, 256, 0, st>>>(src, rows, k, mm, in.lambda, std::max(1e-12, in.lambda), jd);
         MVSK_CUDA(cudaGetLastError());
-        // + lambda r (Hop), then the mean of r o Hop(r)
-        std::vector<double> hr(buf.size());
-        MVSK_CUDA(cudaMemcpyAsync(hr.data(), rows, hr.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-        MVSK_CUDA(cudaStreamSynchronize(st));
-        for (size_t i = 0; i < hr.size(); ++i) hr[i] += in.lambda * buf[i];
-        std::vector<double> dg((size_t)mm, 0.0);
-        for (int p = 0; p < k; ++p)
-            for (int i = 0; i < mm; ++i) dg[(size_t)i] += buf[(size_t)p * mm + i] * hr[(size_t)p * mm + i];
-        const double fl = std::max(1e-12, in.lambda);
-        for (double& v : dg) {
-            v /= (double)k;
-            v = std::max(v, fl);
-        }
-        MVSK_CUDA(cudaMemcpyAsync(jd, dg.data(), mm * sizeof(double), cudaMemcpyHostToDevice, st));
-        MVSK_CUDA(cudaStreamSynchronize(st));
         jdp = jd;
     }
 
@@ -555,19 +621,22 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     reduce_kernel<<<1, kPT, dsm, st>>>(g, H, 1, true, hvec, mm);
     MVSK_CUDA(cudaGetLastError());
 
-    // ---- a: Hutchinson probes or exact trace (:215-237), blocks of K columns
-    int nprobe_total = 0;
+    // ---- a: Hutchinson probes or exact trace (:215-237), blocks of K columns,
+    // accumulated on the device in probe order
     MVSK_CUDA(cudaMemsetAsync(avec, 0, mm * sizeof(double), st));
-    std::vector<double> a_host((size_t)mm, 0.0);
     if (in.has_third) {
-        const int P_all = (int)in.probes.size();
-        nprobe_total = P_all;
+        const int P_all = in.unit_probes ? mm : (int)in.probes.size();
         for (int b0 = 0; b0 < P_all; b0 += K) {
             const int k = std::min(K, P_all - b0);
-            std::vector<double> buf((size_t)k * mm);
-            for (int p = 0; p < k; ++p)
-                std::copy(in.probes[b0 + p].begin(), in.probes[b0 + p].end(), buf.begin() + (size_t)p * mm);
-            MVSK_CUDA(cudaMemcpyAsync(src, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+            if (in.unit_probes) {
+                ++ctx->launches;
+                unit_probe_kernel<<<nb1, 256, 0, st>>>(src, k, mm, b0);
+            } else {
+                for (int p = 0; p < k; ++p)
+                    std::copy(in.probes[b0 + p].begin(), in.probes[b0 + p].end(), stage + (size_t)p * mm);
+                MVSK_CUDA(cudaMemcpyAsync(src, stage, (size_t)k * mm * sizeof(double), cudaMemcpyHostToDevice, st));
+                stage += (size_t)k * mm;
+            }
             cg(k, in.probe_cap, jdp);
             // third_action(U Q s_p, U Q r_p) for the block, one fused pass
             ++ctx->launches;
@@ -586,30 +655,27 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
             ctx->tr += k;
             ++ctx->launches;
             reduce_kernel<<<k, kPT, dsm, st>>>(g, H, k, true, rows, mm);
+            ++ctx->launches;
+            accum_rows_kernel<<<nb1, 256, 0, st>>>(rows, k, mm, avec);
             MVSK_CUDA(cudaGetLastError());
-            // accumulate in probe order on the host (a is an mm-vector)
-            std::vector<double> t3((size_t)k * mm);
-            MVSK_CUDA(cudaMemcpyAsync(t3.data(), rows, t3.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-            MVSK_CUDA(cudaStreamSynchronize(st));
-            for (int p = 0; p < k; ++p)
-                for (int i = 0; i < mm; ++i) a_host[(size_t)i] += t3[(size_t)p * mm + i];
+            if (in.unit_probes && deferred.size() + 2 >= (size_t)kMaxDeferred) {
+                // long exact-trace sweeps: settle the loop counts every few blocks
+                MVSK_CUDA(cudaStreamSynchronize(st));
+                settle_counts();
+            }
         }
-        if (!in.exact_trace)
-            for (double& v : a_host) v /= (double)in.hutchinson_probes;
     }
-    // rhs = h - (||gbar|| / n) a  (:239)
-    std::vector<double> h_host((size_t)mm);
-    MVSK_CUDA(cudaMemcpyAsync(h_host.data(), hvec, mm * sizeof(double), cudaMemcpyDeviceToHost, st));
-    MVSK_CUDA(cudaStreamSynchronize(st));
-    std::vector<double> r_host((size_t)mm);
-    for (int i = 0; i < mm; ++i) r_host[(size_t)i] = h_host[(size_t)i] - (in.gn / (double)m) * a_host[(size_t)i];
-    MVSK_CUDA(cudaMemcpyAsync(src, r_host.data(), mm * sizeof(double), cudaMemcpyHostToDevice, st));
+    // rhs = h - (||gbar|| / n) a  (:239); a averaged over the Hutchinson probes (:236)
+    ++ctx->launches;
+    rhs_kernel<<<nb1, 256, 0, st>>>(hvec, avec, mm, (in.has_third && !in.unit_probes) ? (double)in.hutchinson_probes : 0.0,
+                                    in.gn / (double)m, src);
+    MVSK_CUDA(cudaGetLastError());
     // main CG (:240-241)
     cg(1, in.maxit, jdp);
     out.u.resize((size_t)mm);
     MVSK_CUDA(cudaMemcpyAsync(out.u.data(), X, mm * sizeof(double), cudaMemcpyDeviceToHost, st));
     MVSK_CUDA(cudaStreamSynchronize(st));
-    (void)nprobe_total;
+    settle_counts();
     return out;
 }
 

@@ -20,7 +20,8 @@ struct PcgInput {
     int maxit = 15, probe_cap = 5, hutchinson_probes = 8;
     bool exact_trace = false, has_third = true;
     std::vector<std::vector<double>> jacobi_probes;  // 8 Rademacher probes (m-2) or empty
-    std::vector<std::vector<double>> probes;         // Hutchinson probes / unit vectors (m-2)
+    std::vector<std::vector<double>> probes;         // Hutchinson probes (m-2)
+    bool unit_probes = false;                        // exact trace: probes are e_0..e_{m-3}, made on device
 };
 
 struct PcgOutput {

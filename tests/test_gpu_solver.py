@@ -320,7 +320,9 @@ def test_krylov_graph_replays_bitwise():
         x[drop] = tau
         idx = np.array([i for i in range(n) if i not in drop])
         cases.append((idx, x[idx]))
-    for kw in (dict(lam=1e-4), dict(lam=1e-4, jacobi=True)):
+    # probe_maxit 2 vs krylov_maxit 40: each loop must run with its own cap
+    for kw in (dict(lam=1e-4), dict(lam=1e-4, jacobi=True), dict(lam=1e-4, probe_maxit=2, krylov_maxit=40,
+                                                                  krylov_tol=1e-9)):
         for idx, xf in cases:
             if idx is None:
                 g.set_face()
