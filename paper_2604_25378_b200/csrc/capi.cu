@@ -38,49 +38,6 @@ bool finite(const double* v, long long n) {
     return true;
 }
 
-void alloc_workspaces(mvsk_gpu_ctx* ctx) {
-    const size_t ld = (size_t)ctx->ld;
-    MVSK_CUDA(cudaMalloc(&ctx->mu_dev, ld * sizeof(double)));
-    MVSK_CUDA(cudaMemset(ctx->mu_dev, 0, ld * sizeof(double)));
-    MVSK_CUDA(cudaMemcpy(ctx->mu_dev, ctx->mu.data(), ctx->n * sizeof(double), cudaMemcpyHostToDevice));
-    MVSK_CUDA(cudaMalloc(&ctx->vin, (size_t)MVSK_GPU_MAX_RHS * 2 * ld * sizeof(double)));
-    MVSK_CUDA(cudaMemset(ctx->vin, 0, (size_t)MVSK_GPU_MAX_RHS * 2 * ld * sizeof(double)));
-    MVSK_CUDA(cudaMalloc(&ctx->part_sc, (size_t)ctx->nsm * 4 * kNumScalars * sizeof(double)));
-    MVSK_CUDA(cudaMalloc(&ctx->red, ((size_t)MVSK_GPU_MAX_RHS * ld + kNumScalars) * sizeof(double)));
-    MVSK_CUDA(cudaMalloc(&ctx->outd, (size_t)MVSK_GPU_MAX_RHS * ld * sizeof(double)));
-    MVSK_CUDA(cudaMalloc(&ctx->tvec, (size_t)std::max<long long>(1, ctx->T_local) * sizeof(double)));
-    for (auto& s : ctx->slots) {
-        MVSK_CUDA(cudaMalloc(&s.z, (size_t)std::max<long long>(1, ctx->T_local) * sizeof(double)));
-        MVSK_CUDA(cudaMalloc(&s.g, ld * sizeof(double)));
-        MVSK_CUDA(cudaMalloc(&s.sc, 8 * sizeof(double)));
-    }
-    ensure_host_staging(ctx, std::max<size_t>((size_t)MVSK_GPU_MAX_RHS * 2 * ld, (size_t)ctx->T_local + 16));
-}
-
-void free_all(mvsk_gpu_ctx* ctx) {
-    if (!ctx) return;
-    cudaSetDevice(ctx->device);
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    if (ctx->owns_X && ctx->X) cudaFree(ctx->X);
-    for (double* p : {ctx->mu_dev, ctx->zoff_dev, ctx->vin, ctx->part_acc, ctx->part_sc, ctx->red, ctx->outd,
-                      ctx->tvec, ctx->gram, ctx->gram_part, ctx->tvec2, ctx->pmat})
-        if (p) cudaFree(p);
-    for (auto& s : ctx->slots) {
-        if (s.z) cudaFree(s.z);
-        if (s.g) cudaFree(s.g);
-        if (s.sc) cudaFree(s.sc);
-    }
-    if (ctx->h_in) cudaFreeHost(ctx->h_in);
-    if (ctx->h_out) cudaFreeHost(ctx->h_out);
-    if (ctx->h_mat) cudaFreeHost(ctx->h_mat);
-    for (auto& g : ctx->graphs)
-        if (g.exec) cudaGraphExecDestroy(g.exec);
-    if (ctx->comm) ncclCommDestroy(ctx->comm);
-    pcg_workspace_free(ctx);
-    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
-    delete ctx;
-}
-
 mvsk_gpu_ctx* make_ctx(long long T_local, long long row0, long long T_global, long long n, const double* mu,
                        const mvsk_coeffs* c, int device, int nranks, int rank, const void* id) {
     if (n < 1) throw ApiError(MVSK_DIMENSION_ERROR, "oracle: need at least one asset");
@@ -126,7 +83,7 @@ mvsk_gpu_ctx* make_ctx(long long T_local, long long row0, long long T_global, lo
         }
         return ctx;
     } catch (...) {
-        free_all(ctx);
+        ctx_free(ctx);
         throw;
     }
 }
@@ -188,9 +145,9 @@ int32_t mvsk_gpu_create_sharded(const double* A_rows, int64_t T_local, int64_t r
         mvsk_gpu_ctx* ctx = make_ctx(T_local, row0, T_global, n, mu, c, device, nranks, rank, nccl_unique_id);
         try {
             upload_panel(ctx, A_rows);
-            alloc_workspaces(ctx);
+            ctx_alloc_workspaces(ctx);
         } catch (...) {
-            free_all(ctx);
+            ctx_free(ctx);
             throw;
         }
         *out = ctx;
@@ -211,9 +168,9 @@ int32_t mvsk_gpu_create_from_device(const double* A_dev, int64_t ld, int64_t T_l
             ctx->ld = ld;
             ctx->X = const_cast<double*>(A_dev);
             ctx->owns_X = false;
-            alloc_workspaces(ctx);
+            ctx_alloc_workspaces(ctx);
         } catch (...) {
-            free_all(ctx);
+            ctx_free(ctx);
             throw;
         }
         *out = ctx;
@@ -254,10 +211,10 @@ int32_t mvsk_gpu_create_from_binary(const char* path, const mvsk_coeffs* c, int3
             const size_t bytes = (size_t)std::max<long long>(1, ctx->T_local) * ctx->ld * sizeof(double);
             MVSK_CUDA(cudaMalloc(&ctx->X, bytes));
             ctx->owns_X = true;
-            alloc_workspaces(ctx);
+            ctx_alloc_workspaces(ctx);
             ingest_binary(ctx, path);
         } catch (...) {
-            free_all(ctx);
+            ctx_free(ctx);
             throw;
         }
         *out = ctx;
@@ -276,7 +233,7 @@ int32_t mvsk_gpu_launch_count(const mvsk_gpu_ctx* ctx, uint64_t* launches) {
 }
 
 int32_t mvsk_gpu_destroy(mvsk_gpu_ctx* ctx) {
-    free_all(ctx);
+    ctx_free(ctx);
     return MVSK_OK;
 }
 

@@ -79,6 +79,7 @@ struct mvsk_gpu_ctx {
     mvsk_coeffs c{};
     double* zoff_dev = nullptr;  // T_local or null
     double value_offset = 0.0;
+    double* value_offset_dev = nullptr;  // compact face contexts: the offset lives on the device
 
     // face selected through the C-ABI (mvsk_gpu_set_face)
     mvsk_b200::FaceMap pub_face;
@@ -107,7 +108,12 @@ struct mvsk_gpu_ctx {
     size_t h_mat_elems = 0;
 
     ncclComm_t comm = nullptr;
+    bool owns_comm = true;  // false for a compact face context (it borrows the parent's)
     int nranks = 1, rank = 0;
+    long long ld_alloc = 0;  // row length the ld-sized workspaces were allocated for
+    // compact face context of a solve (face.cu): the reference's face panel
+    // A[:, free] with its pinned offset, gathered once per face when it pays
+    mvsk_gpu_ctx* face_child = nullptr;
 
     uint64_t fwd = 0, tr = 0, phys = 0;
     uint64_t launches = 0;  // kernels this context enqueued (graph replays included)

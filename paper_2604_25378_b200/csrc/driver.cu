@@ -828,6 +828,13 @@ Vec spg_identify(const View& full, Vec x, double tau, int max_steps, int patienc
     return xcur;
 }
 
+// compact a face when it is at most 3/4 of a panel wide enough for the pass
+// bytes to matter (n >= 256); MVSK_NO_FACE_COMPACT keeps index maps throughout
+bool face_compaction(long long n0, long long nf) {
+    static const bool off = std::getenv("MVSK_NO_FACE_COMPACT") != nullptr;
+    return !off && n0 >= 256 && 4 * nf <= 3 * n0;
+}
+
 Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
              const std::function<void(int, double, const Vec&)>& observer) {
     const long long n0 = ctx->n;
@@ -933,7 +940,7 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
             ++it;
             ++it_total;
             ++since_check;
-            if (rebuild) {  // :343-370, as an index map over the resident panel
+            if (rebuild) {  // :343-370
                 nf = n0 - npinned;
                 free_mask.assign((size_t)n0, 0);
                 FaceMap fm;
@@ -945,8 +952,17 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
                         free_mask[(size_t)i] = 1;
                         fm.idx.push_back(i);
                     }
-                if (!fm.active) fm.idx.clear();
-                face.fm = fm;
+                // small faces of a wide panel: the reference's gathered face panel
+                // (Af, zoff, -c1 mu_pin) as a compact device context, so face passes
+                // stream T x nf instead of T x n; otherwise an index map over the
+                // resident panel (no gather)
+                if (fm.active && face_compaction(n0, nf) && !ctx->zoff_dev && ctx->value_offset == 0.0) {
+                    mvsk_gpu_ctx* fc = face_context(ctx, fm.idx, pinned, tau);
+                    face = View{fc, face_child_map(fc, nf)};
+                } else {
+                    if (!fm.active) fm.idx.clear();
+                    face = View{ctx, fm};
+                }
                 mass = 1.0 - (double)npinned * tau;
                 t_cur = tr;
                 rebuild = false;
@@ -1453,6 +1469,7 @@ int32_t mvsk_gpu_solve(mvsk_gpu_ctx* ctx, const mvsk_solver_config* cfg, const d
         g_prof = Prof();
         g_prof.on = std::getenv("MVSK_PROFILE") != nullptr;
         Report r = solve(ctx, sc, xs, obs);
+        fold_face_counters(ctx);
         ctx->pub_face = saved;
         if (g_prof.on)
             std::fprintf(stderr,
@@ -1507,6 +1524,7 @@ int32_t mvsk_gpu_floor_sweep(mvsk_gpu_ctx* ctx, const mvsk_solver_config* cfg, c
         }
         const FaceMap saved = ctx->pub_face;
         const SweepOut o = floor_sweep(ctx, solve_cfg_of(cfg), s, fl, nfloors);
+        fold_face_counters(ctx);
         ctx->pub_face = saved;
         for (int k = 0; k < nfloors; ++k) {
             const FloorEval& e = o.best[(size_t)k];

@@ -31,6 +31,7 @@ struct FinishArgs {
     const double* mu;  // ld
     const double* x;   // ld (FGRAD mu'x)
     double c1, c2, c3, c4, T, value_offset;
+    const double* value_offset_dev;  // if set, read at run time (graph-stable across face rebuilds)
     const int* skip;
     int nskip;
 };
@@ -91,7 +92,8 @@ __device__ __forceinline__ void finish_block(const FinishArgs& f, int ng, int vb
                 for (int w = 0; w < nthr / 32; ++w) mux += part[w];
                 const double s2 = f.red[tot], s3 = f.red[tot + 1], s4 = f.red[tot + 2];
                 // oracle.hpp:62-64
-                f.sc[0] = f.value_offset - f.c1 * mux + (f.c2 * s2 - f.c3 * s3 + f.c4 * s4) / f.T;
+                const double vo = f.value_offset_dev ? *f.value_offset_dev : f.value_offset;
+                f.sc[0] = vo - f.c1 * mux + (f.c2 * s2 - f.c3 * s3 + f.c4 * s4) / f.T;
                 f.sc[1] = mux;
                 f.sc[2] = s2 / f.T;
                 f.sc[3] = s3 / f.T;

@@ -11,6 +11,7 @@
 #include <functional>
 
 #include "host_ops.hpp"
+#include "pcg_device.hpp"
 
 namespace mvsk_b200 {
 
@@ -401,6 +402,53 @@ void op_third_trace_rows(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const d
         copy_out(ctx, ctx->outd, 1, ctx->ld);
     });
     finish_out(ctx, fm, 1, ctx->ld, out);
+}
+
+// ---- context lifecycle (shared by the C-ABI and the compact face contexts) ----
+void ctx_alloc_workspaces(mvsk_gpu_ctx* ctx) {
+    ctx->ld_alloc = ctx->ld;
+    const size_t ld = (size_t)ctx->ld;
+    MVSK_CUDA(cudaMalloc(&ctx->mu_dev, ld * sizeof(double)));
+    MVSK_CUDA(cudaMemset(ctx->mu_dev, 0, ld * sizeof(double)));
+    MVSK_CUDA(cudaMemcpy(ctx->mu_dev, ctx->mu.data(), ctx->n * sizeof(double), cudaMemcpyHostToDevice));
+    MVSK_CUDA(cudaMalloc(&ctx->vin, (size_t)MVSK_GPU_MAX_RHS * 2 * ld * sizeof(double)));
+    MVSK_CUDA(cudaMemset(ctx->vin, 0, (size_t)MVSK_GPU_MAX_RHS * 2 * ld * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ctx->part_sc, (size_t)ctx->nsm * 4 * kNumScalars * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ctx->red, ((size_t)MVSK_GPU_MAX_RHS * ld + kNumScalars) * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ctx->outd, (size_t)MVSK_GPU_MAX_RHS * ld * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ctx->tvec, (size_t)std::max<long long>(1, ctx->T_local) * sizeof(double)));
+    for (auto& s : ctx->slots) {
+        MVSK_CUDA(cudaMalloc(&s.z, (size_t)std::max<long long>(1, ctx->T_local) * sizeof(double)));
+        MVSK_CUDA(cudaMalloc(&s.g, ld * sizeof(double)));
+        MVSK_CUDA(cudaMalloc(&s.sc, 8 * sizeof(double)));
+    }
+    ensure_host_staging(ctx, std::max<size_t>((size_t)MVSK_GPU_MAX_RHS * 2 * ld, (size_t)ctx->T_local + 16));
+}
+
+void ctx_free(mvsk_gpu_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->face_child) ctx_free(ctx->face_child);
+    ctx->face_child = nullptr;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->owns_X && ctx->X) cudaFree(ctx->X);
+    for (double* p : {ctx->value_offset_dev, ctx->mu_dev, ctx->zoff_dev, ctx->vin, ctx->part_acc, ctx->part_sc, ctx->red, ctx->outd,
+                      ctx->tvec, ctx->gram, ctx->gram_part, ctx->tvec2, ctx->pmat})
+        if (p) cudaFree(p);
+    for (auto& s : ctx->slots) {
+        if (s.z) cudaFree(s.z);
+        if (s.g) cudaFree(s.g);
+        if (s.sc) cudaFree(s.sc);
+    }
+    if (ctx->h_in) cudaFreeHost(ctx->h_in);
+    if (ctx->h_out) cudaFreeHost(ctx->h_out);
+    if (ctx->h_mat) cudaFreeHost(ctx->h_mat);
+    for (auto& g : ctx->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (ctx->comm && ctx->owns_comm) ncclCommDestroy(ctx->comm);
+    pcg_workspace_free(ctx);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
 }
 
 }  // namespace mvsk_b200

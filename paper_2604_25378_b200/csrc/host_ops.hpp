@@ -12,6 +12,17 @@ namespace mvsk_b200 {
 using Vec = std::vector<double>;
 
 FaceMap full_face(const mvsk_gpu_ctx* ctx);
+// workspaces sized by ctx->ld (records ld_alloc) / free a context and its face child
+void ctx_alloc_workspaces(mvsk_gpu_ctx* ctx);
+void ctx_free(mvsk_gpu_ctx* ctx);
+// compact face context for the face with these free columns (face.cu); reused
+// across faces while it fits. fold_face_counters adds the child's pass / launch
+// counters into the parent's.
+mvsk_gpu_ctx* face_context(mvsk_gpu_ctx* parent, const std::vector<int64_t>& free_idx, const std::vector<char>& pinned,
+                           double tau);
+void fold_face_counters(mvsk_gpu_ctx* parent);
+// the face view over a compact face context (its first nf columns)
+FaceMap face_child_map(const mvsk_gpu_ctx* child, long long nf);
 void check_slot(const mvsk_gpu_ctx* ctx, int slot, bool need_valid = true);
 
 // make_cache: returns f; throws numeric_error on a non-finite value

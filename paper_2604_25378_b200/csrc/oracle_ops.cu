@@ -528,6 +528,7 @@ static FinishArgs finish_args(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const 
     f.c4 = ctx->c.c4;
     f.T = (double)ctx->T_global;
     f.value_offset = ctx->value_offset;
+    f.value_offset_dev = ctx->value_offset_dev;
     f.skip = io.skip;
     f.nskip = io.nskip;
     if (slot) {

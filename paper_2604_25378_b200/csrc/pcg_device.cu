@@ -315,7 +315,8 @@ struct PcgWorkspace {
         uint64_t phys_per_step, launches_per_step;
     };
     std::vector<LoopGraph> graphs;
-    std::vector<std::pair<int, int>> seen;  // (k, slot) keys that ran once (sized every workspace)
+    std::vector<std::pair<int, int>> seen;  // (k, slot) keys that ran once at seen_epoch
+    uint64_t seen_epoch = ~0ull;
     bool graphs_broken = false;
 };
 
@@ -472,6 +473,10 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         if (no_graph || ws.graphs_broken) return nullptr;
         // the first loop of a key runs host-driven: it sizes the pass workspaces,
         // which must not be (re)allocated while a graph is being captured
+        if (ws.seen_epoch != ctx->epoch) {  // buffers may have been resized: size them eagerly again
+            ws.seen.clear();
+            ws.seen_epoch = ctx->epoch;
+        }
         if (std::find(ws.seen.begin(), ws.seen.end(), std::make_pair(k, slot)) == ws.seen.end()) {
             ws.seen.emplace_back(k, slot);
             return nullptr;

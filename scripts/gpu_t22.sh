@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+bash scripts/gpu_tests.sh
+grep -E "FAIL|Error" gpurun_out/pytest_gpu.log | head -20
+for g in "" 1; do
+echo "== MVSK_NO_FACE_COMPACT=$g"
+if [ -z "$g" ]; then unset MVSK_NO_FACE_COMPACT; else export MVSK_NO_FACE_COMPACT=1; fi
+MVSK_PROFILE=1 timeout 900 python scripts/solve_bench.py --configs C3,C4 --cpu-max-n 0 --reps 1 2>&1 | grep -E "profile|config" | sed -n '2p;3p;5p;6p;8p;9p' | cut -c1-330
+done

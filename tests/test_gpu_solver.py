@@ -337,3 +337,45 @@ def test_krylov_graph_replays_bitwise():
             for d, it, bd, ps in outs[1:]:
                 assert np.array_equal(d, outs[0][0])
                 assert (it, bd, ps) == outs[0][1:]
+
+
+def test_compact_faces_match_cpu_and_index_maps():
+    """Wide panels solve on compact face contexts once most assets are pinned
+    (face.cu: the reference's gathered Af / zoff / -c1 mu_pin face oracle,
+    solver.hpp:343-363). BASELINE config 3 (n = 800, support ~20): the compact
+    path agrees with the CPU restatement and with the index-map faces
+    (MVSK_NO_FACE_COMPACT, run in a subprocess because the switch is read once)
+    on status, active set and objective, weights within the solve envelope."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from paper_2604_25378_b200.datagen import crra, make_panel
+    from paper_2604_25378_b200.gpu_oracle import preset
+    A, mu, _ = make_panel("C3", seed=11)
+    c = crra(5.0)
+    cfg_c, cfg_g = po.preset("large"), preset("large")
+    for cfg in (cfg_c, cfg_g):
+        cfg.has_max_elapsed = 0
+        cfg.epsilon = 1e-10
+    xg, rg = _gpu(A, mu, c).solve(cfg_g)
+    xc, rc = po.solve(A, mu, c, cfg_c)
+    _same_solution(xg, rg, xc, rc, cfg_g.tau, tol=1e-6)
+    code = (
+        "import json, sys, numpy as np\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_2604_25378_b200.datagen import crra, make_panel\n"
+        "from paper_2604_25378_b200.gpu_oracle import GpuOracle, preset\n"
+        "A, mu, _ = make_panel('C3', seed=11)\n"
+        "cfg = preset('large'); cfg.has_max_elapsed = 0; cfg.epsilon = 1e-10\n"
+        "x, r = GpuOracle(A, mu, crra(5.0)).solve(cfg)\n"
+        "print(json.dumps({'x': x.tolist(), 'f': r.f_star, 'status': r.status}))\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MVSK_NO_FACE_COMPACT="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600, check=True)
+    ref = json.loads(out.stdout.strip().splitlines()[-1])
+    xi = np.array(ref["x"])
+    assert ref["status"] == rg.status
+    assert _active(xi, cfg_g.tau) == _active(xg, cfg_g.tau)
+    assert abs(ref["f"] - rg.f_star) <= 1e-12 * (1 + abs(rg.f_star))
+    assert float(np.max(np.abs(xi - xg))) <= 1e-6
