@@ -111,9 +111,13 @@ struct mvsk_gpu_ctx {
     bool owns_comm = true;  // false for a compact face context (it borrows the parent's)
     int nranks = 1, rank = 0;
     long long ld_alloc = 0;  // row length the ld-sized workspaces were allocated for
-    // compact face context of a solve (face.cu): the reference's face panel
-    // A[:, free] with its pinned offset, gathered once per face when it pays
-    mvsk_gpu_ctx* face_child = nullptr;
+    // compact face contexts of a solve (face.cu): the reference's face panel
+    // A[:, free] with its pinned offset, gathered once per face when it pays;
+    // one per power-of-two width class, kept across solves
+    std::vector<mvsk_gpu_ctx*> face_pool;
+    unsigned char* face_scratch = nullptr;       // child: device staging of a rebuild
+    unsigned char* face_scratch_host = nullptr;  // child: pinned staging of a rebuild
+    size_t face_scratch_bytes = 0;
 
     uint64_t fwd = 0, tr = 0, phys = 0;
     uint64_t launches = 0;  // kernels this context enqueued (graph replays included)

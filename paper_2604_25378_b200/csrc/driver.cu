@@ -31,8 +31,8 @@ namespace {
 // ---- optional host-side profile of a solve (MVSK_PROFILE=1 -> stderr) --------
 struct Prof {
     bool on = false;
-    double proj = 0, dir = 0, cache = 0, grad = 0, line = 0, total = 0;
-    long nproj = 0, ndir = 0, ncache = 0, nline = 0;
+    double proj = 0, dir = 0, cache = 0, grad = 0, line = 0, total = 0, face = 0, resid = 0;
+    long nproj = 0, ndir = 0, ncache = 0, nline = 0, nface = 0, nresid = 0;
 };
 Prof g_prof;
 struct Tick {
@@ -231,12 +231,32 @@ Vec project_slice(const Vec& v, double tau, double mass = 1.0) {
     if (!(tau >= 0.0) || !(s > 0.0)) throw ApiError(MVSK_DOMAIN_ERROR, "project_slice: need 0 <= tau < mass/n");
     Vec u(n);
     for (size_t i = 0; i < n; ++i) u[i] = v[i] - tau;
-    std::sort(u.begin(), u.end(), std::greater<double>());
+    // theta comes from the running sums of the sorted values up to the last
+    // index where u[k] > cand, i.e. the support of the projection. Sorting only
+    // the top K (partial sort: the same top-K order as a full sort, so the same
+    // sums and the same bits) suffices when that index is well inside K; a
+    // support reaching K/2 falls back to the full sort.
     double css = 0.0, theta = 0.0;
-    for (size_t k = 0; k < n; ++k) {
-        css += u[k];
-        const double cand = (css - s) / (double)(k + 1);
-        if (u[k] > cand) theta = cand;
+    size_t K = std::min<size_t>(n, 256);
+    for (;;) {
+        if (K < n) {  // top K by selection, then sorted: O(n + K log K)
+            std::nth_element(u.begin(), u.begin() + (long)K - 1, u.end(), std::greater<double>());
+            std::sort(u.begin(), u.begin() + (long)K, std::greater<double>());
+        } else
+            std::sort(u.begin(), u.end(), std::greater<double>());
+        css = 0.0;
+        theta = 0.0;
+        size_t last = 0;
+        for (size_t k = 0; k < K; ++k) {
+            css += u[k];
+            const double cand = (css - s) / (double)(k + 1);
+            if (u[k] > cand) {
+                theta = cand;
+                last = k;
+            }
+        }
+        if (K == n || 2 * (last + 1) <= K) break;
+        K = std::min(n, 8 * K);
     }
     Vec out(n);
     for (size_t i = 0; i < n; ++i) out[i] = std::max(v[i] - tau - theta, 0.0) + tau;
@@ -832,7 +852,9 @@ Vec spg_identify(const View& full, Vec x, double tau, int max_steps, int patienc
 // bytes to matter (n >= 256); MVSK_NO_FACE_COMPACT keeps index maps throughout
 bool face_compaction(long long n0, long long nf) {
     static const bool off = std::getenv("MVSK_NO_FACE_COMPACT") != nullptr;
-    return !off && n0 >= 256 && 4 * nf <= 3 * n0;
+    long long cap = 64;  // face.cu width class
+    while (cap < nf) cap <<= 1;
+    return !off && n0 >= 256 && 4 * cap <= 3 * n0;
 }
 
 Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
@@ -898,6 +920,8 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
         return xn;
     };
     auto full_residual = [&](const Vec& x, Vec& g_out) {
+        Tick tkr(g_prof.resid);
+        ++g_prof.nresid;
         full.make_cache(kSlotTmp, x);
         g_out = full.gradient(kSlotTmp);
         return gradient_mapping_residual(x, g_out, tau);
@@ -957,6 +981,8 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
                 // stream T x nf instead of T x n; otherwise an index map over the
                 // resident panel (no gather)
                 if (fm.active && face_compaction(n0, nf) && !ctx->zoff_dev && ctx->value_offset == 0.0) {
+                    Tick tkf(g_prof.face);
+                    ++g_prof.nface;
                     mvsk_gpu_ctx* fc = face_context(ctx, fm.idx, pinned, tau);
                     face = View{fc, face_child_map(fc, nf)};
                 } else {
@@ -1474,10 +1500,12 @@ int32_t mvsk_gpu_solve(mvsk_gpu_ctx* ctx, const mvsk_solver_config* cfg, const d
         if (g_prof.on)
             std::fprintf(stderr,
                          "[mvsk profile] total %.3f ms | make_cache %.3f ms (%ld) | gradient %.3f ms | direction %.3f "
-                         "ms (%ld) | line_model %.3f ms (%ld) | project_slice %.3f ms (%ld)\n",
+                         "ms (%ld) | line_model %.3f ms (%ld) | project_slice %.3f ms (%ld) | face rebuild %.3f ms (%ld) "
+                         "| full residual %.3f ms (%ld)\n",
                          1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
                          1e3 * g_prof.cache, g_prof.ncache, 1e3 * g_prof.grad, 1e3 * g_prof.dir, g_prof.ndir,
-                         1e3 * g_prof.line, g_prof.nline, 1e3 * g_prof.proj, g_prof.nproj);
+                         1e3 * g_prof.line, g_prof.nline, 1e3 * g_prof.proj, g_prof.nproj, 1e3 * g_prof.face,
+                         g_prof.nface, 1e3 * g_prof.resid, g_prof.nresid);
         std::copy(r.x.begin(), r.x.end(), x_star);
         std::memset(report, 0, sizeof(*report));
         report->f_star = r.f;

@@ -2,8 +2,9 @@
 //
 // The reference rebuilds, at every pin/release event, a face oracle over the
 // gathered panel Af = A[:, free] with the pinned contribution folded into a
-// per-sample offset zoff = tau * sum_{pinned i, ascending} A[:, i] and the value
-// offset -c1 * mu_pin. On the device the face can instead stay an index map over
+// per-sample offset zoff = tau * sum_{pinned i} A[:, i] and the value offset
+// -c1 * mu_pin (here: zoff = A d with d = tau on the pinned columns, one
+// streaming pass, summed in the pass's fixed order). On the device the face can instead stay an index map over
 // the resident panel (host_ops.cu FaceMap): no gather, but every face pass then
 // streams all n columns. Once most assets are pinned (C4: 53 of 5000 free after
 // the identification pass) that is ~100x the bytes the face needs, so the
@@ -17,6 +18,7 @@
 #include <vector>
 
 #include "host_ops.hpp"
+#include "oracle_ops.cuh"
 #include "pcg_device.hpp"
 
 namespace mvsk_b200 {
@@ -31,32 +33,6 @@ __global__ void face_gather_kernel(const double* __restrict__ X, long long T, lo
         const long long t = e / ldf;
         const int j = (int)(e - t * ldf);
         Xf[e] = j < nf ? X[t * ld + idx[j]] : 0.0;
-    }
-}
-
-// zoff[t] = sum over pinned columns in ascending order of tau * X[t, i]: the
-// reference's `zoff += tau * A.col(i)` (solver.hpp:359), a separately rounded
-// product and sum per column (no contraction). One warp per row: lanes load 32
-// consecutive columns, the running sum walks them in column order.
-__global__ void face_zoff_kernel(const double* __restrict__ X, long long T, long long ld, int n0,
-                                 const unsigned char* __restrict__ pinned, double tau, double* __restrict__ zoff) {
-    const int lane = threadIdx.x & 31;
-    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long t = warp; t < T; t += nwarps) {
-        const double* row = X + t * ld;
-        double acc = 0.0;
-        for (int c0 = 0; c0 < n0; c0 += 32) {
-            const int c = c0 + lane;
-            const double v = c < n0 ? row[c] : 0.0;
-            const unsigned pm = __ballot_sync(0xffffffffu, c < n0 && pinned[c]);
-#pragma unroll 4
-            for (int j = 0; j < 32; ++j) {
-                const double vj = __shfl_sync(0xffffffffu, v, j);
-                if (pm & (1u << j)) acc = __dadd_rn(acc, __dmul_rn(tau, vj));
-            }
-        }
-        if (lane == 0) zoff[t] = acc;
     }
 }
 
@@ -101,21 +77,21 @@ mvsk_gpu_ctx* face_context(mvsk_gpu_ctx* p, const std::vector<int64_t>& free_idx
                            double tau) {
     const long long nf = (long long)free_idx.size();
     const long long n0 = p->n;
-    mvsk_gpu_ctx* c = p->face_child;
-    // The child keeps a fixed width n_cap >= nf (zero columns past nf, zero mu):
+    // The child has a fixed width n_cap >= nf (zero columns past nf, zero mu):
     // its shapes, buffers and therefore its captured graphs survive face
     // rebuilds; only the panel data, zoff and the device-side value offset
-    // change. A new child is made when the face outgrows it or shrinks to less
-    // than half of it (passes would stream mostly zero columns).
-    if (c && (nf > c->n || 2 * (nf + 32) < c->n)) {
-        fold_face_counters(p);
-        ctx_free(c);
-        c = p->face_child = nullptr;
-    }
+    // change. Widths are power-of-two classes (<= 2x the face), one child per
+    // class, kept in the parent's pool across faces and solves.
+    long long cap = 64;
+    while (cap < nf) cap <<= 1;
+    cap = std::min(cap, n0);
+    mvsk_gpu_ctx* c = nullptr;
+    for (mvsk_gpu_ctx* q : p->face_pool)
+        if (q->n == cap) c = q;
     if (!c) {
-        const long long cap = std::min<long long>(n0, nf + nf / 4 + 16);
-        c = p->face_child = make_child(p, cap);
+        c = make_child(p, cap);
         MVSK_CUDA(cudaMalloc(&c->value_offset_dev, sizeof(double)));
+        p->face_pool.push_back(c);
     }
     const long long ncap = c->n;
     c->c = p->c;
@@ -136,34 +112,53 @@ mvsk_gpu_ctx* face_context(mvsk_gpu_ctx* p, const std::vector<int64_t>& free_idx
     }
 
     // device work on the shared stream: idx / mask / mu / offset upload, gather, zoff
-    const size_t b_idx = (size_t)nf * sizeof(long long), b_mu = (size_t)c->ld * sizeof(double);
-    const size_t need = b_idx + b_mu + sizeof(double) + (size_t)n0 + 64;
+    const size_t b_idx = ((size_t)nf * sizeof(long long) + 15) / 16 * 16, b_mu = (size_t)c->ld * sizeof(double);
+    const size_t b_d = (size_t)p->ld * sizeof(double);
+    const size_t need = b_idx + b_mu + 16 + b_d;
     std::vector<unsigned char> host(need, 0);
-    std::memcpy(host.data(), free_idx.data(), b_idx);
+    std::memcpy(host.data(), free_idx.data(), (size_t)nf * sizeof(long long));
     std::memcpy(host.data() + b_idx, c->mu.data(), (size_t)ncap * sizeof(double));
     std::memcpy(host.data() + b_idx + b_mu, &c->value_offset, sizeof(double));
-    unsigned char* mask = host.data() + b_idx + b_mu + sizeof(double);
-    for (long long i = 0; i < n0; ++i) mask[i] = pinned[(size_t)i] ? 1 : 0;
-    unsigned char* dbuf = nullptr;
-    MVSK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dbuf), need, p->stream));
-    MVSK_CUDA(cudaMemcpyAsync(dbuf, host.data(), need, cudaMemcpyHostToDevice, p->stream));
+    // d = tau on the pinned columns: zoff = A d is tau * sum_{pinned} A[:, i]
+    // (solver.hpp:359), one streaming pass over the panel
+    double* dh = reinterpret_cast<double*>(host.data() + b_idx + b_mu + 16);
+    for (long long i = 0; i < n0; ++i) dh[i] = pinned[(size_t)i] ? tau : 0.0;
+    // persistent device / pinned staging in the child (sized for the widest face
+    // it can hold against this parent): no allocation per rebuild
+    if (c->face_scratch_bytes < need) {
+        if (c->face_scratch) MVSK_CUDA(cudaFree(c->face_scratch));
+        if (c->face_scratch_host) MVSK_CUDA(cudaFreeHost(c->face_scratch_host));
+        c->face_scratch = nullptr;
+        c->face_scratch_host = nullptr;
+        c->face_scratch_bytes = 0;
+        MVSK_CUDA(cudaMalloc(&c->face_scratch, need));
+        MVSK_CUDA(cudaMallocHost(&c->face_scratch_host, need));
+        c->face_scratch_bytes = need;
+    }
+    std::memcpy(c->face_scratch_host, host.data(), need);
+    unsigned char* dbuf = c->face_scratch;
+    MVSK_CUDA(cudaMemcpyAsync(dbuf, c->face_scratch_host, need, cudaMemcpyHostToDevice, p->stream));
     const long long* didx = reinterpret_cast<const long long*>(dbuf);
     MVSK_CUDA(cudaMemcpyAsync(c->mu_dev, dbuf + b_idx, b_mu, cudaMemcpyDeviceToDevice, p->stream));
     MVSK_CUDA(cudaMemcpyAsync(c->value_offset_dev, dbuf + b_idx + b_mu, sizeof(double), cudaMemcpyDeviceToDevice,
                               p->stream));
-    const unsigned char* dmask = dbuf + b_idx + b_mu + sizeof(double);
+    const double* d_dev = reinterpret_cast<const double*>(dbuf + b_idx + b_mu + 16);
     if (p->T_local > 0) {
         const int nb = 4 * p->nsm;
         ++p->launches;
         face_gather_kernel<<<nb, 256, 0, p->stream>>>(p->X, p->T_local, p->ld, didx, (int)nf, (int)c->ld, c->X);
         MVSK_CUDA(cudaGetLastError());
-        ++p->launches;
-        face_zoff_kernel<<<nb, 256, 0, p->stream>>>(p->X, p->T_local, p->ld, (int)n0, dmask, tau, c->zoff_dev);
-        MVSK_CUDA(cudaGetLastError());
-        p->phys += 1;  // the zoff sweep streams the whole panel once
+        // the fused line-sums pass writes A d per sample (its nine power sums,
+        // against a zeroed z, are discarded)
+        MVSK_CUDA(cudaMemsetAsync(p->tvec, 0, (size_t)p->T_local * sizeof(double), p->stream));
+        PassIO io;
+        io.vin = d_dev;
+        io.z = p->tvec;
+        io.zout = c->zoff_dev;
+        io.out = p->outd;
+        run_pass(p, Op::LINESUMS, 1, io);
     }
-    MVSK_CUDA(cudaFreeAsync(dbuf, p->stream));
-    MVSK_CUDA(cudaStreamSynchronize(p->stream));  // `host` is stack-local
+    MVSK_CUDA(cudaStreamSynchronize(p->stream));  // the pinned staging is reused by the next rebuild
     return c;
 }
 
@@ -180,13 +175,13 @@ FaceMap face_child_map(const mvsk_gpu_ctx* c, long long nf) {
 }
 
 void fold_face_counters(mvsk_gpu_ctx* p) {
-    mvsk_gpu_ctx* c = p->face_child;
-    if (!c) return;
-    p->fwd += c->fwd;
-    p->tr += c->tr;
-    p->phys += c->phys;
-    p->launches += c->launches;
-    c->fwd = c->tr = c->phys = c->launches = 0;
+    for (mvsk_gpu_ctx* c : p->face_pool) {
+        p->fwd += c->fwd;
+        p->tr += c->tr;
+        p->phys += c->phys;
+        p->launches += c->launches;
+        c->fwd = c->tr = c->phys = c->launches = 0;
+    }
 }
 
 }  // namespace mvsk_b200

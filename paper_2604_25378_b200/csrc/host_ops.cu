@@ -427,8 +427,10 @@ void ctx_alloc_workspaces(mvsk_gpu_ctx* ctx) {
 
 void ctx_free(mvsk_gpu_ctx* ctx) {
     if (!ctx) return;
-    if (ctx->face_child) ctx_free(ctx->face_child);
-    ctx->face_child = nullptr;
+    for (mvsk_gpu_ctx* c : ctx->face_pool) ctx_free(c);
+    ctx->face_pool.clear();
+    if (ctx->face_scratch) cudaFree(ctx->face_scratch);
+    if (ctx->face_scratch_host) cudaFreeHost(ctx->face_scratch_host);
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->owns_X && ctx->X) cudaFree(ctx->X);

@@ -65,9 +65,15 @@ const void* select_kernel(Op op, int K, int Q, int RG) {
             if (Q == 1 && RG == 1) return kfn<Op::HVP, 4, 1, 1>();
             if (Q == 1 && RG == 2) return kfn<Op::HVP, 4, 1, 2>();
             if (Q == 2 && RG == 1) return kfn<Op::HVP, 4, 2, 1>();
+        } else if (K == 8) {  // narrow panels (compact faces): one column pair per thread
+            if (Q == 1 && RG == 1) return kfn<Op::HVP, 8, 1, 1>();
         }
         break;
     case Op::THIRD:
+        if (K == 8 || K == 4) {  // narrow panels
+            if (Q == 1 && RG == 1) return K == 8 ? kfn<Op::THIRD, 8, 1, 1>() : kfn<Op::THIRD, 4, 1, 1>();
+            break;
+        }
         if (K == 1) {
             MVSK_QRG(Op::THIRD, 1)
             if (Q == 8 && RG == 1) return kfn<Op::THIRD, 1, 8, 1>();
@@ -81,8 +87,8 @@ const void* select_kernel(Op op, int K, int Q, int RG) {
 
 // largest Q allowed per (op, K) given register budgets (<= ~110 live fp64)
 int max_q(Op op, int K) {
-    if (op == Op::HVP) return K == 1 ? 8 : K == 2 ? 8 : 2;
-    if (op == Op::THIRD) return 8;
+    if (op == Op::HVP) return K == 1 ? 8 : K == 2 ? 8 : K == 4 ? 2 : 1;
+    if (op == Op::THIRD) return K == 1 ? 8 : 1;
     return 8;
 }
 
@@ -489,6 +495,17 @@ void run_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
             if (io.vin2) sub.vin2 = io.vin2 + (size_t)done * ctx->ld;
             sub.out = io.out + (size_t)done * io.ldo;
             int kk = 0;
+            // narrow panels (compact faces, ld <= 256): the k-RHS pass as one
+            // cooperative streaming kernel (fused reduction) beats the cluster
+            // tensor-core kernel, whose per-stage exchange dominates tiny rows
+            if (ctx->ld <= 256)
+                for (int w : {8, 4}) {
+                    Plan tmp;
+                    if (!kk && left >= w && make_plan(ctx, op, w, tmp)) {
+                        run_single(ctx, op, w, sub);
+                        kk = w;
+                    }
+                }
             for (int w : {8, 4})
                 if (!kk && left >= w && run_dmma(ctx, op, w, sub)) kk = w;
             for (int w : {8, 4})

@@ -170,12 +170,8 @@ struct StepParams {
 };
 
 // one capped-CG step per active column, from the HVP rows H (full coordinates)
-__global__ void __launch_bounds__(kPT) cg_step_kernel(const StepParams* sp, const double* H, double* vin) {
-    extern __shared__ double t[];
-    __shared__ double sh[32];
-    const Geo g = sp->g;
-    const CGState s = sp->s;
-    const double lambda = sp->lambda;
+__device__ __forceinline__ void cg_step_col(const Geo& g, const CGState& s, double lambda, const double* H,
+                                            double* vin, double* t, double* sh) {
     const int c = blockIdx.x, mm = s.mm;
     if (!s.active[c]) return;
     // thread 0 rewrites rz only after every thread passed the barriers below
@@ -225,6 +221,30 @@ __global__ void __launch_bounds__(kPT) cg_step_kernel(const StepParams* sp, cons
     // lift the next search direction into the HVP input row (fused lift_kernel;
     // t's reduced-H values are dead here, so it holds q)
     if (still) lift_col(g, P, true, vin + (size_t)c * g.ld, t, sh);
+}
+
+// set_cond (inside the Krylov graph): the last column CTA to finish sets the
+// while-loop condition from every column's activity flag, so a CG step is two
+// kernels (the HVP pass and this one)
+__global__ void __launch_bounds__(kPT) cg_step_kernel(const StepParams* sp, const double* H, double* vin,
+                                                      unsigned* arrive, cudaGraphConditionalHandle h, int set_cond) {
+    extern __shared__ double t[];
+    __shared__ double sh[32];
+    const Geo g = sp->g;
+    const CGState s = sp->s;
+    cg_step_col(g, s, sp->lambda, H, vin, t, sh);
+    if (!set_cond) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();  // this column's activity flag before the arrival
+        if (atomicAdd(arrive, 1u) == gridDim.x - 1) {
+            __threadfence();
+            int any = 0;
+            for (int col = 0; col < (int)gridDim.x; ++col) any |= ((volatile const int*)s.active)[col];
+            *arrive = 0u;
+            cudaGraphSetConditional(h, any ? 1u : 0u);
+        }
+    }
 }
 
 // out = Q^T U^T H (+ lambda e) per column, or a += sum_c Q^T U^T H_c (in column order)
@@ -343,7 +363,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     // face size (they are baked into the instantiated Krylov graphs)
     const long long N = ctx->n;
     const size_t need = 256 * 32 + sizeof(double) * ((size_t)N + N + N + 6 * (size_t)K * N + 4 * N + 4 * K) +
-                        sizeof(long long) * N + sizeof(int) * 4 * K + sizeof(StepParams) + 256;
+                        sizeof(long long) * N + sizeof(int) * 4 * K + sizeof(StepParams) + 512;
     if (!ctx->pcg) ctx->pcg = new PcgWorkspace();
     PcgWorkspace& ws = *ctx->pcg;
     if (ws.bytes < need) {
@@ -390,6 +410,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     int* iters = carve<int>(cur, K);
     int* bdown = carve<int>(cur, K);
     StepParams* sp_dev = carve<StepParams>(cur, 1);
+    unsigned* arrive = carve<unsigned>(cur, 1);
     cudaStream_t st = ctx->stream;
 
     MVSK_CUDA(cudaMemcpyAsync(vU, in.vU.data(), m * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -526,9 +547,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
                 io.ldo = (long long)ld;
                 run_pass(ctx, Op::HVP, k, io);
                 ++ctx->launches;
-                cg_step_kernel<<<k, kPT, dsm_max, st>>>(sp_dev, H, vin);
-                ++ctx->launches;
-                cg_decide_kernel<<<1, 32, 0, st>>>(active, k, h);
+                cg_step_kernel<<<k, kPT, dsm_max, st>>>(sp_dev, H, vin, arrive, h, 1);
             } catch (...) {
                 threw = true;
             }
@@ -555,6 +574,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         StepParams* hp = ws.host_params + deferred.size();
         *hp = StepParams{g, s, in.lambda};
         MVSK_CUDA(cudaMemcpyAsync(sp_dev, hp, sizeof(StepParams), cudaMemcpyHostToDevice, st));
+        MVSK_CUDA(cudaMemsetAsync(arrive, 0, sizeof(unsigned), st));
         ++ctx->launches;
         cg_init_kernel<<<k, kPT, dsm, st>>>(g, s, src, vin);
         MVSK_CUDA(cudaGetLastError());
@@ -579,7 +599,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
             io.nskip = k;
             run_pass(ctx, Op::HVP, k, io);
             ++ctx->launches;
-            cg_step_kernel<<<k, kPT, dsm_max, st>>>(sp_dev, H, vin);
+            cg_step_kernel<<<k, kPT, dsm_max, st>>>(sp_dev, H, vin, arrive, cudaGraphConditionalHandle{}, 0);
             MVSK_CUDA(cudaGetLastError());
             const int nb = (step + 1) & 1;
             MVSK_CUDA(cudaMemcpyAsync(hf + nb * K, active, k * sizeof(int), cudaMemcpyDeviceToHost, st));
