@@ -336,6 +336,7 @@ const void* select_dmma(Op op, int K, int WC, int D) {
         if (op == Op::THIRD && K == 8) {
             if (WC == 64) return dfn<Op::THIRD, 8, 64, 0>();
             if (WC == 80) return dfn<Op::THIRD, 8, 80, 0>();
+            if (WC == 128) return dfn<Op::THIRD, 8, 128, 0>();
         }
     }
     if (D == 1) {
