@@ -333,6 +333,8 @@ const void* select_dmma(Op op, int K, int WC, int D) {
             MVSK_DWC(Op::HVP, 8, 0)
             if (WC == 160) return dfn<Op::HVP, 8, 160, 0>();
         }
+        if (op == Op::HVP && K == 4) { MVSK_DWC(Op::HVP, 4, 0) }
+        if (op == Op::THIRD && K == 4) { MVSK_DWC(Op::THIRD, 4, 0) }
         if (op == Op::THIRD && K == 8) {
             if (WC == 64) return dfn<Op::THIRD, 8, 64, 0>();
             if (WC == 80) return dfn<Op::THIRD, 8, 80, 0>();

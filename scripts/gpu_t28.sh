@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+TUNE_DEFAULT_ONLY=1 timeout 300 python scripts/tune_stream.py C5 hvp4 2>&1 | grep -E "dmma0|dmma4,1"
+MVSK_TUNE_DMMA_FIX="4,1" TUNE_DEFAULT_ONLY=1 timeout 300 python scripts/tune_stream.py C5 hvp4 2>&1 | grep dmma0 | sed 's/^/[D=1] /'
+timeout 300 python -m pytest tests/test_gpu_oracle.py -q -p no:cacheprovider -k multi_rhs 2>&1 | tail -2
