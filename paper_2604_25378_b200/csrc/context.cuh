@@ -15,6 +15,7 @@
 namespace mvsk_b200 {
 
 struct PcgWorkspace;
+struct SpgWorkspace;
 
 struct ApiError : std::runtime_error {
     int code;
@@ -98,6 +99,7 @@ struct mvsk_gpu_ctx {
     double* tvec2 = nullptr; // T_local scratch (lazy)
     double* pmat = nullptr;  // ld x ld (lazy)
     mvsk_b200::PcgWorkspace* pcg = nullptr;  // device-resident PCG buffers (lazy)
+    mvsk_b200::SpgWorkspace* spg = nullptr;  // device-resident SPG preamble (lazy)
     double* gram_part = nullptr;
     size_t gram_part_elems = 0;
     // pinned host staging

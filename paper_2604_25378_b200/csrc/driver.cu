@@ -24,6 +24,7 @@
 
 #include "host_ops.hpp"
 #include "pcg_device.hpp"
+#include "spg_device.hpp"
 
 namespace mvsk_b200 {
 namespace {
@@ -31,7 +32,7 @@ namespace {
 // ---- optional host-side profile of a solve (MVSK_PROFILE=1 -> stderr) --------
 struct Prof {
     bool on = false;
-    double proj = 0, dir = 0, cache = 0, grad = 0, line = 0, total = 0, face = 0, resid = 0;
+    double proj = 0, dir = 0, cache = 0, grad = 0, line = 0, total = 0, face = 0, resid = 0, spg = 0;
     long nproj = 0, ndir = 0, ncache = 0, nline = 0, nface = 0, nresid = 0;
 };
 Prof g_prof;
@@ -786,6 +787,14 @@ Vec spg_identify(const View& full, Vec x, double tau, int max_steps, int patienc
                  const std::function<void(int, double, const Vec&)>& observer) {
     double f = full.make_cache(kSlotTmp, x);
     Vec g = full.gradient(kSlotTmp);
+    // the whole preamble as one device graph (bitwise the loop below) unless an
+    // observer must see every step or the panel is out of the device loop's range
+    if (!observer && !full.fm.active) {
+        Tick tk(g_prof.spg);
+        Vec xd = x;
+        if (spg_identify_device(full.ctx, kSlotTmp, xd, f, g, tau, max_steps, patience, eps_stop, steps_out))
+            return xd;
+    }
     Vec xcur = x;
     double L = 10.0;
     bool have_bb = false;
@@ -1501,11 +1510,11 @@ int32_t mvsk_gpu_solve(mvsk_gpu_ctx* ctx, const mvsk_solver_config* cfg, const d
             std::fprintf(stderr,
                          "[mvsk profile] total %.3f ms | make_cache %.3f ms (%ld) | gradient %.3f ms | direction %.3f "
                          "ms (%ld) | line_model %.3f ms (%ld) | project_slice %.3f ms (%ld) | face rebuild %.3f ms (%ld) "
-                         "| full residual %.3f ms (%ld)\n",
+                         "| full residual %.3f ms (%ld) | spg %.3f ms\n",
                          1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
                          1e3 * g_prof.cache, g_prof.ncache, 1e3 * g_prof.grad, 1e3 * g_prof.dir, g_prof.ndir,
                          1e3 * g_prof.line, g_prof.nline, 1e3 * g_prof.proj, g_prof.nproj, 1e3 * g_prof.face,
-                         g_prof.nface, 1e3 * g_prof.resid, g_prof.nresid);
+                         g_prof.nface, 1e3 * g_prof.resid, g_prof.nresid, 1e3 * g_prof.spg);
         std::copy(r.x.begin(), r.x.end(), x_star);
         std::memset(report, 0, sizeof(*report));
         report->f_star = r.f;

@@ -12,6 +12,7 @@
 
 #include "host_ops.hpp"
 #include "pcg_device.hpp"
+#include "spg_device.hpp"
 
 namespace mvsk_b200 {
 
@@ -449,6 +450,7 @@ void ctx_free(mvsk_gpu_ctx* ctx) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
     if (ctx->comm && ctx->owns_comm) ncclCommDestroy(ctx->comm);
     pcg_workspace_free(ctx);
+    spg_workspace_free(ctx);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }

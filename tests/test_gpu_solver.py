@@ -379,3 +379,45 @@ def test_compact_faces_match_cpu_and_index_maps():
     assert _active(xi, cfg_g.tau) == _active(xg, cfg_g.tau)
     assert abs(ref["f"] - rg.f_star) <= 1e-12 * (1 + abs(rg.f_star))
     assert float(np.max(np.abs(xi - xg))) <= 1e-6
+
+
+@pytest.mark.parametrize("name,kappa", [("C2", 1000.0), ("C3", 1.0)])
+def test_device_spg_preamble_is_bitwise_the_host_loop(name, kappa):
+    """The identification preamble as one device graph (spg_device.cu, opt-in
+    via MVSK_SPG_GRAPH) runs the host loop's arithmetic in the host loop's order
+    (sequential dots and projection sums, no contraction), so the whole
+    large-preset solve is bitwise identical with the host-driven preamble,
+    including the pass counts (the device variant runs in a subprocess because
+    the switch is read once)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from paper_2604_25378_b200.datagen import make_panel
+    from paper_2604_25378_b200.gpu_oracle import preset
+    A, mu, c = make_panel(name, seed=11, kappa=kappa)
+    cfg = preset("large")
+    cfg.has_max_elapsed = 0
+    xg, rg = _gpu(A, mu, c).solve(cfg)  # host-driven preamble (the default)
+    code = (
+        "import json, sys\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_2604_25378_b200.datagen import make_panel\n"
+        "from paper_2604_25378_b200.gpu_oracle import GpuOracle, preset\n"
+        "A, mu, c = make_panel(%r, seed=11, kappa=%r)\n"
+        "cfg = preset('large'); cfg.has_max_elapsed = 0\n"
+        "x, r = GpuOracle(A, mu, c).solve(cfg)\n"
+        "print(json.dumps({'x': x.hex() if hasattr(x, 'hex') else None, 'xs': [float(v).hex() for v in x],"
+        " 'it': r.iterations, 'ident': r.identification_steps, 'passes': r.oracle_passes,"
+        " 'phys': r.physical_passes, 'f': float(r.f_star).hex()}))\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), name, kappa)
+    env = dict(os.environ, MVSK_SPG_GRAPH="1", MVSK_PROFILE="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600, check=True)
+    ref = json.loads(out.stdout.strip().splitlines()[-1])
+    spg_ms = float(out.stderr.split("| spg ")[-1].split(" ms")[0])
+    assert spg_ms > 0.0, out.stderr  # the device preamble ran
+    assert [float(v).hex() for v in xg] == ref["xs"]
+    assert float(rg.f_star).hex() == ref["f"]
+    assert (rg.iterations, rg.identification_steps, rg.oracle_passes, rg.physical_passes) == \
+        (ref["it"], ref["ident"], ref["passes"], ref["phys"])
+    assert rg.identification_steps > 0
