@@ -94,7 +94,13 @@ mvsk_gpu_ctx* face_context(mvsk_gpu_ctx* p, const std::vector<int64_t>& free_idx
         p->face_pool.push_back(c);
     }
     const long long ncap = c->n;
-    c->c = p->c;
+    // follow the parent's stream and coefficients; coefficients are baked into
+    // the child's captured graphs, so a change makes them stale (epoch)
+    c->stream = p->stream;
+    if (std::memcmp(&c->c, &p->c, sizeof(mvsk_coeffs)) != 0) {
+        c->c = p->c;
+        ++c->epoch;
+    }
     std::fill(c->mu.begin(), c->mu.end(), 0.0);
     double mu_pin = 0.0;
     for (long long i = 0, j = 0; i < n0; ++i) {

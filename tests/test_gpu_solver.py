@@ -270,8 +270,8 @@ def test_cpp_host_solves_a_binary_panel(tmp_path):
     assert np.max(np.abs(xg - xc)) <= 1e-7
 
 
-@pytest.mark.parametrize("name,mode", [("C1", "small"), ("C2", "large")])
-def test_floor_sweep_matches_cpu_mirror(name, mode):
+@pytest.mark.parametrize("name,mode,nfloors", [("C1", "small", 3), ("C2", "large", 3), ("C3", "large", 2)])
+def test_floor_sweep_matches_cpu_mirror(name, mode, nfloors):
     """Return-floor sweep (BASELINE config 4, c1 calibration of PAPER.md:757):
     the device sweep (driver.cu floor_sweep over GPU solves) takes the same
     bracketing/bisection decisions as the Python mirror over CPU-oracle solves,
@@ -283,9 +283,11 @@ def test_floor_sweep_matches_cpu_mirror(name, mode):
     for cfg in (cfg_c, cfg_g):
         cfg.has_max_elapsed = 0
         cfg.epsilon = 1e-10
-    ref = rh.floor_sweep_ref(lambda cc, x0: po.solve(A, mu, cc, cfg_c, x0)[0], mu, c, nfloors=3)
+    # C3 (n = 800): the solves run on compact face contexts, whose captured
+    # graphs must follow every c1 change of the sweep
+    ref = rh.floor_sweep_ref(lambda cc, x0: po.solve(A, mu, cc, cfg_c, x0)[0], mu, c, nfloors=nfloors)
     g = _gpu(A, mu, c)
-    out = g.floor_sweep(cfg_g, nfloors=3)
+    out = g.floor_sweep(cfg_g, nfloors=nfloors)
     assert out.total_solves == ref["total"]
     assert out.m_max == ref["m_max"]
     assert abs(out.m_mv - ref["m_mv"]) <= 1e-9 * abs(ref["m_max"] - ref["m_mv"])
