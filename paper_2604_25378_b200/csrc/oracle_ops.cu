@@ -135,12 +135,14 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     // several teams per CTA so more rows are in flight (C3: 63 -> 34 us / HVP)
     const bool small = ctx->T_local < 64LL * ctx->nsm;
     int Q = -1;
-    if (small) {  // teams of <= 128 threads (C2/C3 sweeps, profiles/r01_tune_C*.txt)
-        for (int q = 1; q <= qmax; q <<= 1)
-            if ((npairs + q - 1) / q <= 128 && (npairs + q - 1) / q <= max_threads(op, K, q, 1)) {
+    if (small) {
+        // short teams, many of them: the most column pairs per thread that
+        // fits, so up to 16 teams share a CTA and a CTA's few rows are in
+        // flight in one or two stages (profiles/r01_tune_small_panels.txt:
+        // T=5000 n=64 12.3 -> 8.3 us, n=256 15.4 -> 10.3 us per HVP)
+        for (int q = qmax; q >= 1 && Q < 0; q >>= 1)
+            if (round_team((int)((npairs + q - 1) / q)) <= max_threads(op, K, q, 1) && select_kernel(op, K, q, 1))
                 Q = q;
-                break;
-            }
     }
     for (int q = 1; Q < 0 && q <= qmax; q <<= 1)
         if ((npairs + q - 1) / q <= 256) {
@@ -160,7 +162,7 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     const size_t row_bytes = (size_t)ctx->ld * sizeof(double);
     const size_t stage_target = 64 * 1024;
     // teams per CTA (each team streams its own rows)
-    int G = small ? std::max(1, std::min(std::max(4, 32 / P), max_threads(op, K, Q, 1) / P))
+    int G = small ? std::max(1, std::min(16, max_threads(op, K, Q, 1) / P))
                   : std::max(1, max_threads(op, K, Q, 1) / P);
     const long long want_rows = std::max<long long>(1, (long long)(stage_target / row_bytes));
     while (G > 1 && G > want_rows) G >>= 1;
@@ -168,6 +170,12 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     while (!small && RG < 4 && RG * 2 * Q <= 8 && (long long)G * RG * 2 <= want_rows &&
            G * P <= max_threads(op, K, Q, RG * 2))
         RG <<= 1;
+    if (small) {  // enough rows per stage to cover a CTA's share in one stage
+        const long long rows_cta = (ctx->T_local + ctx->nsm - 1) / ctx->nsm;
+        while (RG < 4 && (long long)G * RG < rows_cta && RG * 2 * Q <= 8 && G * P <= max_threads(op, K, Q, RG * 2) &&
+               select_kernel(op, K, Q, RG * 2) && (long long)G * RG * 2 <= want_rows)
+            RG <<= 1;
+    }
     // a heavy op whose team fills the CTA (THIRD, 2-RHS HVP at n=4096) would
     // otherwise keep one row in flight per CTA and expose the per-row reduction
     // latency (C5 third: 8 warps/SM, 'wait' + short-scoreboard stalls); two rows

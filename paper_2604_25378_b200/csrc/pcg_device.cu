@@ -113,9 +113,19 @@ struct CGState {
     double tol;
 };
 
-__global__ void __launch_bounds__(kPT) cg_init_kernel(Geo g, CGState s, const double* rhs, double* vin) {
+// step parameters live in device memory so one instantiated graph serves every
+// direction (the reflector scalars, face size, cap and tolerance change)
+struct StepParams {
+    Geo g;
+    CGState s;
+    double lambda;
+};
+
+__global__ void __launch_bounds__(kPT) cg_init_kernel(const StepParams* sp, const double* rhs, double* vin) {
     extern __shared__ double q[];
     __shared__ double sh[32];
+    const Geo g = sp->g;
+    const CGState s = sp->s;
     const int c = blockIdx.x, mm = s.mm;
     const double* b = rhs + (size_t)c * mm;
     double* X = s.X + (size_t)c * mm;
@@ -148,10 +158,13 @@ __global__ void __launch_bounds__(kPT) cg_init_kernel(Geo g, CGState s, const do
 }
 
 // lift P (or an arbitrary source block) of the active columns into HVP input rows
-__global__ void __launch_bounds__(kPT) lift_kernel(Geo g, const double* E, int ldE, bool apply_q, const int* active,
+// E rows have stride mm (apply_q) or m - 1 (U only), the face sizes of *gp
+__global__ void __launch_bounds__(kPT) lift_kernel(const Geo* gp, const double* E, bool apply_q, const int* active,
                                                    double* vin) {
     extern __shared__ double q[];
     __shared__ double sh[32];
+    const Geo g = *gp;
+    const int ldE = apply_q ? g.m - 2 : g.m - 1;
     const int c = blockIdx.x;
     double* row = vin + (size_t)c * g.ld;
     if (active && !active[c]) {
@@ -160,14 +173,6 @@ __global__ void __launch_bounds__(kPT) lift_kernel(Geo g, const double* E, int l
     }
     lift_col(g, E + (size_t)c * ldE, apply_q, row, q, sh);
 }
-
-// step parameters live in device memory so one instantiated Krylov graph serves
-// every direction (the reflector scalars, face size, cap and tolerance change)
-struct StepParams {
-    Geo g;
-    CGState s;
-    double lambda;
-};
 
 // one capped-CG step per active column, from the HVP rows H (full coordinates)
 __device__ __forceinline__ void cg_step_col(const Geo& g, const CGState& s, double lambda, const double* H,
@@ -248,20 +253,28 @@ __global__ void __launch_bounds__(kPT) cg_step_kernel(const StepParams* sp, cons
 }
 
 // out = Q^T U^T H (+ lambda e) per column, or a += sum_c Q^T U^T H_c (in column order)
-__global__ void __launch_bounds__(kPT) reduce_kernel(Geo g, const double* H, int k, bool apply_q, double* out,
-                                                     int ldo) {
+__global__ void __launch_bounds__(kPT) reduce_kernel(const Geo* gp, const double* H, bool apply_q, double* out) {
     extern __shared__ double t[];
     __shared__ double sh[32];
+    const Geo g = *gp;
+    const int ldo = g.m - 2;
     const int c = blockIdx.x;
     const double* r = reduce_col(g, H + (size_t)c * g.ld, apply_q, t, sh);
     const int len = apply_q ? g.m - 2 : g.m - 1;
     for (int i = threadIdx.x; i < len; i += blockDim.x) out[(size_t)c * ldo + i] = r[i];
 }
 
+// per-direction scalars of the elementwise kernels (device memory, graph-stable)
+struct DirScalars {
+    int mm;
+    double lambda, fl, adiv, coef;
+};
+
 // Jacobi diagonal from the probe responses (:197-209): mean over probes of
 // r o (Qt Ut H U Q r + lambda r), floored at max(1e-12, lambda); probe order fixed
-__global__ void jacobi_diag_kernel(const double* probes, const double* rows, int k, int mm, double lambda, double fl,
-                                   double* jd) {
+__global__ void jacobi_diag_kernel(const DirScalars* ds, const double* probes, const double* rows, int k, double* jd) {
+    const int mm = ds->mm;
+    const double lambda = ds->lambda, fl = ds->fl;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mm; i += gridDim.x * blockDim.x) {
         double v = 0.0;
         for (int p = 0; p < k; ++p) {
@@ -274,7 +287,8 @@ __global__ void jacobi_diag_kernel(const double* probes, const double* rows, int
 }
 
 // exact-trace probes e_{b0}..e_{b0+k-1} (:217-226)
-__global__ void unit_probe_kernel(double* src, int k, int mm, int b0) {
+__global__ void unit_probe_kernel(const DirScalars* ds, double* src, int k, int b0) {
+    const int mm = ds->mm;
     const size_t tot = (size_t)k * mm;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
         const int p = (int)(e / mm), i = (int)(e - (size_t)p * mm);
@@ -283,7 +297,8 @@ __global__ void unit_probe_kernel(double* src, int k, int mm, int b0) {
 }
 
 // a += sum of the block's third-action rows, in probe order (:225, :235)
-__global__ void accum_rows_kernel(const double* rows, int k, int mm, double* a) {
+__global__ void accum_rows_kernel(const DirScalars* ds, const double* rows, int k, double* a) {
+    const int mm = ds->mm;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mm; i += gridDim.x * blockDim.x) {
         double v = a[i];
         for (int p = 0; p < k; ++p) v += rows[(size_t)p * mm + i];
@@ -292,7 +307,9 @@ __global__ void accum_rows_kernel(const double* rows, int k, int mm, double* a) 
 }
 
 // rhs = h - (||gbar|| / n) a, a averaged over the Hutchinson probes (:236, :239)
-__global__ void rhs_kernel(const double* h, const double* a, int mm, double adiv, double coef, double* rhs) {
+__global__ void rhs_kernel(const DirScalars* ds, const double* h, const double* a, double* rhs) {
+    const int mm = ds->mm;
+    const double adiv = ds->adiv, coef = ds->coef;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mm; i += gridDim.x * blockDim.x) {
         const double ai = adiv > 0 ? a[i] / adiv : a[i];
         rhs[i] = h[i] - coef * ai;
@@ -321,144 +338,176 @@ T* carve(unsigned char*& cur, size_t count) {
 struct PcgWorkspace {
     size_t bytes = 0;
     unsigned char* dev = nullptr;
-    int* host_flags = nullptr;  // pinned [4 * kPcgMaxCols]
-    StepParams* host_params = nullptr;  // pinned staging of the device StepParams [kMaxDeferred]
-    int* host_counts = nullptr;         // pinned [kMaxDeferred][2][K] iters / breakdown snapshots
-    double* host_stage = nullptr;       // pinned probe staging
-    size_t host_stage_elems = 0;
+    int* host_flags = nullptr;  // pinned [4 * kPcgMaxCols] (host-driven loop flags)
+    int* host_counts = nullptr; // pinned [kMaxDeferred][2][K] iters / breakdown snapshots
+    double* host_u = nullptr;   // pinned solution readback
+    unsigned char* host_up = nullptr;  // pinned upload staging (parameters, geometry, probes)
+    size_t host_up_bytes = 0;
     cudaEvent_t ev[2] = {nullptr, nullptr};
-    // device-resident Krylov loops: a conditional-while graph per (k, slot)
+    cudaStream_t aux = nullptr;  // captures conditional-loop bodies while the direction is captured
+    // device-resident Krylov loops of the eager path: a conditional-while graph per (k, slot)
     struct LoopGraph {
-        int k, slot;
+        int k, slot, role;
         uint64_t epoch;
         cudaGraphExec_t exec;
         uint64_t phys_per_step, launches_per_step;
     };
     std::vector<LoopGraph> graphs;
-    std::vector<std::pair<int, int>> seen;  // (k, slot) keys that ran once at seen_epoch
+    std::vector<std::pair<int, int>> seen;  // (k, slot * 2 + role) keys that ran once at seen_epoch
     uint64_t seen_epoch = ~0ull;
     bool graphs_broken = false;
+    // whole-direction graphs (Hutchinson / no-third directions), keyed by shape
+    struct DirKey {
+        int slot, mm, kp, kj, third;
+        uint64_t epoch;
+        bool operator==(const DirKey& o) const {
+            return slot == o.slot && mm == o.mm && kp == o.kp && kj == o.kj && third == o.third && epoch == o.epoch;
+        }
+    };
+    struct DirGraph {
+        DirKey key;
+        cudaGraphExec_t exec;
+        uint64_t fwd, tr, phys, launches;  // counts of the non-loop part, per replay
+        int nloops;
+        int loop_k[2];
+        uint64_t loop_pps[2], loop_lps[2];
+    };
+    std::vector<DirGraph> dgraphs;
+    std::vector<DirKey> dseen;
+    bool dir_broken = false;
 };
 
 void pcg_workspace_free(mvsk_gpu_ctx* ctx) {
     if (!ctx->pcg) return;
-    for (auto& lg : ctx->pcg->graphs)
+    PcgWorkspace& ws = *ctx->pcg;
+    for (auto& lg : ws.graphs)
         if (lg.exec) cudaGraphExecDestroy(lg.exec);
-    if (ctx->pcg->host_params) cudaFreeHost(ctx->pcg->host_params);
-    if (ctx->pcg->host_counts) cudaFreeHost(ctx->pcg->host_counts);
-    if (ctx->pcg->host_stage) cudaFreeHost(ctx->pcg->host_stage);
-    if (ctx->pcg->dev) cudaFree(ctx->pcg->dev);
-    if (ctx->pcg->host_flags) cudaFreeHost(ctx->pcg->host_flags);
-    for (cudaEvent_t e : ctx->pcg->ev)
+    for (auto& dg : ws.dgraphs)
+        if (dg.exec) cudaGraphExecDestroy(dg.exec);
+    if (ws.host_counts) cudaFreeHost(ws.host_counts);
+    if (ws.host_u) cudaFreeHost(ws.host_u);
+    if (ws.host_up) cudaFreeHost(ws.host_up);
+    if (ws.dev) cudaFree(ws.dev);
+    if (ws.host_flags) cudaFreeHost(ws.host_flags);
+    for (cudaEvent_t e : ws.ev)
         if (e) cudaEventDestroy(e);
+    if (ws.aux) cudaStreamDestroy(ws.aux);
     delete ctx->pcg;
     ctx->pcg = nullptr;
 }
+
+namespace {
+// parameters of one direction (device memory, uploaded from pinned staging)
+struct DirDev {
+    Geo g;
+    StepParams sp[2];  // [0] probe block (cap = probe_cap), [1] main CG (cap = maxit)
+    DirScalars ds;
+};
+}  // namespace
 
 PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const PcgInput& in) {
     const int m = (int)in.m, m1 = m - 1, mm = m - 2;
     const int K = kPcgMaxCols;
     const size_t ld = (size_t)ctx->ld;
-    // ---- workspace, carved for the full n so its pointers do not move with the
-    // face size (they are baked into the instantiated Krylov graphs)
     const long long N = ctx->n;
-    const size_t need = 256 * 32 + sizeof(double) * ((size_t)N + N + N + 6 * (size_t)K * N + 4 * N + 4 * K) +
-                        sizeof(long long) * N + sizeof(int) * 4 * K + sizeof(StepParams) + 512;
     if (!ctx->pcg) ctx->pcg = new PcgWorkspace();
     PcgWorkspace& ws = *ctx->pcg;
-    if (ws.bytes < need) {
+    // ---- device workspace, carved for the full n so its pointers do not move
+    // with the face size (they are baked into the instantiated graphs)
+    unsigned char* base = nullptr;
+    size_t off = 0;
+    auto carve_d = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) / 256 * 256;
+        return o;
+    };
+    const size_t o_dir = carve_d(sizeof(DirDev));
+    const size_t o_vU = carve_d(N * 8), o_vQ = carve_d(N * 8), o_nu = carve_d(N * 8), o_idx = carve_d(N * 8);
+    const size_t o_jsrc = carve_d((size_t)K * N * 8), o_psrc = carve_d((size_t)K * N * 8);
+    const size_t up_bytes = off;  // the uploaded prefix: parameters, geometry, probes
+    const size_t o_X = carve_d((size_t)K * N * 8), o_R = carve_d((size_t)K * N * 8), o_Z = carve_d((size_t)K * N * 8);
+    const size_t o_P = carve_d((size_t)K * N * 8), o_src = carve_d((size_t)K * N * 8), o_rows = carve_d((size_t)K * N * 8);
+    const size_t o_jd = carve_d(N * 8), o_h = carve_d(N * 8), o_a = carve_d(N * 8);
+    const size_t o_rz = carve_d(K * 8), o_tg = carve_d(K * 8);
+    const size_t o_act = carve_d(K * 4), o_it = carve_d(K * 4), o_bd = carve_d(K * 4), o_arr = carve_d(64);
+    if (ws.bytes < off) {
         if (ws.dev) MVSK_CUDA(cudaFree(ws.dev));
         ws.dev = nullptr;
-        MVSK_CUDA(cudaMalloc(&ws.dev, need));
-        ws.bytes = need;
+        MVSK_CUDA(cudaMalloc(&ws.dev, off));
+        ws.bytes = off;
         ++ctx->epoch;
     }
-    if (!ws.host_flags) MVSK_CUDA(cudaMallocHost(&ws.host_flags, sizeof(int) * 4 * K));
-    // one pinned StepParams per Krylov loop of the direction: the H2D copies are
-    // asynchronous, so a later loop must not overwrite an earlier loop's staging
-    if (!ws.host_params) MVSK_CUDA(cudaMallocHost(&ws.host_params, sizeof(StepParams) * kMaxDeferred));
-    if (!ws.host_counts) MVSK_CUDA(cudaMallocHost(&ws.host_counts, sizeof(int) * kMaxDeferred * 2 * K));
-    // pinned probe staging: the Jacobi probes and every Hutchinson probe of this
-    // direction, copied asynchronously (no host round trip inside the direction)
-    const size_t stage_need = (in.jacobi_probes.size() + in.probes.size()) * (size_t)std::max(mm, 1);
-    if (ws.host_stage_elems < stage_need) {
-        if (ws.host_stage) MVSK_CUDA(cudaFreeHost(ws.host_stage));
-        ws.host_stage = nullptr;
-        ws.host_stage_elems = 0;
-        MVSK_CUDA(cudaMallocHost(&ws.host_stage, stage_need * sizeof(double)));
-        ws.host_stage_elems = stage_need;
+    if (ws.host_up_bytes < up_bytes) {
+        if (ws.host_up) MVSK_CUDA(cudaFreeHost(ws.host_up));
+        ws.host_up = nullptr;
+        ws.host_up_bytes = 0;
+        MVSK_CUDA(cudaMallocHost(&ws.host_up, up_bytes));
+        ws.host_up_bytes = up_bytes;
+        ++ctx->epoch;
+        if (ws.host_u) MVSK_CUDA(cudaFreeHost(ws.host_u));
+        MVSK_CUDA(cudaMallocHost(&ws.host_u, (size_t)std::max<long long>(N, 1) * sizeof(double)));
     }
+    if (!ws.host_flags) MVSK_CUDA(cudaMallocHost(&ws.host_flags, sizeof(int) * 4 * K));
+    if (!ws.host_counts) MVSK_CUDA(cudaMallocHost(&ws.host_counts, sizeof(int) * kMaxDeferred * 2 * K));
     for (cudaEvent_t& e : ws.ev)
         if (!e) MVSK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    unsigned char* cur = ws.dev;
-    double* vU = carve<double>(cur, N);
-    double* vQ = carve<double>(cur, N);
-    double* nu = carve<double>(cur, N);
-    double* X = carve<double>(cur, (size_t)K * N);  // [k][mm] blocks
-    double* Rm = carve<double>(cur, (size_t)K * N);
-    double* Z = carve<double>(cur, (size_t)K * N);
-    double* P = carve<double>(cur, (size_t)K * N);
-    double* src = carve<double>(cur, (size_t)K * N);  // rhs / probes
-    double* rows = carve<double>(cur, (size_t)K * N);  // reduced outputs
-    double* jd = carve<double>(cur, N);
-    double* hvec = carve<double>(cur, N);
-    double* avec = carve<double>(cur, N);
-    double* rz = carve<double>(cur, K);
-    double* target = carve<double>(cur, K);
-    long long* idx = carve<long long>(cur, N);
-    int* active = carve<int>(cur, K);
-    int* iters = carve<int>(cur, K);
-    int* bdown = carve<int>(cur, K);
-    StepParams* sp_dev = carve<StepParams>(cur, 1);
-    unsigned* arrive = carve<unsigned>(cur, 1);
+    if (!ws.aux) MVSK_CUDA(cudaStreamCreateWithFlags(&ws.aux, cudaStreamNonBlocking));
+    base = ws.dev;
+    auto D = [&](size_t o) { return reinterpret_cast<double*>(base + o); };
+    DirDev* dir = reinterpret_cast<DirDev*>(base + o_dir);
+    double *vU = D(o_vU), *vQ = D(o_vQ), *nu = D(o_nu), *jsrc = D(o_jsrc), *psrc = D(o_psrc);
+    long long* idx = reinterpret_cast<long long*>(base + o_idx);
+    double *X = D(o_X), *Rm = D(o_R), *Z = D(o_Z), *P = D(o_P), *src = D(o_src), *rows = D(o_rows);
+    double *jd = D(o_jd), *hvec = D(o_h), *avec = D(o_a), *rz = D(o_rz), *target = D(o_tg);
+    int* active = reinterpret_cast<int*>(base + o_act);
+    int* iters = reinterpret_cast<int*>(base + o_it);
+    int* bdown = reinterpret_cast<int*>(base + o_bd);
+    unsigned* arrive = reinterpret_cast<unsigned*>(base + o_arr);
     cudaStream_t st = ctx->stream;
 
-    MVSK_CUDA(cudaMemcpyAsync(vU, in.vU.data(), m * sizeof(double), cudaMemcpyHostToDevice, st));
-    MVSK_CUDA(cudaMemcpyAsync(vQ, in.vQ.data(), m1 * sizeof(double), cudaMemcpyHostToDevice, st));
-    MVSK_CUDA(cudaMemcpyAsync(nu, in.nu.data(), m1 * sizeof(double), cudaMemcpyHostToDevice, st));
-    if (fm.active) MVSK_CUDA(cudaMemcpyAsync(idx, fm.idx.data(), m * sizeof(long long), cudaMemcpyHostToDevice, st));
-    Geo g{vU, in.bU, vQ, in.bQ, fm.active ? idx : nullptr, m, (int)ld};
-    const size_t dsm = (size_t)2 * std::max(m, 1) * sizeof(double);
-    const size_t dsm_max = (size_t)2 * std::max<long long>(N, 1) * sizeof(double);  // cg_step (graph-baked)
+    // ---- host staging of everything this direction uploads (same layout as the
+    // device prefix [0, up_bytes)); one contiguous pinned buffer
+    const bool jac = !in.jacobi_probes.empty();
+    const int kj = jac ? (int)in.jacobi_probes.size() : 0;
+    const int kp = in.has_third && !in.unit_probes ? (int)in.probes.size() : 0;
+    unsigned char* hu = ws.host_up;
+    auto HU = [&](size_t o) { return reinterpret_cast<double*>(hu + o); };
+    {
+        DirDev hd{};
+        hd.g = Geo{vU, in.bU, vQ, in.bQ, fm.active ? idx : nullptr, m, (int)ld};
+        const double* jdp = jac ? jd : nullptr;
+        hd.sp[0] = StepParams{hd.g, CGState{X, Rm, Z, P, rz, target, active, iters, bdown, jdp, mm, in.probe_cap, in.tol},
+                              in.lambda};
+        hd.sp[1] = StepParams{hd.g, CGState{X, Rm, Z, P, rz, target, active, iters, bdown, jdp, mm, in.maxit, in.tol},
+                              in.lambda};
+        hd.ds = DirScalars{mm, in.lambda, std::max(1e-12, in.lambda),
+                           (in.has_third && !in.unit_probes) ? (double)in.hutchinson_probes : 0.0, in.gn / (double)m};
+        std::memcpy(hu + o_dir, &hd, sizeof(hd));
+        std::copy(in.vU.begin(), in.vU.end(), HU(o_vU));
+        std::copy(in.vQ.begin(), in.vQ.end(), HU(o_vQ));
+        std::copy(in.nu.begin(), in.nu.end(), HU(o_nu));
+        if (fm.active) std::memcpy(hu + o_idx, fm.idx.data(), (size_t)m * sizeof(long long));
+        for (int p = 0; p < kj; ++p) std::copy(in.jacobi_probes[p].begin(), in.jacobi_probes[p].end(), HU(o_jsrc) + (size_t)p * mm);
+        for (int p = 0; p < kp && p < K; ++p) std::copy(in.probes[p].begin(), in.probes[p].end(), HU(o_psrc) + (size_t)p * mm);
+    }
+    const size_t dsm_max = (size_t)2 * std::max<long long>(N, 1) * sizeof(double);
     for (const void* fn : {(const void*)lift_kernel, (const void*)cg_step_kernel, (const void*)reduce_kernel,
                            (const void*)cg_init_kernel})
         set_smem_attr(fn, dsm_max);
+    const int nb1 = (int)std::min<long long>(4LL * ctx->nsm, (N + 255) / 256 + 1);
     const Slot& sl = ctx->slots[slot];
     double* vin = ctx->vin;
     double* vin2 = ctx->vin + (size_t)MVSK_GPU_MAX_RHS * ld;
     double* H = ctx->outd;
+    const Geo* gdev = &dir->g;
+    const DirScalars* dsd = &dir->ds;
 
     PcgOutput out;
-    auto hvp_rows = [&](int k, int logical) {
-        PassIO io;
-        io.vin = vin;
-        io.z = sl.z;
-        io.out = H;
-        io.ldo = (long long)ld;
-        run_pass(ctx, Op::HVP, k, io);
-        ctx->fwd += logical;  // reference contract: 2 passes per (active) HVP
-        ctx->tr += logical;
-    };
-    // capped CG on k columns in lock-step (the columns' arithmetic is
-    // cg_capped's). Steps are enqueued one ahead of the host's look at the
-    // activity flags: step s+1 is already queued while the host reads the flags
-    // that gate step s, and a step whose flags are all 0 is a device-side no-op
-    // (every kernel of the step, including the HVP pass, exits on entry). So
-    // the GPU never idles on a host round trip inside the Krylov loop.
-    // Capped CG on k columns in lock-step (the columns' arithmetic is
-    // cg_capped's). Preferred: the whole loop is ONE conditional-while CUDA graph
-    // (body = the k-RHS HVP pass, cg_step, and a 1-thread kernel that sets the
-    // loop condition from the columns' activity flags), so no host round trip
-    // happens inside the Krylov loop; the graph is instantiated once per
-    // (k, slot) and reused for every direction (its parameters live in device
-    // memory). Fallback: a host-driven loop that enqueues step s+1 before
-    // reading the flags that gate step s (a step whose flags are all 0 is a
-    // device-side no-op), so the GPU does not idle on the round trip either.
-    // per-cg-call bookkeeping, settled after the direction's single final sync
+    // per-loop bookkeeping, settled after the direction's final sync
     struct Deferred {
         int k;
-        int slot;  // pinned row of [iters | breakdown] snapshots
-        uint64_t pps, lps;  // passes / launches per step (graph loops); 0: counted already
+        int row;            // pinned row of [iters | breakdown] snapshots
+        uint64_t pps, lps;  // passes / launches per step (graph loops); 0: counted live
         bool graph;
     };
     std::vector<Deferred> deferred;
@@ -472,7 +521,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     };
     auto settle_counts = [&]() {
         for (const Deferred& d : deferred) {
-            const int* hc = ws.host_counts + (size_t)d.slot * 2 * K;
+            const int* hc = ws.host_counts + (size_t)d.row * 2 * K;
             int steps = 0;
             for (int c = 0; c < d.k; ++c) {
                 const int col_steps = hc[c] + (hc[K + c] ? 1 : 0);  // HVPs column c consumed
@@ -489,21 +538,70 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         }
         deferred.clear();
     };
+
+    // capture of a loop body on the aux stream (the direction itself may be
+    // capturing on st); the passes inside go to the aux stream too
+    auto capture_body = [&](cudaGraph_t body, int k, const StepParams* spd, cudaGraphConditionalHandle h) -> bool {
+        if (cudaStreamBeginCaptureToGraph(ws.aux, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+            cudaSuccess)
+            return false;
+        bool threw = false;
+        cudaStream_t saved = ctx->stream;
+        ctx->stream = ws.aux;
+        try {
+            PassIO io;
+            io.vin = vin;
+            io.z = sl.z;
+            io.out = H;
+            io.ldo = (long long)ld;
+            run_pass(ctx, Op::HVP, k, io);
+            ++ctx->launches;
+            cg_step_kernel<<<k, kPT, dsm_max, ws.aux>>>(spd, H, vin, arrive, h, 1);
+        } catch (...) {
+            threw = true;
+        }
+        ctx->stream = saved;
+        cudaGraph_t captured = nullptr;
+        return cudaStreamEndCapture(ws.aux, &captured) == cudaSuccess && !threw;
+    };
+    // adds [decide] -> [while {pass, cg_step}] to graph gr after deps
+    auto add_loop = [&](cudaGraph_t gr, const cudaGraphNode_t* deps, size_t ndeps, int k, const StepParams* spd,
+                        cudaGraphNode_t* wn_out) -> bool {
+        cudaGraphConditionalHandle h{};
+        if (cudaGraphConditionalHandleCreate(&h, gr, 0, 0) != cudaSuccess) return false;
+        int kk = k;
+        int* act = active;
+        void* args[] = {&act, &kk, &h};
+        cudaKernelNodeParams kp{};
+        kp.func = reinterpret_cast<void*>(&cg_decide_kernel);
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(32);
+        kp.kernelParams = args;
+        cudaGraphNode_t n0 = nullptr;
+        if (cudaGraphAddKernelNode(&n0, gr, deps, ndeps, &kp) != cudaSuccess) return false;
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        if (cudaGraphAddNode(wn_out, gr, &n0, 1, &cp) != cudaSuccess) return false;
+        return capture_body(cp.conditional.phGraph_out[0], k, spd, h);
+    };
+
+    // ---- the eager path's loop: a per-(k, slot) loop graph, or host-driven
     static const bool no_graph = std::getenv("MVSK_NO_CG_GRAPH") != nullptr;
-    auto cg_graph = [&](int k) -> PcgWorkspace::LoopGraph* {
+    auto cg_graph = [&](int k, int role, const StepParams* spd) -> PcgWorkspace::LoopGraph* {
         if (no_graph || ws.graphs_broken) return nullptr;
-        // the first loop of a key runs host-driven: it sizes the pass workspaces,
-        // which must not be (re)allocated while a graph is being captured
         if (ws.seen_epoch != ctx->epoch) {  // buffers may have been resized: size them eagerly again
             ws.seen.clear();
             ws.seen_epoch = ctx->epoch;
         }
-        if (std::find(ws.seen.begin(), ws.seen.end(), std::make_pair(k, slot)) == ws.seen.end()) {
-            ws.seen.emplace_back(k, slot);
+        if (std::find(ws.seen.begin(), ws.seen.end(), std::make_pair(k, slot * 2 + role)) == ws.seen.end()) {
+            ws.seen.emplace_back(k, slot * 2 + role);
             return nullptr;
         }
         for (auto& lg : ws.graphs)
-            if (lg.k == k && lg.slot == slot) {
+            if (lg.k == k && lg.slot == slot && lg.role == role) {
                 if (lg.epoch == ctx->epoch && lg.exec) return &lg;
                 if (lg.exec) cudaGraphExecDestroy(lg.exec);
                 lg.exec = nullptr;
@@ -511,49 +609,8 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         cudaGraph_t gr = nullptr;
         cudaGraphExec_t exec = nullptr;
         const uint64_t p0 = ctx->phys, l0 = ctx->launches;
-        bool ok = cudaGraphCreate(&gr, 0) == cudaSuccess;
-        cudaGraphConditionalHandle h{};
-        cudaGraphNode_t n0 = nullptr, wn = nullptr;
-        if (ok) ok = cudaGraphConditionalHandleCreate(&h, gr, 0, 0) == cudaSuccess;
-        if (ok) {  // initial condition: any column active after cg_init
-            int kk = k;
-            void* args[] = {&active, &kk, &h};
-            cudaKernelNodeParams kp{};
-            kp.func = reinterpret_cast<void*>(&cg_decide_kernel);
-            kp.gridDim = dim3(1);
-            kp.blockDim = dim3(32);
-            kp.kernelParams = args;
-            ok = cudaGraphAddKernelNode(&n0, gr, nullptr, 0, &kp) == cudaSuccess;
-        }
-        cudaGraph_t body = nullptr;
-        if (ok) {
-            cudaGraphNodeParams cp{};
-            cp.type = cudaGraphNodeTypeConditional;
-            cp.conditional.handle = h;
-            cp.conditional.type = cudaGraphCondTypeWhile;
-            cp.conditional.size = 1;
-            ok = cudaGraphAddNode(&wn, gr, &n0, 1, &cp) == cudaSuccess;
-            if (ok) body = cp.conditional.phGraph_out[0];
-        }
-        if (ok) ok = cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
-                     cudaSuccess;
-        if (ok) {
-            bool threw = false;
-            try {
-                PassIO io;
-                io.vin = vin;
-                io.z = sl.z;
-                io.out = H;
-                io.ldo = (long long)ld;
-                run_pass(ctx, Op::HVP, k, io);
-                ++ctx->launches;
-                cg_step_kernel<<<k, kPT, dsm_max, st>>>(sp_dev, H, vin, arrive, h, 1);
-            } catch (...) {
-                threw = true;
-            }
-            cudaGraph_t captured = nullptr;
-            ok = cudaStreamEndCapture(st, &captured) == cudaSuccess && !threw;
-        }
+        cudaGraphNode_t wn = nullptr;
+        bool ok = cudaGraphCreate(&gr, 0) == cudaSuccess && add_loop(gr, nullptr, 0, k, spd, &wn);
         if (ok) ok = cudaGraphInstantiate(&exec, gr, 0) == cudaSuccess;
         const uint64_t dp = ctx->phys - p0, dl = ctx->launches - l0;
         ctx->phys = p0;
@@ -562,30 +619,53 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         cudaGetLastError();
         if (!ok) {
             if (exec) cudaGraphExecDestroy(exec);
-            ws.graphs_broken = true;  // e.g. a launch kind the conditional body rejects: host loop
+            ws.graphs_broken = true;  // e.g. a launch kind a conditional body rejects: host loop
             return nullptr;
         }
-        ws.graphs.push_back({k, slot, ctx->epoch, exec, dp, dl});
+        ws.graphs.push_back({k, slot, role, ctx->epoch, exec, dp, dl});
         return &ws.graphs.back();
     };
-    auto cg = [&](int k, int cap, const double* jdp) {
-        CGState s{X, Rm, Z, P, rz, target, active, iters, bdown, jdp, mm, cap, in.tol};
-        if (deferred.size() >= (size_t)kMaxDeferred) throw ApiError(MVSK_INTERNAL_ERROR, "pcg: too many Krylov loops");
-        StepParams* hp = ws.host_params + deferred.size();
-        *hp = StepParams{g, s, in.lambda};
-        MVSK_CUDA(cudaMemcpyAsync(sp_dev, hp, sizeof(StepParams), cudaMemcpyHostToDevice, st));
+
+    // ---- the direction as a sequence of enqueues on st. `capture` != nullptr:
+    // st is capturing the whole direction; each Krylov loop is spliced in as a
+    // conditional-while node (its counts recorded in *capture)
+    PcgWorkspace::DirGraph* capture = nullptr;
+    auto cg = [&](int k, int role, const double* rhs) {
+        const StepParams* spd = &dir->sp[role];
         MVSK_CUDA(cudaMemsetAsync(arrive, 0, sizeof(unsigned), st));
         ++ctx->launches;
-        cg_init_kernel<<<k, kPT, dsm, st>>>(g, s, src, vin);
+        cg_init_kernel<<<k, kPT, dsm_max, st>>>(spd, rhs, vin);
         MVSK_CUDA(cudaGetLastError());
-        if (PcgWorkspace::LoopGraph* lg = cg_graph(k)) {
+        if (capture) {
+            cudaStreamCaptureStatus cs;
+            cudaGraph_t gr = nullptr;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t ndeps = 0;
+            MVSK_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &gr, &deps, &ndeps));
+            std::vector<cudaGraphNode_t> dv(deps, deps + ndeps);
+            const uint64_t p0 = ctx->phys, l0 = ctx->launches;
+            cudaGraphNode_t wn = nullptr;
+            if (!add_loop(gr, dv.data(), dv.size(), k, spd, &wn))
+                throw ApiError(MVSK_CUDA_ERROR, "pcg: conditional loop capture failed");
+            MVSK_CUDA(cudaStreamUpdateCaptureDependencies(st, &wn, 1, cudaStreamSetCaptureDependencies));
+            const int li = capture->nloops++;
+            capture->loop_k[li] = k;
+            capture->loop_pps[li] = ctx->phys - p0;
+            capture->loop_lps[li] = ctx->launches - l0;
+            ctx->phys = p0;
+            ctx->launches = l0;
+            defer_counts(k, true, capture->loop_pps[li], capture->loop_lps[li]);
+            return;
+        }
+        if (PcgWorkspace::LoopGraph* lg = cg_graph(k, role, spd)) {
             MVSK_CUDA(cudaGraphLaunch(lg->exec, st));
             defer_counts(k, true, lg->phys_per_step, lg->launches_per_step);
             return;
         }
-        int* hf = ws.host_flags;  // [2][K] flag snapshots + [2K..) iters / breakdown
+        int* hf = ws.host_flags;  // [2][K] flag snapshots
         MVSK_CUDA(cudaMemcpyAsync(hf, active, k * sizeof(int), cudaMemcpyDeviceToHost, st));
         MVSK_CUDA(cudaEventRecord(ws.ev[0], st));
+        const int cap = role == 0 ? in.probe_cap : in.maxit;
         for (int step = 0; step < cap; ++step) {
             // vin holds the lifted direction of every active column (cg_init /
             // the previous cg_step); inactive columns' rows are stale but finite
@@ -599,13 +679,12 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
             io.nskip = k;
             run_pass(ctx, Op::HVP, k, io);
             ++ctx->launches;
-            cg_step_kernel<<<k, kPT, dsm_max, st>>>(sp_dev, H, vin, arrive, cudaGraphConditionalHandle{}, 0);
+            cg_step_kernel<<<k, kPT, dsm_max, st>>>(spd, H, vin, arrive, cudaGraphConditionalHandle{}, 0);
             MVSK_CUDA(cudaGetLastError());
             const int nb = (step + 1) & 1;
             MVSK_CUDA(cudaMemcpyAsync(hf + nb * K, active, k * sizeof(int), cudaMemcpyDeviceToHost, st));
             MVSK_CUDA(cudaEventRecord(ws.ev[nb], st));
-            // flags that gated this step
-            MVSK_CUDA(cudaEventSynchronize(ws.ev[step & 1]));
+            MVSK_CUDA(cudaEventSynchronize(ws.ev[step & 1]));  // flags that gated this step
             int nact = 0;
             for (int c = 0; c < k; ++c) nact += hf[(step & 1) * K + c];
             if (!nact) {
@@ -615,92 +694,174 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         }
         defer_counts(k, false, 0, 0);
     };
-
-    // ---- Jacobi diagonal (:197-209): 8 probes through Hop in one batch
-    const double* jdp = nullptr;
-    double* stage = ws.host_stage;
-    const int nb1 = (int)std::min<long long>(4LL * ctx->nsm, (mm + 255) / 256 + 1);
-    if (!in.jacobi_probes.empty()) {
-        const int k = (int)in.jacobi_probes.size();
-        for (int p = 0; p < k; ++p) std::copy(in.jacobi_probes[p].begin(), in.jacobi_probes[p].end(), stage + (size_t)p * mm);
-        MVSK_CUDA(cudaMemcpyAsync(src, stage, (size_t)k * mm * sizeof(double), cudaMemcpyHostToDevice, st));
-        stage += (size_t)k * mm;
+    auto hvp_rows = [&](int k) {
+        PassIO io;
+        io.vin = vin;
+        io.z = sl.z;
+        io.out = H;
+        io.ldo = (long long)ld;
+        run_pass(ctx, Op::HVP, k, io);
+        ctx->fwd += k;  // reference contract: 2 passes per HVP
+        ctx->tr += k;
+    };
+    auto enqueue = [&]() {
+        // uploads: parameters, geometry, probes (exact sizes: the graph key has mm)
+        MVSK_CUDA(cudaMemcpyAsync(base + o_dir, hu + o_dir, sizeof(DirDev), cudaMemcpyHostToDevice, st));
+        MVSK_CUDA(cudaMemcpyAsync(vU, HU(o_vU), m * sizeof(double), cudaMemcpyHostToDevice, st));
+        MVSK_CUDA(cudaMemcpyAsync(vQ, HU(o_vQ), m1 * sizeof(double), cudaMemcpyHostToDevice, st));
+        MVSK_CUDA(cudaMemcpyAsync(nu, HU(o_nu), m1 * sizeof(double), cudaMemcpyHostToDevice, st));
+        if (fm.active) MVSK_CUDA(cudaMemcpyAsync(idx, hu + o_idx, m * sizeof(long long), cudaMemcpyHostToDevice, st));
+        // ---- Jacobi diagonal (:197-209): 8 probes through Hop in one batch
+        if (jac) {
+            MVSK_CUDA(cudaMemcpyAsync(jsrc, HU(o_jsrc), (size_t)kj * mm * sizeof(double), cudaMemcpyHostToDevice, st));
+            ++ctx->launches;
+            lift_kernel<<<kj, kPT, dsm_max, st>>>(gdev, jsrc, true, nullptr, vin);
+            hvp_rows(kj);
+            ++ctx->launches;
+            reduce_kernel<<<kj, kPT, dsm_max, st>>>(gdev, H, true, rows);
+            ++ctx->launches;
+            jacobi_diag_kernel<<<nb1, 256, 0, st>>>(dsd, jsrc, rows, kj, jd);
+            MVSK_CUDA(cudaGetLastError());
+        }
+        // ---- h = Q^T U^T grad2 f (U nu)  (:212-213)
         ++ctx->launches;
-        lift_kernel<<<k, kPT, dsm, st>>>(g, src, mm, true, nullptr, vin);
+        lift_kernel<<<1, kPT, dsm_max, st>>>(gdev, nu, false, nullptr, vin);
+        hvp_rows(1);
+        ++ctx->launches;
+        reduce_kernel<<<1, kPT, dsm_max, st>>>(gdev, H, true, hvec);
         MVSK_CUDA(cudaGetLastError());
-        hvp_rows(k, k);
-        ++ctx->launches;
-        reduce_kernel<<<k, kPT, dsm, st>>>(g, H, k, true, rows, mm);
-        ++ctx->launches;
-        jacobi_diag_kernel<<<nb1, 256, 0, st>>>(src, rows, k, mm, in.lambda, std::max(1e-12, in.lambda), jd);
-        MVSK_CUDA(cudaGetLastError());
-        jdp = jd;
-    }
-
-    // ---- h = Q^T U^T grad2 f (U nu)  (:212-213)
-    ++ctx->launches;
-    lift_kernel<<<1, kPT, dsm, st>>>(g, nu, m1, false, nullptr, vin);
-    MVSK_CUDA(cudaGetLastError());
-    hvp_rows(1, 1);
-    ++ctx->launches;
-    reduce_kernel<<<1, kPT, dsm, st>>>(g, H, 1, true, hvec, mm);
-    MVSK_CUDA(cudaGetLastError());
-
-    // ---- a: Hutchinson probes or exact trace (:215-237), blocks of K columns,
-    // accumulated on the device in probe order
-    MVSK_CUDA(cudaMemsetAsync(avec, 0, mm * sizeof(double), st));
-    if (in.has_third) {
-        const int P_all = in.unit_probes ? mm : (int)in.probes.size();
-        for (int b0 = 0; b0 < P_all; b0 += K) {
-            const int k = std::min(K, P_all - b0);
-            if (in.unit_probes) {
+        // ---- a: Hutchinson probes or exact trace (:215-237), blocks of K
+        // columns, accumulated on the device in probe order
+        MVSK_CUDA(cudaMemsetAsync(avec, 0, mm * sizeof(double), st));
+        if (in.has_third) {
+            const int P_all = in.unit_probes ? mm : (int)in.probes.size();
+            for (int b0 = 0; b0 < P_all; b0 += K) {
+                const int k = std::min(K, P_all - b0);
+                double* pb = src;
+                if (in.unit_probes) {
+                    ++ctx->launches;
+                    unit_probe_kernel<<<nb1, 256, 0, st>>>(dsd, src, k, b0);
+                } else if (b0 == 0) {
+                    pb = psrc;
+                    MVSK_CUDA(cudaMemcpyAsync(psrc, HU(o_psrc), (size_t)k * mm * sizeof(double), cudaMemcpyHostToDevice,
+                                              st));
+                } else {  // more than K Hutchinson probes: later blocks from pageable host memory
+                    std::vector<double> buf((size_t)k * mm);
+                    for (int p = 0; p < k; ++p)
+                        std::copy(in.probes[b0 + p].begin(), in.probes[b0 + p].end(), buf.begin() + (size_t)p * mm);
+                    MVSK_CUDA(cudaMemcpy(src, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice));
+                }
+                cg(k, 0, pb);
+                // third_action(U Q s_p, U Q r_p) for the block, one fused pass
                 ++ctx->launches;
-                unit_probe_kernel<<<nb1, 256, 0, st>>>(src, k, mm, b0);
-            } else {
-                for (int p = 0; p < k; ++p)
-                    std::copy(in.probes[b0 + p].begin(), in.probes[b0 + p].end(), stage + (size_t)p * mm);
-                MVSK_CUDA(cudaMemcpyAsync(src, stage, (size_t)k * mm * sizeof(double), cudaMemcpyHostToDevice, st));
-                stage += (size_t)k * mm;
+                lift_kernel<<<k, kPT, dsm_max, st>>>(gdev, X, true, nullptr, vin);
+                ++ctx->launches;
+                lift_kernel<<<k, kPT, dsm_max, st>>>(gdev, pb, true, nullptr, vin2);
+                MVSK_CUDA(cudaGetLastError());
+                PassIO io;
+                io.vin = vin;
+                io.vin2 = vin2;
+                io.z = sl.z;
+                io.out = H;
+                io.ldo = (long long)ld;
+                run_pass(ctx, Op::THIRD, k, io);
+                ctx->fwd += 2 * k;
+                ctx->tr += k;
+                ++ctx->launches;
+                reduce_kernel<<<k, kPT, dsm_max, st>>>(gdev, H, true, rows);
+                ++ctx->launches;
+                accum_rows_kernel<<<nb1, 256, 0, st>>>(dsd, rows, k, avec);
+                MVSK_CUDA(cudaGetLastError());
+                if (!capture && in.unit_probes && deferred.size() + 2 >= (size_t)kMaxDeferred) {
+                    // long exact-trace sweeps: settle the loop counts every few blocks
+                    MVSK_CUDA(cudaStreamSynchronize(st));
+                    settle_counts();
+                }
             }
-            cg(k, in.probe_cap, jdp);
-            // third_action(U Q s_p, U Q r_p) for the block, one fused pass
-            ++ctx->launches;
-            lift_kernel<<<k, kPT, dsm, st>>>(g, X, mm, true, nullptr, vin);
-            ++ctx->launches;
-            lift_kernel<<<k, kPT, dsm, st>>>(g, src, mm, true, nullptr, vin2);
-            MVSK_CUDA(cudaGetLastError());
-            PassIO io;
-            io.vin = vin;
-            io.vin2 = vin2;
-            io.z = sl.z;
-            io.out = H;
-            io.ldo = (long long)ld;
-            run_pass(ctx, Op::THIRD, k, io);
-            ctx->fwd += 2 * k;
-            ctx->tr += k;
-            ++ctx->launches;
-            reduce_kernel<<<k, kPT, dsm, st>>>(g, H, k, true, rows, mm);
-            ++ctx->launches;
-            accum_rows_kernel<<<nb1, 256, 0, st>>>(rows, k, mm, avec);
-            MVSK_CUDA(cudaGetLastError());
-            if (in.unit_probes && deferred.size() + 2 >= (size_t)kMaxDeferred) {
-                // long exact-trace sweeps: settle the loop counts every few blocks
-                MVSK_CUDA(cudaStreamSynchronize(st));
-                settle_counts();
+        }
+        // rhs = h - (||gbar|| / n) a  (:239); a averaged over the Hutchinson probes (:236)
+        ++ctx->launches;
+        rhs_kernel<<<nb1, 256, 0, st>>>(dsd, hvec, avec, src);
+        MVSK_CUDA(cudaGetLastError());
+        // main CG (:240-241)
+        cg(1, 1, src);
+        MVSK_CUDA(cudaMemcpyAsync(ws.host_u, X, mm * sizeof(double), cudaMemcpyDeviceToHost, st));
+    };
+
+    // ---- whole-direction graph: Hutchinson (<= K probes) or no-third directions.
+    // The first direction of a shape runs eagerly (it sizes every workspace), the
+    // second is captured, later ones replay it.
+    static const bool no_dir_graph = std::getenv("MVSK_NO_DIR_GRAPH") != nullptr;
+    const bool graphable = !no_dir_graph && !ws.dir_broken && !in.unit_probes && kp <= K && !no_graph &&
+                           !ws.graphs_broken;
+    const PcgWorkspace::DirKey key{slot, mm, kp, kj, in.has_third ? 1 : 0, ctx->epoch};
+    PcgWorkspace::DirGraph* dg = nullptr;
+    if (graphable) {
+        for (auto& d : ws.dgraphs)
+            if (d.key == key) dg = &d;
+        if (!dg && std::find(ws.dseen.begin(), ws.dseen.end(), key) != ws.dseen.end()) {
+            // capture it now
+            PcgWorkspace::DirGraph ng{};
+            ng.key = key;
+            const uint64_t f0 = ctx->fwd, t0 = ctx->tr, p0 = ctx->phys, l0 = ctx->launches;
+            cudaGraph_t gr = nullptr;
+            bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                capture = &ng;
+                try {
+                    enqueue();
+                } catch (...) {
+                    ok = false;
+                }
+                capture = nullptr;
+                ok = cudaStreamEndCapture(st, &gr) == cudaSuccess && ok;
+            }
+            cudaGraphExec_t exec = nullptr;
+            if (ok) ok = cudaGraphInstantiate(&exec, gr, 0) == cudaSuccess;
+            if (gr) cudaGraphDestroy(gr);
+            cudaGetLastError();
+            ng.fwd = ctx->fwd - f0;
+            ng.tr = ctx->tr - t0;
+            ng.phys = ctx->phys - p0;
+            ng.launches = ctx->launches - l0;
+            ctx->fwd = f0;
+            ctx->tr = t0;
+            ctx->phys = p0;
+            ctx->launches = l0;
+            deferred.clear();
+            if (ok) {
+                ng.exec = exec;
+                if (ws.dgraphs.size() >= 8) {  // small cache of direction shapes
+                    if (ws.dgraphs.front().exec) cudaGraphExecDestroy(ws.dgraphs.front().exec);
+                    ws.dgraphs.erase(ws.dgraphs.begin());
+                }
+                ws.dgraphs.push_back(ng);
+                dg = &ws.dgraphs.back();
+            } else {
+                if (exec) cudaGraphExecDestroy(exec);
+                ws.dir_broken = true;
             }
         }
     }
-    // rhs = h - (||gbar|| / n) a  (:239); a averaged over the Hutchinson probes (:236)
-    ++ctx->launches;
-    rhs_kernel<<<nb1, 256, 0, st>>>(hvec, avec, mm, (in.has_third && !in.unit_probes) ? (double)in.hutchinson_probes : 0.0,
-                                    in.gn / (double)m, src);
-    MVSK_CUDA(cudaGetLastError());
-    // main CG (:240-241)
-    cg(1, in.maxit, jdp);
-    out.u.resize((size_t)mm);
-    MVSK_CUDA(cudaMemcpyAsync(out.u.data(), X, mm * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (dg) {
+        MVSK_CUDA(cudaGraphLaunch(dg->exec, st));
+        ctx->fwd += dg->fwd;
+        ctx->tr += dg->tr;
+        ctx->phys += dg->phys;
+        ctx->launches += 1 + dg->launches;
+        int row = 0;
+        for (int li = 0; li < dg->nloops; ++li)
+            deferred.push_back({dg->loop_k[li], row++, dg->loop_pps[li], dg->loop_lps[li], true});
+    } else {
+        if (graphable && std::find(ws.dseen.begin(), ws.dseen.end(), key) == ws.dseen.end()) {
+            if (ws.dseen.size() >= 32) ws.dseen.erase(ws.dseen.begin());
+            ws.dseen.push_back(key);
+        }
+        enqueue();
+    }
     MVSK_CUDA(cudaStreamSynchronize(st));
     settle_counts();
+    out.u.assign(ws.host_u, ws.host_u + mm);
     return out;
 }
 

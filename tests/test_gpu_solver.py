@@ -184,8 +184,24 @@ def test_config_solve_parity(name, kappa, mode):
         cfg.has_max_elapsed = 0
         cfg.epsilon = 1e-10
     xc, rc, env, _ = _cpu_envelope(A, mu, c, cfg_c)
-    xg, rg = _gpu(A, mu, c).solve(cfg_g)
-    _same_solution(xg, rg, xc, rc, cfg_g.tau, envelope=env)
+    g = _gpu(A, mu, c)
+    xg, rg = g.solve(cfg_g)
+    assert rg.status == rc.status, (rg.status, rc.status)
+    assert _active(xg, cfg_g.tau) == _active(xc, cfg_g.tau)
+    assert abs(rg.f_star - rc.f_star) <= 1e-12 * (1 + abs(rc.f_star))
+    dx = float(np.max(np.abs(xg - xc)))
+    if dx > max(1e-8, 10.0 * env):
+        # an epsilon-solution is only determined to ~ residual / curvature: a run
+        # that stops with its residual just under 1e-10 can sit ~5e-8 from one
+        # that overshot to 1e-14 (C2 kappa=1 small). Drive both to 1e-12, where
+        # the weights are determined, and require 1e-8 there.
+        for cfg in (cfg_c, cfg_g):
+            cfg.epsilon = 1e-12
+        xc2, rc2, env2, _ = _cpu_envelope(A, mu, c, cfg_c)
+        xg2, rg2 = g.solve(cfg_g)
+        assert _active(xg2, cfg_g.tau) == _active(xc2, cfg_g.tau)
+        dx2 = float(np.max(np.abs(xg2 - xc2)))
+        assert dx2 <= max(1e-8, 10.0 * env2), (dx, dx2, env2, rg.kkt_residual, rc.kkt_residual)
 
 
 def test_device_pcg_matches_host_pcg(monkeypatch):
@@ -290,12 +306,14 @@ def test_floor_sweep_matches_cpu_mirror(name, mode, nfloors):
     out = g.floor_sweep(cfg_g, nfloors=nfloors)
     assert out.total_solves == ref["total"]
     assert out.m_max == ref["m_max"]
-    assert abs(out.m_mv - ref["m_mv"]) <= 1e-9 * abs(ref["m_max"] - ref["m_mv"])
+    # each mean comes from an epsilon-solution (epsilon = 1e-10): agreement to
+    # ~1e-8 of the span, and identical bracketing decisions
+    assert abs(out.m_mv - ref["m_mv"]) <= 1e-8 * abs(ref["m_max"] - ref["m_mv"])
     span = ref["m_max"] - ref["m_mv"]
     for k, p in enumerate(out.points):
         b = ref["best"][k]
         assert p["c1"] == b["c1"], (k, p["c1"], b["c1"])
-        assert abs(p["mean"] - b["mean"]) <= 1e-8 * span
+        assert abs(p["mean"] - b["mean"]) <= 1e-7 * span
         assert abs(p["mean"] - p["floor"]) <= 1e-3 * span or p["solves"] >= 16
         assert float(np.max(np.abs(out.X[k] - b["x"]))) <= 1e-6
     # coefficients restored
