@@ -491,6 +491,10 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         for (int p = 0; p < kp && p < K; ++p) std::copy(in.probes[p].begin(), in.probes[p].end(), HU(o_psrc) + (size_t)p * mm);
     }
     const size_t dsm_max = (size_t)2 * std::max<long long>(N, 1) * sizeof(double);
+    // threads per column CTA from the context width (stable per context, so the
+    // captured graphs stay valid): narrow faces run their block reductions on
+    // two warps instead of sixteen
+    const int pt = N <= 128 ? 64 : N <= 512 ? 128 : N <= 2048 ? 256 : kPT;
     for (const void* fn : {(const void*)lift_kernel, (const void*)cg_step_kernel, (const void*)reduce_kernel,
                            (const void*)cg_init_kernel})
         set_smem_attr(fn, dsm_max);
@@ -556,7 +560,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
             io.ldo = (long long)ld;
             run_pass(ctx, Op::HVP, k, io);
             ++ctx->launches;
-            cg_step_kernel<<<k, kPT, dsm_max, ws.aux>>>(spd, H, vin, arrive, h, 1);
+            cg_step_kernel<<<k, pt, dsm_max, ws.aux>>>(spd, H, vin, arrive, h, 1);
         } catch (...) {
             threw = true;
         }
@@ -634,7 +638,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         const StepParams* spd = &dir->sp[role];
         MVSK_CUDA(cudaMemsetAsync(arrive, 0, sizeof(unsigned), st));
         ++ctx->launches;
-        cg_init_kernel<<<k, kPT, dsm_max, st>>>(spd, rhs, vin);
+        cg_init_kernel<<<k, pt, dsm_max, st>>>(spd, rhs, vin);
         MVSK_CUDA(cudaGetLastError());
         if (capture) {
             cudaStreamCaptureStatus cs;
@@ -679,7 +683,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
             io.nskip = k;
             run_pass(ctx, Op::HVP, k, io);
             ++ctx->launches;
-            cg_step_kernel<<<k, kPT, dsm_max, st>>>(spd, H, vin, arrive, cudaGraphConditionalHandle{}, 0);
+            cg_step_kernel<<<k, pt, dsm_max, st>>>(spd, H, vin, arrive, cudaGraphConditionalHandle{}, 0);
             MVSK_CUDA(cudaGetLastError());
             const int nb = (step + 1) & 1;
             MVSK_CUDA(cudaMemcpyAsync(hf + nb * K, active, k * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -715,20 +719,20 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         if (jac) {
             MVSK_CUDA(cudaMemcpyAsync(jsrc, HU(o_jsrc), (size_t)kj * mm * sizeof(double), cudaMemcpyHostToDevice, st));
             ++ctx->launches;
-            lift_kernel<<<kj, kPT, dsm_max, st>>>(gdev, jsrc, true, nullptr, vin);
+            lift_kernel<<<kj, pt, dsm_max, st>>>(gdev, jsrc, true, nullptr, vin);
             hvp_rows(kj);
             ++ctx->launches;
-            reduce_kernel<<<kj, kPT, dsm_max, st>>>(gdev, H, true, rows);
+            reduce_kernel<<<kj, pt, dsm_max, st>>>(gdev, H, true, rows);
             ++ctx->launches;
             jacobi_diag_kernel<<<nb1, 256, 0, st>>>(dsd, jsrc, rows, kj, jd);
             MVSK_CUDA(cudaGetLastError());
         }
         // ---- h = Q^T U^T grad2 f (U nu)  (:212-213)
         ++ctx->launches;
-        lift_kernel<<<1, kPT, dsm_max, st>>>(gdev, nu, false, nullptr, vin);
+        lift_kernel<<<1, pt, dsm_max, st>>>(gdev, nu, false, nullptr, vin);
         hvp_rows(1);
         ++ctx->launches;
-        reduce_kernel<<<1, kPT, dsm_max, st>>>(gdev, H, true, hvec);
+        reduce_kernel<<<1, pt, dsm_max, st>>>(gdev, H, true, hvec);
         MVSK_CUDA(cudaGetLastError());
         // ---- a: Hutchinson probes or exact trace (:215-237), blocks of K
         // columns, accumulated on the device in probe order
@@ -754,9 +758,9 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
                 cg(k, 0, pb);
                 // third_action(U Q s_p, U Q r_p) for the block, one fused pass
                 ++ctx->launches;
-                lift_kernel<<<k, kPT, dsm_max, st>>>(gdev, X, true, nullptr, vin);
+                lift_kernel<<<k, pt, dsm_max, st>>>(gdev, X, true, nullptr, vin);
                 ++ctx->launches;
-                lift_kernel<<<k, kPT, dsm_max, st>>>(gdev, pb, true, nullptr, vin2);
+                lift_kernel<<<k, pt, dsm_max, st>>>(gdev, pb, true, nullptr, vin2);
                 MVSK_CUDA(cudaGetLastError());
                 PassIO io;
                 io.vin = vin;
@@ -768,7 +772,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
                 ctx->fwd += 2 * k;
                 ctx->tr += k;
                 ++ctx->launches;
-                reduce_kernel<<<k, kPT, dsm_max, st>>>(gdev, H, true, rows);
+                reduce_kernel<<<k, pt, dsm_max, st>>>(gdev, H, true, rows);
                 ++ctx->launches;
                 accum_rows_kernel<<<nb1, 256, 0, st>>>(dsd, rows, k, avec);
                 MVSK_CUDA(cudaGetLastError());
