@@ -1,16 +1,23 @@
 // Device-resident PCG for the YAND direction (affine_normal.hpp:189-242).
 //
 // The reduced tangent operator H e = Q^T U^T grad2 f (U Q e) + lambda e is
-// applied without leaving the device: a "lift" kernel applies the two
-// Householder reflectors (U: simplex.hpp:63-70, Q: affine_normal.hpp:28-33) to
-// every CG column and scatters it into the HVP input rows (face -> full
-// coordinates), one fused k-RHS HVP pass runs, and an "update" kernel gathers,
-// applies Q^T U^T (:36-39, simplex.hpp:73-78) and performs the capped-CG step
-// of every column (cg_capped, affine_normal.hpp:85-113: per-column alpha/beta,
-// nonpositive curvature -> breakdown, ||r|| <= tol ||rhs|| or the cap -> stop).
-// The host only reads back a k-int activity mask per CG step (and the
-// solution at the end); no n-vector crosses PCIe inside the Krylov loops.
-// One CTA owns one CG column; every reduction has a fixed order.
+// applied without leaving the device: the Householder reflectors (U:
+// simplex.hpp:63-70, Q: affine_normal.hpp:28-33) lift every CG column into the
+// HVP input rows (face -> full coordinates), one fused k-RHS HVP pass runs, and
+// the step kernel gathers, applies Q^T U^T (:36-39, simplex.hpp:73-78),
+// performs the capped-CG step of every column (cg_capped, :85-113: per-column
+// alpha/beta, nonpositive curvature -> breakdown, ||r|| <= tol ||rhs|| or the
+// cap -> stop) and lifts the next search direction. One CTA owns one column;
+// every reduction has a fixed order.
+//
+// Scheduling: each Krylov loop is a conditional-while CUDA graph (the last
+// column CTA sets the loop condition), and a whole Hutchinson / no-third
+// direction - uploads, Jacobi diagonal, h, the probe block, the third-action
+// pass, the rhs, the main CG and the readbacks - is captured once per shape
+// (the loops spliced in as conditional nodes) and replayed with its
+// parameters in device memory: one graph launch and one synchronisation per
+// direction. The first direction of a shape runs eagerly (it sizes every
+// workspace); exact-trace sweeps and > 16 probes stay eager.
 #include <algorithm>
 #include <cmath>
 #include <vector>
