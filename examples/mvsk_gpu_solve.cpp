@@ -5,7 +5,10 @@
 // prints the SolveReport keys of report_json.hpp:12-28.
 //
 //   mvsk_gpu_solve <panel.bin> [--gamma G | --coeffs c1,c2,c3,c4] [--preset small|large]
-//                  [--epsilon E] [--tau T] [--max-iter N] [--no-max-elapsed]
+//                  [--epsilon E] [--tau T] [--max-iter N] [--no-max-elapsed] [--floor-sweep K]
+// --floor-sweep K: BASELINE config 4's return-floor sweep instead of one solve
+// (K floors between the min-variance and max-mean means, c1 calibrated per
+// floor; mvsk_gpu_floor_sweep), printed as one JSON object.
 // exit codes as the reference CLI (mvsk_main.cpp:213-219): 0 converged,
 // 3 budget/stall, 2 bad arguments / domain errors, 1 data or device errors.
 #include <cstdio>
@@ -35,6 +38,7 @@ int main(int argc, char** argv) {
     double eps = -1, tau = -1;
     int max_iter = -1;
     bool no_elapsed = false;
+    int sweep = 0;
     for (int i = 2; i < argc; ++i) {
         const std::string a = argv[i];
         auto next = [&]() -> const char* {
@@ -53,6 +57,7 @@ int main(int argc, char** argv) {
         else if (a == "--tau") tau = std::atof(next());
         else if (a == "--max-iter") max_iter = std::atoi(next());
         else if (a == "--no-max-elapsed") no_elapsed = true;
+        else if (a == "--floor-sweep") sweep = std::atoi(next());
         else {
             std::fprintf(stderr, "unknown option %s\n", a.c_str());
             return 2;
@@ -75,6 +80,25 @@ int main(int argc, char** argv) {
     if (st) return fail(st, mvsk_gpu_last_error(nullptr));
     int64_t T = 0, Tl = 0, n = 0;
     mvsk_gpu_dims(ctx, &T, &Tl, &n);
+    if (sweep > 0) {
+        std::vector<mvsk_floor_point> pts((size_t)sweep);
+        double m_mv = 0, m_max = 0;
+        int32_t solves = 0;
+        st = mvsk_gpu_floor_sweep(ctx, &cfg, nullptr, sweep, nullptr, nullptr, pts.data(), &m_mv, &m_max, &solves);
+        if (st) {
+            const int rc = fail(st, mvsk_gpu_last_error(ctx));
+            mvsk_gpu_destroy(ctx);
+            return rc;
+        }
+        std::printf("{\"m_mv\": %.17g, \"m_max\": %.17g, \"solves\": %d, \"points\": [", m_mv, m_max, solves);
+        for (int k = 0; k < sweep; ++k)
+            std::printf("%s{\"floor\": %.17g, \"c1\": %.17g, \"mean\": %.17g, \"f_star\": %.17g, \"status\": %d}",
+                        k ? ", " : "", pts[(size_t)k].floor, pts[(size_t)k].c1, pts[(size_t)k].mean,
+                        pts[(size_t)k].f_star, pts[(size_t)k].status);
+        std::printf("]}\n");
+        mvsk_gpu_destroy(ctx);
+        return 0;
+    }
     std::vector<double> x((size_t)n);
     mvsk_solve_report rep;
     st = mvsk_gpu_solve(ctx, &cfg, nullptr, x.data(), &rep, nullptr, nullptr);

@@ -391,3 +391,35 @@ def test_graph_replay_tracks_inputs_and_offsets():
         _close(gpu.hvp(gc, v), off.hvp(cc, v))
     assert gpu.passes()[2] > 0
     gpu.close()
+
+
+def test_set_coeffs_and_sweep_contract():
+    """set_coeffs replaces c on a live context (cached slots invalidated, f and
+    g follow the new coefficients); the floor sweep rejects bad arguments and
+    restores the context's coefficients."""
+    from paper_2604_25378_b200.gpu_oracle import DomainError, preset
+    A, mu = rh.lcg_panel(7, 60, 12)
+    c1, c2 = rh.crra(4.0), rh.crra(9.0)
+    g = _gpu(A, mu, c1)
+    x = rh.simplex_point(7, 2)
+    cache = g.make_cache(x)
+    g.set_coeffs(c2)
+    with pytest.raises(DomainError):
+        g.gradient(cache)  # invalidated
+    cpu = po.CpuOracle(A, mu, c2)
+    cc = cpu.make_cache(x)
+    gc = g.make_cache(x)
+    assert abs(g.value(gc) - cpu.value(cc)) <= 1e-12 * (1 + abs(cpu.value(cc)))
+    _close(g.gradient(gc), cpu.gradient(cc))
+    with pytest.raises(DomainError):
+        g.set_coeffs([np.nan, 1.0, 1.0, 1.0])
+    cfg = preset("small")
+    cfg.has_max_elapsed = 0
+    with pytest.raises(DomainError):
+        g.floor_sweep(cfg, floors=[0.1, np.inf])
+    with pytest.raises(DomainError):
+        g.floor_sweep(cfg, nfloors=0)
+    out = g.floor_sweep(cfg, floors=[float(mu.mean())], max_solves=6)
+    assert len(out.points) == 1 and out.total_solves >= 2
+    gc2 = g.make_cache(x)  # coefficients restored to c2
+    assert abs(g.value(gc2) - cpu.value(cc)) <= 1e-12 * (1 + abs(cpu.value(cc)))

@@ -284,6 +284,14 @@ def test_cpp_host_solves_a_binary_panel(tmp_path):
     assert abs(rep["f_star"] - rc.f_star) <= 1e-12 * (1 + abs(rc.f_star))
     assert _active(xg, 1e-8) == _active(xc, 1e-8)
     assert np.max(np.abs(xg - xc)) <= 1e-7
+    # the return-floor sweep through the same C++ host
+    r = subprocess.run([str(exe), str(path), "--gamma", "10", "--preset", "large", "--floor-sweep", "3",
+                        "--no-max-elapsed"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    sw = json.loads(r.stdout)
+    assert len(sw["points"]) == 3 and sw["m_mv"] < sw["m_max"]
+    floors = [p["floor"] for p in sw["points"]]
+    assert all(np.diff(floors) > 0) and all(p["status"] == 0 for p in sw["points"])
 
 
 @pytest.mark.parametrize("name,mode,nfloors", [("C1", "small", 3), ("C2", "large", 3), ("C3", "large", 2)])
