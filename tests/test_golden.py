@@ -1,0 +1,96 @@
+"""Golden fixtures (tests/golden/*.npz, made by tests/golden/make_golden.py from
+the pinned CPU restatement): the restatement must keep reproducing them (CPU),
+and the CUDA path must match them at the north_star bars (GPU): oracle values
+to 1e-11 relative, directions to 1e-9, solved weights to 1e-8 with the same
+active set."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+CASES = sorted(p.stem for p in GOLDEN.glob("*.npz"))
+TAU = 0.0
+
+
+def _load(name):
+    return dict(np.load(GOLDEN / f"{name}.npz"))
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(np.asarray(a) - np.asarray(b)))) / max(float(np.max(np.abs(b))), 1e-300)
+
+
+def _active(x):
+    return tuple(np.nonzero(x <= TAU + 1e-12)[0])
+
+
+def test_fixtures_present():
+    assert set(CASES) >= {"c1_small", "c2_slice_k100"}
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_restatement_reproduces_golden(name):
+    g = _load(name)
+    o = po.CpuOracle(g["A"], g["mu"], g["c"])
+    cc = o.make_cache(g["x"])
+    assert abs(o.value(cc) - g["f"][0]) <= 1e-14 * abs(g["f"][0])
+    assert _rel(o.moments(cc), g["moments"]) <= 1e-14
+    assert _rel(o.gradient(cc), g["g"]) <= 1e-14
+    for i in range(4):
+        assert _rel(o.hvp(cc, g["V"][i]), g["H"][i]) <= 1e-14
+        assert _rel(o.third_action(cc, g["U"][i], g["V"][i]), g["T3"][i]) <= 1e-14
+    assert _rel(o.hessian_diag_weights(cc), g["psi2"]) <= 1e-14
+    assert _rel(o.sample_direction(g["V"][0]), g["Ad"]) <= 1e-14
+    assert _rel(o.line_model(cc, g["V"][0], 0.05), g["line_model"]) <= 1e-13
+    d, _ = o.yand_direction(cc, po.tangent_config("direct", lam=1e-6), 3)
+    assert _rel(d, g["d_direct"]) <= 1e-12
+    for p in ("small", "large"):
+        if f"x_{p}" not in g:
+            continue
+        cfg = po.preset(p)
+        cfg.has_max_elapsed = 0
+        cfg.epsilon = 1e-10
+        xs, rep = po.solve(g["A"], g["mu"], g["c"], cfg)
+        assert rep.status == g[f"status_{p}"][0]
+        assert float(np.max(np.abs(xs - g[f"x_{p}"]))) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_gpu_matches_golden(name):
+    from paper_2604_25378_b200.gpu_oracle import GpuOracle, preset, tangent_config
+    g = _load(name)
+    gpu = GpuOracle(g["A"], g["mu"], g["c"])
+    gc = gpu.make_cache(g["x"])
+    assert abs(gpu.value(gc) - g["f"][0]) <= 1e-11 * abs(g["f"][0])
+    assert _rel(gpu.moments(gc), g["moments"]) <= 1e-11
+    assert _rel(gpu.gradient(gc), g["g"]) <= 1e-11
+    H = gpu.hvp(gc, g["V"])
+    T3 = gpu.third_action(gc, g["U"], g["V"])
+    for i in range(4):
+        assert _rel(H[i], g["H"][i]) <= 1e-11
+        assert _rel(T3[i], g["T3"][i]) <= 1e-11
+    assert _rel(gpu.hessian_diag_weights(gc), g["psi2"]) <= 1e-13
+    assert _rel(gpu.sample_direction(g["V"][0]), g["Ad"]) <= 1e-11
+    lm = gpu.line_model(gc, g["V"][0], 0.05)
+    assert _rel([lm.a0, lm.a1, lm.a2, lm.a3, lm.a4], g["line_model"][:5]) <= 1e-11
+    d, _ = gpu.yand_direction(gc, tangent_config("direct", lam=1e-6), 3)
+    assert _rel(d, g["d_direct"]) <= 1e-9
+    d, _ = gpu.yand_direction(gc, tangent_config("pcg", lam=1e-4, krylov_tol=1e-12, krylov_maxit=200,
+                                                 exact_trace=True), 3)
+    assert _rel(d, g["d_exact"]) <= 1e-8
+    for p in ("small", "large"):
+        if f"x_{p}" not in g:
+            continue
+        cfg = preset(p)
+        cfg.has_max_elapsed = 0
+        cfg.epsilon = 1e-10
+        xs, rep = gpu.solve(cfg)
+        assert rep.status == g[f"status_{p}"][0]
+        assert _active(xs) == _active(g[f"x_{p}"])
+        assert abs(rep.f_star - g[f"f_{p}"][0]) <= 1e-12 * (1 + abs(g[f"f_{p}"][0]))
+        assert float(np.max(np.abs(xs - g[f"x_{p}"]))) <= 1e-8
+    gpu.close()
