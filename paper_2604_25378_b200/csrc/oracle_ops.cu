@@ -319,7 +319,7 @@ bool make_cluster_plan(const mvsk_gpu_ctx* ctx, Op op, int K, CPlan& pl) {
 
 // ---- DMMA cluster plans (multi-RHS HVP / THIRD on the fp64 tensor cores) -------
 struct DPlan {
-    int C = 4, WC = 128, S = 3;
+    int C = 4, WC = 128, S = 3, threads = 256;
     size_t smem = 0;
     int ncl = 1;
     const void* fn = nullptr;
@@ -415,10 +415,65 @@ bool make_dmma_pipe_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
     return true;
 }
 
+template <Op OP, int K, int WC>
+const void* wfn() {
+    return reinterpret_cast<const void*>(&stream_dmma_ws_kernel<OP, K, WC, 4>);
+}
+
+// warp-specialised variant (stream_dmma_ws_kernel): 8 math warps + a helper
+// warpgroup, 4-CTA clusters
+const void* select_dmma_ws(Op op, int K, int WC) {
+    if (op == Op::HVP && K == 8) {
+        if (WC == 64) return wfn<Op::HVP, 8, 64>();
+        if (WC == 128) return wfn<Op::HVP, 8, 128>();
+    }
+    if (op == Op::HVP && K == 4) {
+        if (WC == 64) return wfn<Op::HVP, 4, 64>();
+        if (WC == 128) return wfn<Op::HVP, 4, 128>();
+    }
+    if (op == Op::THIRD && K == 4) {
+        if (WC == 64) return wfn<Op::THIRD, 4, 64>();
+        if (WC == 128) return wfn<Op::THIRD, 4, 128>();
+    }
+    if (op == Op::THIRD && K == 8) {  // 128-column slices spill (twice the V fragments): v1 there
+        if (WC == 64) return wfn<Op::THIRD, 8, 64>();
+    }
+    return nullptr;
+}
+
+bool make_dmma_ws_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
+    const int C = 4;
+    const int ndot = op == Op::THIRD ? 2 * K : K;
+    const int V = 8 * ndot;
+    if (ctx->ld % (2 * C)) return false;
+    const int cw = (int)(ctx->ld / C);
+    int WC = 0;
+    for (int w : {64, 128})
+        if (!WC && 8 * w >= cw && select_dmma_ws(op, K, w)) WC = w;
+    if (!WC) return false;
+    const size_t stage = (size_t)8 * (8 * WC + 4) * sizeof(double);
+    size_t head = 256 + (size_t)(2 * 8 * V + 4 * C * V + 128) * sizeof(double);
+    head = (head + 127) & ~(size_t)127;
+    const int S = (int)std::min<size_t>(8, (ctx->max_smem - head) / stage);
+    if (S < 2) return false;
+    pl.C = C;
+    pl.WC = WC;
+    pl.S = S;
+    pl.threads = 384;
+    pl.smem = head + (size_t)S * stage;
+    pl.fn = select_dmma_ws(op, K, WC);
+    pl.ncl = std::max(1, ctx->nsm / C);
+    return true;
+}
+
 bool make_dmma_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
     if (std::getenv("MVSK_NO_DMMA")) return false;
-    if (!std::getenv("MVSK_DMMA_V1") && !std::getenv("MVSK_TUNE_DMMA") && make_dmma_pipe_plan(ctx, op, K, pl))
-        return true;
+    // warp-specialised kernel first (C5 8-RHS HVP 1.47 ms vs 2.06 pipelined vs
+    // 2.23 v1, profiles/r01_dmma_pipe.txt); MVSK_DMMA_PIPE / MVSK_DMMA_V1 force
+    // the older kernels for A/B runs
+    const bool v1 = std::getenv("MVSK_DMMA_V1") || std::getenv("MVSK_TUNE_DMMA");
+    if (!v1 && !std::getenv("MVSK_DMMA_PIPE") && make_dmma_ws_plan(ctx, op, K, pl)) return true;
+    if (!v1 && make_dmma_pipe_plan(ctx, op, K, pl)) return true;
     int forceC = 0, forceD = 0;
     if (const char* e = std::getenv("MVSK_TUNE_DMMA")) std::sscanf(e, "%d,%d", &forceC, &forceD);
     const int ndot = op == Op::THIRD ? 2 * K : K;
@@ -718,7 +773,7 @@ static bool run_dmma(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     attr[0].val.clusterDim.x = pl.C;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(pl.threads);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = ctx->stream;
     cfg.attrs = attr;

@@ -603,4 +603,312 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_pipe_kernel(const DmmaArgs
     cluster.sync();  // no CTA exits while a peer may still push into it
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised variant: 8 math warps + one helper warpgroup.
+//
+// The pipelined kernel above is bounded by its per-stage skeleton running in
+// lock-step with the DMMA phases in all 8 warps (profiles/r01_dmma_pipe.txt).
+// Here the skeleton moves to a helper warpgroup (registers rebalanced with
+// setmaxnreg: 232 per math thread, 40 per helper thread):
+//   warp 8   TMA producer: refills a ring slot once the 8 math warps released it
+//   warp 9   reducer: sums the 8 warp partials of a stage, pushes the C-CTA
+//            exchange (st.async + tx-count mbarrier on every peer)
+//   warp 10  W builder: waits for the stage's cluster dots, forms
+//            W = psi(z) o Y (rows past the block end -> 0) into a smem buffer
+// and a math warp only runs  phase1(i) -> partial -> [W(i-1) ready] ->
+// phase2(i-1) -> frag(i) -> release.
+// Slot reuse: red[R] and the ring are guarded by empty barriers; the exchange
+// ring E = 4 by the argument: a reducer pushes stage j+4 after its math warps
+// finished phase1(j+4), hence passed W(j+2) ready, hence every CTA pushed j+2,
+// hence every CTA's math warps finished phase1(j+2) and passed W(j) ready, so
+// every W builder consumed stage j. The W buffer (2 deep) is rewritten for
+// stage j+2 only after xfull(j+2), i.e. after this CTA's math warps finished
+// phase1(j+2) and with it phase2(j).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void reg_alloc_232() { asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory"); }
+__device__ __forceinline__ void reg_dealloc_40() { asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory"); }
+
+template <Op OP, int K, int WC, int C>
+__global__ void __launch_bounds__(384, 1) stream_dmma_ws_kernel(const DmmaArgs a) {
+    using Sh = DmmaShape<OP, K>;
+    constexpr int NDOT = Sh::NDOT, NT1 = Sh::NT1, V = Sh::V;
+    constexpr int NW = 8;            // math warps
+    constexpr int E = 4, R = 2;      // exchange / partial ring depths
+    constexpr int KP = WC / 8;
+    constexpr int MP = WC / 16;
+    constexpr int MT = 2 * MP;
+    constexpr int VPL = (V + 31) / 32;  // dots per reducer lane
+    constexpr int RS = 8 * WC + 4;
+    constexpr int NCH = NT1 >= 2 ? MVSK_NCH2 : MVSK_NCH1;
+    static_assert(K <= 8 && WC % 16 == 0 && C % 2 == 0, "shape");
+    if (pass_skipped(a.skip, a.nskip)) return;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int crank = (int)cluster.block_rank();
+    const int ncl = gridDim.x / C;
+    const int ci = blockIdx.x / C;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int cw = a.cw, S = a.S;
+    const long long ld = a.ld;
+    const int col0 = crank * cw;
+
+    // smem: mbarriers [full 8 | empty 8 | xfull 4 | pfull 2 | pempty 2 | wready 2] (256 B)
+    //       [red R x NW x V][xchg E x V x C][wbuf 2 x 64][ring S x 8 x RS]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t* empty = full + 8;
+    uint64_t* xfull = full + 16;
+    uint64_t* pfull = full + 20;
+    uint64_t* pempty = full + 22;
+    uint64_t* wready = full + 24;
+    double* red = reinterpret_cast<double*>(smem_raw + 256);
+    double* xchg = red + R * NW * V;
+    double* wbuf = xchg + E * V * C;
+    size_t off = 256 + (size_t)(R * NW * V + E * V * C + 2 * 64) * sizeof(double);
+    off = (off + 127) & ~(size_t)127;
+    constexpr size_t stage_elems = (size_t)8 * RS;
+    double* ring = reinterpret_cast<double*>(smem_raw + off);
+
+    const long long T = a.T;
+    const long long r0 = T * ci / ncl, r1 = T * (ci + 1) / ncl;
+    const long long nrows = r1 - r0;
+    const int nst = (int)((nrows + 7) / 8);
+    constexpr uint32_t kXBytes = (uint32_t)(C * V * sizeof(double));
+
+    for (size_t i = tid; i < (size_t)S * stage_elems; i += blockDim.x) ring[i] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        for (int e = 0; e < E; ++e) mbar_init(&xfull[e], 1);
+        for (int r = 0; r < R; ++r) {
+            mbar_init(&pfull[r], NW);
+            mbar_init(&pempty[r], 1);
+        }
+        for (int r = 0; r < 2; ++r) mbar_init(&wready[r], 1);
+        for (int e = 0; e < E && e < nst; ++e) mbar_arrive_expect_tx(&xfull[e], kXBytes);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    cluster.sync();  // peers' barriers initialised (and armed) before any push
+
+    if (warp >= NW) {
+        // ======================= helper warpgroup =======================
+        reg_dealloc_40();
+        if (warp == NW) {
+            // ---- TMA producer
+            if (lane == 0) {
+                const uint64_t policy = a.evict_first ? policy_evict_first() : policy_evict_last();
+                int slot = 0;
+                for (int s = 0; s < nst; ++s) {
+                    // the slot's previous stage (s - S) released by all 8 math warps
+                    if (s >= S) mbar_wait(&empty[slot], (uint32_t)(((s / S) - 1) & 1));
+                    const long long rows = (nrows - (long long)s * 8) < 8 ? (nrows - (long long)s * 8) : 8;
+                    mbar_arrive_expect_tx(&full[slot], (uint32_t)(rows * cw * sizeof(double)));
+                    const double* src = a.X + (r0 + (long long)s * 8) * ld + col0;
+                    double* dst = ring + slot * stage_elems;
+                    for (int r = 0; r < rows; ++r)
+                        bulk_g2s(dst + (size_t)r * RS, src + (long long)r * ld, (uint32_t)(cw * sizeof(double)),
+                                 &full[slot], policy);
+                    if (++slot == S) slot = 0;
+                }
+            }
+        } else if (warp == NW + 1) {
+            // ---- reducer
+            const uint32_t xb_self = smem_u32(xchg);
+            for (int j = 0; j < nst; ++j) {
+                const int r = j % R;
+                mbar_wait(&pfull[r], (uint32_t)((j / R) & 1));
+                const double* rb = red + (size_t)r * NW * V;
+                double sum[VPL];
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) {
+                    const int v = lane + 32 * q;
+                    double sacc = 0.0;
+                    if (v < V) {
+#pragma unroll
+                        for (int w = 0; w < NW; ++w) sacc += rb[w * V + v];
+                    }
+                    sum[q] = sacc;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pempty[r]);
+                const int e = j % E;
+                const uint32_t lb = smem_u32(&xfull[e]);
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) {
+                    const int v = lane + 32 * q;
+                    if (v < V) {
+                        const uint32_t la = xb_self + (uint32_t)(((e * V + v) * C + crank) * sizeof(double));
+#pragma unroll
+                        for (int rr = 0; rr < C; ++rr) {
+                            uint32_t ra, rbar;
+                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rr));
+                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(lb), "r"(rr));
+                            st_async_f64(ra, sum[q], rbar);
+                        }
+                    }
+                }
+            }
+        } else if (warp == NW + 2) {
+            // ---- W builder: lane -> (row, g) pairs of the 8 x 8 W tile
+            const double c2 = a.c2, c3 = a.c3, c4 = a.c4;
+            for (int j = 0; j < nst; ++j) {
+                const int e = j % E;
+                const long long srow0 = r0 + (long long)j * 8;
+                double zr[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int row = (lane + 32 * q) >> 3;
+                    zr[q] = (srow0 + row < r1) ? __ldg(a.z + srow0 + row) : 0.0;
+                }
+                mbar_wait(&xfull[e], (uint32_t)((j / E) & 1));
+                if (lane == 0 && j + E < nst) mbar_arrive_expect_tx(&xfull[e], kXBytes);
+                const double* xb = xchg + (size_t)e * V * C;
+                double* wb = wbuf + (j & 1) * 64;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int idx = lane + 32 * q;
+                    const int row = idx >> 3, g = idx & 7;
+                    double w = 0.0;
+                    if (g < K && srow0 + row < r1) {
+                        const double* yp = xb + (size_t)(row * NDOT + g) * C;
+                        double y = 0.0;
+#pragma unroll
+                        for (int c = 0; c < C; c += 2) {
+                            const double2 t = *reinterpret_cast<const double2*>(yp + c);
+                            y += t.x;
+                            y += t.y;
+                        }
+                        const double zt = zr[q];
+                        if constexpr (OP == Op::HVP) {
+                            w = (2.0 * c2 - 6.0 * c3 * zt + 12.0 * c4 * (zt * zt)) * y;
+                        } else {
+                            const double* yq = yp + (size_t)K * C;
+                            double yv = 0.0;
+#pragma unroll
+                            for (int c = 0; c < C; c += 2) {
+                                const double2 t = *reinterpret_cast<const double2*>(yq + c);
+                                yv += t.x;
+                                yv += t.y;
+                            }
+                            w = (-6.0 * c3 + 24.0 * c4 * zt) * y * yv;
+                        }
+                    }
+                    wb[idx] = w;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&wready[j & 1]);
+            }
+        }
+    } else {
+        // ========================= math warps ==========================
+        reg_alloc_232();
+        const int g4 = lane >> 2, t4 = lane & 3;
+        const int wcol = warp * WC;
+        double vb[NT1][2 * KP];
+#pragma unroll
+        for (int nt = 0; nt < NT1; ++nt)
+#pragma unroll
+            for (int ks = 0; ks < 2 * KP; ++ks) {
+                const int c = wcol + 8 * (ks >> 1) + 2 * t4 + (ks & 1);
+                const int j = nt * 8 + g4;
+                double v = 0.0;
+                if (c < cw && j < NDOT) {
+                    const double* src = (OP == Op::THIRD && j >= K) ? a.vin2 + (long long)(j - K) * ld
+                                                                     : a.vin + (long long)j * ld;
+                    v = src[col0 + c];
+                }
+                vb[nt][ks] = v;
+            }
+        double acc[MT][2];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+        double f2[2][MT];
+        const int p1_off = g4 * RS + wcol + 2 * t4;
+        const int p2_off = t4 * RS + wcol + 2 * g4;
+        int slot = 0;
+        uint32_t fpar = 0;
+        for (int i = 0; i <= nst; ++i) {
+            if (i < nst) {
+                // phase 1
+                mbar_wait(&full[slot], fpar);
+                const double* X = ring + slot * stage_elems + p1_off;
+                double cfr[NCH][NT1][2];
+#pragma unroll
+                for (int h = 0; h < NCH; ++h)
+#pragma unroll
+                    for (int nt = 0; nt < NT1; ++nt) cfr[h][nt][0] = cfr[h][nt][1] = 0.0;
+#pragma unroll
+                for (int m = 0; m < KP; ++m) {
+                    const double2 av = *reinterpret_cast<const double2*>(X + 8 * m);
+#pragma unroll
+                    for (int nt = 0; nt < NT1; ++nt) {
+                        dmma884(cfr[(2 * m) % NCH][nt], av.x, vb[nt][2 * m]);
+                        dmma884(cfr[(2 * m + 1) % NCH][nt], av.y, vb[nt][2 * m + 1]);
+                    }
+                }
+#pragma unroll
+                for (int h = 1; h < NCH; ++h)
+#pragma unroll
+                    for (int nt = 0; nt < NT1; ++nt) {
+                        cfr[0][nt][0] += cfr[h][nt][0];
+                        cfr[0][nt][1] += cfr[h][nt][1];
+                    }
+                const int r = i % R;
+                if (i >= R) mbar_wait(&pempty[r], (uint32_t)(((i / R) - 1) & 1));
+                double* rb = red + (size_t)r * NW * V + warp * V + g4 * NDOT;
+#pragma unroll
+                for (int nt = 0; nt < NT1; ++nt)
+                    if (nt * 8 + 2 * t4 < NDOT)
+                        *reinterpret_cast<double2*>(rb + nt * 8 + 2 * t4) = make_double2(cfr[0][nt][0], cfr[0][nt][1]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pfull[r]);
+            }
+            if (i >= 1) {
+                // phase 2 of stage i-1
+                const int j = i - 1;
+                mbar_wait(&wready[j & 1], (uint32_t)((j >> 1) & 1));
+                const double* wb = wbuf + (j & 1) * 64;
+                const double wf0 = wb[t4 * 8 + g4], wf1 = wb[(4 + t4) * 8 + g4];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt], f2[0][mt], wf0);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt], f2[1][mt], wf1);
+            }
+            if (i < nst) {
+                // frag(i), release the slot
+                const double* X = ring + slot * stage_elems + p2_off;
+#pragma unroll
+                for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+                    for (int p = 0; p < MP; ++p) {
+                        const double2 v = *reinterpret_cast<const double2*>(X + kh * 4 * RS + 16 * p);
+                        f2[kh][2 * p] = v.x;
+                        f2[kh][2 * p + 1] = v.y;
+                    }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
+                if (++slot == S) {
+                    slot = 0;
+                    fpar ^= 1;
+                }
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < MP; ++p)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int c = wcol + 16 * p + 2 * g4 + h;
+                    const int k = 2 * t4 + q;
+                    if (c < cw && k < K) a.part_acc[((size_t)ci * K + k) * ld + col0 + c] = acc[2 * p + h][q];
+                }
+    }
+    cluster.sync();  // no CTA exits while a peer may still push into it
+}
+
 }  // namespace mvsk_b200

@@ -1,6 +1,6 @@
-"""A/B timing of the multi-RHS tensor-core passes: pipelined kernel (default)
-vs the v1 kernel (MVSK_DMMA_V1=1), plus a bitwise/relative comparison of the
-two results. python scripts/dmma_ab.py C5 hvp8,third8,hvp4"""
+"""A/B timing of the multi-RHS tensor-core passes: warp-specialised kernel
+(ws, the default) vs pipelined (MVSK_DMMA_PIPE=1) vs v1 (MVSK_DMMA_V1=1), plus a bitwise/relative comparison of the
+two results. python scripts/dmma_ab.py C5 hvp8,third8,hvp4 ws,pipe,v1"""
 import os
 import sys
 from pathlib import Path
@@ -61,11 +61,11 @@ for op in ops:
     res = {}
     for var in variants:
         os.environ.pop("MVSK_DMMA_V1", None)
-        os.environ.pop("MVSK_TUNE_DMMA_PIPE", None)
-        if var == "v1":
+        os.environ.pop("MVSK_DMMA_PIPE", None)
+        if var == "pipe":
+            os.environ["MVSK_DMMA_PIPE"] = "1"
+        elif var == "v1":
             os.environ["MVSK_DMMA_V1"] = "1"
-        elif var.startswith("pipeC"):
-            os.environ["MVSK_TUNE_DMMA_PIPE"] = var[5:]
         out.zero_()
         fn()
         torch.cuda.synchronize()
