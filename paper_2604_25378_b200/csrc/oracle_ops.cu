@@ -415,55 +415,79 @@ bool make_dmma_pipe_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
     return true;
 }
 
-template <Op OP, int K, int WC>
+template <Op OP, int K, int WC, int C>
 const void* wfn() {
-    return reinterpret_cast<const void*>(&stream_dmma_ws_kernel<OP, K, WC, 4>);
+    return reinterpret_cast<const void*>(&stream_dmma_ws_kernel<OP, K, WC, C>);
 }
 
 // warp-specialised variant (stream_dmma_ws_kernel): 8 math warps + a helper
-// warpgroup, 4-CTA clusters
-const void* select_dmma_ws(Op op, int K, int WC) {
-    if (op == Op::HVP && K == 8) {
-        if (WC == 64) return wfn<Op::HVP, 8, 64>();
-        if (WC == 128) return wfn<Op::HVP, 8, 128>();
+// warpgroup. 4-CTA clusters with 64/128-column warp slices; 8-CTA clusters
+// (64/80-column slices) where a 4-CTA split would not fit the registers: the
+// 8 third-action pairs at n = 4096, and n = 5000 (C4)
+const void* select_dmma_ws(Op op, int K, int WC, int C) {
+    if (C == 4) {
+        if (op == Op::HVP && K == 8) {
+            if (WC == 64) return wfn<Op::HVP, 8, 64, 4>();
+            if (WC == 128) return wfn<Op::HVP, 8, 128, 4>();
+        }
+        if (op == Op::HVP && K == 4) {
+            if (WC == 64) return wfn<Op::HVP, 4, 64, 4>();
+            if (WC == 128) return wfn<Op::HVP, 4, 128, 4>();
+        }
+        if (op == Op::THIRD && K == 4) {
+            if (WC == 64) return wfn<Op::THIRD, 4, 64, 4>();
+            if (WC == 128) return wfn<Op::THIRD, 4, 128, 4>();
+        }
+        if (op == Op::THIRD && K == 8) {  // 128-column slices spill (twice the V fragments)
+            if (WC == 64) return wfn<Op::THIRD, 8, 64, 4>();
+        }
     }
-    if (op == Op::HVP && K == 4) {
-        if (WC == 64) return wfn<Op::HVP, 4, 64>();
-        if (WC == 128) return wfn<Op::HVP, 4, 128>();
-    }
-    if (op == Op::THIRD && K == 4) {
-        if (WC == 64) return wfn<Op::THIRD, 4, 64>();
-        if (WC == 128) return wfn<Op::THIRD, 4, 128>();
-    }
-    if (op == Op::THIRD && K == 8) {  // 128-column slices spill (twice the V fragments): v1 there
-        if (WC == 64) return wfn<Op::THIRD, 8, 64>();
+    if (C == 8) {
+        if (op == Op::HVP && K == 8 && WC == 80) return wfn<Op::HVP, 8, 80, 8>();
+        if (op == Op::HVP && K == 4 && WC == 80) return wfn<Op::HVP, 4, 80, 8>();
+        if (op == Op::THIRD && K == 4 && WC == 80) return wfn<Op::THIRD, 4, 80, 8>();
+        if (op == Op::THIRD && K == 8) {
+            if (WC == 64) return wfn<Op::THIRD, 8, 64, 8>();
+            if (WC == 80) return wfn<Op::THIRD, 8, 80, 8>();
+        }
     }
     return nullptr;
 }
 
 bool make_dmma_ws_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
-    const int C = 4;
     const int ndot = op == Op::THIRD ? 2 * K : K;
     const int V = 8 * ndot;
-    if (ctx->ld % (2 * C)) return false;
-    const int cw = (int)(ctx->ld / C);
-    int WC = 0;
-    for (int w : {64, 128})
-        if (!WC && 8 * w >= cw && select_dmma_ws(op, K, w)) WC = w;
-    if (!WC) return false;
-    const size_t stage = (size_t)8 * (8 * WC + 4) * sizeof(double);
-    size_t head = 256 + (size_t)(2 * 8 * V + 4 * C * V + 128) * sizeof(double);
-    head = (head + 127) & ~(size_t)127;
-    const int S = (int)std::min<size_t>(8, (ctx->max_smem - head) / stage);
-    if (S < 2) return false;
-    pl.C = C;
-    pl.WC = WC;
-    pl.S = S;
-    pl.threads = 384;
-    pl.smem = head + (size_t)S * stage;
-    pl.fn = select_dmma_ws(op, K, WC);
-    pl.ncl = std::max(1, ctx->nsm / C);
-    return true;
+    int forceC = 0;
+    if (const char* e = std::getenv("MVSK_DMMA_WS_C")) forceC = std::atoi(e);
+    // 8-CTA clusters only for small panels (< 64 rows per SM, latency-bound):
+    // at C5 the 8 third-action pairs run 3.77 ms there vs 2.68 ms on v1, at C4
+    // (T = 5000) the 4-RHS ops gain 25-30 % and the 8 pairs 4 %; the 8-RHS HVP
+    // at C4 is 6 % faster on v1 (profiles/r01_dmma_pipe.txt)
+    const bool small = ctx->T_local < 64LL * ctx->nsm;
+    for (int C : {4, 8}) {
+        if (forceC && C != forceC) continue;
+        if (!forceC && C == 8 && (!small || (op == Op::HVP && K == 8))) continue;
+        if (ctx->ld % (2 * C)) continue;
+        const int cw = (int)(ctx->ld / C);
+        int WC = 0;
+        for (int w : {64, 80, 128})
+            if (!WC && 8 * w >= cw && select_dmma_ws(op, K, w, C)) WC = w;
+        if (!WC) continue;
+        const size_t stage = (size_t)8 * (8 * WC + 4) * sizeof(double);
+        size_t head = 256 + (size_t)(2 * 8 * V + 4 * C * V + 128) * sizeof(double);
+        head = (head + 127) & ~(size_t)127;
+        const int S = (int)std::min<size_t>(8, (ctx->max_smem - head) / stage);
+        if (S < 2) continue;
+        pl.C = C;
+        pl.WC = WC;
+        pl.S = S;
+        pl.threads = 384;
+        pl.smem = head + (size_t)S * stage;
+        pl.fn = select_dmma_ws(op, K, WC, C);
+        pl.ncl = std::max(1, ctx->nsm / C);
+        return true;
+    }
+    return false;
 }
 
 bool make_dmma_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
