@@ -415,9 +415,9 @@ bool make_dmma_pipe_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
     return true;
 }
 
-template <Op OP, int K, int WC, int C>
+template <Op OP, int K, int WC, int C, bool F2REG = true>
 const void* wfn() {
-    return reinterpret_cast<const void*>(&stream_dmma_ws_kernel<OP, K, WC, C>);
+    return reinterpret_cast<const void*>(&stream_dmma_ws_kernel<OP, K, WC, C, F2REG>);
 }
 
 // warp-specialised variant (stream_dmma_ws_kernel): 8 math warps + a helper
@@ -438,8 +438,9 @@ const void* select_dmma_ws(Op op, int K, int WC, int C) {
             if (WC == 64) return wfn<Op::THIRD, 4, 64, 4>();
             if (WC == 128) return wfn<Op::THIRD, 4, 128, 4>();
         }
-        if (op == Op::THIRD && K == 8) {  // 128-column slices spill (twice the V fragments)
+        if (op == Op::THIRD && K == 8) {  // 128-column slices: phase 2 from the ring (registers)
             if (WC == 64) return wfn<Op::THIRD, 8, 64, 4>();
+            if (WC == 128) return wfn<Op::THIRD, 8, 128, 4, false>();
         }
     }
     if (C == 8) {

@@ -628,7 +628,11 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_pipe_kernel(const DmmaArgs
 __device__ __forceinline__ void reg_alloc_232() { asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory"); }
 __device__ __forceinline__ void reg_dealloc_40() { asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory"); }
 
-template <Op OP, int K, int WC, int C>
+// F2REG = false (the 8 third-action pairs at 128-column slices, whose doubled
+// V fragments leave no room for held phase-2 fragments): phase 2 reads the
+// tile from the ring slot, which is then released after phase 2 instead of
+// after phase 1 (one fill fewer in flight).
+template <Op OP, int K, int WC, int C, bool F2REG = true>
 __global__ void __launch_bounds__(384, 1) stream_dmma_ws_kernel(const DmmaArgs a) {
     using Sh = DmmaShape<OP, K>;
     constexpr int NDOT = Sh::NDOT, NT1 = Sh::NT1, V = Sh::V;
@@ -826,10 +830,10 @@ __global__ void __launch_bounds__(384, 1) stream_dmma_ws_kernel(const DmmaArgs a
         double acc[MT][2];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
-        double f2[2][MT];
+        double f2[F2REG ? 2 : 1][F2REG ? MT : 1];
         const int p1_off = g4 * RS + wcol + 2 * t4;
         const int p2_off = t4 * RS + wcol + 2 * g4;
-        int slot = 0;
+        int slot = 0, prev_slot = 0;
         uint32_t fpar = 0;
         for (int i = 0; i <= nst; ++i) {
             if (i < nst) {
@@ -873,24 +877,41 @@ __global__ void __launch_bounds__(384, 1) stream_dmma_ws_kernel(const DmmaArgs a
                 mbar_wait(&wready[j & 1], (uint32_t)((j >> 1) & 1));
                 const double* wb = wbuf + (j & 1) * 64;
                 const double wf0 = wb[t4 * 8 + g4], wf1 = wb[(4 + t4) * 8 + g4];
+                if constexpr (F2REG) {
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt], f2[0][mt], wf0);
+                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt], f2[0][mt], wf0);
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt], f2[1][mt], wf1);
+                    for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt], f2[1][mt], wf1);
+                } else {
+                    const double* X = ring + prev_slot * stage_elems + p2_off;
+#pragma unroll
+                    for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+                        for (int p = 0; p < MP; ++p) {
+                            const double2 v = *reinterpret_cast<const double2*>(X + kh * 4 * RS + 16 * p);
+                            dmma884(acc[2 * p], v.x, kh ? wf1 : wf0);
+                            dmma884(acc[2 * p + 1], v.y, kh ? wf1 : wf0);
+                        }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[prev_slot]);
+                }
             }
             if (i < nst) {
                 // frag(i), release the slot
-                const double* X = ring + slot * stage_elems + p2_off;
+                if constexpr (F2REG) {
+                    const double* X = ring + slot * stage_elems + p2_off;
 #pragma unroll
-                for (int kh = 0; kh < 2; ++kh)
+                    for (int kh = 0; kh < 2; ++kh)
 #pragma unroll
-                    for (int p = 0; p < MP; ++p) {
-                        const double2 v = *reinterpret_cast<const double2*>(X + kh * 4 * RS + 16 * p);
-                        f2[kh][2 * p] = v.x;
-                        f2[kh][2 * p + 1] = v.y;
-                    }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[slot]);
+                        for (int p = 0; p < MP; ++p) {
+                            const double2 v = *reinterpret_cast<const double2*>(X + kh * 4 * RS + 16 * p);
+                            f2[kh][2 * p] = v.x;
+                            f2[kh][2 * p + 1] = v.y;
+                        }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[slot]);
+                }
+                prev_slot = slot;
                 if (++slot == S) {
                     slot = 0;
                     fpar ^= 1;
