@@ -85,6 +85,16 @@ def test_c5_full_size_parity_and_identities():
     lm = gpu.line_model(gc, V[0], 1.0)
     assert lm.a1 == pytest.approx(g @ V[0], rel=1e-11)
     assert np.max(np.abs(H[0] - H1)) <= 1e-11 * np.max(np.abs(H1))  # tensor-core vs streaming path
+    # 4-RHS and 8-pair third-action tensor-core paths vs the single streaming pass
+    H4 = gpu.hvp(gc, V[4:])
+    assert np.max(np.abs(H4 - H[4:])) <= 1e-11 * np.max(np.abs(H[4:]))
+    W = V[::-1].copy()
+    T8 = gpu.third_action(gc, V, W)
+    for i in (0, 5):
+        Ti = gpu.third_action(gc, V[i], W[i])
+        assert np.max(np.abs(T8[i] - Ti)) <= 1e-11 * np.max(np.abs(Ti))
+    T4 = gpu.third_action(gc, V[:4], W[:4])
+    assert np.max(np.abs(T4 - T8[:4])) <= 1e-11 * np.max(np.abs(T8[:4]))
     # the same bits on the CPU oracle (all host threads, test-only)
     A = X.cpu().numpy()
     del X
