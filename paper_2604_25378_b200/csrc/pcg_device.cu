@@ -19,8 +19,13 @@
 // direction. The first direction of a shape runs eagerly (it sizes every
 // workspace); exact-trace sweeps and > 16 probes stay eager.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "host_ops.hpp"
 #include "pcg_device.hpp"
@@ -333,6 +338,357 @@ __global__ void cg_decide_kernel(const int* active, int k, cudaGraphConditionalH
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Cluster-resident Krylov loop for narrow panels (ld <= 128: compact faces,
+// small problems). One thread-block cluster runs a whole capped-CG loop
+// (cg_capped, affine_normal.hpp:85-113) for k <= 8 columns in lock-step:
+// the CG state lives in shared memory, every HVP pass is streamed by all CTAs
+// of the cluster (row groups of LPR lanes, the panel from L2/HBM), the CTA
+// partials are combined through distributed shared memory in rank order (one
+// cluster barrier per step, double-buffered), and the small per-column algebra
+// (Householder lift / reduce, alpha, beta, the stop test) is computed
+// redundantly by every CTA, one warp per column, on identical bits - so every
+// CTA takes the same branches and no broadcast is needed. Replaces, per CG
+// step, an HVP pass kernel and a cg_step kernel (~20 us on C4 faces) with
+// in-cluster work and one barrier.
+// ---------------------------------------------------------------------------
+constexpr int kCcgMaxLd = 128;
+constexpr int kCcgCS = 16;     // CTAs per cluster (non-portable size)
+constexpr int kCcgWarps = 8;   // warps per CTA
+
+struct CcgArgs {
+    const StepParams* sp;  // geometry + CG state arrays (global) + lambda
+    const double* rhs;     // k x mm
+    const double* X;       // panel T x ld
+    const double* z;       // cached z (T)
+    long long T;
+    int ld, k;
+    double c2, c3, c4, invT;
+    unsigned long long* prof;  // timing studies: per-phase clock64 sums of one CTA (or null)
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// shared memory of cluster_cg_kernel: CG state and scratch, plus (PANEL) the
+// CTA's rows of the panel (stride ld + 2) and their z
+constexpr size_t ccg_smem_bytes() {
+    constexpr int M = kCcgMaxLd;
+    return (size_t)(4 * M + 2 * M + 2 * M + kCcgWarps * M + M + 3 * M + 2) * sizeof(double) +
+           (size_t)(M + 8) * sizeof(int) + 16;
+}
+
+// Cluster-resident capped CG (cg_capped, affine_normal.hpp:85-113) for one
+// column per cluster; k columns run as k clusters side by side. The column's
+// state lives in shared memory; each HVP pass is streamed by the cluster's 16
+// CTAs over contiguous row blocks (PANEL: the block is staged in shared memory
+// once and re-read every step), the partials are combined through distributed
+// shared memory in rank order (one cluster barrier per step, double-buffered)
+// and the per-column algebra (Householder reduce / lift, alpha, beta, the stop
+// test) is computed by warp 0 of every CTA on identical bits, so every CTA
+// takes the same branches. LPR lanes per row, CPL columns per lane.
+template <int LPR, int CPL, bool PANEL>
+__global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const CcgArgs a) {
+    namespace cgs = cooperative_groups;
+    constexpr int M = kCcgMaxLd;
+    constexpr int CS = kCcgCS;
+    static_assert(LPR * CPL <= M && CPL % 2 == 0 && 32 % LPR == 0, "row layout");
+    cgs::cluster_group cluster = cgs::this_cluster();
+    const int crank = (int)cluster.block_rank();
+    const int col = blockIdx.x / CS;  // the CG column of this cluster
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const Geo g = a.sp->g;
+    const CGState s = a.sp->s;
+    const double lambda = a.sp->lambda;
+    const int ld = a.ld, m = g.m, m1 = m - 1, mm = s.mm;
+
+    extern __shared__ __align__(16) double ccg_sm[];
+    double* sX = ccg_sm;
+    double* sR = sX + M;
+    double* sZ = sR + M;
+    double* sP = sZ + M;
+    double* sV = sP + M;          // lifted search direction (panel coordinates), zero past the face
+    double* sH = sV + M;          // HVP row
+    double* sPart = sH + M;       // [2][M] this CTA's pass partial (double-buffered)
+    double* sW = sPart + 2 * M;   // [warps][M] warp partials
+    double* sT = sW + kCcgWarps * M;  // reduce / lift scratch (warp 0)
+    double* sU = sT + M;
+    double* sQ = sU + M;
+    double* sJ = sQ + M;
+    double* sSc = sJ + M;         // [rz, target]
+    int* sIdx = reinterpret_cast<int*>(sSc + 2);
+    int* sFlag = sIdx + M;        // [active, iters, breakdown]
+    const long long T = a.T;
+    const long long r0 = T * crank / CS, r1 = T * (crank + 1) / CS;
+    const int nloc = (int)(r1 - r0);
+    // (offset from ccg_sm so the compiler keeps the shared address space)
+    double* sXp = ccg_sm + ((size_t)(reinterpret_cast<char*>(sFlag + 8) - reinterpret_cast<char*>(ccg_sm)) + 15) / 16 * 2;
+    // smem rows padded by one 16-byte pair (stride ld + 2): the row groups of a
+    // warp fall on distinct bank groups
+    const int lds = ld + 2;
+    double* sZr = sXp + (size_t)nloc * lds;
+    __shared__ uint64_t stage_bar;
+    if constexpr (PANEL) {
+        // the CTA's row block -> shared memory by the bulk-copy engine (one
+        // 16-byte-aligned copy per row, completion as tx-bytes on stage_bar)
+        if (tid == 0) {
+            mbar_init(&stage_bar, 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (warp == 0) {
+            if (lane == 0) mbar_arrive_expect_tx(&stage_bar, (uint32_t)((size_t)nloc * ld * sizeof(double)));
+            __syncwarp();
+            const uint64_t pol = policy_evict_last();
+            for (int r = lane; r < nloc; r += 32)
+                bulk_g2s(sXp + (size_t)r * lds, a.X + (r0 + r) * (long long)ld, (uint32_t)(ld * sizeof(double)),
+                         &stage_bar, pol);
+        }
+        for (int i = tid; i < nloc; i += blockDim.x) sZr[i] = __ldg(a.z + r0 + i);
+    }
+    for (int i = tid; i < m; i += blockDim.x) {
+        sU[i] = g.vU[i];
+        sIdx[i] = g.idx ? (int)g.idx[i] : i;
+    }
+    for (int i = tid; i < m1; i += blockDim.x) sQ[i] = g.vQ[i];
+    for (int i = tid; i < mm; i += blockDim.x) sJ[i] = s.jd ? s.jd[i] : 1.0;
+    for (int i = tid; i < M; i += blockDim.x) sV[i] = 0.0;
+    if constexpr (PANEL) mbar_wait(&stage_bar, 0u);
+    __syncthreads();
+
+    // lift: V = U Q (0, P) (lift_col), warp 0
+    auto lift = [&]() {
+        double* q = sT;
+        double part = 0.0;
+        for (int i = lane; i < m1; i += 32) {
+            const double v = i == 0 ? 0.0 : sP[i - 1];
+            q[i] = v;
+            part += sQ[i] * v;
+        }
+        const double s1 = g.bQ * warp_sum(part);
+        for (int i = lane; i < m1; i += 32) q[i] -= s1 * sQ[i];
+        __syncwarp();
+        double part2 = 0.0;
+        for (int i = lane + 1; i < m; i += 32) part2 += sU[i] * q[i - 1];
+        const double s2 = g.bU * warp_sum(part2);
+        for (int i = lane; i < m; i += 32) sV[sIdx[i]] = (i == 0 ? 0.0 : q[i - 1]) - s2 * sU[i];
+    };
+
+    // ---- cg_init (cg_init_kernel) + the first lift, warp 0
+    if (warp == 0) {
+        const double* b = a.rhs + (size_t)col * mm;
+        double prz = 0.0, pbb = 0.0;
+        for (int i = lane; i < mm; i += 32) {
+            const double r = b[i];
+            const double zz = s.jd ? r / s.jd[i] : r;
+            sX[i] = 0.0;
+            sR[i] = r;
+            sZ[i] = zz;
+            sP[i] = zz;
+            prz += r * zz;
+            pbb += r * r;
+        }
+        const double rz = warp_sum(prz), bb = warp_sum(pbb);
+        const bool act = s.cap > 0 && sqrt(bb) > s.tol * sqrt(bb);  // :94 at it = 0
+        if (lane == 0) {
+            sSc[0] = rz;
+            sSc[1] = s.tol * sqrt(bb);
+            sFlag[0] = act ? 1 : 0;
+            sFlag[1] = 0;
+            sFlag[2] = 0;
+        }
+        __syncwarp();
+        if (act) lift();
+    }
+    __syncthreads();
+
+    constexpr int GPW = 32 / LPR;         // row groups per warp
+    constexpr int NGC = kCcgWarps * GPW;  // row groups per CTA
+    // column pairs interleaved over the LPR lanes of a row group: pair
+    // j2 * LPR + sub holds columns 2p, 2p + 1, so a row group reads contiguous bytes
+    const int sub = lane % LPR;
+    auto colp = [&](int j) { return 2 * ((j >> 1) * LPR + sub) + (j & 1); };
+    int step = 0;
+    unsigned long long prof_t = clock64();
+    int prof_last = -1;
+    const bool prof_on = a.prof && crank == 0 && col == 0 && tid == 0;
+    auto prof_mark = [&](int i) {
+        if (prof_on) {
+            const unsigned long long now = clock64();
+            if (prof_last >= 0) a.prof[prof_last] += now - prof_t;
+            prof_t = now;
+            prof_last = i;
+        }
+    };
+    while (sFlag[0]) {
+        prof_mark(1);
+        // ---- HVP pass over this CTA's rows: acc[j] += x_tj psi''(z_t) <x_t, V>
+        double acc[CPL];
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) acc[j] = 0.0;
+        // every lane of a warp runs the same trip count (the shuffles need the
+        // full warp); rows past the block contribute zeros
+#pragma unroll 2
+        for (int lb = warp * GPW; lb < nloc; lb += NGC) {
+            const int tl = lb + lane / LPR;
+            const bool rv = tl < nloc;
+            double x[CPL];
+            double zt = 0.0;
+            const double* xr = PANEL ? sXp + (size_t)(rv ? tl : 0) * lds : a.X + (r0 + (rv ? tl : 0)) * (long long)ld;
+#pragma unroll
+            for (int j = 0; j < CPL; j += 2) {
+                double2 v = make_double2(0.0, 0.0);
+                if (rv && colp(j) < ld)
+                    v = PANEL ? *reinterpret_cast<const double2*>(xr + colp(j))
+                              : __ldg(reinterpret_cast<const double2*>(xr + colp(j)));
+                x[j] = v.x;
+                x[j + 1] = v.y;
+            }
+            if (rv) zt = PANEL ? sZr[tl] : __ldg(a.z + r0 + tl);
+            const double psi2 = 2.0 * a.c2 - 6.0 * a.c3 * zt + 12.0 * a.c4 * (zt * zt);
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < CPL; j += 2) {
+                const double2 v = *reinterpret_cast<const double2*>(sV + colp(j));
+                d0 = fma(x[j], v.x, d0);
+                d1 = fma(x[j + 1], v.y, d1);
+            }
+            double d = d0 + d1;
+#pragma unroll
+            for (int o = 1; o < LPR; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            const double w = psi2 * d;
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) acc[j] = fma(x[j], w, acc[j]);
+        }
+        prof_mark(2);
+        // combine the warp's row groups (lanes with equal sub), then the warps in order
+#pragma unroll
+        for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+        if (lane < LPR) {
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) sW[warp * M + colp(j)] = acc[j];
+        }
+        __syncthreads();
+        double* buf = sPart + (step & 1) * M;
+        for (int e = tid; e < ld; e += blockDim.x) {
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < kCcgWarps; ++w) v += sW[w * M + e];
+            buf[e] = v;
+        }
+        prof_mark(3);
+        // ---- cluster combine: every CTA sums the CS partials in rank order
+        cluster.sync();
+        for (int e = tid; e < ld; e += blockDim.x) {
+            double pv[CS];
+#pragma unroll
+            for (int r = 0; r < CS; ++r) pv[r] = cluster.map_shared_rank(buf, r)[e];
+            double v = 0.0;
+#pragma unroll
+            for (int r = 0; r < CS; ++r) v += pv[r];
+            sH[e] = v * a.invT;
+        }
+        __syncthreads();
+        ++step;
+        prof_mark(4);
+        // ---- one capped-CG step (cg_step_col) and the next lift, warp 0
+        if (warp == 0) {
+            double* t = sT;
+            const double rz_old = sSc[0];
+            double part = 0.0;
+            for (int i = lane; i < m; i += 32) part += sU[i] * sH[sIdx[i]];
+            const double s1 = g.bU * warp_sum(part);
+            double part2 = 0.0;
+            for (int i = lane; i < m1; i += 32) {
+                const double v = sH[sIdx[i + 1]] - s1 * sU[i + 1];
+                t[i] = v;
+                part2 += sQ[i] * v;
+            }
+            const double s2 = g.bQ * warp_sum(part2);
+            __syncwarp();
+            constexpr int U4 = M / 32;
+            double hp[U4];
+            double pp = 0.0;
+#pragma unroll
+            for (int u = 0; u < U4; ++u) {
+                const int i = lane + 32 * u;
+                hp[u] = 0.0;
+                if (i < mm) {
+                    hp[u] = (t[i + 1] - s2 * sQ[i + 1]) + lambda * sP[i];  // Hop: red + lambda e (:194)
+                    pp += sP[i] * hp[u];
+                }
+            }
+            const double pHp = warp_sum(pp);
+            __syncwarp();
+            if (pHp <= 0.0) {  // :97-100
+                if (lane == 0) {
+                    sFlag[2] = 1;
+                    sFlag[0] = 0;
+                }
+            } else {
+                const double alpha = rz_old / pHp;
+                double prz = 0.0, prr = 0.0;
+#pragma unroll
+                for (int u = 0; u < U4; ++u) {
+                    const int i = lane + 32 * u;
+                    if (i < mm) {
+                        sX[i] += alpha * sP[i];
+                        const double r = sR[i] - alpha * hp[u];
+                        sR[i] = r;
+                        const double zz = s.jd ? r / sJ[i] : r;
+                        sZ[i] = zz;
+                        prz += r * zz;
+                        prr += r * r;
+                    }
+                }
+                const double rz2 = warp_sum(prz), rr = warp_sum(prr);
+                const double beta = rz2 / rz_old;
+#pragma unroll
+                for (int u = 0; u < U4; ++u) {
+                    const int i = lane + 32 * u;
+                    if (i < mm) sP[i] = sZ[i] + beta * sP[i];
+                }
+                const int it = sFlag[1] + 1;
+                const bool still = it < s.cap && sqrt(rr) > sSc[1];  // :94
+                __syncwarp();
+                if (lane == 0) {
+                    sSc[0] = rz2;
+                    sFlag[1] = it;
+                    sFlag[0] = still ? 1 : 0;
+                }
+                __syncwarp();
+                if (still) lift();
+            }
+        }
+        __syncthreads();
+    }
+    prof_mark(5);
+    if (prof_on) a.prof[6] += (unsigned long long)step;
+    // ---- results to the global CG state (CTA 0 of the cluster)
+    if (crank == 0) {
+        for (int i = tid; i < mm; i += blockDim.x) {
+            s.X[(size_t)col * mm + i] = sX[i];
+            s.R[(size_t)col * mm + i] = sR[i];
+            s.Z[(size_t)col * mm + i] = sZ[i];
+            s.P[(size_t)col * mm + i] = sP[i];
+        }
+        if (tid == 0) {
+            s.rz[col] = sSc[0];
+            s.target[col] = sSc[1];
+            s.active[col] = sFlag[0];
+            s.iters[col] = sFlag[1];
+            s.breakdown[col] = sFlag[2];
+        }
+    }
+    cluster.sync();  // no CTA exits while a peer may still read its partials
+}
+
 template <class T>
 T* carve(unsigned char*& cur, size_t count) {
     T* p = reinterpret_cast<T*>(cur);
@@ -641,8 +997,83 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     // st is capturing the whole direction; each Krylov loop is spliced in as a
     // conditional-while node (its counts recorded in *capture)
     PcgWorkspace::DirGraph* capture = nullptr;
+    // narrow panels: the whole Krylov loop in one thread-block cluster
+    // (cluster_cg_kernel); MVSK_NO_CCG keeps the graph / host loops for A/B
+    static const bool no_ccg = std::getenv("MVSK_NO_CCG") != nullptr;
+    const bool ccg_ok = !no_ccg && ctx->nranks == 1 && ld <= (size_t)kCcgMaxLd && m <= (int)ld;
+    auto ccg_launch = [&](int k, const StepParams* spd, const double* rhs) -> bool {
+        if (!ccg_ok || k > 8) return false;
+        // one 16-CTA cluster per column (k clusters side by side); each CTA keeps
+        // its rows in shared memory when they fit
+        const int CS = kCcgCS;
+        const long long nloc = (ctx->T_local + CS - 1) / CS;
+        const size_t panel = (size_t)nloc * (ld + 3) * sizeof(double);  // padded rows + z
+        size_t smem = ccg_smem_bytes();
+        const bool in_smem = smem + panel <= ctx->max_smem;
+        const void* fn;
+        if (in_smem) {
+            smem += panel;
+            fn = ld <= 64 ? (const void*)&cluster_cg_kernel<4, 16, true> : (const void*)&cluster_cg_kernel<8, 16, true>;
+        } else {
+            fn = ld <= 64 ? (const void*)&cluster_cg_kernel<4, 16, false> : (const void*)&cluster_cg_kernel<8, 16, false>;
+        }
+        set_smem_attr(fn, smem);
+        MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CcgArgs ca{};
+        ca.sp = spd;
+        ca.rhs = rhs;
+        ca.X = ctx->X;
+        ca.z = sl.z;
+        ca.T = ctx->T_local;
+        ca.ld = (int)ld;
+        ca.k = k;
+        ca.c2 = ctx->c.c2;
+        ca.c3 = ctx->c.c3;
+        ca.c4 = ctx->c.c4;
+        ca.invT = 1.0 / (double)ctx->T_global;
+        static unsigned long long* prof = nullptr;  // MVSK_CCG_PROF: per-phase cycle sums, printed at exit
+        if (std::getenv("MVSK_CCG_PROF")) {
+            if (!prof) {
+                MVSK_CUDA(cudaMallocManaged(&prof, 8 * sizeof(unsigned long long)));
+                std::memset(prof, 0, 8 * sizeof(unsigned long long));
+                std::atexit([] {
+                    cudaDeviceSynchronize();
+                    std::fprintf(stderr, "[ccg prof] steps %llu | pass %llu combine %llu cluster %llu cg+lift %llu (cycles)\n",
+                                 prof[6], prof[1], prof[2], prof[3], prof[4]);
+                });
+            }
+            ca.prof = prof;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(CS * k);
+        cfg.blockDim = dim3(kCcgWarps * 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        void* args[] = {&ca};
+        MVSK_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+        return true;
+    };
     auto cg = [&](int k, int role, const double* rhs) {
         const StepParams* spd = &dir->sp[role];
+        if (ccg_launch(k, spd, rhs)) {
+            // one launch and one physical pass per step, counted when the
+            // iteration counts come back (settle_counts)
+            if (capture) {
+                const int li = capture->nloops++;
+                capture->loop_k[li] = k;
+                capture->loop_pps[li] = 1;
+                capture->loop_lps[li] = 0;
+            }
+            defer_counts(k, true, 1, 0);
+            return;
+        }
         MVSK_CUDA(cudaMemsetAsync(arrive, 0, sizeof(unsigned), st));
         ++ctx->launches;
         cg_init_kernel<<<k, pt, dsm_max, st>>>(spd, rhs, vin);
