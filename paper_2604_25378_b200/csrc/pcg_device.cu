@@ -1004,19 +1004,17 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     auto ccg_launch = [&](int k, const StepParams* spd, const double* rhs) -> bool {
         if (!ccg_ok || k > 8) return false;
         // one 16-CTA cluster per column (k clusters side by side); each CTA keeps
-        // its rows in shared memory when they fit
+        // its rows in shared memory
         const int CS = kCcgCS;
         const long long nloc = (ctx->T_local + CS - 1) / CS;
         const size_t panel = (size_t)nloc * (ld + 3) * sizeof(double);  // padded rows + z
+        // only when each CTA's row block fits its shared memory: a taller narrow
+        // panel streamed by 16 SMs per step would lose to the 148-CTA pass
         size_t smem = ccg_smem_bytes();
-        const bool in_smem = smem + panel <= ctx->max_smem;
-        const void* fn;
-        if (in_smem) {
-            smem += panel;
-            fn = ld <= 64 ? (const void*)&cluster_cg_kernel<4, 16, true> : (const void*)&cluster_cg_kernel<8, 16, true>;
-        } else {
-            fn = ld <= 64 ? (const void*)&cluster_cg_kernel<4, 16, false> : (const void*)&cluster_cg_kernel<8, 16, false>;
-        }
+        if (smem + panel > ctx->max_smem) return false;
+        smem += panel;
+        const void* fn =
+            ld <= 64 ? (const void*)&cluster_cg_kernel<4, 16, true> : (const void*)&cluster_cg_kernel<8, 16, true>;
         set_smem_attr(fn, smem);
         MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CcgArgs ca{};
