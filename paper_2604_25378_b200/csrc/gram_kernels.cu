@@ -9,6 +9,7 @@
 // mxf4 only), so DMMA through mma.sync is the tensor-core path for fp64.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "oracle_ops.cuh"
 
@@ -21,7 +22,6 @@ constexpr int GBK = 32;             // sample rows per chunk
 constexpr int GST = 3;              // cp.async ring depth
 constexpr int GPAD = 4;             // smem row pad (doubles): conflict-free fragment loads
 constexpr int GLDS = GBM + GPAD;    // smem row stride
-constexpr int GTHREADS = 256;       // 8 warps: 4 (m) x 2 (n), warp tile 32 x 64
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
@@ -44,6 +44,7 @@ struct GramArgs {
     const double* w;  // T sample weights
     long long T;
     int ld;
+    int n;              // valid columns (fragments wholly past n are skipped)
     int ntile;          // tiles per dimension
     int nsplit;         // sample splits
     double* part;       // [nsplit][npairs][GBM*GBM]
@@ -58,7 +59,15 @@ __device__ __forceinline__ void pair_of(int p, int& ti, int& tj) {
     tj = p - i * (i + 1) / 2;
 }
 
-__global__ void __launch_bounds__(GTHREADS, 1) syrk_dmma_kernel(const GramArgs a) {
+// WM x WN warps, warp tile (8 FM) x (8 FN); the sample weight scales the A
+// fragments (WA) or the B fragments. GUARD (n not a multiple of the tile):
+// fragments wholly past n are skipped (C1: 9 of the 512 per k-step are
+// live); the guards cost registers and DMMA interleaving, so full-tile panels
+// (C5: 179 vs 149 ms) use the unguarded instantiation
+template <int WM, int WN, int FM, int FN, bool WA, bool GUARD = false>
+__global__ void __launch_bounds__(WM * WN * 32, 1) syrk_dmma_kernel(const GramArgs a) {
+    static_assert(WM * FM * 8 == GBM && WN * FN * 8 == GBM, "warp grid must cover the tile");
+    constexpr int NT = WM * WN * 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* sA = reinterpret_cast<double*>(smem_raw);           // [GST][GBK][GLDS]
     double* sB = sA + GST * GBK * GLDS;                          // [GST][GBK][GLDS]
@@ -71,13 +80,17 @@ __global__ void __launch_bounds__(GTHREADS, 1) syrk_dmma_kernel(const GramArgs a
     const int nchunk = (int)((t_hi - t_lo + GBK - 1) / GBK);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp >> 1, wn = warp & 1;  // warp tile origin (wm*32, wn*64)
+    const int wm = warp / WN, wn = warp % WN;  // warp tile origin (wm*8FM, wn*8FN)
 
+    // columns of each operand that any computed fragment reads: the valid
+    // extent rounded up to the 8-column fragment (zero-filled past ld)
+    const int wa = min(GBM, (a.n - i0 + 7) & ~7), wb = min(GBM, (a.n - j0 + 7) & ~7);
+    const int pieces = GUARD ? max(wa, wb) / 2 : GBM / 2;  // 16-byte pieces per row
     auto load_chunk = [&](int c, int buf) {
         const long long t0 = t_lo + (long long)c * GBK;
-        // 16 rows x 128 doubles per operand = 1024 16-byte pieces each; 256 threads -> 4 + 4
-        for (int e = tid; e < GBK * (GBM / 2); e += GTHREADS) {
-            const int r = e / (GBM / 2), cp = e - r * (GBM / 2);
+        // GBK rows x (<= 128) doubles per operand = 16-byte pieces spread over the CTA
+        for (int e = tid; e < GBK * pieces; e += NT) {
+            const int r = e / pieces, cp = e - r * pieces;
             const long long t = t0 + r;
             const bool rv = t < t_hi;
             const int ca = i0 + 2 * cp, cb = j0 + 2 * cp;
@@ -92,11 +105,11 @@ __global__ void __launch_bounds__(GTHREADS, 1) syrk_dmma_kernel(const GramArgs a
         }
     };
 
-    double acc[4][8][2];
+    double acc[FM][FN][2];
 #pragma unroll
-    for (int fm = 0; fm < 4; ++fm)
+    for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
-        for (int fn = 0; fn < 8; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
+        for (int fn = 0; fn < FN; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
 
     // GST-deep cp.async ring: one commit group per chunk (possibly empty)
     for (int c = 0; c < GST - 1; ++c) {
@@ -116,64 +129,93 @@ __global__ void __launch_bounds__(GTHREADS, 1) syrk_dmma_kernel(const GramArgs a
         for (int k0 = 0; k0 < GBK; k0 += 4) {
             const int kr = k0 + (lane & 3);
             const double wk = W[kr];
-            double af[4], bf[8];
+            double af[FM], bf[FN];
 #pragma unroll
-            for (int fm = 0; fm < 4; ++fm) af[fm] = A[kr * GLDS + wm * 32 + fm * 8 + (lane >> 2)];
+            for (int fm = 0; fm < FM; ++fm) af[fm] = A[kr * GLDS + wm * 8 * FM + fm * 8 + (lane >> 2)];
 #pragma unroll
-            for (int fn = 0; fn < 8; ++fn) bf[fn] = wk * B[kr * GLDS + wn * 64 + fn * 8 + (lane >> 2)];
+            for (int fn = 0; fn < FN; ++fn) bf[fn] = B[kr * GLDS + wn * 8 * FN + fn * 8 + (lane >> 2)];
+            if constexpr (WA) {
 #pragma unroll
-            for (int fm = 0; fm < 4; ++fm)
+                for (int fm = 0; fm < FM; ++fm) af[fm] *= wk;
+            } else {
 #pragma unroll
-                for (int fn = 0; fn < 8; ++fn) dmma_8x8x4(acc[fm][fn], af[fm], bf[fn]);
+                for (int fn = 0; fn < FN; ++fn) bf[fn] *= wk;
+            }
+#pragma unroll
+            for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+                for (int fn = 0; fn < FN; ++fn)
+                    if (!GUARD || (wm * 8 * FM + fm * 8 < wa && wn * 8 * FN + fn * 8 < wb))
+                        dmma_8x8x4(acc[fm][fn], af[fm], bf[fn]);
         }
     }
     // partial tile out (row-major 128 x 128)
     double* out = a.part + ((size_t)split * gridDim.x + blockIdx.x) * (GBM * GBM);
 #pragma unroll
-    for (int fm = 0; fm < 4; ++fm)
+    for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
-        for (int fn = 0; fn < 8; ++fn) {
-            const int r = wm * 32 + fm * 8 + (lane >> 2);
-            const int cc = wn * 64 + fn * 8 + (lane & 3) * 2;
-            *reinterpret_cast<double2*>(out + r * GBM + cc) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+        for (int fn = 0; fn < FN; ++fn) {
+            const int r = wm * 8 * FM + fm * 8 + (lane >> 2);
+            const int cc = wn * 8 * FN + fn * 8 + (lane & 3) * 2;
+            if (!GUARD || (r < wa && cc < wb))  // the finish reads only the valid block
+                *reinterpret_cast<double2*>(out + r * GBM + cc) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
         }
 }
 
-// sum splits in order, scale, mirror into the dense n x n result
+// sum splits in order, scale, mirror into the dense n x n result. One element
+// per thread (blockIdx.y: 256-element slice of the tile) and the split loads
+// issued 8 at a time before the in-order sum: a single-tile Gram (C1 / C2) is
+// otherwise a chain of dependent L2 round trips (26 us at C2)
 __global__ void gram_finish_kernel(const double* part, int npairs, int nsplit, int n, double scale, double* G,
                                    long long ldg) {
     const int p = blockIdx.x;
     int ti, tj;
     pair_of(p, ti, tj);
-    for (int e = threadIdx.x; e < GBM * GBM; e += blockDim.x) {
-        const int r = e / GBM, c = e - r * GBM;
-        const int i = ti * GBM + r, j = tj * GBM + c;
-        if (i >= n || j >= n) continue;
-        double v = 0.0;
-        for (int s = 0; s < nsplit; ++s) v += part[((size_t)s * npairs + p) * (GBM * GBM) + e];
-        v *= scale;
-        if (ti == tj) {
-            if (j <= i) {
-                G[(long long)i * ldg + j] = v;
-                G[(long long)j * ldg + i] = v;
-            }
-        } else {
-            G[(long long)i * ldg + j] = v;
-            G[(long long)j * ldg + i] = v;
-        }
+    const int e = blockIdx.y * 256 + threadIdx.x;
+    const int r = e / GBM, c = e - r * GBM;
+    const int i = ti * GBM + r, j = tj * GBM + c;
+    if (i >= n || j >= n) return;
+    if (ti == tj && j > i) return;
+    double v = 0.0;
+    for (int s0 = 0; s0 < nsplit; s0 += 8) {
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = s0 + u < nsplit ? part[((size_t)(s0 + u) * npairs + p) * (GBM * GBM) + e] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (s0 + u < nsplit) v += t[u];
     }
+    v *= scale;
+    G[(long long)i * ldg + j] = v;
+    G[(long long)j * ldg + i] = v;
 }
 
-// q_t = x_t^T P x_t for RB rows per block; P is ld x ld (zero outside the face)
-template <int RB>
-__global__ void quadform_kernel(const double* X, long long T, int ld, const double* P, double* q) {
-    extern __shared__ __align__(16) double xs[];  // [RB][ld]
+// q_t = x_t^T P x_t for RB rows per block; P is ld x ld (zero outside the
+// face). PS: P staged in shared memory beside the row block. Both stagings
+// are cp.async 16-byte pieces issued all at once (one memory latency per CTA
+// instead of one per loop trip: these panels are latency-bound, C2 28 -> a
+// few us). With tw set, the kernel writes tw_t = psi3(z_t) q_t / T
+// (affine_normal.hpp:174-177) instead of q. Same summation order on both paths.
+template <int RB, bool PS>
+__global__ void quadform_kernel(const double* X, long long T, int ld, const double* P, double* q, const double* z,
+                                double* tw, double c3, double c4, double Tg) {
+    extern __shared__ __align__(16) double xs[];  // [RB][ld] (+ [ld][ld] when PS)
     const long long t0 = (long long)blockIdx.x * RB;
     const int rows = (int)min((long long)RB, T - t0);
-    for (int e = threadIdx.x; e < RB * ld; e += blockDim.x) {
-        const int r = e / ld;
-        xs[e] = r < rows ? X[(t0 + r) * ld + (e - r * ld)] : 0.0;
+    const int hp = ld / 2;  // ld is even: 16-byte pieces per row
+    for (int e = threadIdx.x; e < RB * hp; e += blockDim.x) {
+        const int r = e / hp, cp = e - r * hp;
+        const bool rv = r < rows;
+        cp_async16(xs + r * ld + 2 * cp, X + (t0 + (rv ? r : 0)) * ld + 2 * cp, rv ? 16 : 0);
     }
+    const double* Pr = P;
+    if constexpr (PS) {
+        double* ps = xs + RB * ld;
+        for (int e = threadIdx.x; e < ld * hp; e += blockDim.x) cp_async16(ps + 2 * e, P + 2 * e, 16);
+        Pr = ps;
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     double part[RB];
 #pragma unroll
@@ -182,8 +224,9 @@ __global__ void quadform_kernel(const double* X, long long T, int ld, const doub
         double y[RB];
 #pragma unroll
         for (int r = 0; r < RB; ++r) y[r] = 0.0;
+#pragma unroll 8
         for (int i = 0; i < ld; ++i) {
-            const double pic = P[(long long)i * ld + c];
+            const double pic = PS ? Pr[(long long)i * ld + c] : __ldg(Pr + (long long)i * ld + c);
 #pragma unroll
             for (int r = 0; r < RB; ++r) y[r] = fma(xs[r * ld + i], pic, y[r]);
         }
@@ -202,7 +245,13 @@ __global__ void quadform_kernel(const double* X, long long T, int ld, const doub
     if (threadIdx.x < RB && threadIdx.x < rows) {
         double v = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[threadIdx.x][w];
-        q[t0 + threadIdx.x] = v;
+        const long long t = t0 + threadIdx.x;
+        if (tw) {
+            const double psi3 = -6.0 * c3 + 24.0 * c4 * z[t];
+            tw[t] = psi3 * v / Tg;
+        } else {
+            q[t] = v;
+        }
     }
 }
 
@@ -221,11 +270,11 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
     const int n = (int)ctx->n;
     const int ntile = (n + GBM - 1) / GBM;
     const int npairs = ntile * (ntile + 1) / 2;
-    // split the sample range so that >= 1 wave of CTAs is busy, min 64 rows
-    // (2 chunks) per split: a single-tile Gram (n <= 128, C1/C2) otherwise runs
-    // on one or a few SMs (C1: one CTA over 500 rows, ~65 us per direction)
+    // split the sample range so that >= 1 wave of CTAs is busy, min one chunk
+    // (32 rows) per split: a single-tile Gram (n <= 128, C1/C2) otherwise runs
+    // on one or a few SMs, DMMA-bound per CTA (C2 at 64+ rows per split: 22 us)
     int nsplit = std::max(1, ctx->nsm / npairs);
-    nsplit = (int)std::max<long long>(1, std::min<long long>(nsplit, ctx->T_local / 64));
+    nsplit = (int)std::max<long long>(1, std::min<long long>(nsplit, (ctx->T_local + GBK - 1) / GBK));
     if (npairs >= ctx->nsm) {
         // one CTA per SM: pick the split whose (tiles x splits) work items fill
         // the last wave best (C5: 528 tiles = 3.57 waves -> 7 splits = 24.97
@@ -254,31 +303,56 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
     a.w = w_rows;
     a.T = ctx->T_local;
     a.ld = (int)ctx->ld;
+    a.n = n;
     a.ntile = ntile;
     a.nsplit = nsplit;
     a.part = ctx->gram_part;
     const size_t smem = (size_t)(2 * GST * GBK * GLDS + GST * GBK) * sizeof(double);
-    set_smem_attr(reinterpret_cast<const void*>(&syrk_dmma_kernel), smem);
+    // warp layout: 1 = 8 warps of 32 x 64, weights on the 4 A fragments
+    // (C5 148.7 ms), 0 = the same with the weights on the 8 B fragments
+    // (151.6 ms), 2 = 16 warps of 32 x 32 (151.8 ms: more warps per scheduler
+    // do not raise the DMMA pipe's 81 % active; scripts/gram_ab.py)
+    int var = 1;
+    if (const char* e = std::getenv("MVSK_GRAM_VAR")) var = std::atoi(e);
+    const bool guard = n % GBM != 0;
+    const void* fn = var == 2   ? reinterpret_cast<const void*>(&syrk_dmma_kernel<4, 4, 4, 4, true>)
+                     : var == 0 ? reinterpret_cast<const void*>(&syrk_dmma_kernel<4, 2, 4, 8, false>)
+                     : guard    ? reinterpret_cast<const void*>(&syrk_dmma_kernel<4, 2, 4, 8, true, true>)
+                                : reinterpret_cast<const void*>(&syrk_dmma_kernel<4, 2, 4, 8, true>);
+    const int nthr = var == 2 ? 512 : 256;
+    set_smem_attr(fn, smem);
     ++ctx->launches;
-    syrk_dmma_kernel<<<dim3(npairs, nsplit), GTHREADS, smem, ctx->stream>>>(a);
-    MVSK_CUDA(cudaGetLastError());
+    void* args[] = {&a};
+    MVSK_CUDA(cudaLaunchKernel(fn, dim3(npairs, nsplit), dim3(nthr), args, smem, ctx->stream));
     ++ctx->launches;
-    gram_finish_kernel<<<npairs, 256, 0, ctx->stream>>>(ctx->gram_part, npairs, nsplit, n, scale, G_dev, n);
+    gram_finish_kernel<<<dim3(npairs, GBM * GBM / 256), 256, 0, ctx->stream>>>(ctx->gram_part, npairs, nsplit, n, scale, G_dev, n);
     MVSK_CUDA(cudaGetLastError());
     ctx->phys += 1;
     if (ctx->comm)
         MVSK_NCCL(ncclAllReduce(G_dev, G_dev, (size_t)n * n, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
 }
 
-void run_quadform(mvsk_gpu_ctx* ctx, const double* P_dev, double* q_dev) {
-    constexpr int RB = 16;
+void run_quadform(mvsk_gpu_ctx* ctx, const double* P_dev, double* q_dev, const double* z, double* tw) {
     const long long T = ctx->T_local;
     if (T <= 0) return;
+    const long long ld = ctx->ld;
+    const double c3 = ctx->c.c3, c4 = ctx->c.c4, Tg = (double)ctx->T_global;
+    const int thr = ld <= 128 ? 128 : 256;
+    // 8-row blocks (C1 / C2: 63 / 125 CTAs); P beside them in shared memory
+    // when it fits (n <= ~160, the direct-mode sizes)
+    constexpr int RB = 8;
     const int nb = (int)((T + RB - 1) / RB);
-    const size_t smem = (size_t)RB * ctx->ld * sizeof(double);
-    if (smem > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(&quadform_kernel<RB>), smem);
+    const size_t smem_ps = (size_t)(RB * ld + ld * ld) * sizeof(double);
     ++ctx->launches;
-    quadform_kernel<RB><<<nb, 256, smem, ctx->stream>>>(ctx->X, T, (int)ctx->ld, P_dev, q_dev);
+    if (smem_ps <= ctx->max_smem) {
+        const void* fn = reinterpret_cast<const void*>(&quadform_kernel<RB, true>);
+        if (smem_ps > 48 * 1024) set_smem_attr(fn, smem_ps);
+        quadform_kernel<RB, true><<<nb, thr, smem_ps, ctx->stream>>>(ctx->X, T, (int)ld, P_dev, q_dev, z, tw, c3, c4, Tg);
+    } else {
+        const size_t smem = (size_t)RB * ld * sizeof(double);
+        if (smem > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(&quadform_kernel<RB, false>), smem);
+        quadform_kernel<RB, false><<<nb, thr, smem, ctx->stream>>>(ctx->X, T, (int)ld, P_dev, q_dev, z, tw, c3, c4, Tg);
+    }
     MVSK_CUDA(cudaGetLastError());
 }
 

@@ -393,8 +393,7 @@ void op_third_trace_rows(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const d
     }
     run_graphed(ctx, kGraphThirdTrace, 1, slot, [&] {
         MVSK_CUDA(cudaMemcpyAsync(ctx->pmat, Pf, (size_t)ld * ld * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        run_quadform(ctx, ctx->pmat, ctx->tvec2);
-        run_third_weights(ctx, ctx->slots[slot].z, ctx->tvec2, ctx->tvec);
+        run_quadform(ctx, ctx->pmat, ctx->tvec2, ctx->slots[slot].z, ctx->tvec);  // fused third weights
         PassIO io;
         io.tw = ctx->tvec;
         io.out = ctx->outd;

@@ -36,7 +36,9 @@ void run_psi2(mvsk_gpu_ctx* ctx, const double* z, double* out, long long T);
 void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, double scale);
 
 // q_t = x_t^T P x_t (P: ld x ld, zero outside the face) for this rank's rows
-void run_quadform(mvsk_gpu_ctx* ctx, const double* P_dev, double* q_dev);
+// with z and tw set: writes the third weights psi3(z) q / T to tw instead of q
+void run_quadform(mvsk_gpu_ctx* ctx, const double* P_dev, double* q_dev, const double* z = nullptr,
+                  double* tw = nullptr);
 // tw_t = psi3(z_t) q_t / T with psi3 the third derivative weight
 void run_third_weights(mvsk_gpu_ctx* ctx, const double* z, const double* q, double* tw);
 
