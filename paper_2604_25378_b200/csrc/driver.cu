@@ -142,38 +142,67 @@ Frame householder_frame(const Vec& g) {
 }
 
 // ---- dense partial-pivot LU (the role of Eigen::PartialPivLU, :171) ---------
+// The O(n^3) loops are cloned for AVX2 (picked at load time by the ifunc
+// resolver, SSE2 otherwise). No FMA target: the vector lanes round each
+// multiply and subtract exactly like the scalar code, so both clones give the
+// same bits.
+__attribute__((target_clones("avx2", "default"))) void lu_factor_rows(double* a, long long* perm, long long n) {
+    for (long long i = 0; i < n; ++i) perm[i] = i;
+    for (long long k = 0; k < n; ++k) {
+        long long piv = k;
+        double big = std::abs(a[k * n + k]);
+        for (long long r = k + 1; r < n; ++r)
+            if (std::abs(a[r * n + k]) > big) {
+                big = std::abs(a[r * n + k]);
+                piv = r;
+            }
+        if (big != 0.0) {
+            if (piv != k) {
+                for (long long c = 0; c < n; ++c) std::swap(a[k * n + c], a[piv * n + c]);
+                std::swap(perm[k], perm[piv]);
+            }
+            const double inv = 1.0 / a[k * n + k];
+            for (long long r = k + 1; r < n; ++r) a[r * n + k] *= inv;
+        }
+        for (long long r = k + 1; r < n; ++r) {
+            const double l = a[r * n + k];
+            if (l != 0.0) {
+                double* __restrict__ ar = a + r * n;
+                const double* __restrict__ ak = a + k * n;
+                for (long long c = k + 1; c < n; ++c) ar[c] -= l * ak[c];
+            }
+        }
+    }
+}
+
+// Z = U^-1 L^-1 in pivot column order (see LU::inverse)
+__attribute__((target_clones("avx2", "default"))) void lu_inverse_rows(const double* a, double* Z, long long n) {
+    for (long long i = 0; i < n; ++i) {
+        double* __restrict__ zi = Z + i * n;
+        zi[i] = 1.0;
+        for (long long c = 0; c < i; ++c) {
+            const double l = a[i * n + c];
+            const double* __restrict__ zc = Z + c * n;
+            for (long long j = 0; j <= c; ++j) zi[j] -= l * zc[j];
+        }
+    }
+    for (long long i = n - 1; i >= 0; --i) {
+        double* __restrict__ zi = Z + i * n;
+        for (long long c = i + 1; c < n; ++c) {
+            const double u = a[i * n + c];
+            const double* __restrict__ zc = Z + c * n;
+            for (long long j = 0; j < n; ++j) zi[j] -= u * zc[j];
+        }
+        const double d = a[i * n + i];
+        for (long long j = 0; j < n; ++j) zi[j] /= d;
+    }
+}
+
 struct LU {
     long long n;
     Vec a;
     std::vector<long long> perm;
-    LU(const Vec& M, long long nn) : n(nn), a(M), perm((size_t)nn) {
-        for (long long i = 0; i < n; ++i) perm[(size_t)i] = i;
-        for (long long k = 0; k < n; ++k) {
-            long long piv = k;
-            double big = std::abs(a[(size_t)(k * n + k)]);
-            for (long long r = k + 1; r < n; ++r)
-                if (std::abs(a[(size_t)(r * n + k)]) > big) {
-                    big = std::abs(a[(size_t)(r * n + k)]);
-                    piv = r;
-                }
-            if (big != 0.0) {
-                if (piv != k) {
-                    for (long long c = 0; c < n; ++c) std::swap(a[(size_t)(k * n + c)], a[(size_t)(piv * n + c)]);
-                    std::swap(perm[(size_t)k], perm[(size_t)piv]);
-                }
-                const double inv = 1.0 / a[(size_t)(k * n + k)];
-                for (long long r = k + 1; r < n; ++r) a[(size_t)(r * n + k)] *= inv;
-            }
-            for (long long r = k + 1; r < n; ++r) {
-                const double l = a[(size_t)(r * n + k)];
-                if (l != 0.0) {
-                    double* ar = &a[(size_t)(r * n)];
-                    const double* ak = &a[(size_t)(k * n)];
-                    for (long long c = k + 1; c < n; ++c) ar[c] -= l * ak[c];
-                }
-            }
-        }
-    }
+    LU(const Vec& M, long long nn) : n(nn), a(M), perm((size_t)nn) { lu_factor_rows(a.data(), perm.data(), n); }
     // A^-1, row-major. Row-oriented substitution on the permuted identity: every
     // entry sees exactly the operation sequence of solve(e_j) (same bits), but
     // the inner loops run along contiguous rows. The forward sweep runs in
@@ -182,25 +211,7 @@ struct LU {
     // (n^3/6 instead of n^3/2 multiply-adds).
     Vec inverse() const {
         Vec Z((size_t)(n * n), 0.0);  // columns in pivot order: Z[i][j'] = Y[i][perm[j']]
-        for (long long i = 0; i < n; ++i) {
-            double* zi = &Z[(size_t)(i * n)];
-            zi[i] = 1.0;
-            for (long long c = 0; c < i; ++c) {
-                const double l = a[(size_t)(i * n + c)];
-                const double* zc = &Z[(size_t)(c * n)];
-                for (long long j = 0; j <= c; ++j) zi[j] -= l * zc[j];
-            }
-        }
-        for (long long i = n - 1; i >= 0; --i) {
-            double* zi = &Z[(size_t)(i * n)];
-            for (long long c = i + 1; c < n; ++c) {
-                const double u = a[(size_t)(i * n + c)];
-                const double* zc = &Z[(size_t)(c * n)];
-                for (long long j = 0; j < n; ++j) zi[j] -= u * zc[j];
-            }
-            const double d = a[(size_t)(i * n + i)];
-            for (long long j = 0; j < n; ++j) zi[j] /= d;
-        }
+        lu_inverse_rows(a.data(), Z.data(), n);
         Vec Y((size_t)(n * n));
         for (long long i = 0; i < n; ++i)
             for (long long j = 0; j < n; ++j) Y[(size_t)(i * n + perm[(size_t)j])] = Z[(size_t)(i * n + j)];

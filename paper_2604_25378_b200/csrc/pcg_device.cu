@@ -398,6 +398,7 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
     constexpr int CS = kCcgCS;
     static_assert(LPR * CPL <= M && CPL % 2 == 0 && 32 % LPR == 0, "row layout");
     cgs::cluster_group cluster = cgs::this_cluster();
+    const unsigned long long t_entry = clock64();
     const int crank = (int)cluster.block_rank();
     const int col = blockIdx.x / CS;  // the CG column of this cluster
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -516,10 +517,13 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
     unsigned long long prof_t = clock64();
     int prof_last = -1;
     const bool prof_on = a.prof && crank == 0 && col == 0 && tid == 0;
-    auto prof_mark = [&](int i) {
+    unsigned long long psum[5] = {prof_t - t_entry, 0, 0, 0, 0};  // [0]: staging + cg_init + first lift
+    auto prof_mark = [&](int i) {  // phase sums in registers, written once at exit
         if (prof_on) {
             const unsigned long long now = clock64();
-            if (prof_last >= 0) a.prof[prof_last] += now - prof_t;
+#pragma unroll
+            for (int q = 1; q < 5; ++q)
+                if (prof_last == q) psum[q] += now - prof_t;
             prof_t = now;
             prof_last = i;
         }
@@ -669,7 +673,12 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
         __syncthreads();
     }
     prof_mark(5);
-    if (prof_on) a.prof[6] += (unsigned long long)step;
+    if (prof_on) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) a.prof[q] += psum[q];
+        a.prof[6] += (unsigned long long)step;
+        a.prof[7] += 1;
+    }
     // ---- results to the global CG state (CTA 0 of the cluster)
     if (crank == 0) {
         for (int i = tid; i < mm; i += blockDim.x) {
@@ -1036,8 +1045,10 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
                 std::memset(prof, 0, 8 * sizeof(unsigned long long));
                 std::atexit([] {
                     cudaDeviceSynchronize();
-                    std::fprintf(stderr, "[ccg prof] steps %llu | pass %llu combine %llu cluster %llu cg+lift %llu (cycles)\n",
-                                 prof[6], prof[1], prof[2], prof[3], prof[4]);
+                    std::fprintf(stderr,
+                                 "[ccg prof] launches %llu steps %llu | prologue %llu pass %llu combine %llu cluster %llu "
+                                 "cg+lift %llu (cycles)\n",
+                                 prof[7], prof[6], prof[0], prof[1], prof[2], prof[3], prof[4]);
                 });
             }
             ca.prof = prof;
