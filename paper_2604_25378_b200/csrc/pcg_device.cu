@@ -186,6 +186,19 @@ __global__ void __launch_bounds__(kPT) lift_kernel(const Geo* gp, const double* 
     lift_col(g, E + (size_t)c * ldE, apply_q, row, q, sh);
 }
 
+// lift two source blocks of k columns each in one launch (the third-action
+// pair u = U Q s_p, v = U Q r_p): blocks [0, k) lift E1 into vin1, [k, 2k) E2 into vin2
+__global__ void __launch_bounds__(kPT) lift_pair_kernel(const Geo* gp, const double* E1, const double* E2, int k,
+                                                        double* vin1, double* vin2) {
+    extern __shared__ double q[];
+    __shared__ double sh[32];
+    const Geo g = *gp;
+    const int ldE = g.m - 2;
+    const bool second = (int)blockIdx.x >= k;
+    const int c = second ? (int)blockIdx.x - k : (int)blockIdx.x;
+    lift_col(g, (second ? E2 : E1) + (size_t)c * ldE, true, (second ? vin2 : vin1) + (size_t)c * g.ld, q, sh);
+}
+
 // one capped-CG step per active column, from the HVP rows H (full coordinates)
 __device__ __forceinline__ void cg_step_col(const Geo& g, const CGState& s, double lambda, const double* H,
                                             double* vin, double* t, double* sh) {
@@ -318,6 +331,21 @@ __global__ void accum_rows_kernel(const DirScalars* ds, const double* rows, int 
     }
 }
 
+// the last probe block's accumulation fused with the rhs (below): a += rows in
+// probe order, then rhs = h - coef * a / adiv, elementwise as the two kernels
+__global__ void accum_rhs_kernel(const DirScalars* ds, const double* rows, int k, double* a, const double* h,
+                                 double* rhs) {
+    const int mm = ds->mm;
+    const double adiv = ds->adiv, coef = ds->coef;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mm; i += gridDim.x * blockDim.x) {
+        double v = a[i];
+        for (int p = 0; p < k; ++p) v += rows[(size_t)p * mm + i];
+        a[i] = v;
+        const double ai = adiv > 0 ? v / adiv : v;
+        rhs[i] = h[i] - coef * ai;
+    }
+}
+
 // rhs = h - (||gbar|| / n) a, a averaged over the Hutchinson probes (:236, :239)
 __global__ void rhs_kernel(const DirScalars* ds, const double* h, const double* a, double* rhs) {
     const int mm = ds->mm;
@@ -436,30 +464,51 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
     if constexpr (PANEL) {
         // the CTA's row block -> shared memory by the bulk-copy engine (one
         // 16-byte-aligned copy per row, completion as tx-bytes on stage_bar)
+        // The byte count is armed before the barrier below, so copies issued by
+        // any warp afterwards cannot complete the phase early; every warp
+        // issues a share of the rows (one issuing warp took ~10 us at C4)
         if (tid == 0) {
             mbar_init(&stage_bar, 1);
             fence_mbar_init();
+            mbar_arrive_expect_tx(&stage_bar, (uint32_t)((size_t)nloc * ld * sizeof(double)));
         }
         __syncthreads();
-        if (warp == 0) {
-            if (lane == 0) mbar_arrive_expect_tx(&stage_bar, (uint32_t)((size_t)nloc * ld * sizeof(double)));
-            __syncwarp();
+        {
             const uint64_t pol = policy_evict_last();
-            for (int r = lane; r < nloc; r += 32)
+            for (int r = tid; r < nloc; r += blockDim.x)
                 bulk_g2s(sXp + (size_t)r * lds, a.X + (r0 + r) * (long long)ld, (uint32_t)(ld * sizeof(double)),
                          &stage_bar, pol);
         }
-        for (int i = tid; i < nloc; i += blockDim.x) sZr[i] = __ldg(a.z + r0 + i);
     }
-    for (int i = tid; i < m; i += blockDim.x) {
-        sU[i] = g.vU[i];
-        sIdx[i] = g.idx ? (int)g.idx[i] : i;
+    // every small operand in ONE batch of independent read-only loads (z rows,
+    // U / Q reflectors, face map, Jacobi diagonal, the column's right-hand side
+    // into sT): the separate loops were a chain of dependent global latencies
+    // (~12 us of prologue per launch on C4 faces)
+    const double* rhs_col = a.rhs + (size_t)col * mm;
+    const int nmax = max(max(nloc, M), mm);
+    for (int i = tid; i < nmax; i += blockDim.x) {
+        const double zr = (PANEL && i < nloc) ? __ldg(a.z + r0 + i) : 0.0;
+        const double u = i < m ? __ldg(g.vU + i) : 0.0;
+        const long long ix = (i < m && g.idx) ? __ldg(g.idx + i) : (long long)i;
+        const double q = i < m1 ? __ldg(g.vQ + i) : 0.0;
+        const double j = (i < mm && s.jd) ? __ldg(s.jd + i) : 1.0;
+        const double b = i < mm ? __ldg(rhs_col + i) : 0.0;
+        if (PANEL && i < nloc) sZr[i] = zr;
+        if (i < m) {
+            sU[i] = u;
+            sIdx[i] = (int)ix;
+        }
+        if (i < m1) sQ[i] = q;
+        if (i < mm) {
+            sJ[i] = j;
+            sT[i] = b;
+        }
+        if (i < M) sV[i] = 0.0;
     }
-    for (int i = tid; i < m1; i += blockDim.x) sQ[i] = g.vQ[i];
-    for (int i = tid; i < mm; i += blockDim.x) sJ[i] = s.jd ? s.jd[i] : 1.0;
-    for (int i = tid; i < M; i += blockDim.x) sV[i] = 0.0;
+    const unsigned long long t_loads = clock64();
     if constexpr (PANEL) mbar_wait(&stage_bar, 0u);
     __syncthreads();
+    const unsigned long long t_staged = clock64();
 
     // lift: V = U Q (0, P) (lift_col), warp 0
     auto lift = [&]() {
@@ -481,11 +530,10 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
 
     // ---- cg_init (cg_init_kernel) + the first lift, warp 0
     if (warp == 0) {
-        const double* b = a.rhs + (size_t)col * mm;
         double prz = 0.0, pbb = 0.0;
         for (int i = lane; i < mm; i += 32) {
-            const double r = b[i];
-            const double zz = s.jd ? r / s.jd[i] : r;
+            const double r = sT[i];  // the right-hand side, staged above
+            const double zz = s.jd ? r / sJ[i] : r;
             sX[i] = 0.0;
             sR[i] = r;
             sZ[i] = zz;
@@ -518,6 +566,11 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
     int prof_last = -1;
     const bool prof_on = a.prof && crank == 0 && col == 0 && tid == 0;
     unsigned long long psum[5] = {prof_t - t_entry, 0, 0, 0, 0};  // [0]: staging + cg_init + first lift
+    if (prof_on) {  // prologue parts: loads issued / staging landed / cg_init + lift
+        atomicAdd(a.prof + 8, t_loads - t_entry);
+        atomicAdd(a.prof + 9, t_staged - t_loads);
+        atomicAdd(a.prof + 10, prof_t - t_staged);
+    }
     auto prof_mark = [&](int i) {  // phase sums in registers, written once at exit
         if (prof_on) {
             const unsigned long long now = clock64();
@@ -867,8 +920,8 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     // captured graphs stay valid): narrow faces run their block reductions on
     // two warps instead of sixteen
     const int pt = N <= 128 ? 64 : N <= 512 ? 128 : N <= 2048 ? 256 : kPT;
-    for (const void* fn : {(const void*)lift_kernel, (const void*)cg_step_kernel, (const void*)reduce_kernel,
-                           (const void*)cg_init_kernel})
+    for (const void* fn : {(const void*)lift_kernel, (const void*)lift_pair_kernel, (const void*)cg_step_kernel,
+                           (const void*)reduce_kernel, (const void*)cg_init_kernel})
         set_smem_attr(fn, dsm_max);
     const int nb1 = (int)std::min<long long>(4LL * ctx->nsm, (N + 255) / 256 + 1);
     const Slot& sl = ctx->slots[slot];
@@ -1041,14 +1094,15 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         static unsigned long long* prof = nullptr;  // MVSK_CCG_PROF: per-phase cycle sums, printed at exit
         if (std::getenv("MVSK_CCG_PROF")) {
             if (!prof) {
-                MVSK_CUDA(cudaMallocManaged(&prof, 8 * sizeof(unsigned long long)));
-                std::memset(prof, 0, 8 * sizeof(unsigned long long));
+                MVSK_CUDA(cudaMallocManaged(&prof, 16 * sizeof(unsigned long long)));
+                std::memset(prof, 0, 16 * sizeof(unsigned long long));
                 std::atexit([] {
                     cudaDeviceSynchronize();
                     std::fprintf(stderr,
                                  "[ccg prof] launches %llu steps %llu | prologue %llu pass %llu combine %llu cluster %llu "
-                                 "cg+lift %llu (cycles)\n",
-                                 prof[7], prof[6], prof[0], prof[1], prof[2], prof[3], prof[4]);
+                                 "cg+lift %llu (cycles); prologue = loads %llu + staging wait %llu + init %llu\n",
+                                 prof[7], prof[6], prof[0], prof[1], prof[2], prof[3], prof[4], prof[8], prof[9],
+                                 prof[10]);
                 });
             }
             ca.prof = prof;
@@ -1157,11 +1211,19 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     };
     auto enqueue = [&]() {
         // uploads: parameters, geometry, probes (exact sizes: the graph key has mm)
-        MVSK_CUDA(cudaMemcpyAsync(base + o_dir, hu + o_dir, sizeof(DirDev), cudaMemcpyHostToDevice, st));
-        MVSK_CUDA(cudaMemcpyAsync(vU, HU(o_vU), m * sizeof(double), cudaMemcpyHostToDevice, st));
-        MVSK_CUDA(cudaMemcpyAsync(vQ, HU(o_vQ), m1 * sizeof(double), cudaMemcpyHostToDevice, st));
-        MVSK_CUDA(cudaMemcpyAsync(nu, HU(o_nu), m1 * sizeof(double), cudaMemcpyHostToDevice, st));
-        if (fm.active) MVSK_CUDA(cudaMemcpyAsync(idx, hu + o_idx, m * sizeof(long long), cudaMemcpyHostToDevice, st));
+        if ((size_t)(N - m) * 3 * sizeof(double) <= 16384) {
+            // parameters + U / Q reflectors + nu (+ face map) as ONE copy of the
+            // staged prefix: the slack between the regions is small here
+            const size_t end = fm.active ? o_idx + (size_t)m * sizeof(long long) : o_nu + (size_t)m1 * sizeof(double);
+            MVSK_CUDA(cudaMemcpyAsync(base + o_dir, hu + o_dir, end - o_dir, cudaMemcpyHostToDevice, st));
+        } else {
+            MVSK_CUDA(cudaMemcpyAsync(base + o_dir, hu + o_dir, sizeof(DirDev), cudaMemcpyHostToDevice, st));
+            MVSK_CUDA(cudaMemcpyAsync(vU, HU(o_vU), m * sizeof(double), cudaMemcpyHostToDevice, st));
+            MVSK_CUDA(cudaMemcpyAsync(vQ, HU(o_vQ), m1 * sizeof(double), cudaMemcpyHostToDevice, st));
+            MVSK_CUDA(cudaMemcpyAsync(nu, HU(o_nu), m1 * sizeof(double), cudaMemcpyHostToDevice, st));
+            if (fm.active)
+                MVSK_CUDA(cudaMemcpyAsync(idx, hu + o_idx, m * sizeof(long long), cudaMemcpyHostToDevice, st));
+        }
         // ---- Jacobi diagonal (:197-209): 8 probes through Hop in one batch
         if (jac) {
             MVSK_CUDA(cudaMemcpyAsync(jsrc, HU(o_jsrc), (size_t)kj * mm * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -1184,6 +1246,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         // ---- a: Hutchinson probes or exact trace (:215-237), blocks of K
         // columns, accumulated on the device in probe order
         MVSK_CUDA(cudaMemsetAsync(avec, 0, mm * sizeof(double), st));
+        bool rhs_done = false;
         if (in.has_third) {
             const int P_all = in.unit_probes ? mm : (int)in.probes.size();
             for (int b0 = 0; b0 < P_all; b0 += K) {
@@ -1205,9 +1268,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
                 cg(k, 0, pb);
                 // third_action(U Q s_p, U Q r_p) for the block, one fused pass
                 ++ctx->launches;
-                lift_kernel<<<k, pt, dsm_max, st>>>(gdev, X, true, nullptr, vin);
-                ++ctx->launches;
-                lift_kernel<<<k, pt, dsm_max, st>>>(gdev, pb, true, nullptr, vin2);
+                lift_pair_kernel<<<2 * k, pt, dsm_max, st>>>(gdev, X, pb, k, vin, vin2);
                 MVSK_CUDA(cudaGetLastError());
                 PassIO io;
                 io.vin = vin;
@@ -1221,7 +1282,12 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
                 ++ctx->launches;
                 reduce_kernel<<<k, pt, dsm_max, st>>>(gdev, H, true, rows);
                 ++ctx->launches;
-                accum_rows_kernel<<<nb1, 256, 0, st>>>(dsd, rows, k, avec);
+                if (b0 + K >= P_all) {  // last block: the rhs in the same kernel
+                    accum_rhs_kernel<<<nb1, 256, 0, st>>>(dsd, rows, k, avec, hvec, src);
+                    rhs_done = true;
+                } else {
+                    accum_rows_kernel<<<nb1, 256, 0, st>>>(dsd, rows, k, avec);
+                }
                 MVSK_CUDA(cudaGetLastError());
                 if (!capture && in.unit_probes && deferred.size() + 2 >= (size_t)kMaxDeferred) {
                     // long exact-trace sweeps: settle the loop counts every few blocks
@@ -1231,9 +1297,11 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
             }
         }
         // rhs = h - (||gbar|| / n) a  (:239); a averaged over the Hutchinson probes (:236)
-        ++ctx->launches;
-        rhs_kernel<<<nb1, 256, 0, st>>>(dsd, hvec, avec, src);
-        MVSK_CUDA(cudaGetLastError());
+        if (!rhs_done) {
+            ++ctx->launches;
+            rhs_kernel<<<nb1, 256, 0, st>>>(dsd, hvec, avec, src);
+            MVSK_CUDA(cudaGetLastError());
+        }
         // main CG (:240-241)
         cg(1, 1, src);
         MVSK_CUDA(cudaMemcpyAsync(ws.host_u, X, mm * sizeof(double), cudaMemcpyDeviceToHost, st));

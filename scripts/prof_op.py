@@ -35,6 +35,7 @@ fn = {
     "third8": lambda: gpu.third_action_device(0, Vd.data_ptr(), Vd.data_ptr(), 8, out.data_ptr()),
     "third": lambda: gpu.third_action_device(0, Vd.data_ptr(), Vd[1:].data_ptr(), 1, out.data_ptr()),
     "gram": lambda: gpu.weighted_gram_device(0, G.data_ptr()),
+    "fgrad": lambda: gpu.make_cache_device(0, xd.data_ptr()),
 }[op]
 for _ in range(reps):
     fn()
