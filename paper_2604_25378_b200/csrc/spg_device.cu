@@ -23,11 +23,15 @@
 // kernels for f and the gradient.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "host_ops.hpp"
 #include "oracle_ops.cuh"
+#include "ptx.cuh"
 #include "spg_device.hpp"
 
 namespace mvsk_b200 {
@@ -109,9 +113,9 @@ struct SpgBufs {
     unsigned char* act;  // n
 };
 
-__global__ void __launch_bounds__(kSpgThreads) spg_prep_kernel(SpgState* st, SpgBufs b) {
-    extern __shared__ double u[];
-    __shared__ double bc[2];
+// one trial's step (solver.hpp:131-145): every thread of the block calls it;
+// u: sort scratch (next power of two >= n), bc: 2 broadcast doubles
+__device__ void spg_prep_body(SpgState* st, const SpgBufs& b, double* u, double* bc) {
     const int n = st->n;
     if (threadIdx.x == 0) ++st->trials;
     if (st->bt == 0 && threadIdx.x == 0) {  // L0 from the BB pair (solver.hpp:131-135)
@@ -138,17 +142,20 @@ __global__ void __launch_bounds__(kSpgThreads) spg_prep_kernel(SpgState* st, Spg
     }
 }
 
-__global__ void __launch_bounds__(kSpgThreads) spg_accept_kernel(SpgState* st, SpgBufs b, const double* gp,
-                                                                 const double* fp_sc, cudaGraphConditionalHandle h,
-                                                                 int set_cond) {
+__global__ void __launch_bounds__(kSpgThreads) spg_prep_kernel(SpgState* st, SpgBufs b) {
     extern __shared__ double u[];
-    __shared__ int s_acc, s_change, s_any, s_done;
     __shared__ double bc[2];
+    spg_prep_body(st, b, u, bc);
+}
+
+// Armijo test and the state update of one trial (solver.hpp:146-174): every
+// thread of the block calls it; fp is the trial value, gp its gradient
+__device__ void spg_accept_body(SpgState* st, const SpgBufs& b, const double* gp, double fp, double* u, double* bc) {
+    __shared__ int s_acc, s_change, s_any, s_done;
     const int n = st->n;
     if (threadIdx.x == 0) {
         int acc = 0;
         if (st->eval_flag) {
-            const double fp = fp_sc[0];
             if (fp <= __dadd_rn(st->f, __dmul_rn(1e-4, st->gdp))) {  // Armijo (solver.hpp:146)
                 acc = 1;
                 st->f = fp;
@@ -223,7 +230,222 @@ __global__ void __launch_bounds__(kSpgThreads) spg_accept_kernel(SpgState* st, S
         }
     }
     __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSpgThreads) spg_accept_kernel(SpgState* st, SpgBufs b, const double* gp,
+                                                                 const double* fp_sc, cudaGraphConditionalHandle h,
+                                                                 int set_cond) {
+    extern __shared__ double u[];
+    __shared__ double bc[2];
+    spg_accept_body(st, b, gp, st->eval_flag ? fp_sc[0] : 0.0, u, bc);
     if (set_cond && threadIdx.x == 0) cudaGraphSetConditional(h, st->done ? 0u : 1u);
+}
+
+// ---------------------------------------------------------------------------
+// Cluster-resident preamble for narrow, short panels (ld <= 128 and each
+// 16th of the rows fits a CTA's shared memory: C1 / C2). The whole loop runs
+// in ONE launch of one 16-CTA cluster: every CTA stages its row block once
+// (bulk copies issued by all warps), then per trial
+//   prep (spg_prep_body)     redundantly in every CTA on identical bits
+//   FGRAD at xp              each CTA over its rows: z = <x_t, xp>, the power
+//                            sums and A^T psi'(z) partials; combined through
+//                            distributed shared memory in rank order behind
+//                            one cluster barrier (double-buffered partials)
+//   accept (spg_accept_body) redundantly, so every CTA takes the same branches
+// A trial costs a cluster barrier instead of three kernel boundaries (or a
+// host round trip). f and the gradient are the oracle's (oracle.hpp:58-64,
+// 82-84) with a different summation order than the streaming pass, so the
+// trajectory matches the host loop to rounding, not bitwise.
+// ---------------------------------------------------------------------------
+constexpr int kSpgCS = 16;     // CTAs per cluster (non-portable size)
+constexpr int kSpgCW = 8;      // warps per CTA
+constexpr int kSpgCM = 128;    // max ld
+constexpr int kSpgCP = kSpgCM + 4;  // partial row: ld gradient entries + 3 power sums
+
+struct SpgClusterArgs {
+    SpgState* st;   // global state: initial in, final out (CTA 0)
+    SpgBufs gb;     // global x (in / out), g, act (in)
+    const double* X;
+    const double* mu;
+    long long T;
+    int ld;
+    double c1, c2, c3, c4, Tg, vo;
+};
+
+constexpr size_t spg_cluster_smem_fixed() {
+    return (size_t)(10 * kSpgCM + 2 * kSpgCP + kSpgCW * kSpgCP) * sizeof(double) + kSpgCM + 64;
+}
+
+template <int LPR, int CPL>
+__global__ void __launch_bounds__(kSpgCW * 32, 1) spg_cluster_kernel(const SpgClusterArgs a) {
+    namespace cgs = cooperative_groups;
+    static_assert(LPR * CPL <= kSpgCM && CPL % 2 == 0 && 32 % LPR == 0, "row layout");
+    constexpr int M = kSpgCM, MP = kSpgCP, CS = kSpgCS;
+    cgs::cluster_group cluster = cgs::this_cluster();
+    const int crank = (int)cluster.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ld = a.ld;
+    extern __shared__ __align__(16) double sp_sm[];
+    double* sx = sp_sm;
+    double* sg = sx + M;
+    double* sxp = sg + M;
+    double* sdp = sxp + M;
+    double* sbs = sdp + M;
+    double* sby = sbs + M;
+    double* sy = sby + M;
+    double* su = sy + M;   // sort scratch
+    double* sgp = su + M;  // trial gradient
+    double* smu = sgp + M;
+    double* spart = smu + M;     // [2][MP]
+    double* sW = spart + 2 * MP;  // [warps][MP]
+    unsigned char* sact = reinterpret_cast<unsigned char*>(sW + kSpgCW * MP);
+    const long long T = a.T;
+    const long long r0 = T * crank / CS, r1 = T * (crank + 1) / CS;
+    const int nloc = (int)(r1 - r0);
+    const int lds = ld + 2;  // padded rows: the row groups of a warp on distinct bank groups
+    double* sXp = sp_sm + (spg_cluster_smem_fixed() + 15) / 16 * 2;
+    __shared__ SpgState sst;
+    __shared__ double sbc[4];
+    __shared__ uint64_t stage_bar;
+    if (tid == 0) {
+        mbar_init(&stage_bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(&stage_bar, (uint32_t)((size_t)nloc * ld * sizeof(double)));
+        sst = *a.st;
+    }
+    __syncthreads();
+    {
+        const uint64_t pol = policy_evict_last();
+        for (int r = tid; r < nloc; r += blockDim.x)
+            bulk_g2s(sXp + (size_t)r * lds, a.X + (r0 + r) * (long long)ld, (uint32_t)(ld * sizeof(double)),
+                     &stage_bar, pol);
+    }
+    const int n = sst.n;
+    for (int i = tid; i < M; i += blockDim.x) {
+        const bool in = i < n;
+        const double x = in ? __ldg(a.gb.x + i) : 0.0, g = in ? __ldg(a.gb.g + i) : 0.0;
+        const double mu = in ? __ldg(a.mu + i) : 0.0;
+        const unsigned char ac = in ? a.gb.act[i] : 0;
+        sx[i] = x;
+        sg[i] = g;
+        smu[i] = mu;
+        sact[i] = ac;
+        sxp[i] = 0.0;  // zero past n: the FGRAD row's padding
+    }
+    mbar_wait(&stage_bar, 0u);
+    __syncthreads();
+    const SpgBufs sb{sx, sg, sxp, sdp, sbs, sby, sy, sact};
+
+    constexpr int GPW = 32 / LPR;
+    constexpr int NGC = kSpgCW * GPW;
+    const int sub = lane % LPR;
+    auto colp = [&](int j) { return 2 * ((j >> 1) * LPR + sub) + (j & 1); };
+    int step = 0;
+    while (!sst.done) {
+        spg_prep_body(&sst, sb, su, sbc);
+        __syncthreads();
+        double fp = 0.0;
+        if (sst.eval_flag) {
+            // ---- FGRAD over this CTA's rows at xp (oracle.hpp:58-64, 82-83)
+            double acc[CPL];
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) acc[j] = 0.0;
+            double s2 = 0.0, s3 = 0.0, s4 = 0.0;
+            for (int lb = warp * GPW; lb < nloc; lb += NGC) {  // warp-uniform trip count
+                const int tl = lb + lane / LPR;
+                const bool rv = tl < nloc;
+                const double* xr = sXp + (size_t)(rv ? tl : 0) * lds;
+                double x[CPL];
+#pragma unroll
+                for (int j = 0; j < CPL; j += 2) {
+                    double2 v = make_double2(0.0, 0.0);
+                    if (rv && colp(j) < ld) v = *reinterpret_cast<const double2*>(xr + colp(j));
+                    x[j] = v.x;
+                    x[j + 1] = v.y;
+                }
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int j = 0; j < CPL; j += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(sxp + colp(j));
+                    d0 = fma(x[j], v.x, d0);
+                    d1 = fma(x[j + 1], v.y, d1);
+                }
+                double zt = d0 + d1;
+#pragma unroll
+                for (int o = 1; o < LPR; o <<= 1) zt += __shfl_xor_sync(0xffffffffu, zt, o);
+                const double z2 = zt * zt, z3 = z2 * zt;
+                const double w = rv ? 2.0 * a.c2 * zt - 3.0 * a.c3 * z2 + 4.0 * a.c4 * z3 : 0.0;
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) acc[j] = fma(x[j], w, acc[j]);
+                if (rv && sub == 0) {
+                    s2 += z2;
+                    s3 += z3;
+                    s4 += z2 * z2;
+                }
+            }
+#pragma unroll
+            for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+                s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+                s4 += __shfl_xor_sync(0xffffffffu, s4, o);
+            }
+            if (lane < LPR) {
+#pragma unroll
+                for (int j = 0; j < CPL; ++j)
+                    if (colp(j) < M) sW[warp * MP + colp(j)] = acc[j];
+            }
+            if (lane == 0) {
+                sW[warp * MP + M] = s2;
+                sW[warp * MP + M + 1] = s3;
+                sW[warp * MP + M + 2] = s4;
+            }
+            __syncthreads();
+            double* buf = spart + (step & 1) * MP;
+            for (int e = tid; e < MP; e += blockDim.x) {
+                if (e >= ld && e < M) continue;
+                double v = 0.0;
+#pragma unroll
+                for (int w2 = 0; w2 < kSpgCW; ++w2) v += sW[w2 * MP + e];
+                buf[e] = v;
+            }
+            // ---- cluster combine: every CTA sums the CS partials in rank order
+            cluster.sync();
+            for (int e = tid; e < MP; e += blockDim.x) {
+                if (e >= n && e < M) continue;
+                if (e >= M + 3) continue;
+                double pv[CS];
+#pragma unroll
+                for (int r = 0; r < CS; ++r) pv[r] = cluster.map_shared_rank(buf, r)[e];
+                double v = 0.0;
+#pragma unroll
+                for (int r = 0; r < CS; ++r) v += pv[r];
+                if (e < M)
+                    sgp[e] = -a.c1 * smu[e] + v / a.Tg;  // oracle.hpp:82-84
+                else
+                    sbc[e - M + 1] = v;  // power sums (sbc[0] is the projection's broadcast)
+            }
+            __syncthreads();
+            if (tid == 0) {  // mu'xp in index order, then f (oracle.hpp:62-64)
+                double mux = 0.0;
+                for (int i = 0; i < n; ++i) mux += smu[i] * sxp[i];
+                sbc[0] = a.vo - a.c1 * mux + (a.c2 * sbc[1] - a.c3 * sbc[2] + a.c4 * sbc[3]) / a.Tg;
+            }
+            __syncthreads();
+            fp = sbc[0];
+            ++step;
+        }
+        spg_accept_body(&sst, sb, sgp, fp, su, sbc);
+        __syncthreads();
+    }
+    if (crank == 0) {
+        for (int i = tid; i < n; i += blockDim.x) a.gb.x[i] = sx[i];
+        if (tid == 0) *a.st = sst;
+    }
+    cluster.sync();  // no CTA exits while a peer may still read its partials
 }
 
 __global__ void spg_cond_kernel(const SpgState* st, cudaGraphConditionalHandle h) {
@@ -266,11 +488,18 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
     // host round trip) and the bitwise-faithful sequential reductions make
     // n = 5000 trials slower (C4: 9 ms vs ~5 ms)
     static const bool enabled = std::getenv("MVSK_SPG_GRAPH") != nullptr;
+    static const bool no_cluster = std::getenv("MVSK_NO_SPG_CLUSTER") != nullptr;
     const int n = (int)ctx->n;
-    if (!enabled || n > kSpgMaxN || n < 2 || ctx->zoff_dev) return false;
+    if (n < 2 || ctx->zoff_dev) return false;
+    // narrow short panels: the whole preamble in one cluster launch (default)
+    const long long nloc = (ctx->T_local + kSpgCS - 1) / kSpgCS;
+    const size_t cl_smem = (spg_cluster_smem_fixed() + 15) / 16 * 16 + (size_t)nloc * (ctx->ld + 2) * sizeof(double);
+    const bool cluster_ok = !no_cluster && ctx->nranks == 1 && ctx->ld <= kSpgCM &&  // no exchange at one rank
+                            ctx->T_local >= kSpgCS && cl_smem <= ctx->max_smem;
+    if (!cluster_ok && (!enabled || n > kSpgMaxN)) return false;
     if (!ctx->spg) ctx->spg = new SpgWorkspace();
     SpgWorkspace& ws = *ctx->spg;
-    if (ws.broken) return false;
+    if (ws.broken && !cluster_ok) return false;
     const size_t ld = (size_t)ctx->ld;
     size_t off = 0;
     const size_t o_st = carve_off(off, sizeof(SpgState));
@@ -321,6 +550,54 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
     MVSK_CUDA(cudaMemsetAsync(b.xp, 0, ld * sizeof(double), sm));  // zero padding of the FGRAD row
 
     Slot& sl = ctx->slots[slot];
+    if (cluster_ok) {
+        SpgClusterArgs ca{};
+        ca.st = st;
+        ca.gb = b;
+        ca.X = ctx->X;
+        ca.mu = ctx->mu_dev;
+        ca.T = ctx->T_local;
+        ca.ld = (int)ld;
+        ca.c1 = ctx->c.c1;
+        ca.c2 = ctx->c.c2;
+        ca.c3 = ctx->c.c3;
+        ca.c4 = ctx->c.c4;
+        ca.Tg = (double)ctx->T_global;
+        ca.vo = ctx->value_offset;
+        const void* fn = ld <= 64 ? (const void*)&spg_cluster_kernel<4, 16> : (const void*)&spg_cluster_kernel<8, 16>;
+        set_smem_attr(fn, cl_smem);
+        MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kSpgCS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(kSpgCS);
+        cfg.blockDim = dim3(kSpgCW * 32);
+        cfg.dynamicSmemBytes = cl_smem;
+        cfg.stream = sm;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        void* args[] = {&ca};
+        ++ctx->launches;
+        MVSK_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+        MVSK_CUDA(cudaMemcpyAsync(&hs, st, sizeof(SpgState), cudaMemcpyDeviceToHost, sm));
+        MVSK_CUDA(cudaMemcpyAsync(x.data(), b.x, n * sizeof(double), cudaMemcpyDeviceToHost, sm));
+        MVSK_CUDA(cudaStreamSynchronize(sm));
+        // a forward pass per evaluated trial, the memoised transpose per accepted one
+        // (oracle.hpp:79-90), one physical pass per evaluation
+        ctx->fwd += (uint64_t)hs.evals;
+        ctx->tr += (uint64_t)hs.accepts;
+        ctx->phys += (uint64_t)hs.evals;
+        static const bool prof = std::getenv("MVSK_PROFILE") != nullptr;
+        if (prof) std::fprintf(stderr, "[spg cluster] trials %d evals %d steps %d\n", hs.trials, hs.evals, hs.steps);
+        sl.valid = false;
+        sl.g_host_valid = false;
+        sl.scalars_host_valid = false;
+        steps_out = hs.steps;
+        return true;
+    }
     PassIO io;
     io.vin = b.xp;
     io.slot = slot;

@@ -409,24 +409,13 @@ def test_compact_faces_match_cpu_and_index_maps():
     assert float(np.max(np.abs(xi - xg))) <= 1e-6
 
 
-@pytest.mark.parametrize("name,kappa", [("C2", 1000.0), ("C3", 1.0)])
-def test_device_spg_preamble_is_bitwise_the_host_loop(name, kappa):
-    """The identification preamble as one device graph (spg_device.cu, opt-in
-    via MVSK_SPG_GRAPH) runs the host loop's arithmetic in the host loop's order
-    (sequential dots and projection sums, no contraction), so the whole
-    large-preset solve is bitwise identical with the host-driven preamble,
-    including the pass counts (the device variant runs in a subprocess because
-    the switch is read once)."""
+def _solve_subprocess(name, kappa, env_extra, eps=None):
+    """A large-preset solve in a fresh process (the preamble switches are read
+    once per process): x and f as hex, counts, and the profile line."""
     import json
     import os
     import subprocess
     import sys
-    from paper_2604_25378_b200.datagen import make_panel
-    from paper_2604_25378_b200.gpu_oracle import preset
-    A, mu, c = make_panel(name, seed=11, kappa=kappa)
-    cfg = preset("large")
-    cfg.has_max_elapsed = 0
-    xg, rg = _gpu(A, mu, c).solve(cfg)  # host-driven preamble (the default)
     code = (
         "import json, sys\n"
         "sys.path.insert(0, %r)\n"
@@ -434,18 +423,60 @@ def test_device_spg_preamble_is_bitwise_the_host_loop(name, kappa):
         "from paper_2604_25378_b200.gpu_oracle import GpuOracle, preset\n"
         "A, mu, c = make_panel(%r, seed=11, kappa=%r)\n"
         "cfg = preset('large'); cfg.has_max_elapsed = 0\n"
+        "if %r is not None: cfg.epsilon = %r\n"
         "x, r = GpuOracle(A, mu, c).solve(cfg)\n"
-        "print(json.dumps({'x': x.hex() if hasattr(x, 'hex') else None, 'xs': [float(v).hex() for v in x],"
+        "print(json.dumps({'xs': [float(v).hex() for v in x], 'status': r.status,"
         " 'it': r.iterations, 'ident': r.identification_steps, 'passes': r.oracle_passes,"
         " 'phys': r.physical_passes, 'f': float(r.f_star).hex()}))\n"
-    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), name, kappa)
-    env = dict(os.environ, MVSK_SPG_GRAPH="1", MVSK_PROFILE="1")
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), name, kappa, eps, eps)
+    env = dict(os.environ, MVSK_PROFILE="1", **env_extra)
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600, check=True)
-    ref = json.loads(out.stdout.strip().splitlines()[-1])
-    spg_ms = float(out.stderr.split("| spg ")[-1].split(" ms")[0])
-    assert spg_ms > 0.0, out.stderr  # the device preamble ran
-    assert [float(v).hex() for v in xg] == ref["xs"]
-    assert float(rg.f_star).hex() == ref["f"]
-    assert (rg.iterations, rg.identification_steps, rg.oracle_passes, rg.physical_passes) == \
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    res["spg_ms"] = float(out.stderr.split("| spg ")[-1].split(" ms")[0])
+    return res
+
+
+@pytest.mark.parametrize("name,kappa", [("C2", 1000.0), ("C3", 1.0)])
+def test_device_spg_preamble_is_bitwise_the_host_loop(name, kappa):
+    """The identification preamble as one device graph (spg_device.cu, opt-in
+    via MVSK_SPG_GRAPH) runs the host loop's arithmetic in the host loop's order
+    (sequential dots and projection sums, no contraction), so the whole
+    large-preset solve is bitwise identical with the host-driven preamble,
+    including the pass counts. Both runs switch the cluster preamble off."""
+    host = _solve_subprocess(name, kappa, {"MVSK_NO_SPG_CLUSTER": "1"})
+    ref = _solve_subprocess(name, kappa, {"MVSK_NO_SPG_CLUSTER": "1", "MVSK_SPG_GRAPH": "1"})
+    assert ref["spg_ms"] > 0.02  # the device preamble ran (the host loop's profile reads ~0.00x ms)
+    assert host["xs"] == ref["xs"]
+    assert host["f"] == ref["f"]
+    assert (host["it"], host["ident"], host["passes"], host["phys"]) == \
         (ref["it"], ref["ident"], ref["passes"], ref["phys"])
-    assert rg.identification_steps > 0
+    assert host["ident"] > 0
+
+
+@pytest.mark.parametrize("name,kappa", [("C1", 1.0), ("C2", 1.0), ("C2", 100.0), ("C2", 1000.0)])
+def test_cluster_spg_preamble_matches_the_host_loop(name, kappa):
+    """The cluster-resident preamble (one launch, f and the gradient summed in
+    its own order) ends the large-preset solve at the host loop's solution.
+    Its trajectory differs by rounding, so the bar is test_config_solve_parity's
+    at epsilon = 1e-10: same status and active set, f to 1e-12, x to 1e-8 -
+    or, where an epsilon-solution is not determined that finely, the same
+    active set and x to 1e-8 with both runs driven to 1e-12."""
+    from paper_2604_25378_b200.gpu_oracle import preset
+    tau = preset("large").tau
+    host = _solve_subprocess(name, kappa, {"MVSK_NO_SPG_CLUSTER": "1"}, eps=1e-10)
+    clus = _solve_subprocess(name, kappa, {}, eps=1e-10)
+    assert clus["spg_ms"] > 0.02 > host["spg_ms"]  # the device preamble ran only in the default run
+    assert clus["ident"] > 0
+    assert clus["status"] == host["status"]
+    xh = np.array([float.fromhex(v) for v in host["xs"]])
+    xc = np.array([float.fromhex(v) for v in clus["xs"]])
+    assert _active(xh, tau) == _active(xc, tau)
+    fh, fc = float.fromhex(host["f"]), float.fromhex(clus["f"])
+    assert abs(fh - fc) <= 1e-12 * (1 + abs(fh))
+    if float(np.max(np.abs(xh - xc))) > 1e-8:
+        host = _solve_subprocess(name, kappa, {"MVSK_NO_SPG_CLUSTER": "1"}, eps=1e-12)
+        clus = _solve_subprocess(name, kappa, {}, eps=1e-12)
+        xh = np.array([float.fromhex(v) for v in host["xs"]])
+        xc = np.array([float.fromhex(v) for v in clus["xs"]])
+        assert _active(xh, tau) == _active(xc, tau)
+        assert float(np.max(np.abs(xh - xc))) <= 1e-8
