@@ -102,6 +102,104 @@ __device__ void project_slice_dev(const double* v, int n, double tau, double mas
     __syncthreads();
 }
 
+// ---- order-free variants for the cluster-resident preamble (n <= 128): the
+// dots as warp-0 reductions and the projection's running sums as a warp scan
+// (fixed orders, so every CTA of the cluster gets the same bits; not the host
+// loop's sequential order)
+__device__ __forceinline__ double wdot(const double* a, const double* b, int n) {  // warp 0; lane 0's value
+    double s = 0.0;
+    for (int i = threadIdx.x & 31; i < n; i += 32) s += a[i] * b[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// the projection of project_slice_dev for n <= 128, in warp 0: the 128 padded
+// values sorted in registers (bitonic network, four per lane: in-lane swaps
+// for strides < 4, shuffles above), the running sums as a warp scan
+__device__ void project_slice_fast(const double* v, int n, double tau, double mass, double* out, double* u,
+                                   double* bcast) {
+    (void)u;
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        double e[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int k = 4 * l + j;
+            e[j] = k < n ? v[k] - tau : -INFINITY;
+        }
+#pragma unroll
+        for (int size = 2; size <= 128; size <<= 1) {
+#pragma unroll
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                if (stride >= 4) {
+                    const bool lower = (l & (stride >> 2)) == 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const bool desc = ((4 * l + j) & size) == 0;
+                        const double w = __shfl_xor_sync(0xffffffffu, e[j], stride >> 2);
+                        // the lower index keeps the larger value in a descending block
+                        e[j] = (lower == desc) ? fmax(e[j], w) : fmin(e[j], w);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if ((j & stride) == 0) {
+                            const int jj = j ^ stride;
+                            const bool desc = ((4 * l + j) & size) == 0;
+                            const double a0 = e[j], a1 = e[jj];
+                            if (desc ? (a0 < a1) : (a0 > a1)) {
+                                e[j] = a1;
+                                e[jj] = a0;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        const double s = mass - (double)n * tau;
+        double p[4];
+        double run = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            run += (4 * l + j) < n ? e[j] : 0.0;
+            p[j] = run;
+        }
+        double inc = run;  // inclusive scan of the lane totals
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (l >= o) inc += t;
+        }
+        const double excl = inc - run;
+        int kb = -1;
+        double cb = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int k = 4 * l + j;
+            if (k < n) {
+                const double cand = (excl + p[j] - s) / (double)(k + 1);
+                if (e[j] > cand) {
+                    kb = k;
+                    cb = cand;
+                }
+            }
+        }
+        int kmax = kb;  // the last support index: theta is its candidate
+#pragma unroll
+        for (int o = 16; o; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+        if (kmax < 0) {
+            if (l == 0) *bcast = 0.0;
+        } else if (kb == kmax) {
+            *bcast = cb;
+        }
+    }
+    __syncthreads();
+    const double theta = *bcast;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = fmax(v[i] - tau - theta, 0.0) + tau;
+    __syncthreads();
+}
+
 struct SpgBufs {
     double* x;    // n, current iterate
     double* g;    // n, gradient at x
@@ -114,11 +212,24 @@ struct SpgBufs {
 };
 
 // one trial's step (solver.hpp:131-145): every thread of the block calls it;
-// u: sort scratch (next power of two >= n), bc: 2 broadcast doubles
+// u: sort scratch (next power of two >= n), bc: 2 broadcast doubles. FAST: the
+// order-free reductions above (cluster preamble, n <= 128)
+template <bool FAST>
 __device__ void spg_prep_body(SpgState* st, const SpgBufs& b, double* u, double* bc) {
     const int n = st->n;
     if (threadIdx.x == 0) ++st->trials;
-    if (st->bt == 0 && threadIdx.x == 0) {  // L0 from the BB pair (solver.hpp:131-135)
+    if constexpr (FAST) {
+        if (st->bt == 0 && threadIdx.x < 32) {  // L0 from the BB pair (solver.hpp:131-135)
+            double L0 = st->L;
+            if (st->have_bb) {
+                const double sy = wdot(b.bbs, b.bby, n), ss = wdot(b.bbs, b.bbs, n);
+                L0 = (ss > 0 && sy > 0) ? sy / ss : st->L;
+                L0 = fmin(fmax(L0, 1e-2), 1e12);
+            }
+            __syncwarp();
+            if (threadIdx.x == 0) st->Lk = L0;
+        }
+    } else if (st->bt == 0 && threadIdx.x == 0) {  // L0 from the BB pair (solver.hpp:131-135)
         double L0 = st->L;
         if (st->have_bb) {
             const double sy = sdot(b.bbs, b.bby, n), ss = sdot(b.bbs, b.bbs, n);
@@ -131,25 +242,31 @@ __device__ void spg_prep_body(SpgState* st, const SpgBufs& b, double* u, double*
     const double Lk = st->Lk;
     for (int i = threadIdx.x; i < n; i += blockDim.x) b.y[i] = b.x[i] - b.g[i] / Lk;
     __syncthreads();
-    project_slice_dev(b.y, n, st->tau, 1.0, b.xp, u, &bc[0]);
+    if constexpr (FAST)
+        project_slice_fast(b.y, n, st->tau, 1.0, b.xp, u, &bc[0]);
+    else
+        project_slice_dev(b.y, n, st->tau, 1.0, b.xp, u, &bc[0]);
     for (int i = threadIdx.x; i < n; i += blockDim.x) b.dp[i] = b.xp[i] - b.x[i];
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const double gdp = sdot(b.g, b.dp, n);
-        st->gdp = gdp;
-        st->eval_flag = gdp < 0 ? 1 : 0;
-        if (gdp < 0) ++st->evals;
+    if (FAST ? threadIdx.x < 32 : threadIdx.x == 0) {
+        const double gdp = FAST ? wdot(b.g, b.dp, n) : sdot(b.g, b.dp, n);
+        if (threadIdx.x == 0) {
+            st->gdp = gdp;
+            st->eval_flag = gdp < 0 ? 1 : 0;
+            if (gdp < 0) ++st->evals;
+        }
     }
 }
 
 __global__ void __launch_bounds__(kSpgThreads) spg_prep_kernel(SpgState* st, SpgBufs b) {
     extern __shared__ double u[];
     __shared__ double bc[2];
-    spg_prep_body(st, b, u, bc);
+    spg_prep_body<false>(st, b, u, bc);
 }
 
 // Armijo test and the state update of one trial (solver.hpp:146-174): every
 // thread of the block calls it; fp is the trial value, gp its gradient
+template <bool FAST>
 __device__ void spg_accept_body(SpgState* st, const SpgBufs& b, const double* gp, double fp, double* u, double* bc) {
     __shared__ int s_acc, s_change, s_any, s_done;
     const int n = st->n;
@@ -218,14 +335,28 @@ __device__ void spg_accept_body(SpgState* st, const SpgBufs& b, const double* gp
         if (!s_done && st->eps_stop > 0 && st->steps % 10 == 0) {
             for (int i = threadIdx.x; i < n; i += blockDim.x) b.y[i] = b.x[i] - b.g[i];
             __syncthreads();
-            project_slice_dev(b.y, n, st->tau, 1.0, b.dp, u, &bc[0]);
-            if (threadIdx.x == 0) {
-                double s = 0.0;
-                for (int i = 0; i < n; ++i) {
-                    const double d = b.x[i] - b.dp[i];
-                    s = __dadd_rn(s, __dmul_rn(d, d));
+            if constexpr (FAST) {
+                project_slice_fast(b.y, n, st->tau, 1.0, b.dp, u, &bc[0]);
+                if (threadIdx.x < 32) {
+                    double s = 0.0;
+                    for (int i = threadIdx.x; i < n; i += 32) {
+                        const double d = b.x[i] - b.dp[i];
+                        s += d * d;
+                    }
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                    if (threadIdx.x == 0 && sqrt(s) <= st->eps_stop) st->done = 1;
                 }
-                if (sqrt(s) <= st->eps_stop) st->done = 1;
+            } else {
+                project_slice_dev(b.y, n, st->tau, 1.0, b.dp, u, &bc[0]);
+                if (threadIdx.x == 0) {
+                    double s = 0.0;
+                    for (int i = 0; i < n; ++i) {
+                        const double d = b.x[i] - b.dp[i];
+                        s = __dadd_rn(s, __dmul_rn(d, d));
+                    }
+                    if (sqrt(s) <= st->eps_stop) st->done = 1;
+                }
             }
         }
     }
@@ -237,7 +368,7 @@ __global__ void __launch_bounds__(kSpgThreads) spg_accept_kernel(SpgState* st, S
                                                                  int set_cond) {
     extern __shared__ double u[];
     __shared__ double bc[2];
-    spg_accept_body(st, b, gp, st->eval_flag ? fp_sc[0] : 0.0, u, bc);
+    spg_accept_body<false>(st, b, gp, st->eval_flag ? fp_sc[0] : 0.0, u, bc);
     if (set_cond && threadIdx.x == 0) cudaGraphSetConditional(h, st->done ? 0u : 1u);
 }
 
@@ -270,6 +401,7 @@ struct SpgClusterArgs {
     long long T;
     int ld;
     double c1, c2, c3, c4, Tg, vo;
+    unsigned long long* prof;  // timing studies (MVSK_SPG_PROF): prep / pass / accept cycle sums of CTA 0
 };
 
 constexpr size_t spg_cluster_smem_fixed() {
@@ -341,9 +473,19 @@ __global__ void __launch_bounds__(kSpgCW * 32, 1) spg_cluster_kernel(const SpgCl
     const int sub = lane % LPR;
     auto colp = [&](int j) { return 2 * ((j >> 1) * LPR + sub) + (j & 1); };
     int step = 0;
+    const bool prof_on = a.prof && crank == 0 && tid == 0;
+    unsigned long long pt[3] = {0, 0, 0}, tc = clock64();
+    auto mark = [&](int i) {
+        if (prof_on) {
+            const unsigned long long now = clock64();
+            pt[i] += now - tc;
+            tc = now;
+        }
+    };
     while (!sst.done) {
-        spg_prep_body(&sst, sb, su, sbc);
+        spg_prep_body<true>(&sst, sb, su, sbc);
         __syncthreads();
+        mark(0);
         double fp = 0.0;
         if (sst.eval_flag) {
             // ---- FGRAD over this CTA's rows at xp (oracle.hpp:58-64, 82-83)
@@ -429,18 +571,21 @@ __global__ void __launch_bounds__(kSpgCW * 32, 1) spg_cluster_kernel(const SpgCl
                     sbc[e - M + 1] = v;  // power sums (sbc[0] is the projection's broadcast)
             }
             __syncthreads();
-            if (tid == 0) {  // mu'xp in index order, then f (oracle.hpp:62-64)
-                double mux = 0.0;
-                for (int i = 0; i < n; ++i) mux += smu[i] * sxp[i];
-                sbc[0] = a.vo - a.c1 * mux + (a.c2 * sbc[1] - a.c3 * sbc[2] + a.c4 * sbc[3]) / a.Tg;
+            if (tid < 32) {  // mu'xp (fixed-order warp reduction), then f (oracle.hpp:62-64)
+                const double mux = wdot(smu, sxp, n);
+                if (tid == 0) sbc[0] = a.vo - a.c1 * mux + (a.c2 * sbc[1] - a.c3 * sbc[2] + a.c4 * sbc[3]) / a.Tg;
             }
             __syncthreads();
             fp = sbc[0];
             ++step;
         }
-        spg_accept_body(&sst, sb, sgp, fp, su, sbc);
+        mark(1);
+        spg_accept_body<true>(&sst, sb, sgp, fp, su, sbc);
         __syncthreads();
+        mark(2);
     }
+    if (prof_on)
+        for (int i = 0; i < 3; ++i) a.prof[i] += pt[i];
     if (crank == 0) {
         for (int i = tid; i < n; i += blockDim.x) a.gb.x[i] = sx[i];
         if (tid == 0) *a.st = sst;
@@ -564,6 +709,19 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
         ca.c4 = ctx->c.c4;
         ca.Tg = (double)ctx->T_global;
         ca.vo = ctx->value_offset;
+        static unsigned long long* prof = nullptr;  // MVSK_SPG_PROF: cycle sums, printed at exit
+        if (std::getenv("MVSK_SPG_PROF")) {
+            if (!prof) {
+                MVSK_CUDA(cudaMallocManaged(&prof, 4 * sizeof(unsigned long long)));
+                std::memset(prof, 0, 4 * sizeof(unsigned long long));
+                std::atexit([] {
+                    cudaDeviceSynchronize();
+                    std::fprintf(stderr, "[spg prof] prep %llu pass %llu accept %llu (cycles)\n", prof[0], prof[1],
+                                 prof[2]);
+                });
+            }
+            ca.prof = prof;
+        }
         const void* fn = ld <= 64 ? (const void*)&spg_cluster_kernel<4, 16> : (const void*)&spg_cluster_kernel<8, 16>;
         set_smem_attr(fn, cl_smem);
         MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -590,8 +748,8 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
         ctx->fwd += (uint64_t)hs.evals;
         ctx->tr += (uint64_t)hs.accepts;
         ctx->phys += (uint64_t)hs.evals;
-        static const bool prof = std::getenv("MVSK_PROFILE") != nullptr;
-        if (prof) std::fprintf(stderr, "[spg cluster] trials %d evals %d steps %d\n", hs.trials, hs.evals, hs.steps);
+        static const bool verbose = std::getenv("MVSK_PROFILE") != nullptr;
+        if (verbose) std::fprintf(stderr, "[spg cluster] trials %d evals %d steps %d\n", hs.trials, hs.evals, hs.steps);
         sl.valid = false;
         sl.g_host_valid = false;
         sl.scalars_host_valid = false;
