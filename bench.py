@@ -127,7 +127,7 @@ def cpu_hvp_rate(A_sample: np.ndarray, mu, c, T_full: int, threads: int, reps: i
 
 def solve_leg():
     """Full YAND solves (solver.hpp:195) through the C-ABI on BASELINE configs
-    2-4, GPU wall time (lower median of 3 after a warm-up; C4: 1 run) next to the
+    1-4 (config 2 at kappa 1 and 1000), GPU wall time (lower median of 3 after a warm-up; C4: 1 run) next to the
     CPU oracle restatement (1 thread, reference-faithful; C4 ~2.3 s since its
     face passes stream only the free columns). max_elapsed is disabled on both
     sides so both do the same work."""
@@ -135,7 +135,9 @@ def solve_leg():
     from paper_2604_25378_b200.datagen import crra, make_panel
     from paper_2604_25378_b200.gpu_oracle import GpuOracle, preset
     out = []
-    for name, kappa, mode, gamma, reps, cpu in (("C2", 1.0, "small", None, 3, True), ("C2", 1.0, "large", None, 3, True),
+    for name, kappa, mode, gamma, reps, cpu in (("C1", 1.0, "small", None, 3, True),
+                                                ("C2", 1.0, "small", None, 3, True), ("C2", 1.0, "large", None, 3, True),
+                                                ("C2", 1000.0, "large", None, 3, True),
                                                 ("C3", 1.0, "large", 5.0, 3, True), ("C3", 1.0, "large", 20.0, 3, True),
                                                 ("C4", 1.0, "large", None, 1, True)):
         A, mu, c = make_panel(name, seed=11, kappa=kappa)
@@ -151,7 +153,7 @@ def solve_leg():
             x, rep = g.solve(cfg)
             ts.append(time.perf_counter() - t0)
         ts.sort()
-        row = {"config": name, "n": A.shape[1], "T": A.shape[0], "preset": mode, "gamma": gamma or 10.0,
+        row = {"config": name, "n": A.shape[1], "T": A.shape[0], "preset": mode, "gamma": gamma or 10.0, "kappa": kappa,
                "gpu_s": ts[(len(ts) - 1) // 2], "status": int(rep.status), "iterations": rep.iterations,
                "kkt": rep.kkt_residual, "physical_passes": int(rep.physical_passes),
                "logical_passes": int(rep.oracle_passes)}
