@@ -162,7 +162,13 @@ def solve_leg():
             cc.has_max_elapsed = 0
             t0 = time.perf_counter()
             xc, rc = po.solve(A, mu, c, cc)
-            row.update(cpu_s=time.perf_counter() - t0, cpu_status=int(rc.status), df=abs(rc.f_star - rep.f_star))
+            row.update(cpu_s=time.perf_counter() - t0, cpu_status=int(rc.status), df=abs(rc.f_star - rep.f_star),
+                       cpu_iterations=rc.iterations)
+            # iteration counts are rounding-chaotic on both sides (the CPU oracle
+            # with 2 threads moves them as much: scripts/iter_survey.py), so the
+            # per-iteration times are the comparable pair
+            row["gpu_ms_per_iter"] = 1e3 * row["gpu_s"] / max(1, rep.iterations)
+            row["cpu_ms_per_iter"] = 1e3 * row["cpu_s"] / max(1, rc.iterations)
         if name == "C4":
             # BASELINE config 4's return-floor sweep: 5 floors between the
             # min-variance and max-mean means, c1 calibrated per floor
