@@ -592,6 +592,60 @@ std::mutex g_attr_mu;
 
 // cudaFuncSetAttribute once per (device, kernel, size): a driver call, not free,
 // and per-device (one process may drive several GPUs)
+static bool cluster_fits_query(const void* fn, int cs, int threads, size_t smem);
+
+// whether at least one cluster of `cs` CTAs x `threads` with `smem` bytes of
+// dynamic shared memory can be resident (non-portable sizes need the opt-in
+// attribute; MIG / MPS partitions may not fit one): the cluster-resident
+// kernels fall back to their launch-per-step paths when it cannot
+bool cluster_fits(const void* fn, int cs, int threads, size_t smem) {
+    struct Entry {
+        int dev;
+        const void* fn;
+        int cs, threads;
+        size_t smem;
+        bool ok;
+    };
+    static std::vector<Entry> seen;  // answers cached per device / kernel / shape
+    static std::mutex mu;
+    int dev = 0;
+    MVSK_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const Entry& e : seen)
+            if (e.dev == dev && e.fn == fn && e.cs == cs && e.threads == threads && e.smem == smem) return e.ok;
+    }
+    const bool ok = cluster_fits_query(fn, cs, threads, smem);
+    std::lock_guard<std::mutex> lk(mu);
+    seen.push_back({dev, fn, cs, threads, smem, ok});
+    return ok;
+}
+
+static bool cluster_fits_query(const void* fn, int cs, int threads, size_t smem) {
+    if (cs > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    set_smem_attr(fn, smem);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int maxcl = 0;
+    if (cudaOccupancyMaxActiveClusters(&maxcl, fn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return maxcl > 0;
+}
+
 void set_smem_attr(const void* fn, size_t smem) {
     struct Entry {
         int dev;

@@ -44,6 +44,7 @@ void run_third_weights(mvsk_gpu_ctx* ctx, const double* z, const double* q, doub
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size)
 void set_smem_attr(const void* fn, size_t smem);
+bool cluster_fits(const void* fn, int cs, int threads, size_t smem);
 
 // device scratch sizing (grows workspaces on demand)
 void ensure_host_staging(mvsk_gpu_ctx* ctx, size_t elems);

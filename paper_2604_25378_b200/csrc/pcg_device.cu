@@ -1077,7 +1077,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
         smem += panel;
         const void* fn =
             ld <= 64 ? (const void*)&cluster_cg_kernel<4, 16, true> : (const void*)&cluster_cg_kernel<8, 16, true>;
-        set_smem_attr(fn, smem);
+        if (!cluster_fits(fn, CS, kCcgWarps * 32, smem)) return false;
         MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         CcgArgs ca{};
         ca.sp = spd;

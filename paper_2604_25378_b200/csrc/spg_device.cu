@@ -639,8 +639,10 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
     // narrow short panels: the whole preamble in one cluster launch (default)
     const long long nloc = (ctx->T_local + kSpgCS - 1) / kSpgCS;
     const size_t cl_smem = (spg_cluster_smem_fixed() + 15) / 16 * 16 + (size_t)nloc * (ctx->ld + 2) * sizeof(double);
+    const void* cl_fn = ctx->ld <= 64 ? (const void*)&spg_cluster_kernel<4, 16> : (const void*)&spg_cluster_kernel<8, 16>;
     const bool cluster_ok = !no_cluster && ctx->nranks == 1 && ctx->ld <= kSpgCM &&  // no exchange at one rank
-                            ctx->T_local >= kSpgCS && cl_smem <= ctx->max_smem;
+                            ctx->T_local >= kSpgCS && cl_smem <= ctx->max_smem &&
+                            cluster_fits(cl_fn, kSpgCS, kSpgCW * 32, cl_smem);
     if (!cluster_ok && (!enabled || n > kSpgMaxN)) return false;
     if (!ctx->spg) ctx->spg = new SpgWorkspace();
     SpgWorkspace& ws = *ctx->spg;
@@ -722,9 +724,7 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
             }
             ca.prof = prof;
         }
-        const void* fn = ld <= 64 ? (const void*)&spg_cluster_kernel<4, 16> : (const void*)&spg_cluster_kernel<8, 16>;
-        set_smem_attr(fn, cl_smem);
-        MVSK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        const void* fn = cl_fn;  // attributes set by cluster_fits
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
