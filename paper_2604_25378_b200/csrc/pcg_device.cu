@@ -461,6 +461,7 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
     const int lds = ld + 2;
     double* sZr = sXp + (size_t)nloc * lds;
     __shared__ uint64_t stage_bar;
+    __shared__ double sCq;  // Q.U(+1) = sum_j Q_j U_{j+1}, fixed per direction
     if constexpr (PANEL) {
         // the CTA's row block -> shared memory by the bulk-copy engine (one
         // 16-byte-aligned copy per row, completion as tx-bytes on stage_bar)
@@ -530,6 +531,10 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
 
     // ---- cg_init (cg_init_kernel) + the first lift, warp 0
     if (warp == 0) {
+        double cq = 0.0;
+        for (int i = lane; i < m1; i += 32) cq += sQ[i] * sU[i + 1];
+        cq = warp_sum(cq);
+        if (lane == 0) sCq = cq;
         double prz = 0.0, pbb = 0.0;
         for (int i = lane; i < mm; i += 32) {
             const double r = sT[i];  // the right-hand side, staged above
@@ -654,35 +659,51 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
         __syncthreads();
         ++step;
         prof_mark(4);
-        // ---- one capped-CG step (cg_step_col) and the next lift, warp 0
+        // ---- one capped-CG step (cg_step_col) and the next lift, warp 0. The
+        // Householder reduce (two dependent sums), p'Hp, and the next lift (two
+        // more) are regrouped by linearity into two rounds of independent sums:
+        //   round 1: A1 = U.H, A2 = Q.H(+1), B1 = P.H(+2), B2 = P.U(+2),
+        //            B3 = P.Q(+1), B4 = P.P  ->  s1, s2, p'Hp
+        //   round 2: r'z, r'r, D1 = Q(+1).z, E1 = U(+2).z  ->  beta, lift s1', s2'
+        // with C = Q.U(+1) fixed per direction (same products, regrouped sums)
         if (warp == 0) {
-            double* t = sT;
             const double rz_old = sSc[0];
-            double part = 0.0;
-            for (int i = lane; i < m; i += 32) part += sU[i] * sH[sIdx[i]];
-            const double s1 = g.bU * warp_sum(part);
-            double part2 = 0.0;
-            for (int i = lane; i < m1; i += 32) {
-                const double v = sH[sIdx[i + 1]] - s1 * sU[i + 1];
-                t[i] = v;
-                part2 += sQ[i] * v;
-            }
-            const double s2 = g.bQ * warp_sum(part2);
-            __syncwarp();
             constexpr int U4 = M / 32;
-            double hp[U4];
-            double pp = 0.0;
+            double a1 = 0.0, a2 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0, b4 = 0.0;
+            double hh[U4];  // H'(j + 2) for j = lane + 32u
 #pragma unroll
             for (int u = 0; u < U4; ++u) {
                 const int i = lane + 32 * u;
-                hp[u] = 0.0;
+                hh[u] = 0.0;
+                if (i < m) {
+                    const double h = sH[sIdx[i]];
+                    a1 += sU[i] * h;
+                    if (i >= 1) a2 += sQ[i - 1] * h;
+                }
                 if (i < mm) {
-                    hp[u] = (t[i + 1] - s2 * sQ[i + 1]) + lambda * sP[i];  // Hop: red + lambda e (:194)
-                    pp += sP[i] * hp[u];
+                    const double h2 = sH[sIdx[i + 2]];
+                    const double p = sP[i];
+                    hh[u] = h2;
+                    b1 += p * h2;
+                    b2 += p * sU[i + 2];
+                    b3 += p * sQ[i + 1];
+                    b4 += p * p;
                 }
             }
-            const double pHp = warp_sum(pp);
-            __syncwarp();
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+                b1 += __shfl_xor_sync(0xffffffffu, b1, o);
+                b2 += __shfl_xor_sync(0xffffffffu, b2, o);
+                b3 += __shfl_xor_sync(0xffffffffu, b3, o);
+                b4 += __shfl_xor_sync(0xffffffffu, b4, o);
+            }
+            // (an xor butterfly leaves the same bits in every lane: each level adds
+            // the same two operands, commuted)
+            const double s1 = g.bU * a1;
+            const double s2 = g.bQ * (a2 - s1 * sCq);
+            const double pHp = b1 - s1 * b2 - s2 * b3 + lambda * b4;  // p'(red + lambda p) (:194)
             if (pHp <= 0.0) {  // :97-100
                 if (lane == 0) {
                     sFlag[2] = 1;
@@ -690,26 +711,39 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
                 }
             } else {
                 const double alpha = rz_old / pHp;
-                double prz = 0.0, prr = 0.0;
+                double prz = 0.0, prr = 0.0, d1 = 0.0, e1 = 0.0;
+                double zr[U4];
 #pragma unroll
                 for (int u = 0; u < U4; ++u) {
                     const int i = lane + 32 * u;
+                    zr[u] = 0.0;
                     if (i < mm) {
+                        const double hp = ((hh[u] - s1 * sU[i + 2]) - s2 * sQ[i + 1]) + lambda * sP[i];
                         sX[i] += alpha * sP[i];
-                        const double r = sR[i] - alpha * hp[u];
+                        const double r = sR[i] - alpha * hp;
                         sR[i] = r;
                         const double zz = s.jd ? r / sJ[i] : r;
                         sZ[i] = zz;
+                        zr[u] = zz;
                         prz += r * zz;
                         prr += r * r;
+                        d1 += sQ[i + 1] * zz;
+                        e1 += sU[i + 2] * zz;
                     }
                 }
-                const double rz2 = warp_sum(prz), rr = warp_sum(prr);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    prz += __shfl_xor_sync(0xffffffffu, prz, o);
+                    prr += __shfl_xor_sync(0xffffffffu, prr, o);
+                    d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+                    e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+                }
+                const double rz2 = prz, rr = prr;
                 const double beta = rz2 / rz_old;
 #pragma unroll
                 for (int u = 0; u < U4; ++u) {
                     const int i = lane + 32 * u;
-                    if (i < mm) sP[i] = sZ[i] + beta * sP[i];
+                    if (i < mm) sP[i] = zr[u] + beta * sP[i];
                 }
                 const int it = sFlag[1] + 1;
                 const bool still = it < s.cap && sqrt(rr) > sSc[1];  // :94
@@ -719,8 +753,15 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
                     sFlag[1] = it;
                     sFlag[0] = still ? 1 : 0;
                 }
+                if (still) {  // lift of the new p: V = U Q (0, p) (lift_col)
+                    const double l1 = g.bQ * (d1 + beta * b3);
+                    const double l2 = g.bU * ((e1 + beta * b2) - l1 * sCq);
+                    for (int i = lane; i < m; i += 32) {
+                        const double qv = i == 0 ? 0.0 : ((i >= 2 ? sP[i - 2] : 0.0) - l1 * sQ[i - 1]);
+                        sV[sIdx[i]] = qv - l2 * sU[i];
+                    }
+                }
                 __syncwarp();
-                if (still) lift();
             }
         }
         __syncthreads();
