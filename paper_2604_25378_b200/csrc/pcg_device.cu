@@ -589,9 +589,14 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
     while (sFlag[0]) {
         prof_mark(1);
         // ---- HVP pass over this CTA's rows: acc[j] += x_tj psi''(z_t) <x_t, V>
-        double acc[CPL];
+        double acc[CPL], vv[CPL];
 #pragma unroll
-        for (int j = 0; j < CPL; ++j) acc[j] = 0.0;
+        for (int j = 0; j < CPL; j += 2) {  // this lane's slice of V, held for the whole pass
+            const double2 v = *reinterpret_cast<const double2*>(sV + colp(j));
+            vv[j] = v.x;
+            vv[j + 1] = v.y;
+            acc[j] = acc[j + 1] = 0.0;
+        }
         // every lane of a warp runs the same trip count (the shuffles need the
         // full warp); rows past the block contribute zeros
 #pragma unroll 2
@@ -615,9 +620,8 @@ __global__ void __launch_bounds__(kCcgWarps * 32, 1) cluster_cg_kernel(const Ccg
             double d0 = 0.0, d1 = 0.0;
 #pragma unroll
             for (int j = 0; j < CPL; j += 2) {
-                const double2 v = *reinterpret_cast<const double2*>(sV + colp(j));
-                d0 = fma(x[j], v.x, d0);
-                d1 = fma(x[j + 1], v.y, d1);
+                d0 = fma(x[j], vv[j], d0);
+                d1 = fma(x[j + 1], vv[j + 1], d1);
             }
             double d = d0 + d1;
 #pragma unroll
