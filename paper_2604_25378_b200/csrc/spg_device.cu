@@ -489,9 +489,14 @@ __global__ void __launch_bounds__(kSpgCW * 32, 1) spg_cluster_kernel(const SpgCl
         double fp = 0.0;
         if (sst.eval_flag) {
             // ---- FGRAD over this CTA's rows at xp (oracle.hpp:58-64, 82-83)
-            double acc[CPL];
+            double acc[CPL], xv[CPL];
 #pragma unroll
-            for (int j = 0; j < CPL; ++j) acc[j] = 0.0;
+            for (int j = 0; j < CPL; j += 2) {  // this lane's slice of xp, held for the pass
+                const double2 v = *reinterpret_cast<const double2*>(sxp + colp(j));
+                xv[j] = v.x;
+                xv[j + 1] = v.y;
+                acc[j] = acc[j + 1] = 0.0;
+            }
             double s2 = 0.0, s3 = 0.0, s4 = 0.0;
             for (int lb = warp * GPW; lb < nloc; lb += NGC) {  // warp-uniform trip count
                 const int tl = lb + lane / LPR;
@@ -508,9 +513,8 @@ __global__ void __launch_bounds__(kSpgCW * 32, 1) spg_cluster_kernel(const SpgCl
                 double d0 = 0.0, d1 = 0.0;
 #pragma unroll
                 for (int j = 0; j < CPL; j += 2) {
-                    const double2 v = *reinterpret_cast<const double2*>(sxp + colp(j));
-                    d0 = fma(x[j], v.x, d0);
-                    d1 = fma(x[j + 1], v.y, d1);
+                    d0 = fma(x[j], xv[j], d0);
+                    d1 = fma(x[j + 1], xv[j + 1], d1);
                 }
                 double zt = d0 + d1;
 #pragma unroll
