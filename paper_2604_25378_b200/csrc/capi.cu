@@ -369,8 +369,7 @@ int32_t mvsk_gpu_weighted_gram_device(mvsk_gpu_ctx* ctx, int32_t slot, double* G
     return guard(ctx, [&] {
         set_device(ctx);
         check_slot(ctx, slot);
-        run_psi2(ctx, ctx->slots[slot].z, ctx->tvec, ctx->T_local);
-        run_weighted_gram(ctx, ctx->tvec, G_dev, 1.0 / (double)ctx->T_global);
+        run_weighted_gram(ctx, nullptr, G_dev, 1.0 / (double)ctx->T_global, ctx->slots[slot].z);
         ctx->fwd += 1;
     });
 }

@@ -41,7 +41,9 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
 
 struct GramArgs {
     const double* X;  // T x ld
-    const double* w;  // T sample weights
+    const double* w;  // T sample weights (or null: psi''(z) from z below)
+    const double* z;  // cached z when the weights are psi''(z) (oracle.hpp:116-119)
+    double c2, c3, c4;
     long long T;
     int ld;
     int n;              // valid columns (fragments wholly past n are skipped)
@@ -101,7 +103,16 @@ __global__ void __launch_bounds__(WM * WN * 32, 1) syrk_dmma_kernel(const GramAr
         }
         if (tid < GBK) {
             const long long t = t0 + tid;
-            sw[buf * GBK + tid] = t < t_hi ? a.w[t] : 0.0;
+            double wt = 0.0;
+            if (t < t_hi) {
+                if (GUARD && a.z) {  // edge-tile (small-n) instantiation: the psi2 weights fused
+                    const double zt = a.z[t];  // into the load, one kernel fewer per round trip
+                    wt = 2.0 * a.c2 - 6.0 * a.c3 * zt + 12.0 * a.c4 * (zt * zt);
+                } else {
+                    wt = a.w[t];
+                }
+            }
+            sw[buf * GBK + tid] = wt;
         }
     };
 
@@ -266,7 +277,7 @@ __global__ void third_weights_kernel(const double* z, const double* q, double* t
 
 }  // namespace
 
-void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, double scale) {
+void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, double scale, const double* z) {
     const int n = (int)ctx->n;
     const int ntile = (n + GBM - 1) / GBM;
     const int npairs = ntile * (ntile + 1) / 2;
@@ -298,16 +309,6 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
         ctx->gram_part_elems = need;
         ++ctx->epoch;
     }
-    GramArgs a{};
-    a.X = ctx->X;
-    a.w = w_rows;
-    a.T = ctx->T_local;
-    a.ld = (int)ctx->ld;
-    a.n = n;
-    a.ntile = ntile;
-    a.nsplit = nsplit;
-    a.part = ctx->gram_part;
-    const size_t smem = (size_t)(2 * GST * GBK * GLDS + GST * GBK) * sizeof(double);
     // warp layout: 1 = 8 warps of 32 x 64, weights on the 4 A fragments
     // (C5 148.7 ms), 0 = the same with the weights on the 8 B fragments
     // (151.6 ms), 2 = 16 warps of 32 x 32 (151.8 ms: more warps per scheduler
@@ -315,6 +316,25 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
     int var = 1;
     if (const char* e = std::getenv("MVSK_GRAM_VAR")) var = std::atoi(e);
     const bool guard = n % GBM != 0;
+    if (z && !(var == 1 && guard)) {  // only the edge-tile kernel computes psi2 itself;
+        run_psi2(ctx, z, ctx->tvec, ctx->T_local);  // the full-tile one keeps its 184 registers
+        w_rows = ctx->tvec;
+        z = nullptr;
+    }
+    GramArgs a{};
+    a.X = ctx->X;
+    a.w = w_rows;
+    a.z = z;
+    a.c2 = ctx->c.c2;
+    a.c3 = ctx->c.c3;
+    a.c4 = ctx->c.c4;
+    a.T = ctx->T_local;
+    a.ld = (int)ctx->ld;
+    a.n = n;
+    a.ntile = ntile;
+    a.nsplit = nsplit;
+    a.part = ctx->gram_part;
+    const size_t smem = (size_t)(2 * GST * GBK * GLDS + GST * GBK) * sizeof(double);
     const void* fn = var == 2   ? reinterpret_cast<const void*>(&syrk_dmma_kernel<4, 4, 4, 4, true>)
                      : var == 0 ? reinterpret_cast<const void*>(&syrk_dmma_kernel<4, 2, 4, 8, false>)
                      : guard    ? reinterpret_cast<const void*>(&syrk_dmma_kernel<4, 2, 4, 8, true, true>)

@@ -362,8 +362,7 @@ void op_weighted_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, double* G)
     ensure_h_mat(ctx, (size_t)ctx->ld * ctx->ld);
     const double* full = ctx->h_mat;
     run_graphed(ctx, kGraphGram, 1, slot, [&] {
-        run_psi2(ctx, ctx->slots[slot].z, ctx->tvec, ctx->T_local);
-        run_weighted_gram(ctx, ctx->tvec, ctx->gram, 1.0 / (double)ctx->T_global);
+        run_weighted_gram(ctx, nullptr, ctx->gram, 1.0 / (double)ctx->T_global, ctx->slots[slot].z);
         MVSK_CUDA(cudaMemcpyAsync(ctx->h_mat, ctx->gram, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToHost,
                                   ctx->stream));
     });
