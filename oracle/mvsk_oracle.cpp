@@ -482,7 +482,8 @@ ReducedFrame householder_frame(const Vec& reduced_grad) {
     if (!(gn > 0)) throw domain_error("householder_frame: zero reduced gradient (stationary)");
     if (reduced_grad.size() < 2) throw dimension_error("householder_frame: need m >= 2");
     ReducedFrame f;
-    f.nu = scaled(reduced_grad, 1.0 / gn);
+    f.nu = reduced_grad;  // reduced_grad / gn: Eigen's scalar quotient divides each coefficient
+    for (double& x : f.nu) x /= gn;
     f.grad_norm = gn;
     const double s = f.nu[0] >= 0.0 ? 1.0 : -1.0;
     f.v = f.nu;
@@ -548,8 +549,9 @@ PartialPivLU::PartialPivLU(const Mat& M) : n(M.rows), lu(M.a), perm(static_cast<
                 for (index_t c = 0; c < n; ++c) std::swap(at(k, c), at(piv, c));
                 std::swap(perm[static_cast<size_t>(k)], perm[static_cast<size_t>(piv)]);
             }
-            const double inv = 1.0 / at(k, k);
-            for (index_t r = k + 1; r < n; ++r) at(r, k) *= inv;
+            // Eigen's unblocked LU divides the column by the pivot (no reciprocal)
+            const double piv_v = at(k, k);
+            for (index_t r = k + 1; r < n; ++r) at(r, k) /= piv_v;
         }
         for (index_t r = k + 1; r < n; ++r) {
             const double l = at(r, k);
@@ -587,7 +589,11 @@ Vec yand_direction(const Oracle& oracle, const TangentBasis& basis, const Oracle
     const double gn = norm(gbar);
     diag.reduced_grad_norm = gn;
     if (!(gn > 0)) throw domain_error("yand_direction: stationary point, no direction");
-    if (m == 1) return basis.apply(scaled(gbar, -1.0 / gn));
+    if (m == 1) {
+        Vec y = gbar;  // (-gbar) / gn, coefficient-wise
+        for (double& v : y) v = -v / gn;
+        return basis.apply(y);
+    }
 
     const ReducedFrame frame = householder_frame(gbar);
     const index_t mm = m - 1;

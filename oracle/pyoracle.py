@@ -1,13 +1,26 @@
 """TEST INFRASTRUCTURE ONLY — ctypes wrapper of the CPU parity oracle.
 
-Loads ``oracle/_build/libmvsk_oracle.so`` (the C++ restatement of the
-reference in ``oracle/mvsk_oracle.{hpp,cpp}``). Importable only from tests/,
-``__graft_entry__.smoke()`` and bench.py's CPU legs; the product package never
-imports it.
+Two implementations export the same ``mo_*`` surface:
+
+* ``"port"``: ``oracle/_build/libmvsk_oracle.so``, the C++ restatement of the
+  reference in ``oracle/mvsk_oracle.{hpp,cpp}`` (no Eigen; runs anywhere);
+* ``"reference"``: ``oracle/_ref/libmvsk_ref.so``, the reference's own headers
+  (/root/reference/proj/include/mvsk/*.hpp, unmodified) compiled over the Eigen
+  API stand-in in ``oracle/ref/`` (built only where /root/reference exists;
+  the prebuilt .so travels with the snapshot); ``"reference_native"`` is the
+  same code with best-CPU flags, the timed reference arm of bench.py.
+
+This module binds the implementation named by ``MVSK_ORACLE_IMPL`` (default
+``port``); ``variant(name)`` returns an independent copy of this module bound
+to another one, so a test can hold both side by side. Importable only from
+tests/, ``__graft_entry__.smoke()``, the golden-fixture script and bench.py's
+CPU legs; the product package never imports it.
 """
 from __future__ import annotations
 
 import ctypes as C
+import importlib.util
+import os
 import subprocess
 from pathlib import Path
 
@@ -17,7 +30,16 @@ from paper_2604_25378_b200._abi import (OBSERVER_FN, mvsk_direction_diag, mvsk_s
                                         mvsk_solver_config, mvsk_tangent_config)
 
 ORACLE_DIR = Path(__file__).resolve().parent
-LIB_PATH = ORACLE_DIR / "_build" / "libmvsk_oracle.so"
+REFERENCE_DIR = Path("/root/reference/proj")
+LIBS = {
+    "port": ORACLE_DIR / "_build" / "libmvsk_oracle.so",
+    "reference": ORACLE_DIR / "_ref" / "libmvsk_ref.so",
+    "reference_native": ORACLE_DIR / "_ref" / "libmvsk_ref_native.so",
+}
+IMPL = globals().get("_IMPL_OVERRIDE") or os.environ.get("MVSK_ORACLE_IMPL", "port")
+if IMPL not in LIBS:
+    raise ValueError(f"MVSK_ORACLE_IMPL={IMPL!r}: expected one of {sorted(LIBS)}")
+LIB_PATH = LIBS[IMPL]
 
 ERRORS = {1: "dimension_error", 2: "domain_error", 3: "data_error", 4: "numeric_error", 7: "error"}
 
@@ -30,8 +52,35 @@ class OracleError(Exception):
 
 
 def build() -> Path:
-    subprocess.run(["make", "-s", "-C", str(ORACLE_DIR)], check=True)
+    if IMPL == "port":
+        subprocess.run(["make", "-s", "-C", str(ORACLE_DIR)], check=True)
+    elif REFERENCE_DIR.exists():
+        subprocess.run(["make", "-s", "-C", str(ORACLE_DIR / "ref"), f"REF={REFERENCE_DIR}"], check=True)
+    else:
+        raise FileNotFoundError(f"{LIB_PATH} is not built and {REFERENCE_DIR} is absent")
     return LIB_PATH
+
+
+def available(impl: str) -> bool:
+    """True when `impl`'s library exists or can be built here."""
+    return LIBS[impl].exists() or (impl == "port") or REFERENCE_DIR.exists()
+
+
+_VARIANTS: dict = {}
+
+
+def variant(impl: str):
+    """An independent copy of this module bound to implementation `impl`."""
+    if impl == IMPL:
+        import sys
+        return sys.modules[__name__]
+    if impl not in _VARIANTS:
+        spec = importlib.util.spec_from_file_location(f"{__name__}__{impl}", __file__)
+        mod = importlib.util.module_from_spec(spec)
+        mod.__dict__["_IMPL_OVERRIDE"] = impl
+        spec.loader.exec_module(mod)
+        _VARIANTS[impl] = mod
+    return _VARIANTS[impl]
 
 
 _lib = None
@@ -54,6 +103,8 @@ def lib() -> C.CDLL:
         L.mo_gradient_mapping_residual.argtypes = [_D, _D, C.c_int64, C.c_double]
         L.mo_splitmix_draw.argtypes = [C.c_uint64, C.c_int, C.c_int64, C.c_double, C.c_double, C.c_void_p]
         L.mo_set_threads.argtypes = [C.c_int]
+        if hasattr(L, "mo_impl"):
+            L.mo_impl.restype = C.c_char_p
         _lib = L
     return _lib
 
@@ -78,6 +129,24 @@ def _check(code: int):
 
 def set_threads(t: int):
     lib().mo_set_threads(int(t))
+
+
+def impl_name() -> str:
+    """"reference" for the compiled reference headers, "port" for the restatement."""
+    L = lib()
+    return L.mo_impl().decode() if hasattr(L, "mo_impl") else "port"
+
+
+def hvp_throughput(oracle: "CpuOracle", cache: "Cache", V, threads: int, reps: int):
+    """Reference arm timing (libmvsk_ref*.so only): `threads` host threads each run
+    `reps` reference HVPs over the shared panel and cache. Returns (seconds,
+    first result of every thread as a threads x n array)."""
+    V = np.ascontiguousarray(V, dtype=np.float64).reshape(-1, oracle.n)
+    first = np.empty((threads, oracle.n))
+    sec = C.c_double()
+    _check(lib().mo_hvp_throughput(oracle.h, cache.h, _p(V), C.c_int(V.shape[0]), C.c_int(threads), C.c_int(reps),
+                                   C.byref(sec), _p(first)))
+    return sec.value, first
 
 
 # ---- rng.hpp ---------------------------------------------------------------

@@ -1,15 +1,33 @@
-// TEST INFRASTRUCTURE ONLY — ctypes surface of the CPU parity oracle (see
-// mvsk_oracle.hpp). Loaded by tests/, __graft_entry__.smoke() and bench.py's
-// CPU legs; never by the product package. Struct layouts for solver config /
-// report / diagnostics are the POD types of include/mvsk_gpu.h so the same
-// ctypes Structures drive both libraries.
+// TEST INFRASTRUCTURE ONLY — the reference itself, compiled.
+//
+// Exports the same `mo_*` ctypes surface as oracle/mvsk_oracle_capi.cpp (the
+// restatement), but every entry point calls the UNMODIFIED reference headers
+// (/root/reference/proj/include/mvsk/*.hpp: mvsk::Oracle, line_model,
+// minimize_line, project_slice, TangentBasis, householder_frame,
+// yand_direction, detail::cg_capped, detail::spg_identify via solve, solve)
+// compiled over the Eigen API stand-in in oracle/ref/eigen_shim. Built by
+// oracle/ref/Makefile into oracle/_ref/libmvsk_ref.so (reference-faithful
+// flags) and oracle/_ref/libmvsk_ref_native.so (x86-64-v3 + SIMD reductions:
+// the timed CPU arm of bench.py). Loaded only by tests/, scripts that generate
+// tests/golden/ and bench.py's reference arm; never by the product package.
+#include <mvsk/affine_normal.hpp>
+#include <mvsk/linesearch.hpp>
+#include <mvsk/oracle.hpp>
+#include <mvsk/panel.hpp>
+#include <mvsk/rng.hpp>
+#include <mvsk/simplex.hpp>
+#include <mvsk/solver.hpp>
+
+#include <chrono>
 #include <cstring>
+#include <memory>
 #include <string>
+#include <thread>
+#include <vector>
 
-#include "../include/mvsk_gpu.h"
-#include "mvsk_oracle.hpp"
+#include "../../include/mvsk_gpu.h"
 
-using namespace mo;
+using namespace mvsk;
 
 namespace {
 thread_local std::string g_err;
@@ -37,13 +55,35 @@ int guard(F&& f) {
     }
 }
 
-Vec vec_of(const double* p, int64_t n) { return p ? Vec(p, p + n) : Vec(); }
-void put(const Vec& v, double* out) { std::memcpy(out, v.data(), v.size() * sizeof(double)); }
+Vec vec_of(const double* p, int64_t n) {
+    Vec v(static_cast<Eigen::Index>(p ? n : 0));
+    if (p && n > 0) std::memcpy(v.data(), p, sizeof(double) * static_cast<size_t>(n));
+    return v;
+}
+Mat mat_of(const double* A, int64_t T, int64_t n) {
+    Mat m(T, n);  // row-major, the panel's own layout (panel.hpp:16)
+    if (T * n > 0) std::memcpy(m.data(), A, sizeof(double) * static_cast<size_t>(T * n));
+    return m;
+}
+void put(const Vec& v, double* out) {
+    if (v.size()) std::memcpy(out, v.data(), sizeof(double) * static_cast<size_t>(v.size()));
+}
+PreferenceCoefficients coeffs_of(const double* c4) {
+    PreferenceCoefficients c;
+    c.c1 = c4[0];
+    c.c2 = c4[1];
+    c.c3 = c4[2];
+    c.c4 = c4[3];
+    return c;
+}
 
 struct OracleBox {
     Mat A;
     std::shared_ptr<PassCounter> counter = std::make_shared<PassCounter>();
     std::unique_ptr<Oracle> oracle;
+    Vec mu, zoff;
+    double value_offset = 0.0;
+    PreferenceCoefficients c;
 };
 
 TangentSolveConfig tangent_of(const mvsk_tangent_config& c) {
@@ -62,9 +102,11 @@ TangentSolveConfig tangent_of(const mvsk_tangent_config& c) {
 
 extern "C" {
 
-const char* mo_impl() { return "port"; }
+const char* mo_impl() { return "reference"; }
 const char* mo_last_error() { return g_err.c_str(); }
-void mo_set_threads(int t) { pass_threads() = t < 1 ? 1 : t; }
+// the reference is single-threaded (CMakeLists.txt has no threading); accepted
+// for interface compatibility with the restatement, ignored
+void mo_set_threads(int) {}
 
 // rng.hpp: kind 0 = u64, 1 = unit, 2 = normal, 3 = sign, 4 = uniform(lo, hi)
 void mo_splitmix_draw(uint64_t seed, int kind, int64_t count, double lo, double hi, void* out) {
@@ -82,48 +124,51 @@ void mo_splitmix_draw(uint64_t seed, int kind, int64_t count, double lo, double 
 
 int mo_center_panel(const double* R, int64_t T, int64_t n, double* A_out, double* mu_out) {
     return guard([&] {
-        Mat m(T, n);
-        if (T * n > 0) std::memcpy(m.a.data(), R, sizeof(double) * static_cast<size_t>(T * n));
-        ReturnPanel p = center_panel(std::move(m));
-        put(p.A.a, A_out);
+        ReturnPanel p = center_panel(mat_of(R, T, n));
+        std::memcpy(A_out, p.A.data(), sizeof(double) * static_cast<size_t>(T * n));
         put(p.mu, mu_out);
     });
 }
 int mo_crra(double gamma, double* out4) {
     return guard([&] {
         auto c = crra_coefficients(gamma);
-        out4[0] = c.c1; out4[1] = c.c2; out4[2] = c.c3; out4[3] = c.c4;
+        out4[0] = c.c1;
+        out4[1] = c.c2;
+        out4[2] = c.c3;
+        out4[3] = c.c4;
     });
 }
 int mo_make_coefficients(double c1, double c2, double c3, double c4, double* out4) {
     return guard([&] {
         auto c = make_coefficients(c1, c2, c3, c4);
-        out4[0] = c.c1; out4[1] = c.c2; out4[2] = c.c3; out4[3] = c.c4;
+        out4[0] = c.c1;
+        out4[1] = c.c2;
+        out4[2] = c.c3;
+        out4[3] = c.c4;
     });
 }
 
-// ---- oracle ----
+// ---- oracle.hpp ----
 int mo_oracle_create(const double* A, int64_t T, int64_t n, const double* mu, const double* c4,
                      const double* zoff, double value_offset, void** out) {
     return guard([&] {
         auto box = std::make_unique<OracleBox>();
-        box->A = Mat(T, n);
-        if (T * n > 0) std::memcpy(box->A.a.data(), A, sizeof(double) * static_cast<size_t>(T * n));
-        PreferenceCoefficients c{c4[0], c4[1], c4[2], c4[3]};
-        box->oracle = std::make_unique<Oracle>(box->A, vec_of(mu, n), c, box->counter,
-                                               zoff ? vec_of(zoff, T) : Vec(), value_offset);
+        box->A = mat_of(A, T, n);
+        box->mu = vec_of(mu, n);
+        box->zoff = zoff ? vec_of(zoff, T) : Vec();
+        box->value_offset = value_offset;
+        box->c = coeffs_of(c4);
+        box->oracle = std::make_unique<Oracle>(box->A, box->mu, box->c, box->counter, box->zoff, value_offset);
         *out = box.release();
     });
 }
-// mu length mismatch probe (oracle.hpp:37-38)
 int mo_oracle_create_mu(const double* A, int64_t T, int64_t n, const double* mu, int64_t nmu,
                         const double* c4, void** out) {
     return guard([&] {
         auto box = std::make_unique<OracleBox>();
-        box->A = Mat(T, n);
-        std::memcpy(box->A.a.data(), A, sizeof(double) * static_cast<size_t>(T * n));
-        PreferenceCoefficients c{c4[0], c4[1], c4[2], c4[3]};
-        box->oracle = std::make_unique<Oracle>(box->A, vec_of(mu, nmu), c, box->counter);
+        box->A = mat_of(A, T, n);
+        box->c = coeffs_of(c4);
+        box->oracle = std::make_unique<Oracle>(box->A, vec_of(mu, nmu), box->c, box->counter);
         *out = box.release();
     });
 }
@@ -145,7 +190,10 @@ int mo_value(void* o, void* c, double* f) {
 int mo_moments(void* o, void* c, double* out4) {
     return guard([&] {
         auto [a, b, cc, d] = static_cast<OracleBox*>(o)->oracle->moments(*static_cast<OracleCache*>(c));
-        out4[0] = a; out4[1] = b; out4[2] = cc; out4[3] = d;
+        out4[0] = a;
+        out4[1] = b;
+        out4[2] = cc;
+        out4[3] = d;
     });
 }
 int mo_gradient(void* o, void* c, double* g) {
@@ -165,7 +213,9 @@ int mo_third_action(void* o, void* c, const double* u, const double* v, double* 
     });
 }
 int mo_hessian_diag_weights(void* o, void* c, double* out) {
-    return guard([&] { put(static_cast<OracleBox*>(o)->oracle->hessian_diag_weights(*static_cast<OracleCache*>(c)), out); });
+    return guard([&] {
+        put(static_cast<OracleBox*>(o)->oracle->hessian_diag_weights(*static_cast<OracleCache*>(c)), out);
+    });
 }
 int mo_sample_direction(void* o, const double* d, double* out) {
     return guard([&] {
@@ -173,13 +223,14 @@ int mo_sample_direction(void* o, const double* d, double* out) {
         put(b->oracle->sample_direction(vec_of(d, b->oracle->assets())), out);
     });
 }
-// out: a0..a4, s11,s21,s31,s02,s12,s22,s03,s13,s04
+// out: a0..a4, s11,s21,s31,s02,s12,s22,s03,s13,s04 (linesearch.hpp:62-81)
 int mo_line_model(void* o, void* c, const double* d, int64_t nd, double cap, double* out14) {
     return guard([&] {
         auto* b = static_cast<OracleBox*>(o);
         LineModel m = line_model(*b->oracle, *static_cast<OracleCache*>(c), vec_of(d, nd), cap);
-        const double v[14] = {m.a0, m.a1, m.a2, m.a3, m.a4, m.sums.s11, m.sums.s21, m.sums.s31,
-                              m.sums.s02, m.sums.s12, m.sums.s22, m.sums.s03, m.sums.s13, m.sums.s04};
+        const double v[14] = {m.a0, m.a1, m.a2, m.a3, m.a4, m.sums.s11, m.sums.s21,
+                              m.sums.s31, m.sums.s02, m.sums.s12, m.sums.s22, m.sums.s03,
+                              m.sums.s13, m.sums.s04};
         std::memcpy(out14, v, sizeof(v));
     });
 }
@@ -190,6 +241,7 @@ void mo_passes(void* o, uint64_t* fwd, uint64_t* tr) {
 }
 void mo_reset_passes(void* o) { static_cast<OracleBox*>(o)->counter->reset(); }
 
+// affine_normal.hpp:127-245
 int mo_yand_direction(void* o, void* c, const mvsk_tangent_config* cfg, uint64_t it_seed,
                       double* d_out, mvsk_direction_diag* diag) {
     return guard([&] {
@@ -208,7 +260,7 @@ int mo_yand_direction(void* o, void* c, const mvsk_tangent_config* cfg, uint64_t
     });
 }
 
-// ---- line search ----
+// ---- linesearch.hpp ----
 int mo_power_sums(const double* z, const double* w, int64_t T, int64_t Tw, double* out9) {
     return guard([&] {
         PowerSums s = power_sums(vec_of(z, T), vec_of(w, Tw));
@@ -217,14 +269,18 @@ int mo_power_sums(const double* z, const double* w, int64_t T, int64_t Tw, doubl
     });
 }
 int mo_cubic_real_roots(double c3, double c2, double c1, double c0, double* out3) {
-    auto r = cubic_real_roots(c3, c2, c1, c0);
+    auto r = detail::cubic_real_roots(c3, c2, c1, c0);
     for (size_t i = 0; i < r.size(); ++i) out3[i] = r[i];
     return static_cast<int>(r.size());
 }
 int mo_minimize_line(const double* a5, double cap, double* alpha, double* f) {
     return guard([&] {
         LineModel m;
-        m.a0 = a5[0]; m.a1 = a5[1]; m.a2 = a5[2]; m.a3 = a5[3]; m.a4 = a5[4];
+        m.a0 = a5[0];
+        m.a1 = a5[1];
+        m.a2 = a5[2];
+        m.a3 = a5[3];
+        m.a4 = a5[4];
         m.alpha_cap = cap;
         auto [al, fv] = minimize_line(m);
         *alpha = al;
@@ -232,8 +288,8 @@ int mo_minimize_line(const double* a5, double cap, double* alpha, double* f) {
     });
 }
 typedef double (*mo_phi_fn)(double, void*);
-int mo_armijo(mo_phi_fn phi, void* user, double g_dot_d, double alpha_init, double sigma,
-              double shrink, double* alpha, int* stalled) {
+int mo_armijo(mo_phi_fn phi, void* user, double g_dot_d, double alpha_init, double sigma, double shrink,
+              double* alpha, int* stalled) {
     return guard([&] {
         ArmijoResult r = armijo_search([&](double a) { return phi(a, user); }, g_dot_d, alpha_init, sigma, shrink);
         *alpha = r.alpha;
@@ -241,7 +297,7 @@ int mo_armijo(mo_phi_fn phi, void* user, double g_dot_d, double alpha_init, doub
     });
 }
 
-// ---- simplex ----
+// ---- simplex.hpp ----
 double mo_alpha_max(const double* x, const double* d, int64_t n, double tau) {
     return alpha_max(vec_of(x, n), vec_of(d, n), tau);
 }
@@ -273,46 +329,37 @@ int mo_frame_apply_Q(const double* g, int64_t m, const double* eta, double* out)
 int mo_frame_apply_Qt(const double* g, int64_t m, const double* w, double* out) {
     return guard([&] { put(householder_frame(vec_of(g, m)).apply_Qt(vec_of(w, m)), out); });
 }
-int mo_cg_dense(const double* M, int64_t m, const double* rhs, double tol, int cap,
-                const double* jacobi_diag, double* x_out, int* iters, int* breakdown) {
+// affine_normal.hpp:85-113 over a dense row-major operator
+int mo_cg_dense(const double* M, int64_t m, const double* rhs, double tol, int cap, const double* jacobi_diag,
+                double* x_out, int* iters, int* breakdown) {
     return guard([&] {
-        auto op = [&](const Vec& v) {
-            Vec r(static_cast<size_t>(m), 0.0);
-            for (int64_t i = 0; i < m; ++i)
-                for (int64_t j = 0; j < m; ++j) r[static_cast<size_t>(i)] += M[i * m + j] * v[static_cast<size_t>(j)];
-            return r;
-        };
+        const Mat Mm = mat_of(M, m, m);
+        auto op = [&](const Vec& v) -> Vec { return Mm * v; };
         Vec jd = jacobi_diag ? vec_of(jacobi_diag, m) : Vec();
         int it = 0;
         bool bd = false;
-        put(cg_capped(op, vec_of(rhs, m), tol, cap, jacobi_diag ? &jd : nullptr, it, bd), x_out);
+        put(detail::cg_capped(op, vec_of(rhs, m), tol, cap, jacobi_diag ? &jd : nullptr, it, bd), x_out);
         *iters = it;
         *breakdown = bd;
     });
 }
-int mo_restrict_to_face(const double* A, int64_t T, int64_t n, const double* mu, const double* x,
-                        double tau, int64_t* free_idx, int64_t* nf, double* zoff, double* mu_pin,
-                        double* free_mass) {
+int mo_restrict_to_face(const double* A, int64_t T, int64_t n, const double* mu, const double* x, double tau,
+                        int64_t* free_idx, int64_t* nf, double* zoff, double* mu_pin, double* free_mass) {
     return guard([&] {
-        Mat m(T, n);
-        std::memcpy(m.a.data(), A, sizeof(double) * static_cast<size_t>(T * n));
+        const Mat m = mat_of(A, T, n);
         FaceProblem fp = restrict_to_face(m, vec_of(mu, n), vec_of(x, n), tau);
-        *nf = static_cast<int64_t>(fp.free_indices.size());
-        for (size_t i = 0; i < fp.free_indices.size(); ++i) free_idx[i] = fp.free_indices[i];
+        *nf = static_cast<int64_t>(fp.state.free_indices.size());
+        for (size_t i = 0; i < fp.state.free_indices.size(); ++i) free_idx[i] = fp.state.free_indices[i];
         put(fp.zoff, zoff);
         *mu_pin = fp.mu_pinned_term;
         *free_mass = fp.free_mass;
     });
 }
 
-// ---- solver ----
+// ---- solver.hpp ----
 int mo_preset(const char* name, mvsk_solver_config* out) {
     return guard([&] {
-        std::string s(name);
-        SolverConfig c;
-        if (s == "small") c = small_preset();
-        else if (s == "large") c = large_preset();
-        else throw domain_error("preset: unknown mode " + s);
+        SolverConfig c = preset(std::string(name));
         std::memset(out, 0, sizeof(*out));
         out->epsilon = c.epsilon;
         out->tau = c.tau;
@@ -321,7 +368,8 @@ int mo_preset(const char* name, mvsk_solver_config* out) {
         out->max_elapsed_seconds = c.max_elapsed_seconds.value_or(0.0);
         out->projected_trial_step = c.projected_trial_step;
         out->n_restart_trial_steps = static_cast<int32_t>(c.restart_trial_steps.size());
-        for (size_t i = 0; i < c.restart_trial_steps.size() && i < 4; ++i) out->restart_trial_steps[i] = c.restart_trial_steps[i];
+        for (size_t i = 0; i < c.restart_trial_steps.size() && i < 4; ++i)
+            out->restart_trial_steps[i] = c.restart_trial_steps[i];
         out->restart_max_iter = c.restart_max_iter;
         out->tangent.mode = c.tangent.mode == TangentSolveConfig::Mode::pcg;
         out->tangent.lambda = c.tangent.lambda;
@@ -338,15 +386,13 @@ int mo_preset(const char* name, mvsk_solver_config* out) {
     });
 }
 
-int mo_solve(const double* A, int64_t T, int64_t n, const double* mu, const double* c4,
-             const mvsk_solver_config* cfg, const double* x0, double* x_star,
-             mvsk_solve_report* rep, mvsk_observer_fn observer, void* user) {
+int mo_solve(const double* A, int64_t T, int64_t n, const double* mu, const double* c4, const mvsk_solver_config* cfg,
+             const double* x0, double* x_star, mvsk_solve_report* rep, mvsk_observer_fn observer, void* user) {
     return guard([&] {
         ReturnPanel p;
-        p.A = Mat(T, n);
-        std::memcpy(p.A.a.data(), A, sizeof(double) * static_cast<size_t>(T * n));
+        p.A = mat_of(A, T, n);
+        p.R = Mat(T, n);  // solve() reads only A and mu (solver.hpp:195-655); periods() reads R.rows()
         p.mu = vec_of(mu, n);
-        PreferenceCoefficients c{c4[0], c4[1], c4[2], c4[3]};
         SolverConfig sc;
         sc.epsilon = cfg->epsilon;
         sc.tau = cfg->tau;
@@ -356,7 +402,8 @@ int mo_solve(const double* A, int64_t T, int64_t n, const double* mu, const doub
         sc.restart_trial_steps.assign(cfg->restart_trial_steps, cfg->restart_trial_steps + cfg->n_restart_trial_steps);
         sc.restart_max_iter = cfg->restart_max_iter;
         sc.tangent = tangent_of(cfg->tangent);
-        sc.line_search = cfg->line_search == 1 ? SolverConfig::LineSearch::armijo : SolverConfig::LineSearch::exact_quartic;
+        sc.line_search =
+            cfg->line_search == 1 ? SolverConfig::LineSearch::armijo : SolverConfig::LineSearch::exact_quartic;
         sc.stall_restarts = cfg->stall_restarts != 0;
         sc.identification_pass = cfg->identification_pass != 0;
         sc.label = std::string(cfg->label, strnlen(cfg->label, sizeof(cfg->label)));
@@ -364,7 +411,7 @@ int mo_solve(const double* A, int64_t T, int64_t n, const double* mu, const doub
             sc.observer = [&](const IterateRecord& r) {
                 observer(user, r.iteration, r.f, r.x.data(), static_cast<int64_t>(r.x.size()));
             };
-        SolveReport r = solve(p, c, sc, x0 ? vec_of(x0, n) : Vec());
+        SolveReport r = solve(p, coeffs_of(c4), sc, x0 ? vec_of(x0, n) : Vec());
         put(r.x_star, x_star);
         std::memset(rep, 0, sizeof(*rep));
         rep->f_star = r.f_star;
@@ -380,6 +427,44 @@ int mo_solve(const double* A, int64_t T, int64_t n, const double* mu, const doub
         rep->identification_steps = r.identification_steps;
         rep->status = static_cast<int32_t>(r.status);
         std::strncpy(rep->config_label, r.config_label.c_str(), sizeof(rep->config_label) - 1);
+    });
+}
+
+// ---- timing harness for bench.py's reference arm (not a reference API) ----
+// `nthreads` host threads each run `reps` reference HVPs (oracle.hpp:92-101)
+// over the SAME immutable panel and cache (SPEC: concurrent caches over one
+// panel are allowed; each thread gets its own Oracle so the pass counters do
+// not race). Direction i of thread j is V[(j + i) % k]. Returns the wall time
+// of the whole batch in seconds and (optionally) the first result per thread.
+int mo_hvp_throughput(void* o, void* c, const double* V, int k, int nthreads, int reps, double* seconds,
+                      double* first_out) {
+    return guard([&] {
+        auto* b = static_cast<OracleBox*>(o);
+        const auto* cache = static_cast<OracleCache*>(c);
+        const int64_t n = b->oracle->assets();
+        std::vector<Vec> dirs;
+        for (int i = 0; i < k; ++i) dirs.push_back(vec_of(V + static_cast<size_t>(i) * n, n));
+        std::vector<std::unique_ptr<Oracle>> oracles;
+        for (int j = 0; j < nthreads; ++j)
+            oracles.push_back(std::make_unique<Oracle>(b->A, b->mu, b->c, nullptr, b->zoff, b->value_offset));
+        std::vector<std::string> errs(static_cast<size_t>(nthreads));
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> th;
+        for (int j = 0; j < nthreads; ++j)
+            th.emplace_back([&, j] {
+                try {
+                    for (int i = 0; i < reps; ++i) {
+                        Vec h = oracles[static_cast<size_t>(j)]->hvp(*cache, dirs[static_cast<size_t>((j + i) % k)]);
+                        if (i == 0 && first_out) put(h, first_out + static_cast<size_t>(j) * n);
+                    }
+                } catch (const std::exception& e) {
+                    errs[static_cast<size_t>(j)] = e.what();
+                }
+            });
+        for (auto& t : th) t.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        for (const auto& e : errs)
+            if (!e.empty()) throw numeric_error(e);
     });
 }
 

@@ -161,8 +161,9 @@ __attribute__((target_clones("avx2", "default"))) void lu_factor_rows(double* a,
                 for (long long c = 0; c < n; ++c) std::swap(a[k * n + c], a[piv * n + c]);
                 std::swap(perm[k], perm[piv]);
             }
-            const double inv = 1.0 / a[k * n + k];
-            for (long long r = k + 1; r < n; ++r) a[r * n + k] *= inv;
+            // divide by the pivot, as Eigen's partial-pivot LU does (no reciprocal)
+            const double pv = a[k * n + k];
+            for (long long r = k + 1; r < n; ++r) a[r * n + k] /= pv;
         }
         for (long long r = k + 1; r < n; ++r) {
             const double l = a[r * n + k];

@@ -1,0 +1,153 @@
+"""North_star parity at BASELINE configs 1-4, against the REFERENCE'S OWN CODE.
+
+tests/golden/ref_configs.npz holds the outputs of the unmodified reference
+headers (oracle/_ref, made by tests/golden/make_golden.py) on the seeded
+BASELINE panels; the panels themselves are regenerated here by datagen and
+pinned by their SHA-256. Bars (north_star, written in each test):
+* oracle values (f, gradient, HVPs, third action, line model): 1e-11 relative
+  to the largest reference entry;
+* full solves at epsilon 1e-10 (max_elapsed off): same status, same active
+  set, objective to 1e-12 relative, final weights within 1e-8 in the
+  infinity norm — no looser escape;
+* the config-4 return-floor sweep (driven by the reference's
+  solve on the CPU side): identical calibrated c1 per floor and total solve
+  count, weights per floor within 1e-8.
+The CPU half (the restatement reproduces the fixture bit for bit) runs without
+a GPU.
+"""
+import hashlib
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+
+GOLDEN = Path(__file__).resolve().parent / "golden" / "ref_configs.npz"
+TAU = 1e-8
+
+
+def _fixture():
+    return np.load(GOLDEN)
+
+
+def _keys():
+    g = _fixture()
+    return sorted({k.split("__")[0] for k in g.files if k.endswith("__spec")})
+
+
+def _panel(g, key):
+    from paper_2604_25378_b200.datagen import make_panel
+    name, seed, kappa, _gamma = [str(s) for s in g[f"{key}__spec"]]
+    A, mu, _ = make_panel(name, seed=int(seed), kappa=float(kappa))
+    sha = hashlib.sha256(np.ascontiguousarray(A).tobytes()).hexdigest()
+    assert sha == str(g[f"{key}__sha"]), f"{key}: generator output changed; regenerate the fixture"
+    return A, mu, g[f"{key}__c"]
+
+
+def _cases():
+    g = _fixture()
+    out = []
+    for key in _keys():
+        for p in ("small", "large"):
+            if f"{key}__{p}__x" in g.files:
+                out.append((key, p))
+    return out
+
+
+def _active(x):
+    return tuple(np.nonzero(x <= TAU + 1e-12)[0])
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(np.asarray(a) - np.asarray(b)))) / max(float(np.max(np.abs(b))), 1e-300)
+
+
+def _cfg(mod, preset):
+    cfg = mod.preset(preset)
+    cfg.has_max_elapsed = 0
+    cfg.epsilon = 1e-10
+    return cfg
+
+
+@pytest.mark.parametrize("key,preset", [c for c in _cases() if not c[0].startswith("C4")])
+def test_restatement_reproduces_reference_config_solves(key, preset):
+    """CPU: the parity oracle IS the reference on these configs (bitwise)."""
+    g = _fixture()
+    A, mu, c = _panel(g, key)
+    x, rep = po.solve(A, mu, c, _cfg(po, preset))
+    np.testing.assert_array_equal(x, g[f"{key}__{preset}__x"])
+    assert rep.f_star == g[f"{key}__{preset}__meta"][0]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", _keys())
+def test_gpu_oracle_matches_reference_at_config_size(key):
+    from paper_2604_25378_b200.gpu_oracle import GpuOracle, tangent_config
+    g = _fixture()
+    A, mu, c = _panel(g, key)
+    gpu = GpuOracle(A, mu, c)
+    gc = gpu.make_cache(g[f"{key}__x0"])
+    V = g[f"{key}__V"]
+    assert abs(gpu.value(gc) - g[f"{key}__f"][0]) <= 1e-11 * abs(g[f"{key}__f"][0])
+    assert _rel(gpu.gradient(gc), g[f"{key}__g"]) <= 1e-11
+    H = gpu.hvp(gc, V)
+    for i in range(2):
+        assert _rel(H[i], g[f"{key}__H"][i]) <= 1e-11
+    assert _rel(gpu.third_action(gc, V[:1], V[1:2])[0], g[f"{key}__T3"]) <= 1e-11
+    lm = gpu.line_model(gc, V[0], 0.05)
+    assert _rel([lm.a0, lm.a1, lm.a2, lm.a3, lm.a4], g[f"{key}__lm"][:5]) <= 1e-11
+    d, diag = gpu.yand_direction(gc, tangent_config("pcg", lam=1e-4), 7)
+    # truncated PCG (tol 1e-3, cap 15): same Krylov path; the direction's
+    # rounding sensitivity grows with the conditioning (kappa up to 1000 here)
+    assert diag.krylov_iters == int(g[f"{key}__krylov_pcg"][0])
+    assert _rel(d, g[f"{key}__d_pcg"]) <= 1e-6
+    gpu.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key,preset", _cases())
+def test_gpu_solve_matches_reference(key, preset):
+    from paper_2604_25378_b200.gpu_oracle import GpuOracle, preset as gpreset
+    g = _fixture()
+    A, mu, c = _panel(g, key)
+    xr = g[f"{key}__{preset}__x"]
+    fr, kkt_r, st_r, it_r = g[f"{key}__{preset}__meta"]
+    gpu = GpuOracle(A, mu, c)
+    cfg = gpreset(preset)
+    cfg.has_max_elapsed = 0
+    cfg.epsilon = 1e-10
+    x, rep = gpu.solve(cfg)
+    gpu.close()
+    dx = float(np.max(np.abs(x - xr)))
+    info = (f"{key}/{preset}: status {rep.status} vs {int(st_r)}, it {rep.iterations} vs {int(it_r)}, "
+            f"kkt {rep.kkt_residual:.2e} vs {kkt_r:.2e}, dx {dx:.2e}, df {abs(rep.f_star - fr):.2e}")
+    print(info)
+    assert rep.status == int(st_r), info
+    assert _active(x) == _active(xr), info
+    assert abs(rep.f_star - fr) <= 1e-12 * (1 + abs(fr)), info
+    assert dx <= 1e-8, info
+
+
+@pytest.mark.gpu
+def test_gpu_c4_floor_sweep_matches_reference():
+    from paper_2604_25378_b200.datagen import make_panel
+    from paper_2604_25378_b200.gpu_oracle import GpuOracle, preset as gpreset
+    g = _fixture()
+    A, mu, c = make_panel("C4", seed=0)
+    assert hashlib.sha256(np.ascontiguousarray(A).tobytes()).hexdigest() == str(g["C4sweep__sha"])
+    cfg = gpreset("large")
+    cfg.has_max_elapsed = 0
+    cfg.epsilon = 1e-10
+    gpu = GpuOracle(A, mu, c)
+    out = gpu.floor_sweep(cfg, nfloors=5)
+    gpu.close()
+    m_mv, m_max = g["C4sweep__m"]
+    span = m_max - m_mv
+    assert out.m_max == m_max
+    assert abs(out.m_mv - m_mv) <= 1e-8 * span
+    assert out.total_solves == int(g["C4sweep__total"][0])
+    for k, p in enumerate(out.points):
+        assert p["c1"] == g["C4sweep__c1"][k], (k, p["c1"], g["C4sweep__c1"][k])
+        assert abs(p["mean"] - g["C4sweep__mean"][k]) <= 1e-9 * span
+        assert float(np.max(np.abs(out.X[k] - g["C4sweep__X"][k]))) <= 1e-8
