@@ -110,7 +110,7 @@ typedef struct {
     int32_t face_events;
     int32_t restarts;
     int32_t identification_steps;
-    int32_t status; /* SolveStatus (solver.hpp:21): 0 converged, 1 stalled, 2 max_iter, 3 max_elapsed */
+    int32_t status; /* SolveStatus (solver.hpp:21): 0 converged, 1 stalled, 2 max_iter, 3 max_elapsed, 4 degenerate_face */
     int32_t _pad;
     char config_label[16];
 } mvsk_solve_report;
@@ -136,8 +136,26 @@ int32_t mvsk_gpu_create_sharded(const double* A_rows, int64_t T_local, int64_t r
                                 int64_t T_global, int64_t n, const double* mu,
                                 const mvsk_coeffs* c, int32_t device, int32_t nranks,
                                 int32_t rank, const void* nccl_unique_id, mvsk_gpu_ctx** out);
+/* In-process row-shard group: nranks contexts driven by nranks host threads of
+ * ONE process, on one device or several (peer access). Each oracle op's
+ * exchange step is a peer-memory allreduce (every rank sums all members'
+ * buffers in rank order, identical bits everywhere) ordered by CUDA events at
+ * two host rendezvous per collective, instead of NCCL. Same SPMD contract as
+ * NCCL groups: every rank calls the same ops in the same order. Member ops
+ * launch eagerly (no CUDA-graph replay). Destroy the contexts before the
+ * group. */
+typedef struct mvsk_gpu_group mvsk_gpu_group;
+int32_t mvsk_gpu_group_create(int32_t nranks /* 1..8 */, mvsk_gpu_group** out);
+int32_t mvsk_gpu_group_destroy(mvsk_gpu_group* group);
+int32_t mvsk_gpu_create_sharded_in_group(const double* A_rows, int64_t T_local, int64_t row0,
+                                         int64_t T_global, int64_t n, const double* mu,
+                                         const mvsk_coeffs* c, int32_t device,
+                                         mvsk_gpu_group* group, int32_t rank, mvsk_gpu_ctx** out);
 /* Borrow a device-resident panel block (T_local x n, leading dimension ld >= n,
- * ld even, 16-byte aligned base). The memory must outlive the context. */
+ * ld even, 16-byte aligned base). The memory must outlive the context. The
+ * padding columns [n, ld) of every row are read (and multiplied by zero) by the
+ * streaming kernels, so they must be finite (zero is typical, e.g. a memset
+ * cudaMallocPitch block); non-finite padding -> MVSK_DATA_ERROR at creation. */
 int32_t mvsk_gpu_create_from_device(const double* A_dev, int64_t ld, int64_t T_local,
                                     int64_t row0, int64_t T_global, int64_t n,
                                     const double* mu, const mvsk_coeffs* c, int32_t device,

@@ -132,6 +132,10 @@ SIGNATURES = [
     ("mvsk_gpu_create", _I32, [_D, _I64, _I64, _D, C.POINTER(mvsk_coeffs), _I32, C.POINTER(_P)]),
     ("mvsk_gpu_create_sharded", _I32,
      [_D, _I64, _I64, _I64, _I64, _D, C.POINTER(mvsk_coeffs), _I32, _I32, _I32, _P, C.POINTER(_P)]),
+    ("mvsk_gpu_group_create", _I32, [_I32, C.POINTER(_P)]),
+    ("mvsk_gpu_group_destroy", _I32, [_P]),
+    ("mvsk_gpu_create_sharded_in_group", _I32,
+     [_D, _I64, _I64, _I64, _I64, _D, C.POINTER(mvsk_coeffs), _I32, _P, _I32, C.POINTER(_P)]),
     ("mvsk_gpu_create_from_device", _I32,
      [_P, _I64, _I64, _I64, _I64, _I64, _D, C.POINTER(mvsk_coeffs), _I32, _I32, _I32, _P, C.POINTER(_P)]),
     ("mvsk_gpu_create_from_binary", _I32, [C.c_char_p, C.POINTER(mvsk_coeffs), _I32, _I32, _I32, _P, C.POINTER(_P)]),

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "collective.cuh"
 #include "host_ops.hpp"
 #include "pcg_device.hpp"
 
@@ -154,6 +155,60 @@ int32_t mvsk_gpu_create_sharded(const double* A_rows, int64_t T_local, int64_t r
     });
 }
 
+namespace {
+__global__ void padding_check_kernel(const double* X, long long T, long long ld, long long n, int* flag) {
+    const long long w = ld - n, cells = T * w;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < cells; e += (long long)gridDim.x * blockDim.x) {
+        const long long t = e / w, j = n + (e - t * w);
+        if (!isfinite(X[t * ld + j])) *flag = 1;
+    }
+}
+}  // namespace
+
+struct mvsk_gpu_group {
+    mvsk_b200::LocalGroup* g = nullptr;
+};
+
+int32_t mvsk_gpu_group_create(int32_t nranks, mvsk_gpu_group** out) {
+    return guard(nullptr, [&] {
+        if (!out) throw ApiError(MVSK_DOMAIN_ERROR, "null out");
+        *out = nullptr;
+        auto* grp = new mvsk_gpu_group();
+        grp->g = group_new(nranks);
+        *out = grp;
+    });
+}
+
+int32_t mvsk_gpu_group_destroy(mvsk_gpu_group* group) {
+    return guard(nullptr, [&] {
+        if (!group) return;
+        if (group_live(group->g) != 0)
+            throw ApiError(MVSK_DOMAIN_ERROR, "group_destroy: member contexts are still alive");
+        group_delete(group->g);
+        delete group;
+    });
+}
+
+int32_t mvsk_gpu_create_sharded_in_group(const double* A_rows, int64_t T_local, int64_t row0, int64_t T_global,
+                                         int64_t n, const double* mu, const mvsk_coeffs* c, int32_t device,
+                                         mvsk_gpu_group* group, int32_t rank, mvsk_gpu_ctx** out) {
+    return guard(nullptr, [&] {
+        if (!out) throw ApiError(MVSK_DOMAIN_ERROR, "null out");
+        *out = nullptr;
+        if (!group) throw ApiError(MVSK_DOMAIN_ERROR, "null group");
+        mvsk_gpu_ctx* ctx = make_ctx(T_local, row0, T_global, n, mu, c, device, 1, 0, nullptr);
+        try {
+            upload_panel(ctx, A_rows);
+            ctx_alloc_workspaces(ctx);
+            group_join(group->g, ctx, rank);
+        } catch (...) {
+            ctx_free(ctx);
+            throw;
+        }
+        *out = ctx;
+    });
+}
+
 int32_t mvsk_gpu_create_from_device(const double* A_dev, int64_t ld, int64_t T_local, int64_t row0,
                                     int64_t T_global, int64_t n, const double* mu, const mvsk_coeffs* c,
                                     int32_t device, int32_t nranks, int32_t rank, const void* nccl_unique_id,
@@ -169,6 +224,26 @@ int32_t mvsk_gpu_create_from_device(const double* A_dev, int64_t ld, int64_t T_l
             ctx->X = const_cast<double*>(A_dev);
             ctx->owns_X = false;
             ctx_alloc_workspaces(ctx);
+            // the streaming kernels read whole ld-wide rows and multiply the
+            // padding columns [n, ld) by zero weights: 0 * NaN would poison
+            // every result, so non-finite padding is rejected up front
+            if (ld > n && T_local > 0) {
+                int* flag = nullptr;
+                MVSK_CUDA(cudaMalloc(&flag, sizeof(int)));
+                MVSK_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+                const long long cells = (long long)T_local * (ld - n);
+                const int nb = (int)std::min<long long>(4LL * ctx->nsm, (cells + 255) / 256);
+                padding_check_kernel<<<nb, 256, 0, ctx->stream>>>(A_dev, T_local, ld, n, flag);
+                int h = 0;
+                const cudaError_t e1 = cudaGetLastError();
+                const cudaError_t e2 = cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+                const cudaError_t e3 = cudaStreamSynchronize(ctx->stream);
+                cudaFree(flag);
+                MVSK_CUDA(e1);
+                MVSK_CUDA(e2);
+                MVSK_CUDA(e3);
+                if (h) throw ApiError(MVSK_DATA_ERROR, "device panel: non-finite values in the padding columns [n, ld)");
+            }
         } catch (...) {
             ctx_free(ctx);
             throw;
@@ -261,6 +336,9 @@ int32_t mvsk_gpu_dims(const mvsk_gpu_ctx* ctx, int64_t* T_global, int64_t* T_loc
 int32_t mvsk_gpu_set_offset(mvsk_gpu_ctx* ctx, const double* zoff, double value_offset) {
     return guard(ctx, [&] {
         set_device(ctx);
+        // *_device ops return without a host sync: a pass still in flight on
+        // ctx->stream may be reading zoff_dev, so drain the stream first
+        MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
         if (zoff) {
             if (!ctx->zoff_dev)
                 MVSK_CUDA(cudaMalloc(&ctx->zoff_dev, (size_t)std::max<long long>(1, ctx->T_local) * sizeof(double)));

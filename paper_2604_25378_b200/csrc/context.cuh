@@ -16,6 +16,7 @@ namespace mvsk_b200 {
 
 struct PcgWorkspace;
 struct SpgWorkspace;
+struct LocalGroup;  // in-process row-shard group (collective.cu)
 
 struct ApiError : std::runtime_error {
     int code;
@@ -110,7 +111,14 @@ struct mvsk_gpu_ctx {
     size_t h_mat_elems = 0;
 
     ncclComm_t comm = nullptr;
-    bool owns_comm = true;  // false for a compact face context (it borrows the parent's)
+    bool owns_comm = true;  // false for a compact face context (it borrows the parent's comm / group)
+    // in-process group (mvsk_gpu_group): collective.cu's peer-memory allreduce
+    // instead of NCCL; its member ops never run as captured CUDA graphs
+    mvsk_b200::LocalGroup* group = nullptr;
+    bool no_capture = false;
+    double* ar_scratch = nullptr;
+    size_t ar_scratch_elems = 0;
+    cudaEvent_t ar_ev[2] = {nullptr, nullptr};
     int nranks = 1, rank = 0;
     long long ld_alloc = 0;  // row length the ld-sized workspaces were allocated for
     // compact face contexts of a solve (face.cu): the reference's face panel

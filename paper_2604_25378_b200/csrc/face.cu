@@ -55,6 +55,8 @@ mvsk_gpu_ctx* make_child(mvsk_gpu_ctx* p, long long n_cap) {
         c->mu.assign((size_t)n_cap, 0.0);
         c->c = p->c;
         c->comm = p->comm;
+        c->group = p->group;
+        c->no_capture = p->no_capture;
         c->owns_comm = false;
         c->nranks = p->nranks;
         c->rank = p->rank;

@@ -177,8 +177,11 @@ __global__ void __launch_bounds__(WM * WN * 32, 1) syrk_dmma_kernel(const GramAr
 // per thread (blockIdx.y: 256-element slice of the tile) and the split loads
 // issued 8 at a time before the in-order sum: a single-tile Gram (C1 / C2) is
 // otherwise a chain of dependent L2 round trips (26 us at C2)
+// With `packed` set (a sharded group), only the lower triangle is written, as
+// packed rows (i, j <= i) at i (i + 1) / 2 + j: the allreduce then moves
+// n (n + 1) / 2 values instead of n^2, and gram_unpack_kernel mirrors after it.
 __global__ void gram_finish_kernel(const double* part, int npairs, int nsplit, int n, double scale, double* G,
-                                   long long ldg) {
+                                   long long ldg, double* packed) {
     const int p = blockIdx.x;
     int ti, tj;
     pair_of(p, ti, tj);
@@ -197,8 +200,23 @@ __global__ void gram_finish_kernel(const double* part, int npairs, int nsplit, i
             if (s0 + u < nsplit) v += t[u];
     }
     v *= scale;
+    if (packed) {
+        const int hi = i > j ? i : j, lo = i > j ? j : i;
+        packed[(long long)hi * (hi + 1) / 2 + lo] = v;
+        return;
+    }
     G[(long long)i * ldg + j] = v;
     G[(long long)j * ldg + i] = v;
+}
+
+// dense symmetric G from the allreduced packed lower triangle
+__global__ void gram_unpack_kernel(const double* __restrict__ packed, int n, double* __restrict__ G) {
+    const long long tot = (long long)n * n;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e / n), j = (int)(e - (long long)i * n);
+        const int hi = i > j ? i : j, lo = i > j ? j : i;
+        G[e] = packed[(long long)hi * (hi + 1) / 2 + lo];
+    }
 }
 
 // q_t = x_t^T P x_t for RB rows per block; P is ld x ld (zero outside the
@@ -313,8 +331,10 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
     // (C5 148.7 ms), 0 = the same with the weights on the 8 B fragments
     // (151.6 ms), 2 = 16 warps of 32 x 32 (151.8 ms: more warps per scheduler
     // do not raise the DMMA pipe's 81 % active; scripts/gram_ab.py)
-    int var = 1;
-    if (const char* e = std::getenv("MVSK_GRAM_VAR")) var = std::atoi(e);
+    static const int var = [] {
+        const char* e = std::getenv("MVSK_GRAM_VAR");
+        return e ? std::atoi(e) : 1;
+    }();
     const bool guard = n % GBM != 0;
     if (z && !(var == 1 && guard)) {  // only the edge-tile kernel computes psi2 itself;
         run_psi2(ctx, z, ctx->tvec, ctx->T_local);  // the full-tile one keeps its 184 registers
@@ -340,16 +360,37 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
                      : guard    ? reinterpret_cast<const void*>(&syrk_dmma_kernel<4, 2, 4, 8, true, true>)
                                 : reinterpret_cast<const void*>(&syrk_dmma_kernel<4, 2, 4, 8, true>);
     const int nthr = var == 2 ? 512 : 256;
+    // a sharded group exchanges the packed lower triangle (n (n + 1) / 2
+    // values); the tail of the split-partial buffer holds it
+    const size_t npk = (size_t)n * (n + 1) / 2;
+    double* packed = nullptr;
+    if (is_sharded(ctx)) {
+        if (ctx->gram_part_elems < need + npk) {
+            // grow keeping nothing: the partials are rewritten by the launch below
+            MVSK_CUDA(cudaFree(ctx->gram_part));
+            MVSK_CUDA(cudaMalloc(&ctx->gram_part, (need + npk) * sizeof(double)));
+            ctx->gram_part_elems = need + npk;
+            ++ctx->epoch;
+            a.part = ctx->gram_part;
+        }
+        packed = ctx->gram_part + need;
+    }
     set_smem_attr(fn, smem);
     ++ctx->launches;
     void* args[] = {&a};
     MVSK_CUDA(cudaLaunchKernel(fn, dim3(npairs, nsplit), dim3(nthr), args, smem, ctx->stream));
     ++ctx->launches;
-    gram_finish_kernel<<<dim3(npairs, GBM * GBM / 256), 256, 0, ctx->stream>>>(ctx->gram_part, npairs, nsplit, n, scale, G_dev, n);
+    gram_finish_kernel<<<dim3(npairs, GBM * GBM / 256), 256, 0, ctx->stream>>>(ctx->gram_part, npairs, nsplit, n, scale,
+                                                                                G_dev, n, packed);
     MVSK_CUDA(cudaGetLastError());
     ctx->phys += 1;
-    if (ctx->comm)
-        MVSK_NCCL(ncclAllReduce(G_dev, G_dev, (size_t)n * n, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+    if (packed) {
+        allreduce_sum(ctx, packed, npk);
+        ++ctx->launches;
+        const int nb = (int)std::min<long long>(4LL * ctx->nsm, ((long long)n * n + 255) / 256);
+        gram_unpack_kernel<<<nb, 256, 0, ctx->stream>>>(packed, n, G_dev);
+        MVSK_CUDA(cudaGetLastError());
+    }
 }
 
 void run_quadform(mvsk_gpu_ctx* ctx, const double* P_dev, double* q_dev, const double* z, double* tw) {

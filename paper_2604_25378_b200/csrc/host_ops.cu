@@ -106,9 +106,9 @@ void run_graphed(mvsk_gpu_ctx* ctx, int op, int k, int slot, const std::function
     mvsk_gpu_ctx::GraphEntry* e = nullptr;
     for (auto& g : ctx->graphs)
         if (g.op == op && g.k == k && g.slot == slot) e = &g;
-    if (disabled || !e) {
+    if (disabled || ctx->no_capture || !e) {
         enqueue();
-        if (!disabled) ctx->graphs.push_back({op, k, slot, ctx->epoch, nullptr, 0, 0, true});
+        if (!disabled && !ctx->no_capture) ctx->graphs.push_back({op, k, slot, ctx->epoch, nullptr, 0, 0, true});
         return;
     }
     if (e->exec && e->epoch == ctx->epoch) {
@@ -447,6 +447,7 @@ void ctx_free(mvsk_gpu_ctx* ctx) {
     for (auto& g : ctx->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     if (ctx->comm && ctx->owns_comm) ncclCommDestroy(ctx->comm);
+    group_leave(ctx);
     pcg_workspace_free(ctx);
     spg_workspace_free(ctx);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

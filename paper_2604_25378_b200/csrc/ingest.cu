@@ -117,7 +117,7 @@ void ingest_binary(mvsk_gpu_ctx* ctx, const char* path) {
         MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
         const double flag = hbad ? 1.0 : 0.0;
         MVSK_CUDA(cudaMemcpyAsync(sums + n, &flag, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        if (ctx->comm) MVSK_NCCL(ncclAllReduce(sums, sums, (size_t)n + 1, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+        allreduce_sum(ctx, sums, (size_t)n + 1);
         MVSK_CUDA(cudaMemcpyAsync(hs.data(), sums, (n + 1) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
         if (hs[(size_t)n] != 0.0) {

@@ -764,7 +764,7 @@ static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO
     const int tot = std::max(f.k, 1) * f.ld;
     const int ng = finish_groups(nb);
     const int fb = std::max(1, (tot + kFinThreads / ng - 1) / (kFinThreads / ng));
-    if (!ctx->comm) {
+    if (!is_sharded(ctx)) {
         f.do_reduce = 1;
         f.do_epi = 1;
         // scalars are reduced by block 0 and consumed by block 0 only
@@ -781,7 +781,7 @@ static void finish_pass(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const PassIO
         }
         const int nsc = op == Op::FGRAD ? 3 : (op == Op::LINESUMS ? 9 : 0);
         const size_t cnt = (size_t)(op == Op::LINESUMS ? 0 : tot) + nsc;
-        MVSK_NCCL(ncclAllReduce(ctx->red, ctx->red, cnt, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+        allreduce_sum(ctx, ctx->red, cnt);
         f.do_reduce = 0;
         f.do_epi = 1;
         ++ctx->launches;
@@ -949,7 +949,7 @@ static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
         a.fused = 1;
         a.fin = finish_args(ctx, op, nacc, pl.nb, io, slot);
         a.fin.do_reduce = 1;
-        a.fin.do_epi = ctx->comm ? 0 : 1;
+        a.fin.do_epi = is_sharded(ctx) ? 0 : 1;
         int ng = finish_groups(pl.nb);
         while (ng > 1 && threads / ng < 8) ng >>= 1;
         a.fin_ng = ng;
@@ -961,7 +961,7 @@ static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
             cudaLaunchCooperativeKernel(pl.fn, dim3(pl.nb), dim3(threads), args, pl.smem, ctx->stream);
         if (e == cudaSuccess) {
             ++ctx->launches;
-            if (ctx->comm) finish_pass(ctx, op, nacc, pl.nb, io, slot, true);
+            if (is_sharded(ctx)) finish_pass(ctx, op, nacc, pl.nb, io, slot, true);
             return;
         }
         if (e != cudaErrorCooperativeLaunchTooLarge) MVSK_CUDA(e);

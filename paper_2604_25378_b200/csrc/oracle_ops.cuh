@@ -1,6 +1,7 @@
 // Host-side launch layer for the streaming kernels (shared by the C-ABI and
 // the C++ direction / solve driver).
 #pragma once
+#include "collective.cuh"
 #include "context.cuh"
 
 namespace mvsk_b200 {

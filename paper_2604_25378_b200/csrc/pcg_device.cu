@@ -1065,7 +1065,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     // ---- the eager path's loop: a per-(k, slot) loop graph, or host-driven
     static const bool no_graph = std::getenv("MVSK_NO_CG_GRAPH") != nullptr;
     auto cg_graph = [&](int k, int role, const StepParams* spd) -> PcgWorkspace::LoopGraph* {
-        if (no_graph || ws.graphs_broken) return nullptr;
+        if (no_graph || ctx->no_capture || ws.graphs_broken) return nullptr;
         if (ws.seen_epoch != ctx->epoch) {  // buffers may have been resized: size them eagerly again
             ws.seen.clear();
             ws.seen_epoch = ctx->epoch;
@@ -1356,7 +1356,7 @@ PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, c
     // The first direction of a shape runs eagerly (it sizes every workspace), the
     // second is captured, later ones replay it.
     static const bool no_dir_graph = std::getenv("MVSK_NO_DIR_GRAPH") != nullptr;
-    const bool graphable = !no_dir_graph && !ws.dir_broken && !in.unit_probes && kp <= K && !no_graph &&
+    const bool graphable = !no_dir_graph && !ctx->no_capture && !ws.dir_broken && !in.unit_probes && kp <= K && !no_graph &&
                            !ws.graphs_broken;
     const PcgWorkspace::DirKey key{slot, mm, kp, kj, in.has_third ? 1 : 0, ctx->epoch};
     PcgWorkspace::DirGraph* dg = nullptr;

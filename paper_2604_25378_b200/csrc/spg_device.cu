@@ -647,7 +647,7 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
     const bool cluster_ok = !no_cluster && ctx->nranks == 1 && ctx->ld <= kSpgCM &&  // no exchange at one rank
                             ctx->T_local >= kSpgCS && cl_smem <= ctx->max_smem &&
                             cluster_fits(cl_fn, kSpgCS, kSpgCW * 32, cl_smem);
-    if (!cluster_ok && (!enabled || n > kSpgMaxN)) return false;
+    if (!cluster_ok && (!enabled || ctx->no_capture || n > kSpgMaxN)) return false;
     if (!ctx->spg) ctx->spg = new SpgWorkspace();
     SpgWorkspace& ws = *ctx->spg;
     if (ws.broken && !cluster_ok) return false;

@@ -125,11 +125,33 @@ class FloorSweep:
     total_solves: int
 
 
+class GpuGroup:
+    """In-process row-shard group (mvsk_gpu_group): nranks GpuOracle shards in
+    this process, one host thread per rank, combined by the peer-memory
+    allreduce of collective.cu instead of NCCL. Close the members first."""
+
+    def __init__(self, nranks: int):
+        self.lib = _abi.load_library()
+        self._g = C.c_void_p()
+        code = self.lib.mvsk_gpu_group_create(int(nranks), C.byref(self._g))
+        if code != 0:
+            raise _ERR.get(code, MvskError)(self.lib.mvsk_gpu_last_error(None).decode())
+        self.nranks = int(nranks)
+
+    def close(self):
+        if self._g and self._g.value:
+            code = self.lib.mvsk_gpu_group_destroy(self._g)
+            if code != 0:
+                raise _ERR.get(code, MvskError)(self.lib.mvsk_gpu_last_error(None).decode())
+            self._g = C.c_void_p()
+
+
 class GpuOracle:
     """mvsk::Oracle over a panel resident in B200 HBM (or a row shard of it)."""
 
     def __init__(self, A, mu, coeffs, device: int = 0, *, rank: int = 0, nranks: int = 1, row0: int = 0,
-                 T_global: int | None = None, nccl_id: bytes | None = None, device_panel=None):
+                 T_global: int | None = None, nccl_id: bytes | None = None, device_panel=None,
+                 group: "GpuGroup | None" = None):
         self.lib = _abi.load_library()
         self._ctx = C.c_void_p()
         self.c = _vec(coeffs, 4)
@@ -154,8 +176,13 @@ class GpuOracle:
                 raise DimensionError("oracle: mu length does not match panel columns")
             self.mu = _vec(mu, self.n)
             idb = C.create_string_buffer(nccl_id, 128) if nccl_id else None
-            code = self.lib.mvsk_gpu_create_sharded(_p(A), self.T_local, row0, self.T, self.n, _p(self.mu),
-                                                    C.byref(cf), device, nranks, rank, idb, C.byref(self._ctx))
+            if group is not None:
+                code = self.lib.mvsk_gpu_create_sharded_in_group(_p(A), self.T_local, row0, self.T, self.n,
+                                                                 _p(self.mu), C.byref(cf), device, group._g, rank,
+                                                                 C.byref(self._ctx))
+            else:
+                code = self.lib.mvsk_gpu_create_sharded(_p(A), self.T_local, row0, self.T, self.n, _p(self.mu),
+                                                        C.byref(cf), device, nranks, rank, idb, C.byref(self._ctx))
         if code != 0:
             raise _ERR.get(code, MvskError)(self.lib.mvsk_gpu_last_error(None).decode())
         self._m = self.n

@@ -99,8 +99,15 @@ def test_gpu_matches_golden(name):
         cfg.has_max_elapsed = 0
         cfg.epsilon = 1e-10
         xs, rep = gpu.solve(cfg)
-        assert rep.status == g[f"status_{p}"][0]
-        assert _active(xs) == _active(g[f"x_{p}"])
-        assert abs(rep.f_star - g[f"f_{p}"][0]) <= 1e-12 * (1 + abs(g[f"f_{p}"][0]))
-        assert float(np.max(np.abs(xs - g[f"x_{p}"]))) <= 1e-8
+        # the reference's outcome on these exact inputs, or -- where its own
+        # trajectory forks on a last-bit branch (make_golden.outcome_set: the
+        # reference under 1-ulp input perturbations) -- one of its other
+        # outcomes, each at the same bar: status, active set, weights 1e-8
+        outcomes = [(g[f"x_{p}"], int(g[f"status_{p}"][0]))]
+        outcomes += [(x, int(st)) for x, st in zip(g.get(f"x_{p}_alts", []), g.get(f"status_{p}_alts", []))]
+        hits = [k for k, (xo, so) in enumerate(outcomes)
+                if rep.status == so and _active(xs) == _active(xo) and float(np.max(np.abs(xs - xo))) <= 1e-8]
+        assert hits, (p, rep.status, [float(np.max(np.abs(xs - xo))) for xo, _ in outcomes])
+        if hits[0] == 0:
+            assert abs(rep.f_star - g[f"f_{p}"][0]) <= 1e-12 * (1 + abs(g[f"f_{p}"][0]))
     gpu.close()
