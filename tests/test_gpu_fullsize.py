@@ -95,16 +95,42 @@ def test_c5_full_size_parity_and_identities():
         assert np.max(np.abs(T8[i] - Ti)) <= 1e-11 * np.max(np.abs(Ti))
     T4 = gpu.third_action(gc, V[:4], W[:4])
     assert np.max(np.abs(T4 - T8[:4])) <= 1e-11 * np.max(np.abs(T8[:4]))
-    # the same bits on the CPU oracle (all host threads, test-only)
+    lm8 = np.array([lm.a0, lm.a1, lm.a2, lm.a3, lm.a4, *lm.sums])
+    G = gpu.weighted_gram(gc)  # DMMA Gram over the full 8 GiB panel
+    # the same bits on the CPU oracle (all host threads, test-only): every
+    # tensor-core multi-RHS result, the line model and the Gram, not just one HVP
     A = X.cpu().numpy()
     del X
     po.set_threads(os.cpu_count() or 1)
     try:
         cpu = po.CpuOracle(A, mu, c)
         cc = cpu.make_cache(x)
-        g_s, h_s = _scales(A, c, x, V[:1])
+        g_s, h_s = _scales(A, c, x, V)
         _close(gpu.value(gc), cpu.value(cc), 0.0)
         _close(g, cpu.gradient(cc), g_s)
         _close(H1, cpu.hvp(cc, V[0]), h_s[0])
+        Hc = [cpu.hvp(cc, V[i]) for i in range(8)]
+        for i in range(8):  # 8-RHS tensor-core HVP
+            _close(H[i], Hc[i], h_s[i])
+        z = A @ x
+        psi3 = np.abs(-6 * c[2] + 24 * c[3] * z)
+        absA = np.abs(A)
+        for i in range(8):  # 8-pair tensor-core third action
+            t_s = float(np.max(absA.T @ (psi3 * np.abs(A @ V[i]) * np.abs(A @ W[i])) / T))
+            _close(T8[i], cpu.third_action(cc, V[i], W[i]), t_s)
+        del absA
+        lmc = cpu.line_model(cc, V[0], 1.0)  # a0..a4 and the nine power sums
+        np.testing.assert_allclose(lm8, lmc, rtol=1e-11, atol=1e-15 * np.max(np.abs(lmc)))
+        # Gram: G v = H v for every tangent v (the same contraction, oracle.hpp:92-101
+        # vs affine_normal.hpp:169), and exact entries G_ij = sum psi''_t a_ti a_tj / T
+        for i in range(8):
+            _close(G @ V[i], Hc[i], h_s[i])
+        psi2 = cpu.hessian_diag_weights(cc)
+        rng = np.random.default_rng(3)
+        for i, j in rng.integers(0, n, size=(24, 2)):
+            ref = float(np.dot(psi2 * A[:, i], A[:, j])) / T
+            scale = float(np.dot(np.abs(psi2 * A[:, i]), np.abs(A[:, j]))) / T
+            assert abs(G[i, j] - ref) <= 1e-11 * scale, (i, j, G[i, j], ref)
+        np.testing.assert_array_equal(G, G.T)
     finally:
         po.set_threads(1)

@@ -191,7 +191,10 @@ def test_typed_errors():  # test_oracle.cpp:208-225
 
 
 def test_weighted_gram_dmma():
-    for (n, T, seed) in [(20, 500, 1), (100, 1000, 2), (131, 777, 3), (300, 2000, 4)]:
+    # 128 / 256: the full-tile kernel (psi'' precomputed by run_psi2), the others
+    # the edge-tile kernel (psi'' in its load)
+    for (n, T, seed) in [(20, 500, 1), (100, 1000, 2), (131, 777, 3), (300, 2000, 4), (128, 900, 5),
+                         (256, 1500, 6)]:
         A, mu = rh.lcg_panel(n, T, seed) if n <= 33 else (np.random.default_rng(seed).uniform(-0.1, 0.4, (T, n)), None)
         if mu is None:
             A = A - A.mean(axis=0)
@@ -207,6 +210,54 @@ def test_weighted_gram_dmma():
         scale = float(np.max((np.abs(A) * np.abs(psi2)[:, None]).T @ np.abs(A) / T))
         _close(G, ref, scale)
         assert np.array_equal(G, G.T)
+
+
+def test_weighted_gram_variants_subprocess():
+    """MVSK_GRAM_VAR (read once per process) selects the warp layout of the
+    full-tile Gram kernel; variants 0 and 2 against fp64 numpy at n = 128."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, json, numpy as np\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_2604_25378_b200.gpu_oracle import GpuOracle\n"
+        "rng = np.random.default_rng(7); A = rng.uniform(-0.1, 0.4, (1000, 128)); A -= A.mean(0)\n"
+        "c = np.array([1.0, 5.0, 55.0 / 3.0, 55.0]); x = np.full(128, 1 / 128)\n"
+        "g = GpuOracle(A, np.zeros(128), c); G = g.weighted_gram(g.make_cache(x))\n"
+        "z = A @ x; p2 = 2 * c[1] - 6 * c[2] * z + 12 * c[3] * z * z\n"
+        "ref = (A * p2[:, None]).T @ A / 1000\n"
+        "sc = float(np.max((np.abs(A) * np.abs(p2)[:, None]).T @ np.abs(A) / 1000))\n"
+        "print(json.dumps({'err': float(np.max(np.abs(G - ref))) / sc, 'sym': bool(np.array_equal(G, G.T))}))\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for var in ("0", "2"):
+        out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, MVSK_GRAM_VAR=var),
+                             capture_output=True, text=True, timeout=300, check=True)
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+        assert r["err"] <= 1e-11 and r["sym"], (var, r)
+
+
+def test_borrowed_panel_nonfinite_padding_is_rejected():
+    """create_from_device reads whole ld-wide rows; NaN padding would turn into
+    0 * NaN in every result, so it is rejected with a data error."""
+    torch = pytest.importorskip("torch")
+    from paper_2604_25378_b200.gpu_oracle import DataError, GpuOracle
+    T, n, ld = 64, 9, 12
+    rng = np.random.default_rng(1)
+    A = rng.uniform(-0.1, 0.4, (T, n))
+    A -= A.mean(0)
+    buf = torch.full((T, ld), float("nan"), dtype=torch.float64, device="cuda")
+    buf[:, :n] = torch.from_numpy(A).cuda()
+    c = rh.crra(5.0)
+    with pytest.raises(DataError):
+        GpuOracle(None, np.zeros(n), c, device_panel=(buf.data_ptr(), ld, T, n))
+    buf[:, n:] = 0.0
+    g = GpuOracle(None, np.zeros(n), c, device_panel=(buf.data_ptr(), ld, T, n))
+    x = rh.simplex_point(n, 2)
+    cpu = po.CpuOracle(A, np.zeros(n), c)
+    assert abs(g.value(g.make_cache(x)) - cpu.value(cpu.make_cache(x))) <= 1e-12
+    g.close()
 
 
 def test_datagen_configs_parity():

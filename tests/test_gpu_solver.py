@@ -20,26 +20,44 @@ def _active(x, tau):
     return tuple(np.nonzero(x <= tau + 1e-12)[0])
 
 
-def _same_solution(xg, rg, xc, rc, tau, tol=1e-8, envelope=0.0):
-    """Same status and active set, objective to 1e-12 relative, weights within
-    max(tol, 10 x the reference's own summation-order envelope)."""
+def _same_solution(xg, rg, xc, rc, tau):
+    """north_star: same status and active set, objective to 1e-12 relative,
+    weights within 1e-8 in the infinity norm."""
     assert rg.status == rc.status, (rg.status, rc.status)
     assert _active(xg, tau) == _active(xc, tau)
     assert abs(rg.f_star - rc.f_star) <= 1e-12 * (1 + abs(rc.f_star))
     dx = float(np.max(np.abs(xg - xc)))
-    assert dx <= max(tol, 10.0 * envelope), (dx, envelope)
+    assert dx <= 1e-8, dx
 
 
-def _cpu_envelope(A, mu, c, cfg):
-    """The reference's own trajectory sensitivity: the same restated solve
-    with a different (still deterministic) summation order (2 host threads)."""
-    x1, r1 = po.solve(A, mu, c, cfg)
-    po.set_threads(2)
-    try:
-        x2, r2 = po.solve(A, mu, c, cfg)
-    finally:
-        po.set_threads(1)
-    return x1, r1, float(np.max(np.abs(x1 - x2))), r2.status
+def _matches(xg, rg, xo, so, tau):
+    return (rg.status == so and _active(xg, tau) == _active(xo, tau)
+            and float(np.max(np.abs(xg - xo))) <= 1e-8)
+
+
+def _reference_outcome_match(A, mu, c, cfg_c, xg, rg, trials=40):
+    """The GPU solve must equal the reference's solve on the same inputs
+    (po is bit-identical to the compiled reference, tests/test_reference_build.py)
+    at the north_star bar. The reference branches on last-bit thresholds
+    (solver.hpp:467-492), so on some panels it forks on rounding alone; only
+    then, the GPU may instead equal -- at the same bar -- one of the outcomes
+    the reference itself produces under 1-ulp perturbations of the panel.
+    Returns the index of the matched outcome (0 = the unperturbed one)."""
+    xc, rc = po.solve(A, mu, c, cfg_c)
+    if _matches(xg, rg, xc, rc.status, cfg_c.tau):
+        assert abs(rg.f_star - rc.f_star) <= 1e-12 * (1 + abs(rc.f_star))
+        return 0
+    rng = np.random.default_rng(12345)
+    dxs = [float(np.max(np.abs(xg - xc)))]
+    for k in range(trials):
+        Ap = A.copy()
+        m = rng.random(Ap.shape) < 0.3
+        Ap[m] = np.nextafter(Ap[m], np.where(rng.random(int(m.sum())) < 0.5, -np.inf, np.inf))
+        xp, rp = po.solve(Ap, mu, c, cfg_c)
+        if _matches(xg, rg, xp, rp.status, cfg_c.tau):
+            return k + 1
+        dxs.append(float(np.max(np.abs(xg - xp))))
+    raise AssertionError(f"GPU outcome (status {rg.status}) matches no reference outcome: dx {min(dxs):.3e}")
 
 
 def test_descent_identity_and_direction_parity():  # test_affine_normal.cpp:44-73
@@ -105,27 +123,23 @@ def test_two_asset_and_stationary():  # test_affine_normal.cpp:102-119, 146-159
 def test_small_preset_parity(seed, eps):  # test_solver.cpp:47-70
     """The reference driver branches on last-bit thresholds (e.g. al > 0 with a
     cap of (x_i - tau)/(-d_i) at a floor coordinate, solver.hpp:486-492), so its
-    trajectory changes under any summation reorder (profiles/r01_solve_parity_survey.txt).
+    trajectory can fork on rounding alone (_reference_outcome_match).
     At the default epsilon both sides converge (KKT <= eps) to the same active
-    set and objective; at a tight epsilon the weights agree to 1e-8 (or within
-    the reference's own reorder envelope)."""
+    set and objective; at a tight epsilon the weights agree to 1e-8."""
     from paper_2604_25378_b200.gpu_oracle import preset
     n = 5 + 3 * seed
     A, mu = rh.lcg_panel(n, 60, seed + 7)
     c = rh.crra(4.0 + seed)
     cfg_c, cfg_g = po.preset("small"), preset("small")
     cfg_c.epsilon = cfg_g.epsilon = eps
-    xc, rc, env, st2 = _cpu_envelope(A, mu, c, cfg_c)
+    xc, rc = po.solve(A, mu, c, cfg_c)
     xg, rg = _gpu(A, mu, c).solve(cfg_g)
     if eps == 1e-6:
         assert rg.status == rc.status == 0 and rg.kkt_residual <= eps and rc.kkt_residual <= eps
         assert _active(xg, 1e-8) == _active(xc, 1e-8)
         assert abs(rg.f_star - rc.f_star) <= 1e-10 * (1 + abs(rc.f_star))
     else:
-        if st2 != rc.status:  # the reference itself changes status under reordering
-            assert rg.status in (rc.status, st2)
-            rg.status = rc.status
-        _same_solution(xg, rg, xc, rc, 1e-8, envelope=env)
+        _reference_outcome_match(A, mu, c, cfg_c, xg, rg)
 
 
 def test_two_asset_closed_form():  # test_solver.cpp:32-45
@@ -161,8 +175,8 @@ def test_dominated_pin_observer_and_determinism():  # test_solver.cpp:72-119, 18
             assert r1.face_events >= 1
         cfg_c = po.preset(label)
         cfg_c.has_max_elapsed = 0
-        xc, rc, env, _ = _cpu_envelope(A, mu, c, cfg_c)
-        _same_solution(x1, r1, xc, rc, 1e-8, envelope=env)
+        xc, rc = po.solve(A, mu, c, cfg_c)
+        _same_solution(x1, r1, xc, rc, 1e-8)
         if label == "large":
             # the SPG preamble's step count is itself reorder-sensitive
             assert r1.identification_steps > 0 and rc.identification_steps > 0
@@ -173,9 +187,10 @@ def test_dominated_pin_observer_and_determinism():  # test_solver.cpp:72-119, 18
                                              ("C2", 10.0, "large"), ("C2", 100.0, "large"), ("C2", 1000.0, "large")])
 def test_config_solve_parity(name, kappa, mode):
     """BASELINE configs 1-2 (direct and PCG, kappa sweep) at a tight epsilon:
-    same status and active set, objective to 1e-12, weights to 1e-8 (or the
-    reference's own reorder envelope). max_elapsed is disabled so the outcome
-    cannot depend on speed (SURVEY.md §7 hard part a)."""
+    same status and active set, objective to 1e-12, weights to 1e-8 against
+    the reference's solve (or, where the reference itself forks on rounding,
+    one of its own outcomes: _reference_outcome_match). max_elapsed is
+    disabled so the outcome cannot depend on speed (SURVEY.md §7 hard part a)."""
     from paper_2604_25378_b200.datagen import make_panel
     from paper_2604_25378_b200.gpu_oracle import preset
     A, mu, c = make_panel(name, seed=11, kappa=kappa)
@@ -183,25 +198,8 @@ def test_config_solve_parity(name, kappa, mode):
     for cfg in (cfg_c, cfg_g):
         cfg.has_max_elapsed = 0
         cfg.epsilon = 1e-10
-    xc, rc, env, _ = _cpu_envelope(A, mu, c, cfg_c)
-    g = _gpu(A, mu, c)
-    xg, rg = g.solve(cfg_g)
-    assert rg.status == rc.status, (rg.status, rc.status)
-    assert _active(xg, cfg_g.tau) == _active(xc, cfg_g.tau)
-    assert abs(rg.f_star - rc.f_star) <= 1e-12 * (1 + abs(rc.f_star))
-    dx = float(np.max(np.abs(xg - xc)))
-    if dx > max(1e-8, 10.0 * env):
-        # an epsilon-solution is only determined to ~ residual / curvature: a run
-        # that stops with its residual just under 1e-10 can sit ~5e-8 from one
-        # that overshot to 1e-14 (C2 kappa=1 small). Drive both to 1e-12, where
-        # the weights are determined, and require 1e-8 there.
-        for cfg in (cfg_c, cfg_g):
-            cfg.epsilon = 1e-12
-        xc2, rc2, env2, _ = _cpu_envelope(A, mu, c, cfg_c)
-        xg2, rg2 = g.solve(cfg_g)
-        assert _active(xg2, cfg_g.tau) == _active(xc2, cfg_g.tau)
-        dx2 = float(np.max(np.abs(xg2 - xc2)))
-        assert dx2 <= max(1e-8, 10.0 * env2), (dx, dx2, env2, rg.kkt_residual, rc.kkt_residual)
+    xg, rg = _gpu(A, mu, c).solve(cfg_g)
+    _reference_outcome_match(A, mu, c, cfg_c, xg, rg)
 
 
 def test_device_pcg_matches_host_pcg(monkeypatch):
@@ -283,7 +281,7 @@ def test_cpp_host_solves_a_binary_panel(tmp_path):
     assert rc.status == 0
     assert abs(rep["f_star"] - rc.f_star) <= 1e-12 * (1 + abs(rc.f_star))
     assert _active(xg, 1e-8) == _active(xc, 1e-8)
-    assert np.max(np.abs(xg - xc)) <= 1e-7
+    assert np.max(np.abs(xg - xc)) <= 1e-8
     # the return-floor sweep through the same C++ host
     r = subprocess.run([str(exe), str(path), "--gamma", "10", "--preset", "large", "--floor-sweep", "3",
                         "--no-max-elapsed"], capture_output=True, text=True, timeout=300)
@@ -321,9 +319,9 @@ def test_floor_sweep_matches_cpu_mirror(name, mode, nfloors):
     for k, p in enumerate(out.points):
         b = ref["best"][k]
         assert p["c1"] == b["c1"], (k, p["c1"], b["c1"])
-        assert abs(p["mean"] - b["mean"]) <= 1e-7 * span
+        assert abs(p["mean"] - b["mean"]) <= 1e-9 * span
         assert abs(p["mean"] - p["floor"]) <= 1e-3 * span or p["solves"] >= 16
-        assert float(np.max(np.abs(out.X[k] - b["x"]))) <= 1e-6
+        assert float(np.max(np.abs(out.X[k] - b["x"]))) <= 1e-8
     # coefficients restored
     x = rh.simplex_point(A.shape[1], 3, 1e-3)
     cc = po.CpuOracle(A, mu, c).make_cache(x)
@@ -373,7 +371,7 @@ def test_compact_faces_match_cpu_and_index_maps():
     solver.hpp:343-363). BASELINE config 3 (n = 800, support ~20): the compact
     path agrees with the CPU restatement and with the index-map faces
     (MVSK_NO_FACE_COMPACT, run in a subprocess because the switch is read once)
-    on status, active set and objective, weights within the solve envelope."""
+    on status, active set and objective, weights to 1e-8."""
     import json
     import os
     import subprocess
@@ -388,7 +386,7 @@ def test_compact_faces_match_cpu_and_index_maps():
         cfg.epsilon = 1e-10
     xg, rg = _gpu(A, mu, c).solve(cfg_g)
     xc, rc = po.solve(A, mu, c, cfg_c)
-    _same_solution(xg, rg, xc, rc, cfg_g.tau, tol=1e-6)
+    _same_solution(xg, rg, xc, rc, cfg_g.tau)
     code = (
         "import json, sys, numpy as np\n"
         "sys.path.insert(0, %r)\n"
@@ -406,7 +404,7 @@ def test_compact_faces_match_cpu_and_index_maps():
     assert ref["status"] == rg.status
     assert _active(xi, cfg_g.tau) == _active(xg, cfg_g.tau)
     assert abs(ref["f"] - rg.f_star) <= 1e-12 * (1 + abs(rg.f_star))
-    assert float(np.max(np.abs(xi - xg))) <= 1e-6
+    assert float(np.max(np.abs(xi - xg))) <= 1e-8
 
 
 def _solve_subprocess(name, kappa, env_extra, eps=None):
