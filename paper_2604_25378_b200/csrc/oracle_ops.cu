@@ -17,14 +17,37 @@ namespace {
 
 struct Plan {
     int Q = 1, P = 32, G = 1, RG = 1, S = 2;
+    bool VS = false;  // input vectors in shared memory (stream_kernel<..., VS>)
     size_t smem = 0;
     int nb = 1;
     const void* fn = nullptr;
 };
 
-template <Op OP, int K, int Q, int RG>
+template <Op OP, int K, int Q, int RG, bool VS = false>
 const void* kfn() {
-    return reinterpret_cast<const void*>(&stream_kernel<OP, K, Q, RG>);
+    return reinterpret_cast<const void*>(&stream_kernel<OP, K, Q, RG, VS>);
+}
+
+// wide rows on short panels (C4: 34 rows of 40 KB per SM): the input vector in
+// shared memory frees the registers for two 160-thread row teams per CTA
+const void* select_kernel_vs(Op op, int K, int Q, int RG) {
+    if (RG != 1 || K != 1) return nullptr;
+    switch (op) {
+    case Op::FGRAD:
+        if (Q == 8) return kfn<Op::FGRAD, 1, 8, 1, true>();
+        if (Q == 16) return kfn<Op::FGRAD, 1, 16, 1, true>();
+        break;
+    case Op::LINESUMS:
+        if (Q == 8) return kfn<Op::LINESUMS, 1, 8, 1, true>();
+        if (Q == 16) return kfn<Op::LINESUMS, 1, 16, 1, true>();
+        break;
+    case Op::HVP:
+        if (Q == 8) return kfn<Op::HVP, 1, 8, 1, true>();
+        if (Q == 16) return kfn<Op::HVP, 1, 16, 1, true>();
+        break;
+    default: break;
+    }
+    return nullptr;
 }
 
 // (Q, RG) pairs instantiated for every op: RG * Q <= 8 keeps the staged row
@@ -98,8 +121,8 @@ int op_ndot(Op op, int K) {
 int op_nacc(Op op, int K) { return (op == Op::HVP || op == Op::THIRD) ? K : (op == Op::LINESUMS ? 0 : 1); }
 
 // mirror of StreamRegs<>::max_threads (stream_kernels.cuh)
-int max_threads(Op op, int K, int Q, int RG) {
-    const int nv = std::max(op_ndot(op, K), 1), na = std::max(op_nacc(op, K), 1);
+int max_threads(Op op, int K, int Q, int RG, bool vs = false) {
+    const int nv = vs ? 0 : std::max(op_ndot(op, K), 1), na = std::max(op_nacc(op, K), 1);
     const int live = 2 * Q * (nv + na + RG);
     return live <= 48 ? 512 : (live <= 64 ? 384 : 256);
 }
@@ -116,12 +139,55 @@ int round_team(int need) {
 // MVSK_TUNE="Q,G,RG,S,OCC" (0 = heuristic) overrides the plan; used by the
 // tuning sweep only (scripts/tune_stream.py)
 struct TuneOverride {
-    int Q = 0, G = 0, RG = 0, S = 0, OCC = 0;
+    int Q = 0, G = 0, RG = 0, S = 0, OCC = 0, VS = -1;
 };
 TuneOverride tune_override() {
     TuneOverride t;
-    if (const char* e = std::getenv("MVSK_TUNE")) std::sscanf(e, "%d,%d,%d,%d,%d", &t.Q, &t.G, &t.RG, &t.S, &t.OCC);
+    if (const char* e = std::getenv("MVSK_TUNE"))
+        std::sscanf(e, "%d,%d,%d,%d,%d,%d", &t.Q, &t.G, &t.RG, &t.S, &t.OCC, &t.VS);
     return t;
+}
+
+// wide-row plan for short panels: the input vector in shared memory, Q = 16
+// column pairs per thread, two row teams per CTA (MVSK_TUNE 6th field: 1/0
+// forces it on / off for the ops that have it)
+// Default only for f+grad, where it measured faster (C4: 50.6 -> 46.6 us; the
+// 1-RHS HVP and line sums were unchanged, profiles/r02_tune_c4_vs.txt)
+bool make_plan_vs(const mvsk_gpu_ctx* ctx, Op op, int K, const TuneOverride& tov, Plan& pl) {
+    const long long npairs = ctx->ld / 2;
+    const bool small = ctx->T_local < 64LL * ctx->nsm;
+    const bool want = tov.VS >= 0 ? tov.VS == 1 : (small && npairs >= 1024 && op == Op::FGRAD);
+    if (!want) return false;
+    const int Q = tov.Q > 0 ? tov.Q : 16;
+    if (!select_kernel_vs(op, K, Q, 1)) return false;
+    const int P = round_team((int)((npairs + Q - 1) / Q));
+    const int mt = max_threads(op, K, Q, 1, true);
+    int G = tov.G > 0 ? tov.G : std::max(1, std::min(4, mt / P));
+    if (G * P > mt) return false;
+    const size_t row_bytes = (size_t)ctx->ld * sizeof(double);
+    const size_t stage_bytes = ((size_t)G * row_bytes + 127) & ~(size_t)127;
+    const int ndot = op_ndot(op, K), nacc = op_nacc(op, K);
+    const int nwp = P >= 32 ? P / 32 : 1;
+    const size_t red_bytes = (((size_t)2 * G * std::max(ndot, 1) * nwp * sizeof(double)) + 127) & ~(size_t)127;
+    const size_t vs_bytes = ((size_t)ndot * ctx->ld * sizeof(double) + 127) & ~(size_t)127;
+    const size_t combine = ((size_t)G * std::max(nacc, 1) * ctx->ld + 16 + (size_t)G * 16) * sizeof(double);
+    const size_t combine_all = std::max(combine, (size_t)(G * P) * sizeof(double));
+    const int nst_total = (int)std::max<long long>(1, (ctx->T_local + G - 1) / G);
+    int S = tov.S >= 2 ? tov.S : 3;
+    S = std::min(S, std::max(2, nst_total));
+    auto smem_of = [&](int s) { return 128 + red_bytes + vs_bytes + std::max((size_t)s * stage_bytes, combine_all); };
+    while (S > 2 && smem_of(S) > ctx->max_smem) --S;
+    if (smem_of(S) > ctx->max_smem) return false;
+    pl.Q = Q;
+    pl.P = P;
+    pl.G = G;
+    pl.RG = 1;
+    pl.S = S;
+    pl.VS = true;
+    pl.smem = smem_of(S);
+    pl.fn = select_kernel_vs(op, K, Q, 1);
+    pl.nb = (int)std::min<long long>(ctx->nsm, std::max<long long>(1, (ctx->T_local + G - 1) / G));
+    return true;
 }
 
 // Launch plan. Measured on B200 at C5 (profiles/r01_tune_c5.txt): teams of
@@ -129,6 +195,7 @@ TuneOverride tune_override() {
 // different rows, a 2-deep ring of 64 KB stages -> 7.1-7.4 TB/s streamed.
 bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     const TuneOverride tov = tune_override();
+    if (make_plan_vs(ctx, op, K, tov, pl)) return true;
     const long long npairs = ctx->ld / 2;
     const int qmax = max_q(op, K);
     // small panels (< 64 rows per SM) are latency-bound: favour short teams and

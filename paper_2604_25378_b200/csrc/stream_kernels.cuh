@@ -83,20 +83,23 @@ struct OpShape {
 // fp64 values a thread keeps live across a stage: input vectors, accumulators
 // and the staged row slice. Heavy variants are capped at 384 / 256 threads so
 // they may use up to 168 / 255 registers; light ones allow 512 (128 registers).
-template <Op OP, int K, int Q, int RG>
+// VS: the input vectors live in shared memory instead of registers (wide rows
+// on short panels: the freed registers let two row teams share a CTA).
+template <Op OP, int K, int Q, int RG, bool VS = false>
 struct StreamRegs {
-    static constexpr int NV = OpShape<OP, K>::NDOT > 0 ? OpShape<OP, K>::NDOT : 1;
+    static constexpr int NV = VS ? 0 : (OpShape<OP, K>::NDOT > 0 ? OpShape<OP, K>::NDOT : 1);
     static constexpr int NA = OpShape<OP, K>::NACC > 0 ? OpShape<OP, K>::NACC : 1;
     static constexpr int live = 2 * Q * (NV + NA + RG);
     static constexpr int max_threads = live <= 48 ? 512 : (live <= 64 ? 384 : 256);
 };
 
-template <Op OP, int K, int Q, int RG>
-__global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG>::max_threads, 1) stream_kernel(const StreamArgs a) {
+template <Op OP, int K, int Q, int RG, bool VS = false>
+__global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG, VS>::max_threads, 1) stream_kernel(const StreamArgs a) {
     using Sh = OpShape<OP, K>;
     constexpr int NDOT = Sh::NDOT;
     constexpr int NACC = Sh::NACC;
-    constexpr int NV = NDOT > 0 ? NDOT : 1;
+    static_assert(!VS || NDOT > 0, "VS needs input vectors");
+    constexpr int NV = (NDOT > 0 && !VS) ? NDOT : 1;
     constexpr int NA = NACC > 0 ? NACC : 1;
     constexpr int NDR = NDOT > 0 ? NDOT : 1;
 
@@ -112,11 +115,13 @@ __global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG>::max_threads, 1) stre
     const int wg = P >= 32 ? p >> 5 : 0;   // warp index within team
     const long long ld = a.ld;
 
-    // ---- shared memory carve: [mbar S][red 2 x R x NDR x nwp][stages S x R x ld]
+    // ---- shared memory carve: [mbar S][red 2 x R x NDR x nwp][VS: NDOT x ld][stages S x R x ld]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     double* red = reinterpret_cast<double*>(smem_raw + 128);
     const int red_elems = 2 * R * NDR * nwp;
     size_t off = 128 + (((size_t)red_elems * sizeof(double) + 127) & ~(size_t)127);
+    double* vsm = reinterpret_cast<double*>(smem_raw + off);
+    if constexpr (VS) off += ((size_t)NDOT * ld * sizeof(double) + 127) & ~(size_t)127;
     const size_t stage_bytes = ((size_t)R * ld * sizeof(double) + 127) & ~(size_t)127;
     unsigned char* stage_base = smem_raw + off;
 
@@ -131,6 +136,17 @@ __global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG>::max_threads, 1) stre
     if (tid == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
         fence_mbar_init();
+    }
+    if constexpr (VS) {  // input vectors -> shared memory once (L2-resident, a few KB)
+        for (int e = tid; e < NDOT * (int)a.npairs; e += (int)blockDim.x) {
+            const int k = e / a.npairs, j = e - k * a.npairs;
+            const double* src;
+            if constexpr (OP == Op::THIRD)
+                src = (k < K) ? a.vin + (long long)k * ld : a.vin2 + (long long)(k - K) * ld;
+            else
+                src = a.vin + (long long)k * ld;
+            reinterpret_cast<double2*>(vsm + (long long)k * ld)[j] = reinterpret_cast<const double2*>(src)[j];
+        }
     }
     __syncthreads();
     if (tid == 0) {
@@ -152,7 +168,7 @@ __global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG>::max_threads, 1) stre
         for (int q = 0; q < Q; ++q) {
             const int j = p + q * P;
             double2 v = make_double2(0.0, 0.0);
-            if constexpr (NDOT > 0) {
+            if constexpr (NDOT > 0 && !VS) {
                 if (j < a.npairs) {
                     const double* src;
                     if constexpr (OP == Op::THIRD)
@@ -227,8 +243,16 @@ __global__ void __launch_bounds__(StreamRegs<OP, K, Q, RG>::max_threads, 1) stre
                 if constexpr (NDOT > 0) {
 #pragma unroll
                     for (int q = 0; q < Q; ++q) {
-                        d0 = fma(x[rr][q].x, vreg[k][q].x, d0);
-                        d1 = fma(x[rr][q].y, vreg[k][q].y, d1);
+                        double2 vv;
+                        if constexpr (VS) {
+                            const int j = p + q * P;
+                            vv = j < a.npairs ? reinterpret_cast<const double2*>(vsm + (long long)k * ld)[j]
+                                              : make_double2(0.0, 0.0);
+                        } else {
+                            vv = vreg[k][q];
+                        }
+                        d0 = fma(x[rr][q].x, vv.x, d0);
+                        d1 = fma(x[rr][q].y, vv.y, d1);
                     }
                 }
                 dot[rr][k] = d0 + d1;
