@@ -17,6 +17,7 @@ namespace mvsk_b200 {
 struct PcgWorkspace;
 struct SpgWorkspace;
 struct LocalGroup;  // in-process row-shard group (collective.cu)
+struct GramPcgWs;   // Gram-PCG direction workspace (gram_pcg.cu)
 
 struct ApiError : std::runtime_error {
     int code;
@@ -101,6 +102,7 @@ struct mvsk_gpu_ctx {
     double* pmat = nullptr;  // ld x ld (lazy)
     mvsk_b200::PcgWorkspace* pcg = nullptr;  // device-resident PCG buffers (lazy)
     mvsk_b200::SpgWorkspace* spg = nullptr;  // device-resident SPG preamble (lazy)
+    mvsk_b200::GramPcgWs* gpcg = nullptr;     // reduced-Hessian PCG directions (lazy)
     double* gram_part = nullptr;
     size_t gram_part_elems = 0;
     // pinned host staging

@@ -700,7 +700,9 @@ Vec yand_direction(const View& O, int slot, const TangentCfg& cfg, uint64_t it_s
                 }
             }
         }
-        PcgOutput po = pcg_direction_device(ctx, slot, O.fm, in);
+        static const bool no_gram_pcg = std::getenv("MVSK_NO_GRAM_PCG") != nullptr;
+        PcgOutput po;
+        if (no_gram_pcg || !pcg_direction_gram(ctx, slot, O.fm, in, po)) po = pcg_direction_device(ctx, slot, O.fm, in);
         u = std::move(po.u);
         diag.krylov_iters += po.iters;
         if (po.breakdown) diag.pcg_breakdown = 1;

@@ -449,6 +449,7 @@ void ctx_free(mvsk_gpu_ctx* ctx) {
     if (ctx->comm && ctx->owns_comm) ncclCommDestroy(ctx->comm);
     group_leave(ctx);
     pcg_workspace_free(ctx);
+    gram_pcg_workspace_free(ctx);
     spg_workspace_free(ctx);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;

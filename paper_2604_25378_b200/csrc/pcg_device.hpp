@@ -33,5 +33,10 @@ struct PcgOutput {
 struct PcgWorkspace;
 PcgOutput pcg_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const PcgInput& in);
 void pcg_workspace_free(mvsk_gpu_ctx* ctx);
+// narrow faces (m <= 112, Hutchinson or no third term): every Hop through the
+// reduced Hessian M = (UQ)^T G (UQ) built from one weighted-Gram pass
+// (gram_pcg.cu); false when the face is out of its range
+bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const PcgInput& in, PcgOutput& out);
+void gram_pcg_workspace_free(mvsk_gpu_ctx* ctx);
 
 }  // namespace mvsk_b200
