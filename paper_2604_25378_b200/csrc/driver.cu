@@ -991,6 +991,10 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
         long long nf = n0;
         double mass = 1.0;
         View face{ctx, full_face(ctx)};
+        // the face cache made right after a move (at the merged point, below)
+        // serves the next iteration's cache when its face point is that point
+        bool face_cached = false;
+        Vec face_cached_xf;
 
         while (it < budget) {
             if (config.max_elapsed && elapsed() > *config.max_elapsed) {
@@ -1028,6 +1032,7 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
                 mass = 1.0 - (double)npinned * tau;
                 t_cur = tr;
                 rebuild = false;
+                face_cached = false;
             }
             Vec xf((size_t)nf);
             {
@@ -1035,7 +1040,9 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
                 for (long long i = 0; i < n0; ++i)
                     if (free_mask[(size_t)i]) xf[j++] = x[(size_t)i];
             }
-            const double fcur = face.make_cache(kSlotFace, xf);
+            const double fcur = (face_cached && xf == face_cached_xf) ? op_value(face.ctx, kSlotFace)
+                                                                       : face.make_cache(kSlotFace, xf);
+            face_cached = false;
             const Vec gf = face.gradient(kSlotFace);
             const double gf_mean = vmean(gf);
             double face_res = 0.0;
@@ -1217,7 +1224,21 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
             }
             if (moved) {  // :564-581
                 x = merge(xf, free_mask, pinned);
-                const double fv_new = full_value(x);
+                // f(x) through the face oracle at the merged point: the face
+                // panel, its pinned offset zoff and value offset make face values
+                // equal full objective values (oracle.hpp:31-45, solver.hpp:357-363;
+                // merge puts the pinned coordinates exactly at tau), so one narrow
+                // pass replaces the reference's full-panel evaluation, and the
+                // next iteration reuses the cache
+                Vec xfn((size_t)nf);
+                {
+                    size_t j = 0;
+                    for (long long i = 0; i < n0; ++i)
+                        if (free_mask[(size_t)i]) xfn[j++] = x[(size_t)i];
+                }
+                const double fv_new = face.make_cache(kSlotFace, xfn);
+                face_cached = true;
+                face_cached_xf = std::move(xfn);
                 const double dec = (fcur - fv_new) / (1.0 + std::abs(fcur));
                 if (dec < 1e-12) t_cur = std::max(std::min(0.5 * t_cur, 0.99 * amax), 1e-10);
                 if (dec >= 1e-12 || face_res <= 0.9 * face_ref) {

@@ -19,8 +19,12 @@
 //
 // The logical pass counters follow the reference's contract (2 per Hop,
 // 3 per third action; common.hpp:27-37), from the per-column HVP counts.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 
@@ -82,6 +86,7 @@ struct GramPcgWs {
     double* t3 = nullptr;        // third-action rows (np x ld)
     double* res = nullptr;       // u (mm), counters (16)
     double* h_res = nullptr;     // pinned readback
+    double* Gf = nullptr;        // group members: the m x m face Gram before / after the allreduce
 };
 
 namespace {
@@ -122,54 +127,47 @@ __device__ void warp_reflect(double* y, const double* v, double beta, int n, int
     __syncwarp();
 }
 
-// Capped CG (cg_capped, affine_normal.hpp:85-113) for `nc` columns in
-// lock-step on M (mm x mm, row stride ldm) + lambda I, Jacobi-preconditioned
-// when jd != null. Column c: rhs in B + c*mm; solution written to X + c*mm.
-// Scratch: R, Z, P, HP (nc x mm each). Per-column counters: it (iterations),
-// nhvp (operator applications), bd (breakdown). Whole CTA.
-__device__ void cg_block(const double* M, int ldm, int mm, int nc, double lambda, const double* jd, double tol,
-                         int cap, const double* B, double* X, double* R, double* Z, double* P, double* HP,
-                         int* it, int* nhvp, int* bd, int* active, double* rz, double* target) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // init (warp c owns column c)
-    if (warp < nc) {
-        const int c = warp;
-        const double* b = B + c * mm;
-        double* x = X + c * mm;
-        double* r = R + c * mm;
-        double* z = Z + c * mm;
-        double* p = P + c * mm;
-        for (int i = lane; i < mm; i += 32) {
-            x[i] = 0.0;
-            r[i] = b[i];
-            z[i] = jd ? b[i] / jd[i] : b[i];
-            p[i] = z[i];
-        }
-        __syncwarp();
-        const double rzc = warp_dot(r, z, mm, lane);
-        const double bn = sqrt(warp_dot(b, b, mm, lane));
-        const double rn = sqrt(warp_dot(r, r, mm, lane));
-        if (lane == 0) {
-            rz[c] = rzc;
-            target[c] = tol * bn;
-            it[c] = 0;
-            nhvp[c] = 0;
-            bd[c] = 0;
-            active[c] = (0 < cap && rn > tol * bn) ? 1 : 0;
-        }
+// row stride of M in shared / global memory: = 1 (mod 16), so the lanes of a
+// warp reading rows i = lane + 32k hit distinct bank pairs
+__host__ __device__ inline int m_stride(int mm) { return (mm + 15) / 16 * 16 + 1; }
+
+// Capped CG (cg_capped, affine_normal.hpp:85-113) on M + lambda I, one warp per
+// column, no block synchronisation: Hop(p) = M p + lambda p with each lane
+// computing rows lane, lane + 32, ... (two FMA chains, index order), the dots
+// as lane-strided sums + a fixed butterfly. Jacobi-preconditioned when jd !=
+// null. b: rhs; x: solution; r, z, p, hp: scratch (mm each). Returns through
+// it (iterations, the reference's `it`), nh (operator applications) and bd
+// (nonpositive curvature).
+__device__ void cg_warp(const double* M, int ldm, int mm, double lambda, const double* jd, double tol, int cap,
+                        const double* b, double* x, double* r, double* z, double* p, double* hp, int& it, int& nh,
+                        int& bd) {
+    const int lane = threadIdx.x & 31;
+    double srz = 0.0, sbb = 0.0;
+    for (int i = lane; i < mm; i += 32) {
+        const double bi = b[i];
+        const double zi = jd ? bi / jd[i] : bi;
+        x[i] = 0.0;
+        r[i] = bi;
+        z[i] = zi;
+        p[i] = zi;
+        srz = fma(bi, zi, srz);
+        sbb = fma(bi, bi, sbb);
     }
-    __syncthreads();
-    for (;;) {
-        int any = 0;
-        for (int c = 0; c < nc; ++c) any |= active[c];
-        if (!any) break;
-        // HP_c = M p_c + lambda p_c for the active columns (the whole CTA; one
-        // thread per (row, column) task, the row dot in index order)
-        for (int e = tid; e < nc * mm; e += blockDim.x) {
-            const int c = e / mm, i = e - c * mm;
-            if (!active[c]) continue;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        srz += __shfl_xor_sync(0xffffffffu, srz, o);
+        sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
+    }
+    __syncwarp();
+    double rz = srz;
+    const double target = tol * sqrt(sbb);
+    double rn = sqrt(sbb);  // r = b
+    it = 0;
+    nh = 0;
+    bd = 0;
+    while (it < cap && rn > target) {
+        for (int i = lane; i < mm; i += 32) {
             const double* mr = M + (size_t)i * ldm;
-            const double* p = P + c * mm;
             double s0 = 0.0, s1 = 0.0;
             int j = 0;
             for (; j + 1 < mm; j += 2) {
@@ -177,45 +175,39 @@ __device__ void cg_block(const double* M, int ldm, int mm, int nc, double lambda
                 s1 = fma(mr[j + 1], p[j + 1], s1);
             }
             if (j < mm) s0 = fma(mr[j], p[j], s0);
-            HP[c * mm + i] = (s0 + s1) + lambda * p[i];
+            hp[i] = (s0 + s1) + lambda * p[i];
         }
-        __syncthreads();
-        if (warp < nc && active[warp]) {
-            const int c = warp;
-            double* x = X + c * mm;
-            double* r = R + c * mm;
-            double* z = Z + c * mm;
-            double* p = P + c * mm;
-            const double* hp = HP + c * mm;
-            const double pHp = warp_dot(p, hp, mm, lane);
-            if (lane == 0) nhvp[c] += 1;
-            if (pHp <= 0.0) {
-                if (lane == 0) {
-                    bd[c] = 1;
-                    active[c] = 0;
-                }
-            } else {
-                const double alpha = rz[c] / pHp;
-                for (int i = lane; i < mm; i += 32) {
-                    x[i] += alpha * p[i];
-                    r[i] -= alpha * hp[i];
-                    z[i] = jd ? r[i] / jd[i] : r[i];
-                }
-                __syncwarp();
-                const double rz2 = warp_dot(r, z, mm, lane);
-                const double beta = rz2 / rz[c];
-                for (int i = lane; i < mm; i += 32) p[i] = z[i] + beta * p[i];
-                __syncwarp();
-                const double rn = sqrt(warp_dot(r, r, mm, lane));
-                if (lane == 0) {
-                    rz[c] = rz2;
-                    it[c] += 1;
-                    active[c] = (it[c] < cap && rn > target[c]) ? 1 : 0;
-                }
-            }
+        __syncwarp();
+        const double pHp = warp_dot(p, hp, mm, lane);
+        ++nh;
+        if (pHp <= 0.0) {
+            bd = 1;
+            break;
         }
-        __syncthreads();
+        const double alpha = rz / pHp;
+        double a_rz = 0.0, a_rr = 0.0;
+        for (int i = lane; i < mm; i += 32) {
+            x[i] += alpha * p[i];
+            const double ri = r[i] - alpha * hp[i];
+            const double zi = jd ? ri / jd[i] : ri;
+            r[i] = ri;
+            z[i] = zi;
+            a_rz = fma(ri, zi, a_rz);
+            a_rr = fma(ri, ri, a_rr);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            a_rz += __shfl_xor_sync(0xffffffffu, a_rz, o);
+            a_rr += __shfl_xor_sync(0xffffffffu, a_rr, o);
+        }
+        const double beta = a_rz / rz;
+        for (int i = lane; i < mm; i += 32) p[i] = z[i] + beta * p[i];
+        __syncwarp();
+        rz = a_rz;
+        rn = sqrt(a_rr);
+        ++it;
     }
+    __syncwarp();
 }
 
 // [H S H]_11 (reflect_sym, driver.cu): S k x k (stride lds) -> O (k-1) x (k-1)
@@ -230,10 +222,9 @@ __device__ void reflect_sym_block(const double* S, int lds, int k, const double*
         a[i] = s;
     }
     __syncthreads();
-    if (tid == 0) {
-        double s = 0.0;
-        for (int j = 0; j < k; ++j) s += v[j] * a[j];
-        cbuf[0] = beta * beta * s;
+    if (tid < 32) {
+        const double s = warp_dot(v, a, k, tid);
+        if (tid == 0) cbuf[0] = beta * beta * s;
     }
     __syncthreads();
     const double c = cbuf[0];
@@ -249,49 +240,62 @@ __device__ void reflect_sym_block(const double* S, int lds, int k, const double*
 }
 
 struct SetupArgs {
-    const double* G;   // ctx->n x ctx->n weighted Gram (row-major)
-    int ldg;           // ctx->n
     const double* par; // parameter doubles (GpParams first)
     int ld;            // panel row stride (lifted rows)
-    double* Mg;        // out: M (mm x (mm + 1))
+    double* Mg;        // out: M (mm x m_stride(mm))
     double* vec;       // out: h (mm), jd (mm)
     double* vin1;      // out: U Q s_p rows
     double* vin2;      // out: U Q r_p rows
     double* res;       // out: counters [16 + ...]
 };
 
-// shared-memory plan of the setup kernel (doubles)
-__host__ __device__ inline size_t gp_setup_smem_doubles(int m) {
+// the face Gram on one cluster: G_f = sum_t psi''(z_t) a_t a_t^T * scale over
+// this rank's rows, a_t the face columns of row t (gathered through the
+// face index), the CTAs splitting the rows
+struct GramArgsC {
+    const double* X;   // T_local x ld panel rows
+    long long T;
+    int ld;
+    const double* z;   // slot z
+    double c2, c3, c4, scale;
+    double* Gout;      // !FUSED: the m x m face Gram (row-major)
+    int stage_rows;    // rows staged in shared memory per chunk
+};
+
+// shared-memory plan (doubles): [region: S | W, also the row staging][ws stage_rows][tail 6m + 64]
+__host__ __device__ inline size_t gp_s_doubles(int m) {
     const int mm = m - 2;
-    const size_t A = (size_t)m * m, B = (size_t)(m - 1) * (m - 1);
-    const size_t cg = (size_t)kGpMaxCols * mm * 6;  // B (rhs), X, R, Z, P, HP
-    return A + std::max(B, cg) + 6 * (size_t)m + 64;
+    return std::max((size_t)m * m, (size_t)mm * m_stride(mm));
+}
+__host__ __device__ inline size_t gp_w_doubles(int m) {
+    const int mm = m - 2;
+    return std::max((size_t)m * m, (size_t)kGpMaxCols * mm * 6);
+}
+__host__ __device__ inline size_t gp_region_doubles(int m, int stage_rows) {
+    const int mp = (m + 3) & ~3;
+    return std::max(gp_s_doubles(m) + gp_w_doubles(m), (size_t)stage_rows * mp);
+}
+__host__ __device__ inline size_t gp_setup_smem_doubles(int m, int stage_rows) {
+    return gp_region_doubles(m, stage_rows) + (size_t)stage_rows + 6 * (size_t)m + 64;
 }
 
-__global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_setup_kernel(const SetupArgs a) {
-    extern __shared__ __align__(16) double sm[];
-    const GpParams P = GpParams::load(a.par);
+// Everything of the direction that precedes the third-action pass, on one CTA,
+// with the face Gram already in S (m x m): h, M, the Jacobi diagonal, the
+// probe CGs and the lifted third-action inputs.
+__device__ void setup_phases(const SetupArgs& a, const GpParams& P, double* S, double* W, double* tail) {
     const int m = P.m, mm = P.mm, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const GpLayout L(m, mm, P.np);
-    double* S = sm;                           // m x m: G_face, then M (mm x (mm + 1))
-    double* W = S + (size_t)m * m;            // (m-1) x (m-1) / CG state
-    double* vU = W + std::max((size_t)(m - 1) * (m - 1), (size_t)kGpMaxCols * mm * 6);
+    double* vU = tail;
     double* vQ = vU + m;
     double* av = vQ + m;   // scratch a (m)
     double* w = av + m;    // U nu, then G U nu (m)
     double* t = w + m;     // scratch (m)
     double* jd = t + m;    // jacobi diagonal (mm)
     double* misc = jd + m; // 64 doubles: scalars
-    __shared__ int s_it[kGpMaxCols], s_nh[kGpMaxCols], s_bd[kGpMaxCols], s_act[kGpMaxCols];
-    __shared__ double s_rz[kGpMaxCols], s_tg[kGpMaxCols];
+    __shared__ int s_it[kGpMaxCols], s_nh[kGpMaxCols], s_bd[kGpMaxCols];
     const double* par = a.par;
     auto col = [&](int i) -> int { return P.face_active ? (int)par[L.idx + i] : i; };
-
-    // ---- G_face -> S, reflectors -> smem
-    for (int e = tid; e < m * m; e += blockDim.x) {
-        const int i = e / m, j = e - i * m;
-        S[e] = a.G[(size_t)col(i) * a.ldg + col(j)];
-    }
+    const long long tp0 = clock64();
     for (int i = tid; i < m; i += blockDim.x) {
         vU[i] = par[L.vU + i];
         if (i < m - 1) vQ[i] = par[L.vQ + i];
@@ -318,11 +322,13 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_setup_kernel(const Set
         for (int i = lane; i < mm; i += 32) a.vec[i] = t[2 + i];
     }
     __syncthreads();
-    // ---- M = [H_Q [H_U G H_U]_11 H_Q]_11 + nothing (lambda enters Hop)
+    if (tid == 0) a.res[52] = (double)(clock64() - tp0);
+    // ---- M = [H_Q [H_U G H_U]_11 H_Q]_11 (lambda enters Hop)
     reflect_sym_block(S, m, m, vU, P.bU, W, m - 1, av, misc);
-    const int ldm = mm + 1;
+    const int ldm = m_stride(mm);
     reflect_sym_block(W, m - 1, m - 1, vQ, P.bQ, S, ldm, av, misc);
     for (int e = tid; e < mm * ldm; e += blockDim.x) a.Mg[e] = S[e];
+    if (tid == 0) a.res[53] = (double)(clock64() - tp0);
     // ---- Jacobi diagonal (:197-209): mean over 8 probes of r o Hop(r), floored
     double* B = W;
     double* X = B + (size_t)kGpMaxCols * mm;
@@ -358,22 +364,33 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_setup_kernel(const Set
         __syncthreads();
         jdp = jd;
     }
-    // ---- Hutchinson probe CGs in lock-step (:227-233)
+    if (tid == 0) a.res[54] = (double)(clock64() - tp0);
+    // ---- Hutchinson probe CGs, one warp per probe (:227-233)
     if (P.has_third && P.np > 0) {
         for (int e = tid; e < P.np * mm; e += blockDim.x) B[e] = par[L.pr + e];
-        __syncthreads();
-        cg_block(S, ldm, mm, P.np, P.lambda, jdp, P.tol, P.probe_cap, B, X, R, Z, PP, HP, s_it, s_nh, s_bd, s_act,
-                 s_rz, s_tg);
-        // lift U Q s_p (into vin1) and U Q r_p (into vin2), full-row coordinates
         for (int e = tid; e < P.np * a.ld; e += blockDim.x) {
             a.vin1[e] = 0.0;
             a.vin2[e] = 0.0;
         }
         __syncthreads();
+        if (warp < P.np) {
+            const int c = warp;
+            int itc, nhc, bdc;
+            cg_warp(S, ldm, mm, P.lambda, jdp, P.tol, P.probe_cap, B + c * mm, X + c * mm, R + c * mm, Z + c * mm,
+                    PP + c * mm, HP + c * mm, itc, nhc, bdc);
+            if (lane == 0) {
+                s_it[c] = itc;
+                s_nh[c] = nhc;
+                s_bd[c] = bdc;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) a.res[55] = (double)(clock64() - tp0);
+        // lift U Q s_p (into vin1) and U Q r_p (into vin2), full-row coordinates
         if (warp < 2 * P.np) {
             const int c = warp % P.np;
             const double* src = (warp < P.np ? X : B) + c * mm;
-            double* y = R + (size_t)warp * m;  // R/Z scratch: 2 np rows of m (2 x 8 x 112 <= 2 x 8 x mm + ...)
+            double* y = R + (size_t)warp * m;  // R..HP scratch: 2 np rows of m
             for (int i = lane; i < m; i += 32) y[i] = (i < 2) ? 0.0 : src[i - 2];
             __syncwarp();
             warp_reflect(y + 1, vQ, P.bQ, m - 1, lane);  // Q e (pad, reflect)
@@ -387,6 +404,162 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_setup_kernel(const Set
             a.res[16 + 2 * kGpMaxCols + tid] = s_bd[tid];
         }
     }
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
+                 : "memory");
+}
+
+// One cluster of CS CTAs: the face Gram (rows split over the CTAs; each CTA
+// stages its rows' face columns in shared memory with 8-byte async copies and
+// accumulates 4 x 4 register blocks of the lower block triangle), the
+// partials summed over the cluster through distributed shared memory in rank
+// order (each CTA reduces a slice and stores it into CTA 0), then - FUSED -
+// CTA 0 continues with the setup phases; otherwise it writes G_f for the
+// group allreduce.
+template <bool FUSED>
+__global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_cluster_kernel(const GramArgsC g, const SetupArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    namespace cgx = cooperative_groups;
+    cgx::cluster_group cluster = cgx::this_cluster();
+    const GpParams P = GpParams::load(a.par);
+    const int m = P.m, mp = (m + 3) & ~3, tid = threadIdx.x;
+    const GpLayout L(m, P.mm, P.np);
+    const int rank = (int)cluster.block_rank(), CS = (int)cluster.num_blocks();
+    const long long tg0 = clock64();
+    const int SR = g.stage_rows;
+    double* S = sm;
+    double* W = S + gp_s_doubles(m);
+    double* xs = sm;  // the staging area overlays S | W
+    double* ws = sm + gp_region_doubles(m, SR);
+    double* tail = ws + SR;
+    const double* par = a.par;
+    int* cols = reinterpret_cast<int*>(tail);
+    for (int j = tid; j < mp; j += blockDim.x) cols[j] = j < m ? (P.face_active ? (int)par[L.idx + j] : j) : -1;
+    const int nbk = mp / 4;
+    const int nblk = nbk * (nbk + 1) / 2;
+    // RS adjacent lanes share a block, each summing the rows t = part (mod RS);
+    // their partials are combined by a fixed butterfly after the row loop
+    int RS = 1;
+    while (RS < 32 && nblk * RS * 2 <= (int)blockDim.x) RS <<= 1;
+    const int blk = tid / RS, part = tid - (tid / RS) * RS;
+    int bi = -1, bj = -1;
+    if (blk < nblk) {  // lower block triangle, row-major over block rows
+        int r = 0, e = blk;
+        while (e > r) {
+            e -= r + 1;
+            ++r;
+        }
+        bi = r;
+        bj = e;
+    }
+    double acc[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc[k][l] = 0.0;
+    __syncthreads();
+    const long long r0 = g.T * rank / CS, r1 = g.T * (rank + 1) / CS;
+    for (long long c0 = r0; c0 < r1; c0 += SR) {
+        const int rows = (int)min((long long)SR, r1 - c0);
+        for (int e = tid; e < rows * mp; e += blockDim.x) {
+            const int t = e / mp, j = e - t * mp;
+            if (cols[j] >= 0)
+                cp_async8(xs + e, g.X + (c0 + t) * g.ld + cols[j]);
+            else
+                xs[e] = 0.0;
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        for (int t = tid; t < rows; t += blockDim.x) {
+            const double zt = g.z[c0 + t];
+            ws[t] = 2.0 * g.c2 - 6.0 * g.c3 * zt + 12.0 * g.c4 * (zt * zt);  // oracle.hpp:116-119
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        if (bi >= 0) {
+            for (int t = part; t < rows; t += RS) {
+                const double* xr = xs + (size_t)t * mp;
+                const double wt = ws[t];
+                double av[4], bv[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    av[k] = xr[4 * bi + k] * wt;
+                    bv[k] = xr[4 * bj + k];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) acc[k][l] = fma(av[k], bv[l], acc[k][l]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int l = 0; l < 4; ++l)
+            for (int o = 1; o < RS; o <<= 1) acc[k][l] += __shfl_xor_sync(0xffffffffu, acc[k][l], o);
+    // partial -> W (m x m, lower triangle of the face)
+    if (bi >= 0 && part == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const int i = 4 * bi + k, j = 4 * bj + l;
+                if (i < m && j < m && j <= i) W[(size_t)i * m + j] = acc[k][l];
+            }
+    }
+    const long long tg1 = clock64();
+    cluster.sync();
+    // ---- each CTA sums a slice of the entries over the cluster (rank order)
+    // and stores it, mirrored and scaled, into CTA 0's S
+    {
+        double* S0 = cluster.map_shared_rank(S, 0);
+        const int ntri = m * (m + 1) / 2;
+        for (int e = rank * (int)blockDim.x + tid; e < ntri; e += CS * (int)blockDim.x) {
+            int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+            while (i * (i + 1) / 2 > e) --i;
+            while ((i + 1) * (i + 2) / 2 <= e) ++i;
+            const int j = e - i * (i + 1) / 2;
+            const size_t off = (size_t)i * m + j;
+            double pv[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) pv[q] = q < CS ? cluster.map_shared_rank(W, q)[off] : 0.0;
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (q < CS) v += pv[q];
+            v *= g.scale;
+            S0[(size_t)i * m + j] = v;
+            S0[(size_t)j * m + i] = v;
+        }
+    }
+    cluster.sync();  // CTA 0 holds G_f; no CTA leaves while its partial may still be read
+    if (rank != 0) return;
+    if (tid == 0) {
+        a.res[48] = (double)(tg1 - tg0);
+        a.res[49] = (double)(clock64() - tg1);
+    }
+    if constexpr (!FUSED) {
+        for (int e = tid; e < m * m; e += blockDim.x) g.Gout[e] = S[e];
+    } else {
+        setup_phases(a, P, S, W, tail);
+    }
+}
+
+// group members: the allreduced face Gram from global memory, then the setup
+__global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_setup_kernel(const double* Gf, const SetupArgs a,
+                                                                       int stage_rows) {
+    extern __shared__ __align__(16) double sm[];
+    const GpParams P = GpParams::load(a.par);
+    const int m = P.m;
+    double* S = sm;
+    double* W = S + gp_s_doubles(m);
+    double* tail = sm + gp_region_doubles(m, stage_rows) + stage_rows;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) S[e] = Gf[e];
+    __syncthreads();
+    setup_phases(a, P, S, W, tail);
 }
 
 struct MainArgs {
@@ -403,7 +576,7 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_main_kernel(const Main
     const GpParams P = GpParams::load(a.par);
     const int m = P.m, mm = P.mm, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const GpLayout L(m, mm, P.np);
-    const int ldm = mm + 1;
+    const int ldm = m_stride(mm);
     double* M = sm;
     double* rhs = M + (size_t)mm * ldm;
     double* X = rhs + mm;
@@ -416,8 +589,7 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_main_kernel(const Main
     double* rows = av + mm;              // np x m reduced third actions
     double* vU = rows + (size_t)kGpMaxCols * m;
     double* vQ = vU + m;
-    __shared__ int s_it[1], s_nh[1], s_bd[1], s_act[1];
-    __shared__ double s_rz[1], s_tg[1];
+    const long long tm0 = clock64();
     const double* par = a.par;
     auto col = [&](int i) -> int { return P.face_active ? (int)par[L.idx + i] : i; };
     for (int e = tid; e < mm * ldm; e += blockDim.x) M[e] = a.Mg[e];
@@ -448,23 +620,29 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_main_kernel(const Main
         }
         __syncthreads();
     }
-    // rhs = h - (||gbar|| / n) a  (:239)
+    const long long tm1 = clock64();
+    // rhs = h - (||gbar|| / n) a  (:239), then the main CG (:240-241) on warp 0
     const double coef = P.gn / P.n_d;
     for (int i = tid; i < mm; i += blockDim.x) rhs[i] = a.vec[i] - coef * av[i];
     __syncthreads();
-    cg_block(M, ldm, mm, 1, P.lambda, P.jacobi ? jd : nullptr, P.tol, P.maxit, rhs, X, R, Z, PP, HP, s_it, s_nh,
-             s_bd, s_act, s_rz, s_tg);
-    for (int i = tid; i < mm; i += blockDim.x) a.res[64 + i] = X[i];
-    if (tid == 0) {
-        a.res[0] = s_it[0];
-        a.res[1] = s_nh[0];
-        a.res[2] = s_bd[0];
+    if (warp == 0) {
+        int itc, nhc, bdc;
+        cg_warp(M, ldm, mm, P.lambda, P.jacobi ? jd : nullptr, P.tol, P.maxit, rhs, X, R, Z, PP, HP, itc, nhc, bdc);
+        for (int i = lane; i < mm; i += 32) a.res[64 + i] = X[i];
+        if (lane == 0) {
+            a.res[0] = itc;
+            a.res[1] = nhc;
+            a.res[2] = bdc;
+            a.res[56] = (double)(tm1 - tm0);
+            a.res[57] = (double)(clock64() - tm1);
+        }
     }
 }
 
 size_t main_smem_bytes(int m) {
     const int mm = m - 2;
-    return ((size_t)mm * (mm + 1) + 8 * (size_t)mm + (size_t)kGpMaxCols * m + 2 * (size_t)m + 16) * sizeof(double);
+    return ((size_t)mm * m_stride(mm) + 9 * (size_t)mm + (size_t)kGpMaxCols * m + 2 * (size_t)m + 16) *
+           sizeof(double);
 }
 
 }  // namespace
@@ -475,7 +653,14 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
     if (in.exact_trace || m < 4 || m > kGpMaxM || np > kGpMaxCols || (in.has_third && np == 0)) return false;
     if (in.jacobi_probes.size() != 0 && in.jacobi_probes.size() != 8) return false;
     const int mm = m - 2;
-    const size_t setup_smem = gp_setup_smem_doubles(m) * sizeof(double);
+    // rows staged per chunk: as many as fit beside the setup's vectors, at most
+    // one 8-CTA share of this rank's rows
+    const int mp = (m + 3) & ~3;
+    const long long avail = (long long)(ctx->max_smem / sizeof(double)) - (6LL * m + 64) - 64;
+    long long SR = std::min<long long>(avail / (mp + 1), (ctx->T_local + 7) / 8);
+    SR = std::max<long long>(SR, 1);
+    const int stage_rows = (int)SR;
+    const size_t setup_smem = gp_setup_smem_doubles(m, stage_rows) * sizeof(double);
     if (setup_smem > ctx->max_smem || main_smem_bytes(m) > ctx->max_smem) return false;
     if (!ctx->gpcg) ctx->gpcg = new GramPcgWs();
     GramPcgWs& ws = *ctx->gpcg;
@@ -483,7 +668,7 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
     const size_t ld = (size_t)ctx->ld;
     // workspace (sized for the largest face seen; growth invalidates graphs)
     if (ws.cap_m < (size_t)kGpMaxM || ws.cap_ld < ld) {
-        for (double* p : {ws.par, ws.Mg, ws.vec, ws.vin1, ws.vin2, ws.t3, ws.res})
+        for (double* p : {ws.par, ws.Mg, ws.vec, ws.vin1, ws.vin2, ws.t3, ws.res, ws.Gf})
             if (p) MVSK_CUDA(cudaFree(p));
         for (double* p : {ws.h_par, ws.h_res})
             if (p) MVSK_CUDA(cudaFreeHost(p));
@@ -492,6 +677,7 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
         MVSK_CUDA(cudaMalloc(&ws.par, ws.par_elems * sizeof(double)));
         MVSK_CUDA(cudaMallocHost(&ws.h_par, ws.par_elems * sizeof(double)));
         MVSK_CUDA(cudaMalloc(&ws.Mg, (size_t)kGpMaxM * (kGpMaxM + 1) * sizeof(double)));
+        MVSK_CUDA(cudaMalloc(&ws.Gf, (size_t)kGpMaxM * kGpMaxM * sizeof(double)));
         MVSK_CUDA(cudaMalloc(&ws.vec, (size_t)2 * kGpMaxM * sizeof(double)));
         MVSK_CUDA(cudaMalloc(&ws.vin1, (size_t)kGpMaxCols * ld * sizeof(double)));
         MVSK_CUDA(cudaMalloc(&ws.vin2, (size_t)kGpMaxCols * ld * sizeof(double)));
@@ -503,7 +689,15 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
         ws.cap_ld = ld;
         ++ctx->epoch;
     }
-    if (!ctx->gram) MVSK_CUDA(cudaMalloc(&ctx->gram, (size_t)ctx->n * ctx->n * sizeof(double)));
+    // the Gram cluster: 16 CTAs where a non-portable cluster of this size is
+    // resident, else 8 (portable)
+    const bool sharded = is_sharded(ctx);
+    const void* cfn = sharded ? reinterpret_cast<const void*>(&gram_pcg_cluster_kernel<false>)
+                              : reinterpret_cast<const void*>(&gram_pcg_cluster_kernel<true>);
+    int CS = 0;
+    for (int cs : {16, 8})
+        if (!CS && cluster_fits(cfn, cs, kGpThreads, setup_smem)) CS = cs;
+    if (!CS) return false;
     // parameters -> pinned staging (read by the graph's H2D node at replay)
     double* hp = ws.h_par;
     std::copy(in.vU.begin(), in.vU.end(), hp + L.vU);
@@ -532,12 +726,10 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
     const Slot& sl = ctx->slots[slot];
     // graph key: the face width and probe count fix every launch shape
     const int key = m * 64 + np * 2 + P.jacobi;
+    (void)mp;
     run_graphed(ctx, kGraphGramPcg, key, slot, [&] {
         MVSK_CUDA(cudaMemcpyAsync(ws.par, ws.h_par, L.total * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        run_weighted_gram(ctx, nullptr, ctx->gram, 1.0 / (double)ctx->T_global, sl.z);
         SetupArgs sa{};
-        sa.G = ctx->gram;
-        sa.ldg = (int)ctx->n;
         sa.par = ws.par;
         sa.ld = (int)ld;
         sa.Mg = ws.Mg;
@@ -545,10 +737,41 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
         sa.vin1 = ws.vin1;
         sa.vin2 = ws.vin2;
         sa.res = ws.res;
-        set_smem_attr(reinterpret_cast<const void*>(&gram_pcg_setup_kernel), setup_smem);
+        GramArgsC ga{};
+        ga.X = ctx->X;
+        ga.T = ctx->T_local;
+        ga.ld = (int)ld;
+        ga.z = sl.z;
+        ga.c2 = ctx->c.c2;
+        ga.c3 = ctx->c.c3;
+        ga.c4 = ctx->c.c4;
+        ga.scale = 1.0 / (double)ctx->T_global;
+        ga.Gout = ws.Gf;
+        ga.stage_rows = stage_rows;
+        set_smem_attr(cfn, setup_smem);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(CS);
+        cfg.blockDim = dim3(kGpThreads);
+        cfg.dynamicSmemBytes = setup_smem;
+        cfg.stream = ctx->stream;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        void* cargs[] = {&ga, &sa};
         ++ctx->launches;
-        gram_pcg_setup_kernel<<<1, kGpThreads, setup_smem, ctx->stream>>>(sa);
-        MVSK_CUDA(cudaGetLastError());
+        MVSK_CUDA(cudaLaunchKernelExC(&cfg, cfn, cargs));
+        ctx->phys += 1;  // the Gram streams the face panel once
+        if (sharded) {
+            allreduce_sum(ctx, ws.Gf, (size_t)m * m);
+            set_smem_attr(reinterpret_cast<const void*>(&gram_pcg_setup_kernel), setup_smem);
+            ++ctx->launches;
+            gram_pcg_setup_kernel<<<1, kGpThreads, setup_smem, ctx->stream>>>(ws.Gf, sa, stage_rows);
+            MVSK_CUDA(cudaGetLastError());
+        }
         if (np > 0) {
             PassIO io;
             io.vin = ws.vin1;
@@ -586,6 +809,12 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
     }
     out.iters = iters;
     out.breakdown = bd;
+    static const bool prof = std::getenv("MVSK_GPCG_PROF") != nullptr;
+    if (prof)
+        std::fprintf(stderr,
+                     "[gpcg] m=%d np=%d cycles: gram %.0f reduce %.0f | setup h %.0f M %.0f jacobi %.0f probes %.0f "
+                     "| main a %.0f cg %.0f | iters %d\n",
+                     m, np, r[48], r[49], r[52], r[53] - r[52], r[54] - r[53], r[55] - r[54], r[56], r[57], iters);
     // reference contract (common.hpp:27-37): 2 passes per Hop, 3 per third action
     ctx->fwd += (uint64_t)(hvps + 2LL * np);
     ctx->tr += (uint64_t)(hvps + np);
@@ -595,7 +824,7 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
 void gram_pcg_workspace_free(mvsk_gpu_ctx* ctx) {
     if (!ctx->gpcg) return;
     GramPcgWs& ws = *ctx->gpcg;
-    for (double* p : {ws.par, ws.Mg, ws.vec, ws.vin1, ws.vin2, ws.t3, ws.res})
+    for (double* p : {ws.par, ws.Mg, ws.vec, ws.vin1, ws.vin2, ws.t3, ws.res, ws.Gf})
         if (p) cudaFree(p);
     for (double* p : {ws.h_par, ws.h_res})
         if (p) cudaFreeHost(p);

@@ -101,6 +101,8 @@ void fetch_out(mvsk_gpu_ctx* ctx, const FaceMap& fm, const double* dev, int k, l
 // graph keys beyond the Op values
 constexpr int kGraphGram = 100, kGraphThirdTrace = 101;
 
+}  // namespace
+
 void run_graphed(mvsk_gpu_ctx* ctx, int op, int k, int slot, const std::function<void()>& enqueue) {
     static const bool disabled = std::getenv("MVSK_NO_GRAPHS") != nullptr;
     mvsk_gpu_ctx::GraphEntry* e = nullptr;
@@ -159,6 +161,8 @@ void run_graphed(mvsk_gpu_ctx* ctx, int op, int k, int slot, const std::function
     e->ok = false;  // not capturable here: stay eager
     enqueue();
 }
+
+namespace {
 
 void ensure_tvec2(mvsk_gpu_ctx* ctx) {
     if (!ctx->tvec2) MVSK_CUDA(cudaMalloc(&ctx->tvec2, (size_t)std::max<long long>(1, ctx->T_local) * sizeof(double)));

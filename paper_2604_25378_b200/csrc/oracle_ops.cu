@@ -157,7 +157,8 @@ bool make_plan_vs(const mvsk_gpu_ctx* ctx, Op op, int K, const TuneOverride& tov
     const long long npairs = ctx->ld / 2;
     const bool small = ctx->T_local < 64LL * ctx->nsm;
     const bool want = tov.VS >= 0 ? tov.VS == 1 : (small && npairs >= 1024 && op == Op::FGRAD);
-    if (!want) return false;
+    // the same width range as every other op of this build (n <= 8192)
+    if (!want || npairs > 4096) return false;
     const int Q = tov.Q > 0 ? tov.Q : 16;
     if (!select_kernel_vs(op, K, Q, 1)) return false;
     const int P = round_team((int)((npairs + Q - 1) / Q));
