@@ -170,6 +170,7 @@ __device__ void cg_warp(const double* M, int ldm, int mm, double lambda, const d
             const double* mr = M + (size_t)i * ldm;
             double s0 = 0.0, s1 = 0.0;
             int j = 0;
+#pragma unroll 4
             for (; j + 1 < mm; j += 2) {
                 s0 = fma(mr[j], p[j], s0);
                 s1 = fma(mr[j + 1], p[j + 1], s1);
@@ -478,6 +479,7 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_cluster_kernel(const G
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         if (bi >= 0) {
+#pragma unroll 4
             for (int t = part; t < rows; t += RS) {
                 const double* xr = xs + (size_t)t * mp;
                 const double wt = ws[t];

@@ -200,6 +200,100 @@ __device__ void project_slice_fast(const double* v, int n, double tau, double ma
     __syncthreads();
 }
 
+// ---- block-parallel variants for wide panels (PAR): deterministic tree
+// reductions and a block scan instead of the host loop's sequential sums
+// (n up to kSpgMaxN; the trajectory matches the host loop to rounding)
+__device__ double bsum(double v, double* red) {  // every thread returns the block total
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        double t = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) red[32] = t;
+    }
+    __syncthreads();
+    return red[32];
+}
+__device__ double bdot(const double* a, const double* b, int n, double* red) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s = fma(a[i], b[i], s);
+    return bsum(s, red);
+}
+
+// project_slice with the sorted running sums as a block scan: each thread
+// owns a contiguous chunk of the sorted values; theta is the candidate of the
+// last index k with u[k] > (css_k - s) / (k + 1) (simplex.hpp:106-113)
+__device__ void project_slice_par(const double* v, int n, double tau, double mass, double* out, double* u,
+                                  double* bcast, double* red) {
+    int m = 1;
+    while (m < n) m <<= 1;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) u[i] = i < n ? v[i] - tau : -INFINITY;
+    bitonic_desc(u, m);
+    const int nt = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int chunk = (n + nt - 1) / nt;
+    const int k0 = min(n, tid * chunk), k1 = min(n, k0 + chunk);
+    double tot = 0.0;
+    for (int k = k0; k < k1; ++k) tot += u[k];
+    // exclusive prefix of the thread totals: warp scans, then the warp totals
+    double inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) red[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = (nt + 31) >> 5;
+        double w = lane < nw ? red[lane] : 0.0;
+        double wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        red[64 + lane] = wi - w;  // exclusive warp offsets
+    }
+    __syncthreads();
+    double css = red[64 + warp] + (inc - tot);
+    const double s = mass - (double)n * tau;
+    int kb = -1;
+    double cb = 0.0;
+    for (int k = k0; k < k1; ++k) {
+        css += u[k];
+        const double cand = (css - s) / (double)(k + 1);
+        if (u[k] > cand) {
+            kb = k;
+            cb = cand;
+        }
+    }
+    // the largest such k over the block (its thread publishes theta)
+    int kmax = kb;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    __syncthreads();
+    if (lane == 0) reinterpret_cast<int*>(red + 96)[warp] = kmax;
+    __syncthreads();
+    if (tid == 0) {
+        int best = -1;
+        const int nw = (nt + 31) >> 5;
+        for (int w = 0; w < nw; ++w) best = max(best, reinterpret_cast<int*>(red + 96)[w]);
+        reinterpret_cast<int*>(red + 96)[40] = best;
+        if (best < 0) *bcast = 0.0;
+    }
+    __syncthreads();
+    if (kb >= 0 && kb == reinterpret_cast<int*>(red + 96)[40]) *bcast = cb;
+    __syncthreads();
+    const double theta = *bcast;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = fmax(v[i] - tau - theta, 0.0) + tau;
+    __syncthreads();
+}
+
 struct SpgBufs {
     double* x;    // n, current iterate
     double* g;    // n, gradient at x
@@ -214,11 +308,23 @@ struct SpgBufs {
 // one trial's step (solver.hpp:131-145): every thread of the block calls it;
 // u: sort scratch (next power of two >= n), bc: 2 broadcast doubles. FAST: the
 // order-free reductions above (cluster preamble, n <= 128)
-template <bool FAST>
+template <bool FAST, bool PAR = false>
 __device__ void spg_prep_body(SpgState* st, const SpgBufs& b, double* u, double* bc) {
+    __shared__ double red[160];
     const int n = st->n;
     if (threadIdx.x == 0) ++st->trials;
-    if constexpr (FAST) {
+    if constexpr (PAR) {
+        if (st->bt == 0) {  // L0 from the BB pair (solver.hpp:131-135)
+            double L0 = st->L;
+            if (st->have_bb) {
+                const double sy = bdot(b.bbs, b.bby, n, red), ss = bdot(b.bbs, b.bbs, n, red);
+                L0 = (ss > 0 && sy > 0) ? sy / ss : st->L;
+                L0 = fmin(fmax(L0, 1e-2), 1e12);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) st->Lk = L0;
+        }
+    } else if constexpr (FAST) {
         if (st->bt == 0 && threadIdx.x < 32) {  // L0 from the BB pair (solver.hpp:131-135)
             double L0 = st->L;
             if (st->have_bb) {
@@ -242,13 +348,22 @@ __device__ void spg_prep_body(SpgState* st, const SpgBufs& b, double* u, double*
     const double Lk = st->Lk;
     for (int i = threadIdx.x; i < n; i += blockDim.x) b.y[i] = b.x[i] - b.g[i] / Lk;
     __syncthreads();
-    if constexpr (FAST)
+    if constexpr (PAR)
+        project_slice_par(b.y, n, st->tau, 1.0, b.xp, u, &bc[0], red);
+    else if constexpr (FAST)
         project_slice_fast(b.y, n, st->tau, 1.0, b.xp, u, &bc[0]);
     else
         project_slice_dev(b.y, n, st->tau, 1.0, b.xp, u, &bc[0]);
     for (int i = threadIdx.x; i < n; i += blockDim.x) b.dp[i] = b.xp[i] - b.x[i];
     __syncthreads();
-    if (FAST ? threadIdx.x < 32 : threadIdx.x == 0) {
+    if constexpr (PAR) {
+        const double gdp = bdot(b.g, b.dp, n, red);
+        if (threadIdx.x == 0) {
+            st->gdp = gdp;
+            st->eval_flag = gdp < 0 ? 1 : 0;
+            if (gdp < 0) ++st->evals;
+        }
+    } else if (FAST ? threadIdx.x < 32 : threadIdx.x == 0) {
         const double gdp = FAST ? wdot(b.g, b.dp, n) : sdot(b.g, b.dp, n);
         if (threadIdx.x == 0) {
             st->gdp = gdp;
@@ -258,17 +373,19 @@ __device__ void spg_prep_body(SpgState* st, const SpgBufs& b, double* u, double*
     }
 }
 
+template <bool PAR>
 __global__ void __launch_bounds__(kSpgThreads) spg_prep_kernel(SpgState* st, SpgBufs b) {
     extern __shared__ double u[];
     __shared__ double bc[2];
-    spg_prep_body<false>(st, b, u, bc);
+    spg_prep_body<false, PAR>(st, b, u, bc);
 }
 
 // Armijo test and the state update of one trial (solver.hpp:146-174): every
 // thread of the block calls it; fp is the trial value, gp its gradient
-template <bool FAST>
+template <bool FAST, bool PAR = false>
 __device__ void spg_accept_body(SpgState* st, const SpgBufs& b, const double* gp, double fp, double* u, double* bc) {
     __shared__ int s_acc, s_change, s_any, s_done;
+    __shared__ double red[160];
     const int n = st->n;
     if (threadIdx.x == 0) {
         int acc = 0;
@@ -335,7 +452,16 @@ __device__ void spg_accept_body(SpgState* st, const SpgBufs& b, const double* gp
         if (!s_done && st->eps_stop > 0 && st->steps % 10 == 0) {
             for (int i = threadIdx.x; i < n; i += blockDim.x) b.y[i] = b.x[i] - b.g[i];
             __syncthreads();
-            if constexpr (FAST) {
+            if constexpr (PAR) {
+                project_slice_par(b.y, n, st->tau, 1.0, b.dp, u, &bc[0], red);
+                double s = 0.0;
+                for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                    const double d = b.x[i] - b.dp[i];
+                    s = fma(d, d, s);
+                }
+                s = bsum(s, red);
+                if (threadIdx.x == 0 && sqrt(s) <= st->eps_stop) st->done = 1;
+            } else if constexpr (FAST) {
                 project_slice_fast(b.y, n, st->tau, 1.0, b.dp, u, &bc[0]);
                 if (threadIdx.x < 32) {
                     double s = 0.0;
@@ -363,12 +489,13 @@ __device__ void spg_accept_body(SpgState* st, const SpgBufs& b, const double* gp
     __syncthreads();
 }
 
+template <bool PAR>
 __global__ void __launch_bounds__(kSpgThreads) spg_accept_kernel(SpgState* st, SpgBufs b, const double* gp,
                                                                  const double* fp_sc, cudaGraphConditionalHandle h,
                                                                  int set_cond) {
     extern __shared__ double u[];
     __shared__ double bc[2];
-    spg_accept_body<false>(st, b, gp, st->eval_flag ? fp_sc[0] : 0.0, u, bc);
+    spg_accept_body<false, PAR>(st, b, gp, st->eval_flag ? fp_sc[0] : 0.0, u, bc);
     if (set_cond && threadIdx.x == 0) cudaGraphSetConditional(h, st->done ? 0u : 1u);
 }
 
@@ -647,7 +774,12 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
     const bool cluster_ok = !no_cluster && ctx->nranks == 1 && ctx->ld <= kSpgCM &&  // no exchange at one rank
                             ctx->T_local >= kSpgCS && cl_smem <= ctx->max_smem &&
                             cluster_fits(cl_fn, kSpgCS, kSpgCW * 32, cl_smem);
-    if (!cluster_ok && (!enabled || ctx->no_capture || n > kSpgMaxN)) return false;
+    // wide panels (no cluster preamble): the conditional-while graph with the
+    // block-parallel reductions by default (MVSK_NO_SPG_GRAPH: host loop);
+    // MVSK_SPG_GRAPH keeps the bitwise-host-order variant for A/B
+    static const bool no_graph = std::getenv("MVSK_NO_SPG_GRAPH") != nullptr;
+    const bool par = !enabled;
+    if (!cluster_ok && ((!enabled && (no_graph || ctx->ld <= kSpgCM)) || ctx->no_capture || n > kSpgMaxN)) return false;
     if (!ctx->spg) ctx->spg = new SpgWorkspace();
     SpgWorkspace& ws = *ctx->spg;
     if (ws.broken && !cluster_ok) return false;
@@ -677,8 +809,12 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
     int m2 = 1;
     while (m2 < n) m2 <<= 1;
     const size_t smem = (size_t)m2 * sizeof(double);
-    set_smem_attr(reinterpret_cast<const void*>(&spg_prep_kernel), smem);
-    set_smem_attr(reinterpret_cast<const void*>(&spg_accept_kernel), smem);
+    const void* prep_fn = par ? reinterpret_cast<const void*>(&spg_prep_kernel<true>)
+                              : reinterpret_cast<const void*>(&spg_prep_kernel<false>);
+    const void* acc_fn = par ? reinterpret_cast<const void*>(&spg_accept_kernel<true>)
+                             : reinterpret_cast<const void*>(&spg_accept_kernel<false>);
+    set_smem_attr(prep_fn, smem);
+    set_smem_attr(acc_fn, smem);
 
     // initial state (solver.hpp:116-129): x, g, f; active set of x
     SpgState& hs = *ws.host_state;
@@ -803,10 +939,16 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
             bool threw = false;
             try {
                 ++ctx->launches;
-                spg_prep_kernel<<<1, kSpgThreads, smem, sm>>>(st, b);
+                if (par)
+                    spg_prep_kernel<true><<<1, kSpgThreads, smem, sm>>>(st, b);
+                else
+                    spg_prep_kernel<false><<<1, kSpgThreads, smem, sm>>>(st, b);
                 run_pass(ctx, Op::FGRAD, 1, io);
                 ++ctx->launches;
-                spg_accept_kernel<<<1, kSpgThreads, smem, sm>>>(st, b, sl.g, sl.sc, h, 1);
+                if (par)
+                    spg_accept_kernel<true><<<1, kSpgThreads, smem, sm>>>(st, b, sl.g, sl.sc, h, 1);
+                else
+                    spg_accept_kernel<false><<<1, kSpgThreads, smem, sm>>>(st, b, sl.g, sl.sc, h, 1);
             } catch (...) {
                 threw = true;
             }
