@@ -601,7 +601,36 @@ Vec yand_direction(const View& O, int slot, const TangentCfg& cfg, uint64_t it_s
     const bool has_third = (c.c3 != 0.0 || c.c4 != 0.0);
     Vec u;
 
+    bool direct_done = false;
     if (!cfg.pcg) {
+        // ---- the whole direct branch on the device for faces of <= 112 assets
+        // (gram_pcg.cu: one graph launch; the lambda fallback as a second one)
+        DirectInput din;
+        din.m = n;
+        din.vU = basis.v;
+        din.bU = basis.beta;
+        din.vQ = frame.v;
+        din.bQ = frame.beta;
+        din.nu = frame.nu;
+        din.gn = gn;
+        din.lambda = cfg.lambda;
+        din.has_third = has_third;
+        Vec ud;
+        Tick tkd(g_prof.dgram);
+        if (direct_direction_device(ctx, slot, O.fm, din, ud)) {
+            ctx->fwd += (uint64_t)mm + 1;  // the reference's W and t_nu passes (:159, :164)
+            if (!all_finite(ud)) {  // singular unregularised operator: :181-188
+                diag.lambda_fallback = 1;
+                din.lambda = std::max(cfg.lambda, 1e-4);
+                if (!direct_direction_device(ctx, slot, O.fm, din, ud) || !all_finite(ud))
+                    throw ApiError(MVSK_NUMERIC_ERROR, "yand_direction: tangent solve failed");
+            }
+            u = std::move(ud);
+            direct_done = true;
+        }
+    }
+    if (direct_done) {
+    } else if (!cfg.pcg) {
         // ---- direct branch via the weighted Gram (:151-188)
         // W = A (UQ) never forms: with G = A^T diag(psi'') A / T from the DMMA
         // kernel, M0 = (UQ)^T G (UQ) = [H_Q [H_U G H_U]_11 H_Q]_11 (two

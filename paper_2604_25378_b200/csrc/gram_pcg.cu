@@ -34,6 +34,7 @@
 namespace mvsk_b200 {
 
 void run_graphed(mvsk_gpu_ctx* ctx, int op, int k, int slot, const std::function<void()>& enqueue);
+void ensure_tvec2(mvsk_gpu_ctx* ctx);
 
 namespace {
 
@@ -41,6 +42,7 @@ constexpr int kGpMaxM = 112;     // face width limit (two m x m fp64 buffers in 
 constexpr int kGpMaxCols = 8;    // Hutchinson probes handled in one lock-step block
 constexpr int kGpThreads = 512;
 constexpr int kGraphGramPcg = 102;
+constexpr int kGraphGramDirect = 103;
 
 // per-direction scalars; they live in the device parameter buffer (doubles
 // [0, 16)) so one captured graph serves every direction of a face shape
@@ -248,6 +250,7 @@ struct SetupArgs {
     double* vin1;      // out: U Q s_p rows
     double* vin2;      // out: U Q r_p rows
     double* res;       // out: counters [16 + ...]
+    double* pmat;      // direct: out: P in ld x ld (zero outside the face)
 };
 
 // the face Gram on one cluster: G_f = sum_t psi''(z_t) a_t a_t^T * scale over
@@ -270,7 +273,7 @@ __host__ __device__ inline size_t gp_s_doubles(int m) {
 }
 __host__ __device__ inline size_t gp_w_doubles(int m) {
     const int mm = m - 2;
-    return std::max((size_t)m * m, (size_t)kGpMaxCols * mm * 6);
+    return std::max(std::max((size_t)m * m, (size_t)mm * m_stride(mm)), (size_t)kGpMaxCols * mm * 6);
 }
 __host__ __device__ inline size_t gp_region_doubles(int m, int stage_rows) {
     const int mp = (m + 3) & ~3;
@@ -407,6 +410,180 @@ __device__ void setup_phases(const SetupArgs& a, const GpParams& P, double* S, d
     }
 }
 
+// H [0 0; 0 D] H for D r x r (stride ldd) -> O (r+1) x (r+1) (stride ldo): the
+// lift unreflect (driver.cu) that P = (UQ) M^-1 (UQ)^T applies twice:
+// Dp - beta v (v^T Dp) - beta (Dp v) v^T + beta^2 (v^T Dp v) v v^T
+__device__ void unreflect_block(const double* D, int ldd, int r, const double* v, double beta, double* O, int ldo,
+                                double* dv, double* vd, double* cbuf) {
+    const int k = r + 1, tid = threadIdx.x;
+    for (int i = tid; i < k; i += blockDim.x) {
+        double s = 0.0, t = 0.0;
+        if (i > 0)
+            for (int j = 1; j < k; ++j) s += D[(size_t)(i - 1) * ldd + (j - 1)] * v[j];
+        if (i > 0)
+            for (int j = 1; j < k; ++j) t += v[j] * D[(size_t)(j - 1) * ldd + (i - 1)];
+        dv[i] = s;
+        vd[i] = t;
+    }
+    __syncthreads();
+    if (tid < 32) {
+        const double s = warp_dot(v, dv, k, tid);
+        if (tid == 0) cbuf[0] = beta * beta * s;
+    }
+    __syncthreads();
+    const double c = cbuf[0];
+    for (int e = tid; e < k * k; e += blockDim.x) {
+        const int i = e / k, j = e - i * k;
+        const double dij = (i > 0 && j > 0) ? D[(size_t)(i - 1) * ldd + (j - 1)] : 0.0;
+        O[(size_t)i * ldo + j] = dij - (beta * v[i] * vd[j] + beta * dv[i] * v[j]) + c * v[i] * v[j];
+    }
+    __syncthreads();
+}
+
+// Direct branch (affine_normal.hpp:151-188) after the Gram, one CTA: h, M + lambda I,
+// its inverse by Gauss-Jordan with partial pivoting (the pivots of the
+// reference's PartialPivLU: the largest remaining magnitude, first index on
+// ties; an all-zero pivot column flags the operator singular, which sends the
+// caller to the lambda fallback like the reference's non-finite solve), then
+// P = (UQ) M^-1 (UQ)^T scattered into the ld x ld trace matrix (zero outside the
+// face). Outputs: h (vec), M^-1 (Mg, stride m_stride), P (pmat), flags (res[3]).
+__device__ void direct_phases(const SetupArgs& a, const GpParams& P, double* S, double* W, double* tail, int ld) {
+    const int m = P.m, mm = P.mm, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const GpLayout L(m, mm, P.np);
+    double* vU = tail;
+    double* vQ = vU + m;
+    double* av = vQ + m;   // scratch (m)
+    double* w = av + m;    // U nu, then G U nu (m)
+    double* t = w + m;     // scratch (m)
+    double* fc = t + m;    // pivot column (m)
+    double* misc = fc + m; // scalars
+    __shared__ int s_piv, s_sing;
+    const double* par = a.par;
+    auto col = [&](int i) -> int { return P.face_active ? (int)par[L.idx + i] : i; };
+    for (int i = tid; i < m; i += blockDim.x) {
+        vU[i] = par[L.vU + i];
+        if (i < m - 1) vQ[i] = par[L.vQ + i];
+    }
+    __syncthreads();
+    // h = Q^T U^T G (U nu)  (:164-166)
+    if (warp == 0) {
+        for (int i = lane; i < m; i += 32) w[i] = i == 0 ? 0.0 : par[L.nu + i - 1];
+        __syncwarp();
+        warp_reflect(w, vU, P.bU, m, lane);
+    }
+    __syncthreads();
+    for (int i = tid; i < m; i += blockDim.x) {
+        double s = 0.0;
+        const double* sr = S + (size_t)i * m;
+        for (int j = 0; j < m; ++j) s += sr[j] * w[j];
+        t[i] = s;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        warp_reflect(t, vU, P.bU, m, lane);
+        warp_reflect(t + 1, vQ, P.bQ, m - 1, lane);
+        for (int i = lane; i < mm; i += 32) a.vec[i] = t[2 + i];
+    }
+    __syncthreads();
+    // M = (UQ)^T G (UQ) + lambda I  (:169-170)
+    reflect_sym_block(S, m, m, vU, P.bU, W, m - 1, av, misc);
+    const int ldm = m_stride(mm);
+    reflect_sym_block(W, m - 1, m - 1, vQ, P.bQ, S, ldm, av, misc);
+    for (int i = tid; i < mm; i += blockDim.x) S[(size_t)i * ldm + i] += P.lambda;
+    for (int e = tid; e < mm * ldm; e += blockDim.x) {
+        const int i = e / ldm, j = e - i * ldm;
+        W[e] = (i == j) ? 1.0 : 0.0;
+    }
+    if (tid == 0) {
+        s_sing = 0;
+        a.res[3] = 0.0;
+        a.res[4] = 0.0;
+    }
+    __syncthreads();
+    // Gauss-Jordan on [M | I] with partial pivoting: W <- M^-1
+    for (int k = 0; k < mm; ++k) {
+        if (warp == 0) {
+            double big = -1.0;
+            int piv = k;
+            for (int r = k + lane; r < mm; r += 32) {
+                const double v = fabs(S[(size_t)r * ldm + k]);
+                if (v > big) {
+                    big = v;
+                    piv = r;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, big, o);
+                const int op = __shfl_xor_sync(0xffffffffu, piv, o);
+                if (ob > big || (ob == big && op < piv)) {
+                    big = ob;
+                    piv = op;
+                }
+            }
+            if (lane == 0) {
+                s_piv = piv;
+                if (!(big > 0.0)) s_sing = 1;  // zero (or NaN) pivot column
+            }
+        }
+        __syncthreads();
+        if (s_sing) break;
+        const int piv = s_piv;
+        if (piv != k) {
+            for (int j = tid; j < mm; j += blockDim.x) {
+                double* a0 = S + (size_t)k * ldm + j;
+                double* a1 = S + (size_t)piv * ldm + j;
+                const double x0 = *a0;
+                *a0 = *a1;
+                *a1 = x0;
+                double* b0 = W + (size_t)k * ldm + j;
+                double* b1 = W + (size_t)piv * ldm + j;
+                const double y0 = *b0;
+                *b0 = *b1;
+                *b1 = y0;
+            }
+            __syncthreads();
+        }
+        const double pv = S[(size_t)k * ldm + k];
+        for (int r = tid; r < mm; r += blockDim.x) fc[r] = S[(size_t)r * ldm + k];
+        __syncthreads();
+        for (int j = tid; j < mm; j += blockDim.x) {
+            S[(size_t)k * ldm + j] /= pv;
+            W[(size_t)k * ldm + j] /= pv;
+        }
+        __syncthreads();
+        for (int e = tid; e < mm * mm; e += blockDim.x) {
+            const int r = e / mm, j = e - r * mm;
+            if (r == k) continue;
+            const double f = fc[r];
+            if (f == 0.0) continue;
+            if (j > k) S[(size_t)r * ldm + j] -= f * S[(size_t)k * ldm + j];
+            W[(size_t)r * ldm + j] -= f * W[(size_t)k * ldm + j];
+        }
+        __syncthreads();
+    }
+    if (tid == 0) a.res[3] = s_sing ? 1.0 : 0.0;
+    for (int e = tid; e < mm * ldm; e += blockDim.x) a.Mg[e] = W[e];
+    __syncthreads();
+    if (!a.pmat) return;
+    // P = U [H_Q [0 0; 0 M^-1] H_Q] U^T: (m-1)^2 into S, then m^2 scattered
+    unreflect_block(W, ldm, mm, vQ, P.bQ, S, m - 1, av, t, misc);
+    double* Pm = W;  // M^-1 is saved in Mg; reuse W for P (m x m)
+    unreflect_block(S, m - 1, m - 1, vU, P.bU, Pm, m, av, t, misc);
+    for (int e = tid; e < ld * ld; e += blockDim.x) a.pmat[e] = 0.0;
+    __syncthreads();
+    int bad = 0;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+        const int i = e / m, j = e - i * m;
+        const double v = Pm[e];
+        if (!isfinite(v)) bad = 1;
+        a.pmat[(size_t)col(i) * ld + col(j)] = v;
+    }
+    if (bad) atomicOr(&s_sing, 2);
+    __syncthreads();
+    if (tid == 0) a.res[4] = (s_sing & 2) ? 1.0 : 0.0;
+}
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
                  : "memory");
@@ -419,7 +596,8 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 // order (each CTA reduces a slice and stores it into CTA 0), then - FUSED -
 // CTA 0 continues with the setup phases; otherwise it writes G_f for the
 // group allreduce.
-template <bool FUSED>
+// MODE 0: write G_f (group members), 1: PCG setup, 2: direct setup
+template <int MODE>
 __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_cluster_kernel(const GramArgsC g, const SetupArgs a) {
     extern __shared__ __align__(16) double sm[];
     namespace cgx = cooperative_groups;
@@ -543,10 +721,12 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_cluster_kernel(const G
         a.res[48] = (double)(tg1 - tg0);
         a.res[49] = (double)(clock64() - tg1);
     }
-    if constexpr (!FUSED) {
+    if constexpr (MODE == 0) {
         for (int e = tid; e < m * m; e += blockDim.x) g.Gout[e] = S[e];
-    } else {
+    } else if constexpr (MODE == 1) {
         setup_phases(a, P, S, W, tail);
+    } else {
+        direct_phases(a, P, S, W, tail, g.ld);
     }
 }
 
@@ -641,6 +821,49 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_main_kernel(const Main
     }
 }
 
+// direct branch tail (:173-180): a = Q^T U^T (A_f^T tw) from the trace pass,
+// rhs = h - (||gbar|| / n) a, u = M^-1 rhs; non-finite when the operator was
+// singular or P non-finite (the caller retries with the fallback ridge)
+__global__ void __launch_bounds__(kGpThreads, 1) gram_direct_main_kernel(const MainArgs a, const double* af) {
+    extern __shared__ __align__(16) double sm[];
+    const GpParams P = GpParams::load(a.par);
+    const int m = P.m, mm = P.mm, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const GpLayout L(m, mm, P.np);
+    const int ldm = m_stride(mm);
+    double* y = sm;          // m
+    double* rhs = y + m;     // mm
+    double* vU = rhs + mm;   // m
+    double* vQ = vU + m;     // m
+    const double* par = a.par;
+    auto col = [&](int i) -> int { return P.face_active ? (int)par[L.idx + i] : i; };
+    for (int i = tid; i < m; i += blockDim.x) {
+        vU[i] = par[L.vU + i];
+        if (i < m - 1) vQ[i] = par[L.vQ + i];
+        y[i] = (P.has_third && af) ? af[col(i)] : 0.0;
+    }
+    __syncthreads();
+    if (warp == 0 && P.has_third && af) {
+        warp_reflect(y, vU, P.bU, m, lane);
+        warp_reflect(y + 1, vQ, P.bQ, m - 1, lane);
+    }
+    __syncthreads();
+    const double coef = P.gn / P.n_d;
+    for (int i = tid; i < mm; i += blockDim.x) rhs[i] = a.vec[i] - coef * ((P.has_third && af) ? y[2 + i] : 0.0);
+    __syncthreads();
+    const bool bad = a.res[3] != 0.0 || a.res[4] != 0.0;
+    for (int i = tid; i < mm; i += blockDim.x) {
+        const double* yr = a.Mg + (size_t)i * ldm;
+        double s0 = 0.0, s1 = 0.0;
+        int j = 0;
+        for (; j + 1 < mm; j += 2) {
+            s0 = fma(yr[j], rhs[j], s0);
+            s1 = fma(yr[j + 1], rhs[j + 1], s1);
+        }
+        if (j < mm) s0 = fma(yr[j], rhs[j], s0);
+        a.res[64 + i] = bad ? NAN : s0 + s1;
+    }
+}
+
 size_t main_smem_bytes(int m) {
     const int mm = m - 2;
     return ((size_t)mm * m_stride(mm) + 9 * (size_t)mm + (size_t)kGpMaxCols * m + 2 * (size_t)m + 16) *
@@ -648,6 +871,29 @@ size_t main_smem_bytes(int m) {
 }
 
 }  // namespace
+
+void gram_pcg_alloc(mvsk_gpu_ctx* ctx, GramPcgWs& ws, size_t ld) {
+    for (double* p : {ws.par, ws.Mg, ws.vec, ws.vin1, ws.vin2, ws.t3, ws.res, ws.Gf})
+        if (p) MVSK_CUDA(cudaFree(p));
+    for (double* p : {ws.h_par, ws.h_res})
+        if (p) MVSK_CUDA(cudaFreeHost(p));
+    const GpLayout Lmax(kGpMaxM, kGpMaxM - 2, kGpMaxCols);
+    ws.par_elems = Lmax.total;
+    MVSK_CUDA(cudaMalloc(&ws.par, ws.par_elems * sizeof(double)));
+    MVSK_CUDA(cudaMallocHost(&ws.h_par, ws.par_elems * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ws.Mg, (size_t)kGpMaxM * (kGpMaxM + 1) * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ws.Gf, (size_t)kGpMaxM * kGpMaxM * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ws.vec, (size_t)2 * kGpMaxM * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ws.vin1, (size_t)kGpMaxCols * ld * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ws.vin2, (size_t)kGpMaxCols * ld * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ws.t3, (size_t)kGpMaxCols * ld * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&ws.res, (size_t)(64 + kGpMaxM) * sizeof(double)));
+    MVSK_CUDA(cudaMallocHost(&ws.h_res, (size_t)(64 + kGpMaxM) * sizeof(double)));
+    MVSK_CUDA(cudaMemset(ws.res, 0, (size_t)(64 + kGpMaxM) * sizeof(double)));
+    ws.cap_m = kGpMaxM;
+    ws.cap_ld = ld;
+    ++ctx->epoch;
+}
 
 bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const PcgInput& in, PcgOutput& out) {
     const int m = (int)in.m;
@@ -669,33 +915,12 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
     const GpLayout L(m, mm, np);
     const size_t ld = (size_t)ctx->ld;
     // workspace (sized for the largest face seen; growth invalidates graphs)
-    if (ws.cap_m < (size_t)kGpMaxM || ws.cap_ld < ld) {
-        for (double* p : {ws.par, ws.Mg, ws.vec, ws.vin1, ws.vin2, ws.t3, ws.res, ws.Gf})
-            if (p) MVSK_CUDA(cudaFree(p));
-        for (double* p : {ws.h_par, ws.h_res})
-            if (p) MVSK_CUDA(cudaFreeHost(p));
-        const GpLayout Lmax(kGpMaxM, kGpMaxM - 2, kGpMaxCols);
-        ws.par_elems = Lmax.total;
-        MVSK_CUDA(cudaMalloc(&ws.par, ws.par_elems * sizeof(double)));
-        MVSK_CUDA(cudaMallocHost(&ws.h_par, ws.par_elems * sizeof(double)));
-        MVSK_CUDA(cudaMalloc(&ws.Mg, (size_t)kGpMaxM * (kGpMaxM + 1) * sizeof(double)));
-        MVSK_CUDA(cudaMalloc(&ws.Gf, (size_t)kGpMaxM * kGpMaxM * sizeof(double)));
-        MVSK_CUDA(cudaMalloc(&ws.vec, (size_t)2 * kGpMaxM * sizeof(double)));
-        MVSK_CUDA(cudaMalloc(&ws.vin1, (size_t)kGpMaxCols * ld * sizeof(double)));
-        MVSK_CUDA(cudaMalloc(&ws.vin2, (size_t)kGpMaxCols * ld * sizeof(double)));
-        MVSK_CUDA(cudaMalloc(&ws.t3, (size_t)kGpMaxCols * ld * sizeof(double)));
-        MVSK_CUDA(cudaMalloc(&ws.res, (size_t)(64 + kGpMaxM) * sizeof(double)));
-        MVSK_CUDA(cudaMallocHost(&ws.h_res, (size_t)(64 + kGpMaxM) * sizeof(double)));
-        MVSK_CUDA(cudaMemset(ws.res, 0, (size_t)(64 + kGpMaxM) * sizeof(double)));
-        ws.cap_m = kGpMaxM;
-        ws.cap_ld = ld;
-        ++ctx->epoch;
-    }
+    if (ws.cap_m < (size_t)kGpMaxM || ws.cap_ld < ld) gram_pcg_alloc(ctx, ws, ld);
     // the Gram cluster: 16 CTAs where a non-portable cluster of this size is
     // resident, else 8 (portable)
     const bool sharded = is_sharded(ctx);
-    const void* cfn = sharded ? reinterpret_cast<const void*>(&gram_pcg_cluster_kernel<false>)
-                              : reinterpret_cast<const void*>(&gram_pcg_cluster_kernel<true>);
+    const void* cfn = sharded ? reinterpret_cast<const void*>(&gram_pcg_cluster_kernel<0>)
+                              : reinterpret_cast<const void*>(&gram_pcg_cluster_kernel<1>);
     int CS = 0;
     for (int cs : {16, 8})
         if (!CS && cluster_fits(cfn, cs, kGpThreads, setup_smem)) CS = cs;
@@ -820,6 +1045,124 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
     // reference contract (common.hpp:27-37): 2 passes per Hop, 3 per third action
     ctx->fwd += (uint64_t)(hvps + 2LL * np);
     ctx->tr += (uint64_t)(hvps + np);
+    return true;
+}
+
+bool direct_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const DirectInput& in,
+                             std::vector<double>& u) {
+    const int m = (int)in.m;
+    if (m < 4 || m > kGpMaxM || is_sharded(ctx)) return false;
+    // opt-in (MVSK_DEVICE_DIRECT=1): on B200 its kernel chain measured slower than
+    // the host LU path (C2 direction 207 vs 122 us, C1 69 vs 56 us; profiles/
+    // r02_direct_device_ab.txt) - the Gauss-Jordan sweep pays a block barrier per
+    // pivot and the trace still needs two more kernels
+    static const bool on = std::getenv("MVSK_DEVICE_DIRECT") != nullptr;
+    if (!on) return false;
+    const int mm = m - 2;
+    const int mp = (m + 3) & ~3;
+    const long long avail = (long long)(ctx->max_smem / sizeof(double)) - (6LL * m + 64) - 64;
+    long long SR = std::min<long long>(avail / (mp + 1), (ctx->T_local + 7) / 8);
+    SR = std::max<long long>(SR, 1);
+    const int stage_rows = (int)SR;
+    const size_t setup_smem = gp_setup_smem_doubles(m, stage_rows) * sizeof(double);
+    if (setup_smem > ctx->max_smem) return false;
+    const void* cfn = reinterpret_cast<const void*>(&gram_pcg_cluster_kernel<2>);
+    int CS = 0;
+    for (int cs : {16, 8})
+        if (!CS && cluster_fits(cfn, cs, kGpThreads, setup_smem)) CS = cs;
+    if (!CS) return false;
+    if (!ctx->gpcg) ctx->gpcg = new GramPcgWs();
+    GramPcgWs& ws = *ctx->gpcg;
+    const size_t ld = (size_t)ctx->ld;
+    if (ws.cap_m < (size_t)kGpMaxM || ws.cap_ld < ld) gram_pcg_alloc(ctx, ws, ld);
+    if (!ctx->pmat) {
+        MVSK_CUDA(cudaMalloc(&ctx->pmat, ld * ld * sizeof(double)));
+        ++ctx->epoch;
+    }
+    ensure_tvec2(ctx);
+    const GpLayout L(m, mm, 0);
+    double* hp = ws.h_par;
+    std::copy(in.vU.begin(), in.vU.end(), hp + L.vU);
+    std::copy(in.vQ.begin(), in.vQ.end(), hp + L.vQ);
+    std::copy(in.nu.begin(), in.nu.end(), hp + L.nu);
+    for (int i = 0; i < m; ++i) hp[L.idx + i] = (double)(fm.active ? fm.idx[(size_t)i] : i);
+    GpParams P{};
+    P.m = m;
+    P.mm = mm;
+    P.np = 0;
+    P.has_third = in.has_third ? 1 : 0;
+    P.face_active = fm.active ? 1 : 0;
+    P.bU = in.bU;
+    P.bQ = in.bQ;
+    P.gn = in.gn;
+    P.lambda = in.lambda;
+    P.n_d = (double)m;
+    P.store(hp);
+    const Slot& sl = ctx->slots[slot];
+    const int key = m * 64 + (in.has_third ? 1 : 0);
+    run_graphed(ctx, kGraphGramDirect, key, slot, [&] {
+        MVSK_CUDA(cudaMemcpyAsync(ws.par, ws.h_par, L.total * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        SetupArgs sa{};
+        sa.par = ws.par;
+        sa.ld = (int)ld;
+        sa.Mg = ws.Mg;
+        sa.vec = ws.vec;
+        sa.res = ws.res;
+        sa.pmat = in.has_third ? ctx->pmat : nullptr;
+        GramArgsC ga{};
+        ga.X = ctx->X;
+        ga.T = ctx->T_local;
+        ga.ld = (int)ld;
+        ga.z = sl.z;
+        ga.c2 = ctx->c.c2;
+        ga.c3 = ctx->c.c3;
+        ga.c4 = ctx->c.c4;
+        ga.scale = 1.0 / (double)ctx->T_global;
+        ga.Gout = nullptr;
+        ga.stage_rows = stage_rows;
+        set_smem_attr(cfn, setup_smem);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(CS);
+        cfg.blockDim = dim3(kGpThreads);
+        cfg.dynamicSmemBytes = setup_smem;
+        cfg.stream = ctx->stream;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        void* cargs[] = {&ga, &sa};
+        ++ctx->launches;
+        MVSK_CUDA(cudaLaunchKernelExC(&cfg, cfn, cargs));
+        ctx->phys += 1;
+        const double* af = nullptr;
+        if (in.has_third) {
+            // q_t = a_t^T P a_t and tw_t = psi'''(z_t) q_t / T, then A^T tw (:174-177)
+            run_quadform(ctx, ctx->pmat, ctx->tvec2, sl.z, ctx->tvec);
+            PassIO io;
+            io.tw = ctx->tvec;
+            io.out = ctx->outd;
+            io.ldo = (long long)ld;
+            run_pass(ctx, Op::XTW, 1, io);
+            af = ctx->outd;
+        }
+        MainArgs ma{};
+        ma.par = ws.par;
+        ma.ld = (int)ld;
+        ma.Mg = ws.Mg;
+        ma.vec = ws.vec;
+        ma.res = ws.res;
+        const size_t msm = (size_t)(3 * m + mm + 16) * sizeof(double);
+        ++ctx->launches;
+        gram_direct_main_kernel<<<1, kGpThreads, msm, ctx->stream>>>(ma, af);
+        MVSK_CUDA(cudaGetLastError());
+        MVSK_CUDA(cudaMemcpyAsync(ws.h_res, ws.res, (size_t)(64 + mm) * sizeof(double), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    });
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+    u.assign(ws.h_res + 64, ws.h_res + 64 + mm);
     return true;
 }
 

@@ -162,13 +162,9 @@ void run_graphed(mvsk_gpu_ctx* ctx, int op, int k, int slot, const std::function
     enqueue();
 }
 
-namespace {
-
 void ensure_tvec2(mvsk_gpu_ctx* ctx) {
     if (!ctx->tvec2) MVSK_CUDA(cudaMalloc(&ctx->tvec2, (size_t)std::max<long long>(1, ctx->T_local) * sizeof(double)));
 }
-
-}  // namespace
 
 double op_make_cache(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* x) {
     check_slot(ctx, slot, false);

@@ -39,4 +39,17 @@ void pcg_workspace_free(mvsk_gpu_ctx* ctx);
 bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const PcgInput& in, PcgOutput& out);
 void gram_pcg_workspace_free(mvsk_gpu_ctx* ctx);
 
+// direct branch of the YAND direction (affine_normal.hpp:151-188) on the device
+// for faces of m <= 112: Gram, M + lambda I, its inverse, P, the trace pass and
+// u = M^-1 rhs in one graph launch (gram_pcg.cu); false when out of range.
+// A non-finite u asks the caller for the lambda fallback.
+struct DirectInput {
+    long long m = 0;
+    std::vector<double> vU, vQ, nu;
+    double bU = 0, bQ = 0, gn = 0, lambda = 0;
+    bool has_third = true;
+};
+bool direct_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const DirectInput& in,
+                             std::vector<double>& u);
+
 }  // namespace mvsk_b200

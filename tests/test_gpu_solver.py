@@ -465,7 +465,9 @@ def test_cluster_spg_preamble_matches_the_host_loop(name, kappa):
     from paper_2604_25378_b200.datagen import make_panel
     host = _solve_subprocess(name, kappa, {"MVSK_NO_SPG_CLUSTER": "1", "MVSK_NO_SPG_GRAPH": "1"}, eps=1e-10)
     clus = _solve_subprocess(name, kappa, {}, eps=1e-10)
-    assert clus["spg_ms"] > 0.02 > host["spg_ms"]  # the device preamble ran only in the default run
+    # the device preamble ran only in the default run (the host loop's profile
+    # entry is the failed device attempt only)
+    assert clus["spg_ms"] > max(0.05, 3.0 * host["spg_ms"]), (clus["spg_ms"], host["spg_ms"])
     assert clus["ident"] > 0
     A, mu, c = make_panel(name, seed=11, kappa=kappa)
     cfg_c = po.preset("large")
