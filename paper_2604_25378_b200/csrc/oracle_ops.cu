@@ -31,7 +31,13 @@ const void* kfn() {
 // wide rows on short panels (C4: 34 rows of 40 KB per SM): the input vector in
 // shared memory frees the registers for two 160-thread row teams per CTA
 const void* select_kernel_vs(Op op, int K, int Q, int RG) {
-    if (RG != 1 || K != 1) return nullptr;
+    if (K != 1) return nullptr;
+    if (RG == 2) {
+        if (Q == 8 && op == Op::FGRAD) return kfn<Op::FGRAD, 1, 8, 2, true>();
+        if (Q == 8 && op == Op::HVP) return kfn<Op::HVP, 1, 8, 2, true>();
+        return nullptr;
+    }
+    if (RG != 1) return nullptr;
     switch (op) {
     case Op::FGRAD:
         if (Q == 8) return kfn<Op::FGRAD, 1, 8, 1, true>();
@@ -67,10 +73,12 @@ const void* select_kernel(Op op, int K, int Q, int RG) {
     case Op::FGRAD:
         MVSK_QRG(Op::FGRAD, 1)
         if (Q == 8 && RG == 1) return kfn<Op::FGRAD, 1, 8, 1>();
+        if (Q == 8 && RG == 2) return kfn<Op::FGRAD, 1, 8, 2>();
         break;
     case Op::LINESUMS:
         MVSK_QRG(Op::LINESUMS, 1)
         if (Q == 8 && RG == 1) return kfn<Op::LINESUMS, 1, 8, 1>();
+        if (Q == 8 && RG == 2) return kfn<Op::LINESUMS, 1, 8, 2>();
         break;
     case Op::XTW:
         MVSK_QRG(Op::XTW, 1)
@@ -80,6 +88,7 @@ const void* select_kernel(Op op, int K, int Q, int RG) {
         if (K == 1) {
             MVSK_QRG(Op::HVP, 1)
             if (Q == 8 && RG == 1) return kfn<Op::HVP, 1, 8, 1>();
+            if (Q == 8 && RG == 2) return kfn<Op::HVP, 1, 8, 2>();
         } else if (K == 2) {
             MVSK_QRG(Op::HVP, 2)
             if (Q == 8 && RG == 1) return kfn<Op::HVP, 2, 8, 1>();
@@ -151,29 +160,30 @@ TuneOverride tune_override() {
 // wide-row plan for short panels: the input vector in shared memory, Q = 16
 // column pairs per thread, two row teams per CTA (MVSK_TUNE 6th field: 1/0
 // forces it on / off for the ops that have it)
-// Default only for f+grad, where it measured faster (C4: 50.6 -> 46.6 us; the
-// 1-RHS HVP and line sums were unchanged, profiles/r02_tune_c4_vs.txt)
+// An A/B variant (MVSK_TUNE 6th field = 1): it beat the one-row plan for
+// f+grad at C4 (50.6 -> 46.6 us) but two rows per team in registers beat both
+// (42.6 us; profiles/r02_tune_c4_vs.txt), so it is not a default
 bool make_plan_vs(const mvsk_gpu_ctx* ctx, Op op, int K, const TuneOverride& tov, Plan& pl) {
     const long long npairs = ctx->ld / 2;
-    const bool small = ctx->T_local < 64LL * ctx->nsm;
-    const bool want = tov.VS >= 0 ? tov.VS == 1 : (small && npairs >= 1024 && op == Op::FGRAD);
+    const bool want = tov.VS == 1;
     // the same width range as every other op of this build (n <= 8192)
     if (!want || npairs > 4096) return false;
     const int Q = tov.Q > 0 ? tov.Q : 16;
-    if (!select_kernel_vs(op, K, Q, 1)) return false;
+    const int RG = tov.RG > 0 ? tov.RG : 1;
+    if (!select_kernel_vs(op, K, Q, RG)) return false;
     const int P = round_team((int)((npairs + Q - 1) / Q));
-    const int mt = max_threads(op, K, Q, 1, true);
+    const int mt = max_threads(op, K, Q, RG, true);
     int G = tov.G > 0 ? tov.G : std::max(1, std::min(4, mt / P));
     if (G * P > mt) return false;
     const size_t row_bytes = (size_t)ctx->ld * sizeof(double);
-    const size_t stage_bytes = ((size_t)G * row_bytes + 127) & ~(size_t)127;
+    const size_t stage_bytes = ((size_t)G * RG * row_bytes + 127) & ~(size_t)127;
     const int ndot = op_ndot(op, K), nacc = op_nacc(op, K);
     const int nwp = P >= 32 ? P / 32 : 1;
-    const size_t red_bytes = (((size_t)2 * G * std::max(ndot, 1) * nwp * sizeof(double)) + 127) & ~(size_t)127;
+    const size_t red_bytes = (((size_t)2 * G * RG * std::max(ndot, 1) * nwp * sizeof(double)) + 127) & ~(size_t)127;
     const size_t vs_bytes = ((size_t)ndot * ctx->ld * sizeof(double) + 127) & ~(size_t)127;
     const size_t combine = ((size_t)G * std::max(nacc, 1) * ctx->ld + 16 + (size_t)G * 16) * sizeof(double);
     const size_t combine_all = std::max(combine, (size_t)(G * P) * sizeof(double));
-    const int nst_total = (int)std::max<long long>(1, (ctx->T_local + G - 1) / G);
+    const int nst_total = (int)std::max<long long>(1, (ctx->T_local + G * RG - 1) / (G * RG));
     int S = tov.S >= 2 ? tov.S : 3;
     S = std::min(S, std::max(2, nst_total));
     auto smem_of = [&](int s) { return 128 + red_bytes + vs_bytes + std::max((size_t)s * stage_bytes, combine_all); };
@@ -182,12 +192,12 @@ bool make_plan_vs(const mvsk_gpu_ctx* ctx, Op op, int K, const TuneOverride& tov
     pl.Q = Q;
     pl.P = P;
     pl.G = G;
-    pl.RG = 1;
+    pl.RG = RG;
     pl.S = S;
     pl.VS = true;
     pl.smem = smem_of(S);
-    pl.fn = select_kernel_vs(op, K, Q, 1);
-    pl.nb = (int)std::min<long long>(ctx->nsm, std::max<long long>(1, (ctx->T_local + G - 1) / G));
+    pl.fn = select_kernel_vs(op, K, Q, RG);
+    pl.nb = (int)std::min<long long>(ctx->nsm, std::max<long long>(1, (ctx->T_local + G * RG - 1) / (G * RG)));
     return true;
 }
 
@@ -250,6 +260,13 @@ bool make_plan(const mvsk_gpu_ctx* ctx, Op op, int K, Plan& pl) {
     // per team interleave two independent chains
     if (!small && G == 1 && RG == 1 && Q == 8 && P <= max_threads(op, K, Q, 2) &&
         select_kernel(op, K, Q, 2) != nullptr && want_rows >= 2)
+        RG = 2;
+    // short panels of wide rows (C4: 34 rows of 40 KB per SM, one 320-thread team):
+    // two rows per team per stage interleave two reduction chains (f+grad
+    // 48.3 -> 42.6 us, HVP 44.5 -> 40.5, line sums 40.4 -> 38.9;
+    // profiles/r02_tune_c4_vs.txt)
+    if (small && G == 1 && RG == 1 && Q == 8 && P >= 256 && select_kernel(op, K, 8, 2) &&
+        G * P <= max_threads(op, K, 8, 2) && want_rows >= 1)
         RG = 2;
     if (tov.G > 0 && tov.G * P <= max_threads(op, K, Q, RG)) G = tov.G;
     if (tov.RG > 0 && (tov.RG * Q <= 8 || select_kernel(op, K, Q, tov.RG)) && G * P <= max_threads(op, K, Q, tov.RG))

@@ -1,0 +1,11 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+prof() {  # name kernel-regex skip cmd...
+  local name=$1 kre=$2 skip=$3; shift 3
+  timeout 900 ncu --set full --clock-control none --cache-control none --warp-sampling-interval 0 --import-source on -k regex:$kre -s $skip -c 1 -o /tmp/$name "$@" > gpurun_out/$name.log 2>&1
+  echo "$name rc $?"
+  ncu -i /tmp/$name.ncu-rep --page source --csv --print-source sass > gpurun_out/${name}_sass.csv 2>/dev/null
+  ncu -i /tmp/$name.ncu-rep --page details > gpurun_out/${name}_details.txt 2>/dev/null
+  rm -f /tmp/$name.ncu-rep
+}
+prof r2_gpcg_cluster2 gram_pcg_cluster 5 python scripts/one_solve_prof.py C4

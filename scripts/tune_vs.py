@@ -64,8 +64,8 @@ def timeit(fn, reps=20):
     return a.elapsed_time(b) / reps
 
 
-plans = ["", "0,0,0,0,0,0", "16,2,1,2,0,1", "16,2,1,3,0,1", "16,2,1,4,0,1", "16,1,1,4,0,1", "16,1,1,6,0,1",
-         "8,1,1,3,0,1", "8,1,1,5,0,1", "16,3,1,2,0,1"]
+plans = ["", "0,0,0,0,0,0", "16,2,1,3,0,1", "8,1,2,2,0,0", "8,1,2,3,0,0", "8,1,2,2,0,1", "8,1,2,3,0,1",
+         "8,1,1,3,0,0", "8,1,1,4,0,0", "8,1,1,5,0,0"]
 for op, (fn, get) in FN.items():
     ref = None
     for p in plans:
