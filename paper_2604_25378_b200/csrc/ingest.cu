@@ -14,21 +14,51 @@
 namespace mvsk_b200 {
 namespace {
 
-// column sums of a T x ld block (one thread per column, rows in order) and a
-// non-finite flag
-__global__ void colsum_kernel(const double* X, long long T, int ld, int n, double* sums, int* bad) {
+// column sums of a T x ld block in two fixed-order stages (deterministic): each
+// block sums one row chunk for a slice of columns (coalesced rows), then the
+// chunk partials are summed in chunk order; plus a non-finite flag
+__global__ void colsum_part_kernel(const double* X, long long T, int ld, int n, long long rows_per, double* part,
+                                   int* bad) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const long long t0 = (long long)blockIdx.y * rows_per, t1 = min(T, t0 + rows_per);
     if (c >= n) return;
     double s = 0.0;
     int nf = 0;
-    for (long long t = 0; t < T; ++t) {
+    for (long long t = t0; t < t1; ++t) {
         const double v = X[t * ld + c];
         s += v;
         nf |= !isfinite(v);
     }
-    sums[c] = s;
+    part[(size_t)blockIdx.y * n + c] = s;
     if (nf) atomicOr(bad, 1);
 }
+__global__ void colsum_finish_kernel(const double* part, int nsplit, int n, double* sums) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    double s = 0.0;
+    for (int k = 0; k < nsplit; ++k) s += part[(size_t)k * n + c];
+    sums[c] = s;
+}
+
+// RAII holders for the ingest's temporaries (freed on every exit path)
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+struct PinBuf {
+    void* p = nullptr;
+    ~PinBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+struct Event {
+    cudaEvent_t e = nullptr;
+    ~Event() {
+        if (e) cudaEventDestroy(e);
+    }
+};
 
 __global__ void center_kernel(double* X, long long T, int ld, int n, const double* mu) {
     const long long tot = T * (long long)ld;
@@ -79,77 +109,66 @@ void ingest_binary(mvsk_gpu_ctx* ctx, const char* path) {
     const size_t row_bytes = (size_t)n * sizeof(double);
     // pinned double buffer of ~16 MB row blocks
     const long long rows_per = std::max<long long>(1, (16LL << 20) / (long long)row_bytes);
-    double* pin[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2];
-    MVSK_CUDA(cudaMallocHost(&pin[0], rows_per * row_bytes));
-    MVSK_CUDA(cudaMallocHost(&pin[1], rows_per * row_bytes));
-    MVSK_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-    MVSK_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
-    bool ok = true;
-    std::string err;
-    try {
-        if (ld != n) MVSK_CUDA(cudaMemsetAsync(ctx->X, 0, (size_t)std::max<long long>(1, T_loc) * ld * sizeof(double), ctx->stream));
-        if (std::fseek(f.get(), 12 + (long)(ctx->row0 * (long long)row_bytes), SEEK_SET) != 0)
-            throw ApiError(MVSK_DATA_ERROR, std::string(path) + ": truncated payload");
-        int b = 0;
-        for (long long r = 0; r < T_loc; r += rows_per, b ^= 1) {
-            const long long rows = std::min(rows_per, T_loc - r);
-            MVSK_CUDA(cudaEventSynchronize(ev[b]));  // the H2D that last used this buffer is done
-            if (std::fread(pin[b], row_bytes, (size_t)rows, f.get()) != (size_t)rows)
-                throw ApiError(MVSK_DATA_ERROR, std::string(path) + ": truncated payload");
-            MVSK_CUDA(cudaMemcpy2DAsync(ctx->X + r * ld, ld * sizeof(double), pin[b], row_bytes, row_bytes, rows,
-                                        cudaMemcpyHostToDevice, ctx->stream));
-            MVSK_CUDA(cudaEventRecord(ev[b], ctx->stream));
-        }
-        // global column means (allreduce of the per-shard column sums)
-        double* sums = nullptr;
-        int* bad = nullptr;
-        MVSK_CUDA(cudaMalloc(&sums, (n + 1) * sizeof(double)));
-        MVSK_CUDA(cudaMalloc(&bad, sizeof(int)));
-        MVSK_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
-        ++ctx->launches;
-        colsum_kernel<<<(int)((n + 127) / 128), 128, 0, ctx->stream>>>(ctx->X, T_loc, (int)ld, (int)n, sums, bad);
-        MVSK_CUDA(cudaGetLastError());
-        int hbad = 0;
-        std::vector<double> hs((size_t)n + 1, 0.0);
-        // append the flag as a double so one allreduce carries both
-        MVSK_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
-        const double flag = hbad ? 1.0 : 0.0;
-        MVSK_CUDA(cudaMemcpyAsync(sums + n, &flag, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        allreduce_sum(ctx, sums, (size_t)n + 1);
-        MVSK_CUDA(cudaMemcpyAsync(hs.data(), sums, (n + 1) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
-        if (hs[(size_t)n] != 0.0) {
-            cudaFree(sums);
-            cudaFree(bad);
-            throw ApiError(MVSK_DATA_ERROR, "center_panel: non-finite return entry");
-        }
-        ctx->mu.resize((size_t)n);
-        for (long long j = 0; j < n; ++j) ctx->mu[(size_t)j] = hs[(size_t)j] / (double)ctx->T_global;
-        MVSK_CUDA(cudaMemcpyAsync(sums, ctx->mu.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        ++ctx->launches;
-        center_kernel<<<4 * ctx->nsm, 256, 0, ctx->stream>>>(ctx->X, T_loc, (int)ld, (int)n, sums);
-        MVSK_CUDA(cudaGetLastError());
-        MVSK_CUDA(cudaMemcpyAsync(ctx->mu_dev, ctx->mu.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
-        cudaFree(sums);
-        cudaFree(bad);
-    } catch (const std::exception& e) {
-        ok = false;
-        err = e.what();
-        cudaStreamSynchronize(ctx->stream);
-        cudaFreeHost(pin[0]);
-        cudaFreeHost(pin[1]);
-        cudaEventDestroy(ev[0]);
-        cudaEventDestroy(ev[1]);
-        throw;
+    PinBuf pin[2];
+    Event ev[2];
+    // the stream may hold this rank's earlier work; every exit path below
+    // drains it before the RAII holders free what it may still touch
+    struct Drain {
+        cudaStream_t s;
+        ~Drain() { cudaStreamSynchronize(s); }
+    } drain{ctx->stream};
+    for (int i = 0; i < 2; ++i) {
+        MVSK_CUDA(cudaMallocHost(&pin[i].p, rows_per * row_bytes));
+        MVSK_CUDA(cudaEventCreateWithFlags(&ev[i].e, cudaEventDisableTiming));
     }
-    cudaFreeHost(pin[0]);
-    cudaFreeHost(pin[1]);
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
-    (void)ok;
+    if (ld != n) MVSK_CUDA(cudaMemsetAsync(ctx->X, 0, (size_t)std::max<long long>(1, T_loc) * ld * sizeof(double), ctx->stream));
+    if (std::fseek(f.get(), 12 + (long)(ctx->row0 * (long long)row_bytes), SEEK_SET) != 0)
+        throw ApiError(MVSK_DATA_ERROR, std::string(path) + ": truncated payload");
+    int b = 0;
+    for (long long r = 0; r < T_loc; r += rows_per, b ^= 1) {
+        const long long rows = std::min(rows_per, T_loc - r);
+        MVSK_CUDA(cudaEventSynchronize(ev[b].e));  // the H2D that last used this buffer is done
+        if (std::fread(pin[b].p, row_bytes, (size_t)rows, f.get()) != (size_t)rows)
+            throw ApiError(MVSK_DATA_ERROR, std::string(path) + ": truncated payload");
+        MVSK_CUDA(cudaMemcpy2DAsync(ctx->X + r * ld, ld * sizeof(double), pin[b].p, row_bytes, row_bytes, rows,
+                                    cudaMemcpyHostToDevice, ctx->stream));
+        MVSK_CUDA(cudaEventRecord(ev[b].e, ctx->stream));
+    }
+    // global column means (allreduce of the per-shard column sums)
+    const int cb = (int)((n + 127) / 128);
+    const long long rows_chunk = std::max<long long>(64, (T_loc + 4LL * ctx->nsm / cb) / std::max(1, 4 * ctx->nsm / cb));
+    const int nsplit = (int)std::max<long long>(1, (T_loc + rows_chunk - 1) / rows_chunk);
+    DevBuf part, sums, bad;
+    MVSK_CUDA(cudaMalloc(&part.p, (size_t)nsplit * n * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&sums.p, (n + 1) * sizeof(double)));
+    MVSK_CUDA(cudaMalloc(&bad.p, sizeof(int)));
+    double* sp = static_cast<double*>(sums.p);
+    MVSK_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
+    ctx->launches += 2;
+    colsum_part_kernel<<<dim3(cb, nsplit), 128, 0, ctx->stream>>>(ctx->X, T_loc, (int)ld, (int)n, rows_chunk,
+                                                                  static_cast<double*>(part.p), static_cast<int*>(bad.p));
+    MVSK_CUDA(cudaGetLastError());
+    colsum_finish_kernel<<<cb, 128, 0, ctx->stream>>>(static_cast<double*>(part.p), nsplit, (int)n, sp);
+    MVSK_CUDA(cudaGetLastError());
+    int hbad = 0;
+    std::vector<double> hs((size_t)n + 1, 0.0);
+    // append the flag as a double so one allreduce carries both
+    MVSK_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double flag = hbad ? 1.0 : 0.0;
+    MVSK_CUDA(cudaMemcpyAsync(sp + n, &flag, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    allreduce_sum(ctx, sp, (size_t)n + 1);
+    MVSK_CUDA(cudaMemcpyAsync(hs.data(), sp, (n + 1) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hs[(size_t)n] != 0.0) throw ApiError(MVSK_DATA_ERROR, "center_panel: non-finite return entry");
+    ctx->mu.resize((size_t)n);
+    for (long long j = 0; j < n; ++j) ctx->mu[(size_t)j] = hs[(size_t)j] / (double)ctx->T_global;
+    MVSK_CUDA(cudaMemcpyAsync(sp, ctx->mu.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ++ctx->launches;
+    center_kernel<<<4 * ctx->nsm, 256, 0, ctx->stream>>>(ctx->X, T_loc, (int)ld, (int)n, sp);
+    MVSK_CUDA(cudaGetLastError());
+    MVSK_CUDA(cudaMemcpyAsync(ctx->mu_dev, ctx->mu.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 }  // namespace mvsk_b200
