@@ -477,3 +477,33 @@ def test_cluster_spg_preamble_matches_the_host_loop(name, kappa):
         xg = np.array([float.fromhex(v) for v in run["xs"]])
         rg = SimpleNamespace(status=run["status"], f_star=float.fromhex(run["f"]))
         _reference_outcome_match(A, mu, c, cfg_c, xg, rg)
+
+
+@pytest.mark.parametrize("profile", [(10.0, 1.0, 10.0, 1.0), (1.0, 10.0, 1.0, 10.0), (10.0, 10.0, 10.0, 10.0)])
+def test_stress_profiles_direct_and_pcg(profile):
+    """bench.hpp:81-90 stress calibrations (return-seeking is outside the convex
+    cone: psi'' changes sign, M = (UQ)^T G (UQ) can be indefinite, so the direct
+    branch must take the pivoted-LU path rather than the Cholesky shortcut).
+    Directions vs the reference (same Krylov counts, 1e-9 relative) and solves at
+    the north_star bar (_reference_outcome_match)."""
+    from paper_2604_25378_b200.gpu_oracle import preset, tangent_config
+    c = np.array(profile)
+    for seed, (n, T) in enumerate([(6, 40), (12, 80), (25, 200)]):
+        A, mu = rh.lcg_panel(n, T, seed + 31)
+        cpu, gpu = po.CpuOracle(A, mu, c), _gpu(A, mu, c)
+        x = rh.simplex_point(n, seed + 3, 1e-6)
+        cc, gc = cpu.make_cache(x), gpu.make_cache(x)
+        for mode, lam in (("direct", 0.0), ("direct", 1e-6), ("pcg", 1e-4)):
+            dc, ddc = cpu.yand_direction(cc, po.tangent_config(mode, lam=lam), seed)
+            dg, ddg = gpu.yand_direction(gc, tangent_config(mode, lam=lam), seed)
+            assert ddg.lambda_fallback == ddc.lambda_fallback
+            assert ddg.krylov_iters == ddc.krylov_iters
+            assert np.max(np.abs(dg - dc)) <= 1e-9 * (1 + np.max(np.abs(dc))), (profile, n, mode)
+        for pre in ("small", "large"):
+            cfg_c, cfg_g = po.preset(pre), preset(pre)
+            for cfg in (cfg_c, cfg_g):
+                cfg.has_max_elapsed = 0
+                cfg.epsilon = 1e-10
+            xg, rg = gpu.solve(cfg_g)
+            _reference_outcome_match(A, mu, c, cfg_c, xg, rg)
+        gpu.close()
