@@ -48,6 +48,12 @@ struct SpgState {
     // parameters
     int n, ld, max_steps, patience;
     double tau, eps_stop;
+    // device-side timing of the graph variant's prep / accept kernels (cycles)
+    long long cyc_prep, cyc_acc;
+    // PAR switches: sort = 1 keeps the sorting projection (MVSK_SPG_SORT);
+    // prof = 1 adds the phase cycle sums below (MVSK_PROFILE)
+    int sort, prof, rounds_max, sort_fallbacks;
+    long long cyc_ph[8];
 };
 
 __device__ __forceinline__ double sdot(const double* a, const double* b, int n) {
@@ -294,6 +300,92 @@ __device__ void project_slice_par(const double* v, int n, double tau, double mas
     __syncthreads();
 }
 
+// ---- register-blocked PAR bodies (wide panels, the graph variant): each of the
+// kSpgThreads threads owns the kSpgE entries i = tid + j * kSpgThreads, so every
+// n-vector is read with all of a thread's loads in flight at once (the loops
+// above serialise one global round trip per entry), and the projection's
+// threshold comes without the sort (spg_theta_fixed_point)
+constexpr int kSpgE = kSpgMaxN / kSpgThreads;
+
+// block-wide sums of two values (every thread returns both totals)
+__device__ __forceinline__ void bsum2(double& a, double& b, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    __syncthreads();
+    if (lane == 0) {
+        red[warp] = a;
+        red[32 + warp] = b;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double t = lane < nw ? red[lane] : 0.0, t2 = lane < nw ? red[32 + lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            t += __shfl_xor_sync(0xffffffffu, t, o);
+            t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+        }
+        if (lane == 0) {
+            red[64] = t;
+            red[65] = t2;
+        }
+    }
+    __syncthreads();
+    a = red[64];
+    b = red[65];
+}
+
+// theta of project_slice (simplex.hpp:93-117) without sorting. The reference
+// takes theta = (css_k - s) / (k + 1) at the last k of the descending order with
+// u[k] > (css_k - s) / (k + 1): the support is S = {u > theta} and theta =
+// (sum_S u - s) / |S|. That fixed point is reached from S = all by iterating
+// theta <- (sum_{u > theta} u - s) / |{u > theta}| (theta nondecreasing, S
+// shrinking; Michelot's algorithm), a few block reductions instead of a
+// log^2(n)-stage sorting network. Returns false if S has not settled within
+// kRounds rounds (the caller then sorts); rounds: the count used.
+__device__ bool spg_theta_fixed_point(const double (&e)[kSpgE], double s, double& theta, int& rounds, double* red) {
+    constexpr int kRounds = 48;
+    double th = -INFINITY, cprev = -1.0;
+    for (int it = 0; it < kRounds; ++it) {
+        double sum = 0.0, cnt = 0.0;
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j)
+            if (e[j] > th) {
+                sum += e[j];
+                cnt += 1.0;
+            }
+        bsum2(sum, cnt, red);
+        if (cnt == cprev) {
+            theta = th;
+            rounds = it;
+            return true;
+        }
+        th = (sum - s) / cnt;
+        cprev = cnt;
+    }
+    rounds = kRounds;
+    return false;
+}
+
+__device__ __forceinline__ void spg_phase(SpgState* st, int k, long long& t) {
+    if (st->prof) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const long long now = clock64();
+            st->cyc_ph[k] += now - t;
+            t = now;
+        }
+    }
+}
+
+struct SpgBufs;
+__device__ void spg_prep_par(SpgState* st, const SpgBufs& b, double* u, double* bc);
+__device__ void spg_accept_par(SpgState* st, const SpgBufs& b, const double* gp, const double* fp_sc, double* u,
+                               double* bc);
+
 struct SpgBufs {
     double* x;    // n, current iterate
     double* g;    // n, gradient at x
@@ -377,7 +469,13 @@ template <bool PAR>
 __global__ void __launch_bounds__(kSpgThreads) spg_prep_kernel(SpgState* st, SpgBufs b) {
     extern __shared__ double u[];
     __shared__ double bc[2];
-    spg_prep_body<false, PAR>(st, b, u, bc);
+    const long long t0 = clock64();
+    if (PAR && !st->sort)
+        spg_prep_par(st, b, u, bc);
+    else
+        spg_prep_body<false, PAR>(st, b, u, bc);
+    __syncthreads();
+    if (threadIdx.x == 0) st->cyc_prep += clock64() - t0;
 }
 
 // Armijo test and the state update of one trial (solver.hpp:146-174): every
@@ -489,13 +587,263 @@ __device__ void spg_accept_body(SpgState* st, const SpgBufs& b, const double* gp
     __syncthreads();
 }
 
+// PAR trial step (spg_prep_body's PAR branch, register-blocked)
+__device__ void spg_prep_par(SpgState* st, const SpgBufs& b, double* u, double* bc) {
+    __shared__ double red[160];
+    const int n = st->n, tid = threadIdx.x;
+    long long t = clock64();
+    if (tid == 0) ++st->trials;
+    const int bt = st->bt;
+    double Lk;
+    if (bt == 0) {  // L0 from the BB pair (solver.hpp:131-135)
+        double L0 = st->L;
+        if (st->have_bb) {
+            double sy = 0.0, ss = 0.0;
+            double bs[kSpgE], by[kSpgE];
+#pragma unroll
+            for (int j = 0; j < kSpgE; ++j) {
+                const int i = tid + j * kSpgThreads;
+                bs[j] = i < n ? b.bbs[i] : 0.0;
+                by[j] = i < n ? b.bby[i] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < kSpgE; ++j) {
+                sy = fma(bs[j], by[j], sy);
+                ss = fma(bs[j], bs[j], ss);
+            }
+            bsum2(sy, ss, red);
+            L0 = (ss > 0 && sy > 0) ? sy / ss : st->L;
+            L0 = fmin(fmax(L0, 1e-2), 1e12);
+        }
+        Lk = L0;
+        if (tid == 0) st->Lk = L0;
+    } else {
+        Lk = st->Lk;
+    }
+    spg_phase(st, 0, t);
+    // u = y - tau with y = x - g / Lk (the values project_slice sorts)
+    const double tau = st->tau;
+    double e[kSpgE];
+    {
+        double xr[kSpgE], gr[kSpgE];
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j) {
+            const int i = tid + j * kSpgThreads;
+            xr[j] = i < n ? b.x[i] : 0.0;
+            gr[j] = i < n ? b.g[i] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j) e[j] = tid + j * kSpgThreads < n ? (xr[j] - gr[j] / Lk) - tau : -INFINITY;
+    }
+    spg_phase(st, 1, t);
+    const double s = 1.0 - (double)n * tau;
+    double theta = 0.0;
+    int rounds = 0;
+    const bool fixed = spg_theta_fixed_point(e, s, theta, rounds, red);
+    spg_phase(st, 2, t);
+    double xp[kSpgE];
+    if (fixed) {
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j) {
+            const int i = tid + j * kSpgThreads;
+            xp[j] = fmax(e[j] - theta, 0.0) + tau;
+            if (i < n) b.xp[i] = xp[j];
+        }
+    } else {  // S did not settle: the sorting projection
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j) {
+            const int i = tid + j * kSpgThreads;
+            if (i < n) b.y[i] = b.x[i] - b.g[i] / Lk;
+        }
+        __syncthreads();
+        project_slice_par(b.y, n, tau, 1.0, b.xp, u, &bc[0], red);
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j) {
+            const int i = tid + j * kSpgThreads;
+            xp[j] = i < n ? b.xp[i] : 0.0;
+        }
+    }
+    if (tid == 0) {
+        st->rounds_max = max(st->rounds_max, rounds);
+        if (!fixed) ++st->sort_fallbacks;
+    }
+    // dp = xp - x and gdp = g'dp
+    double gdp = 0.0, zero = 0.0;
+    {
+        double xr[kSpgE], gr[kSpgE];
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j) {
+            const int i = tid + j * kSpgThreads;
+            xr[j] = i < n ? b.x[i] : 0.0;
+            gr[j] = i < n ? b.g[i] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j) {
+            const int i = tid + j * kSpgThreads;
+            const double d = xp[j] - xr[j];
+            if (i < n) {
+                b.dp[i] = d;
+                gdp = fma(gr[j], d, gdp);
+            }
+        }
+    }
+    bsum2(gdp, zero, red);
+    if (tid == 0) {
+        st->gdp = gdp;
+        st->eval_flag = gdp < 0 ? 1 : 0;
+        if (gdp < 0) ++st->evals;
+    }
+    spg_phase(st, 3, t);
+}
+
+// PAR Armijo test and state update (spg_accept_body's PAR branch,
+// register-blocked; solver.hpp:146-174)
+__device__ void spg_accept_par(SpgState* st, const SpgBufs& b, const double* gp, const double* fp_sc, double* u,
+                               double* bc) {
+    __shared__ int s_acc, s_change, s_any, s_done;
+    __shared__ double red[160];
+    const int n = st->n, tid = threadIdx.x;
+    long long t = clock64();
+    if (tid == 0) {
+        const double fp = fp_sc[0];  // read unconditionally: only used when the pass ran
+        int acc = 0;
+        if (st->eval_flag) {
+            if (fp <= __dadd_rn(st->f, __dmul_rn(1e-4, st->gdp))) {  // Armijo (solver.hpp:146)
+                acc = 1;
+                st->f = fp;
+                st->L = st->Lk;
+                st->have_bb = 1;
+                ++st->accepts;
+            }
+        }
+        s_acc = acc;
+        s_change = 0;
+        s_any = 0;
+        if (!acc) {
+            if (st->Lk > 1e13 || st->bt + 1 >= 40) {  // no step: the preamble ends (:159-160)
+                st->done = 1;
+            } else {
+                st->Lk *= 2.0;
+                ++st->bt;
+            }
+        }
+    }
+    __syncthreads();
+    if (!s_acc) {
+        spg_phase(st, 4, t);
+        return;
+    }
+    // BB pair, iterate and gradient; active set (<= tau + 1e-12) and patience (:163-172)
+    const double thr = st->tau + 1e-12;
+    int chg = 0, any = 0;
+    {
+        double dp[kSpgE], gold[kSpgE], xn[kSpgE], gn[kSpgE];
+        unsigned char a0[kSpgE];
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j) {
+            const int i = tid + j * kSpgThreads;
+            const bool in = i < n;
+            dp[j] = in ? b.dp[i] : 0.0;
+            gn[j] = in ? gp[i] : 0.0;
+            gold[j] = in ? b.g[i] : 0.0;
+            xn[j] = in ? b.xp[i] : 0.0;
+            a0[j] = in ? b.act[i] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j) {
+            const int i = tid + j * kSpgThreads;
+            if (i < n) {
+                b.bbs[i] = dp[j];
+                b.bby[i] = gn[j] - gold[j];
+                b.x[i] = xn[j];
+                b.g[i] = gn[j];
+                const unsigned char a = xn[j] <= thr ? 1 : 0;
+                if (a != a0[j]) chg = 1;
+                if (a) any = 1;
+                b.act[i] = a;
+            }
+        }
+    }
+    chg = __syncthreads_or(chg);
+    any = __syncthreads_or(any);
+    if (tid == 0) {
+        const int steps = ++st->steps;
+        st->bt = 0;
+        ++st->k;
+        int done = 0;
+        if (chg) {
+            st->last_change = steps;
+        } else if (any && steps - st->last_change >= st->patience) {
+            done = 1;
+        }
+        if (st->k >= st->max_steps) done = 1;
+        s_done = done;
+        st->done = done;
+    }
+    __syncthreads();
+    spg_phase(st, 5, t);
+    // every 10 steps: gradient-mapping residual ||x - P(x - g)|| (:173-174)
+    if (!s_done && st->eps_stop > 0 && st->steps % 10 == 0) {
+        const double tau = st->tau;
+        double e[kSpgE], xn[kSpgE];
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j) {
+            const int i = tid + j * kSpgThreads;
+            xn[j] = i < n ? b.x[i] : 0.0;
+            e[j] = i < n ? b.g[i] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kSpgE; ++j) e[j] = tid + j * kSpgThreads < n ? (xn[j] - e[j]) - tau : -INFINITY;
+        const double s = 1.0 - (double)n * tau;
+        double theta = 0.0, r2 = 0.0, zero = 0.0;
+        int rounds = 0;
+        if (spg_theta_fixed_point(e, s, theta, rounds, red)) {
+#pragma unroll
+            for (int j = 0; j < kSpgE; ++j)
+                if (tid + j * kSpgThreads < n) {
+                    const double d = xn[j] - (fmax(e[j] - theta, 0.0) + tau);
+                    r2 = fma(d, d, r2);
+                }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kSpgE; ++j) {
+                const int i = tid + j * kSpgThreads;
+                if (i < n) b.y[i] = xn[j] - b.g[i];
+            }
+            __syncthreads();
+            project_slice_par(b.y, n, tau, 1.0, b.dp, u, &bc[0], red);
+#pragma unroll
+            for (int j = 0; j < kSpgE; ++j) {
+                const int i = tid + j * kSpgThreads;
+                if (i < n) {
+                    const double d = xn[j] - b.dp[i];
+                    r2 = fma(d, d, r2);
+                }
+            }
+            if (tid == 0) ++st->sort_fallbacks;
+        }
+        bsum2(r2, zero, red);
+        if (tid == 0) {
+            st->rounds_max = max(st->rounds_max, rounds);
+            if (sqrt(r2) <= st->eps_stop) st->done = 1;
+        }
+        spg_phase(st, 6, t);
+    }
+    __syncthreads();
+}
+
 template <bool PAR>
 __global__ void __launch_bounds__(kSpgThreads) spg_accept_kernel(SpgState* st, SpgBufs b, const double* gp,
                                                                  const double* fp_sc, cudaGraphConditionalHandle h,
                                                                  int set_cond) {
     extern __shared__ double u[];
     __shared__ double bc[2];
-    spg_accept_body<false, PAR>(st, b, gp, st->eval_flag ? fp_sc[0] : 0.0, u, bc);
+    const long long t0 = clock64();
+    if (PAR && !st->sort)
+        spg_accept_par(st, b, gp, fp_sc, u, bc);
+    else
+        spg_accept_body<false, PAR>(st, b, gp, st->eval_flag ? fp_sc[0] : 0.0, u, bc);
+    if (threadIdx.x == 0) st->cyc_acc += clock64() - t0;
     if (set_cond && threadIdx.x == 0) cudaGraphSetConditional(h, st->done ? 0u : 1u);
 }
 
@@ -828,6 +1176,10 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
     hs.tau = tau;
     hs.eps_stop = eps_stop;
     hs.done = max_steps <= 0 ? 1 : 0;
+    static const bool sort_proj = std::getenv("MVSK_SPG_SORT") != nullptr;
+    static const bool prof_ph = std::getenv("MVSK_PROFILE") != nullptr;
+    hs.sort = sort_proj ? 1 : 0;
+    hs.prof = prof_ph ? 1 : 0;
     std::vector<unsigned char> act0((size_t)n);
     for (int i = 0; i < n; ++i) act0[(size_t)i] = x[(size_t)i] <= tau + 1e-12 ? 1 : 0;
     MVSK_CUDA(cudaMemcpyAsync(st, &hs, sizeof(SpgState), cudaMemcpyHostToDevice, sm));
@@ -977,6 +1329,15 @@ bool spg_identify_device(mvsk_gpu_ctx* ctx, int slot, std::vector<double>& x, do
     MVSK_CUDA(cudaMemcpyAsync(&hs, st, sizeof(SpgState), cudaMemcpyDeviceToHost, sm));
     MVSK_CUDA(cudaMemcpyAsync(x.data(), b.x, n * sizeof(double), cudaMemcpyDeviceToHost, sm));
     MVSK_CUDA(cudaStreamSynchronize(sm));
+    static const bool verbose_g = std::getenv("MVSK_PROFILE") != nullptr;
+    if (verbose_g)
+        std::fprintf(stderr,
+                     "[spg graph] trials %d evals %d steps %d prep %.1f us accept %.1f us (sum, at 1.9 GHz) "
+                     "sort %d rounds_max %d fallbacks %d phases us: L0 %.1f load %.1f theta %.1f out %.1f "
+                     "reject %.1f update %.1f resid %.1f\n",
+                     hs.trials, hs.evals, hs.steps, hs.cyc_prep / 1.9e3, hs.cyc_acc / 1.9e3, hs.sort, hs.rounds_max,
+                     hs.sort_fallbacks, hs.cyc_ph[0] / 1.9e3, hs.cyc_ph[1] / 1.9e3, hs.cyc_ph[2] / 1.9e3,
+                     hs.cyc_ph[3] / 1.9e3, hs.cyc_ph[4] / 1.9e3, hs.cyc_ph[5] / 1.9e3, hs.cyc_ph[6] / 1.9e3);
     // counters: every trial ran prep + accept; the pass ran (and counts) only for
     // the trials with gdp < 0 (a forward pass each; the gradient of an accepted
     // point is the memoised transpose pass, oracle.hpp:79-90, as on the host path)
