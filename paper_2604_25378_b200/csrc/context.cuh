@@ -108,6 +108,7 @@ struct mvsk_gpu_ctx {
     // pinned host staging
     double* h_in = nullptr;
     double* h_out = nullptr;
+    double* h_out_dev = nullptr;  // device alias of h_out (mapped)
     size_t h_elems = 0;
     double* h_mat = nullptr;  // pinned n x n staging (direct branch: Gram out, P in)
     size_t h_mat_elems = 0;

@@ -34,6 +34,7 @@ struct FinishArgs {
     const double* value_offset_dev;  // if set, read at run time (graph-stable across face rebuilds)
     const int* skip;
     int nskip;
+    double* hout;  // optional mapped host mirror of the results (PassIO::hout)
 };
 
 // one virtual block `vb`; every thread of the CTA calls it (it synchronises)
@@ -79,7 +80,11 @@ __device__ __forceinline__ void finish_block(const FinishArgs& f, int ng, int vb
     if (!f.do_epi) return;
     // 2) epilogue (each element by the thread that reduced it; scalars by block 0)
     if (f.op == 0) {
-        if (grp == 0 && i < f.ld) f.g[i] = i < f.n ? (-f.c1 * f.mu[i] + f.red[i] / f.T) : 0.0;  // oracle.hpp:82-84
+        if (grp == 0 && i < f.ld) {
+            const double gi = i < f.n ? (-f.c1 * f.mu[i] + f.red[i] / f.T) : 0.0;  // oracle.hpp:82-84
+            f.g[i] = gi;
+            if (f.hout) f.hout[8 + i] = gi;
+        }
         if (vb == 0) {
             double sacc = 0.0;
             for (int j = tid; j < f.n; j += nthr) sacc += f.mu[j] * f.x[j];
@@ -98,16 +103,27 @@ __device__ __forceinline__ void finish_block(const FinishArgs& f, int ng, int vb
                 f.sc[2] = s2 / f.T;
                 f.sc[3] = s3 / f.T;
                 f.sc[4] = s4 / f.T;
+                if (f.hout)
+                    for (int q = 0; q < 5; ++q) f.hout[q] = f.sc[q];
             }
             __syncthreads();
         }
     } else if (f.op == 3) {
-        if (vb == 0 && tid < 9) f.out[tid] = f.red[tot + tid] / f.T;
+        if (vb == 0 && tid < 9) {
+            const double v = f.red[tot + tid] / f.T;
+            f.out[tid] = v;
+            if (f.hout) f.hout[tid] = v;
+        }
     } else if (grp == 0 && i < tot) {
         const int k = i / f.ld, c = i - k * f.ld;
         // HVP / THIRD: A^T(w)/T with the 1/T folded out of the per-row weights
-        if (c < f.n) f.out[(size_t)k * f.ldo + c] = f.op == 4 /* XTW */ ? f.red[i] : f.red[i] / f.T;
+        if (c < f.n) {
+            const double v = f.op == 4 /* XTW */ ? f.red[i] : f.red[i] / f.T;
+            f.out[(size_t)k * f.ldo + c] = v;
+            if (f.hout) f.hout[(size_t)k * f.ldo + c] = v;
+        }
     }
+    if (f.hout) __threadfence_system();
 }
 
 }  // namespace mvsk_b200

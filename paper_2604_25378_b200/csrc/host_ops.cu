@@ -74,10 +74,6 @@ void copy_in(mvsk_gpu_ctx* ctx, int k, size_t base) {
     MVSK_CUDA(cudaMemcpyAsync(ctx->vin + base * ld, ctx->h_in + base * ld, (size_t)k * ld * sizeof(double),
                               cudaMemcpyHostToDevice, ctx->stream));
 }
-void copy_out(mvsk_gpu_ctx* ctx, const double* dev, int k, long long stride_dev) {
-    MVSK_CUDA(cudaMemcpyAsync(ctx->h_out, dev, (size_t)k * stride_dev * sizeof(double), cudaMemcpyDeviceToHost,
-                              ctx->stream));
-}
 void finish_out(mvsk_gpu_ctx* ctx, const FaceMap& fm, int k, long long stride_dev, double* out) {
     MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int i = 0; i < k; ++i) from_full(ctx, fm, ctx->h_out + (size_t)i * stride_dev, out + (size_t)i * fm.m);
@@ -181,11 +177,11 @@ double op_make_cache(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const doubl
         io.vin = ctx->vin;
         io.slot = slot;
         io.x_for_mux = ctx->vin;
-        run_pass(ctx, Op::FGRAD, 1, io);
         // scalars and the gradient come back in the same round trip (the gradient
-        // is almost always requested next: oracle.hpp:79, solver.hpp:378-379)
-        MVSK_CUDA(cudaMemcpyAsync(h, s.sc, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        MVSK_CUDA(cudaMemcpyAsync(h + 8, s.g, ctx->ld * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        // is almost always requested next: oracle.hpp:79, solver.hpp:378-379),
+        // written to the mapped staging buffer by the pass epilogue
+        io.hout = ctx->h_out_dev;
+        run_pass(ctx, Op::FGRAD, 1, io);
     });
     ctx->fwd += 1;  // oracle.hpp:127
     MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -252,8 +248,8 @@ void op_hvp(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* V, int
         io.z = ctx->slots[slot].z;
         io.out = ctx->outd;
         io.ldo = ctx->ld;
+        io.hout = ctx->h_out_dev;
         run_pass(ctx, Op::HVP, k, io);
-        copy_out(ctx, ctx->outd, k, ctx->ld);
     });
     ctx->fwd += k;  // oracle.hpp:134
     ctx->tr += k;   // oracle.hpp:138
@@ -276,8 +272,8 @@ void op_third(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* U, c
         io.z = ctx->slots[slot].z;
         io.out = ctx->outd;
         io.ldo = ctx->ld;
+        io.hout = ctx->h_out_dev;
         run_pass(ctx, Op::THIRD, k, io);
-        copy_out(ctx, ctx->outd, k, ctx->ld);
     });
     ctx->fwd += 2 * k;
     ctx->tr += k;
@@ -326,8 +322,8 @@ void op_line_model(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double*
         io.vin = ctx->vin;
         io.z = ctx->slots[slot].z;
         io.out = ctx->outd;
+        io.hout = ctx->h_out_dev;
         run_pass(ctx, Op::LINESUMS, 1, io);
-        copy_out(ctx, ctx->outd, 1, 9);
     });
     ctx->fwd += 1;
     MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -397,8 +393,8 @@ void op_third_trace_rows(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const d
         io.tw = ctx->tvec;
         io.out = ctx->outd;
         io.ldo = ctx->ld;
+        io.hout = ctx->h_out_dev;
         run_pass(ctx, Op::XTW, 1, io);
-        copy_out(ctx, ctx->outd, 1, ctx->ld);
     });
     finish_out(ctx, fm, 1, ctx->ld, out);
 }

@@ -9,6 +9,7 @@
 #include "oracle_ops.cuh"
 #include "stream_cluster.cuh"
 #include "stream_dmma.cuh"
+#include "small_pass.cuh"
 
 namespace mvsk_b200 {
 
@@ -756,9 +757,12 @@ void ensure_host_staging(mvsk_gpu_ctx* ctx, size_t elems) {
     if (ctx->h_elems >= elems) return;
     if (ctx->h_in) cudaFreeHost(ctx->h_in);
     if (ctx->h_out) cudaFreeHost(ctx->h_out);
-    ctx->h_in = ctx->h_out = nullptr;
+    ctx->h_in = ctx->h_out = ctx->h_out_dev = nullptr;
     MVSK_CUDA(cudaMallocHost(&ctx->h_in, elems * sizeof(double)));
-    MVSK_CUDA(cudaMallocHost(&ctx->h_out, elems * sizeof(double)));
+    // results come back through the mapped alias (PassIO::hout): the epilogue
+    // writes them over the bus, no device-to-host copy node per op
+    MVSK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_out), elems * sizeof(double), cudaHostAllocMapped));
+    MVSK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->h_out_dev), ctx->h_out, 0));
     ctx->h_elems = elems;
     ++ctx->epoch;
 }
@@ -778,6 +782,7 @@ void run_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
             sub.vin = io.vin + (size_t)done * ctx->ld;
             if (io.vin2) sub.vin2 = io.vin2 + (size_t)done * ctx->ld;
             sub.out = io.out + (size_t)done * io.ldo;
+            if (io.hout) sub.hout = io.hout + (size_t)done * io.ldo;
             int kk = 0;
             // narrow panels (compact faces, ld <= 256): the k-RHS pass as one
             // cooperative streaming kernel (fused reduction) beats the cluster
@@ -832,6 +837,7 @@ static FinishArgs finish_args(mvsk_gpu_ctx* ctx, Op op, int nacc, int nb, const 
     f.value_offset_dev = ctx->value_offset_dev;
     f.skip = io.skip;
     f.nskip = io.nskip;
+    f.hout = io.hout;
     if (slot) {
         f.g = slot->g;
         f.sc = slot->sc;
@@ -979,7 +985,65 @@ static bool run_dmma(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     return true;
 }
 
+template <Op OP>
+static const void* small_pass_fn(int ld) {
+    if (ld <= 32) return reinterpret_cast<const void*>(&small_pass_kernel<OP, 2, 16>);
+    if (ld <= 64) return reinterpret_cast<const void*>(&small_pass_kernel<OP, 4, 16>);
+    return reinterpret_cast<const void*>(&small_pass_kernel<OP, 8, 16>);
+}
+
+// the one-cluster pass (small_pass.cuh) when the whole local panel fits the
+// cluster's shared memory: single rank, one right-hand side, ld <= 128
+static bool run_small_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io, Slot* slot) {
+    static const bool off = std::getenv("MVSK_NO_SMALL_PASS") != nullptr;
+    if (off || k != 1 || ctx->ld > kSpM || ctx->T_local < kSpCS) return false;
+    const long long nloc = (ctx->T_local + kSpCS - 1) / kSpCS;
+    const size_t smem = small_pass_smem(nloc, (int)ctx->ld);
+    if (smem > ctx->max_smem) return false;
+    const void* fn = nullptr;
+    switch (op) {
+    case Op::FGRAD: fn = small_pass_fn<Op::FGRAD>((int)ctx->ld); break;
+    case Op::HVP: fn = small_pass_fn<Op::HVP>((int)ctx->ld); break;
+    case Op::THIRD: fn = small_pass_fn<Op::THIRD>((int)ctx->ld); break;
+    case Op::LINESUMS: fn = small_pass_fn<Op::LINESUMS>((int)ctx->ld); break;
+    case Op::XTW: fn = small_pass_fn<Op::XTW>((int)ctx->ld); break;
+    }
+    if (!fn || !cluster_fits(fn, kSpCS, kSpW * 32, smem)) return false;
+    set_smem_attr(fn, smem);
+    SmallPassArgs a{};
+    a.X = ctx->X;
+    a.T = ctx->T_local;
+    a.ld = (int)ctx->ld;
+    a.vin = io.vin;
+    a.vin2 = io.vin2;
+    a.rowv = op == Op::FGRAD ? ctx->zoff_dev : (op == Op::XTW ? io.tw : io.z);
+    a.zout = op == Op::FGRAD ? slot->z : io.zout;
+    a.fin = finish_args(ctx, op, op == Op::LINESUMS ? 0 : 1, 1, io, slot);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kSpCS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(kSpCS);
+    cfg.blockDim = dim3(kSpW * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[] = {&a};
+    const bool sharded = is_sharded(ctx);
+    a.fin.do_reduce = 0;
+    a.fin.do_epi = sharded ? 0 : 1;
+    MVSK_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+    ++ctx->launches;
+    ctx->phys += 1;
+    if (sharded) finish_pass(ctx, op, op == Op::LINESUMS ? 0 : 1, 1, io, slot, true);
+    return true;
+}
+
 static void run_single(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
+    if (run_small_pass(ctx, op, k, io, op == Op::FGRAD ? &ctx->slots[io.slot] : nullptr)) return;
     Plan pl;
     if (!make_plan(ctx, op, k, pl))
         throw ApiError(MVSK_DIMENSION_ERROR, "no streaming-kernel plan for n=" + std::to_string(ctx->n) +

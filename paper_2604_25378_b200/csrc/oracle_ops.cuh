@@ -25,6 +25,11 @@ struct PassIO {
     int nskip = 0;
     int slot = -1;        // FGRAD target slot
     const double* x_for_mux = nullptr;  // FGRAD: x (ld) for mu'x
+    // optional mapped pinned host buffer (device alias) the epilogue also writes
+    // its results to, so a host-API op needs no device-to-host copy node:
+    // FGRAD [0, 5) scalars and [8, 8 + ld) the gradient; LINESUMS [0, 9) the
+    // power sums; HVP / THIRD / XTW the outputs at stride ldo
+    double* hout = nullptr;
 };
 
 void run_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io);
