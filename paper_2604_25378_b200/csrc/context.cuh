@@ -110,7 +110,8 @@ struct mvsk_gpu_ctx {
     double* h_out = nullptr;
     double* h_out_dev = nullptr;  // device alias of h_out (mapped)
     size_t h_elems = 0;
-    double* h_mat = nullptr;  // pinned n x n staging (direct branch: Gram out, P in)
+    double* h_mat = nullptr;  // pinned n x n staging (direct branch: Gram out, P in), mapped
+    double* h_mat_dev = nullptr;  // device alias of h_mat
     size_t h_mat_elems = 0;
 
     ncclComm_t comm = nullptr;

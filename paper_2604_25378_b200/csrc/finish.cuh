@@ -123,7 +123,6 @@ __device__ __forceinline__ void finish_block(const FinishArgs& f, int ng, int vb
             if (f.hout) f.hout[(size_t)k * f.ldo + c] = v;
         }
     }
-    if (f.hout) __threadfence_system();
 }
 
 }  // namespace mvsk_b200

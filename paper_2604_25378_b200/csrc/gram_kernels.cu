@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(WM * WN * 32, 1) syrk_dmma_kernel(const GramAr
 // packed rows (i, j <= i) at i (i + 1) / 2 + j: the allreduce then moves
 // n (n + 1) / 2 values instead of n^2, and gram_unpack_kernel mirrors after it.
 __global__ void gram_finish_kernel(const double* part, int npairs, int nsplit, int n, double scale, double* G,
-                                   long long ldg, double* packed) {
+                                   long long ldg, double* packed, double* Gh) {
     const int p = blockIdx.x;
     int ti, tj;
     pair_of(p, ti, tj);
@@ -207,15 +207,21 @@ __global__ void gram_finish_kernel(const double* part, int npairs, int nsplit, i
     }
     G[(long long)i * ldg + j] = v;
     G[(long long)j * ldg + i] = v;
+    if (Gh) {  // mapped host mirror (host-API readback without a copy node)
+        Gh[(long long)i * ldg + j] = v;
+        Gh[(long long)j * ldg + i] = v;
+    }
 }
 
 // dense symmetric G from the allreduced packed lower triangle
-__global__ void gram_unpack_kernel(const double* __restrict__ packed, int n, double* __restrict__ G) {
+__global__ void gram_unpack_kernel(const double* __restrict__ packed, int n, double* __restrict__ G, double* Gh) {
     const long long tot = (long long)n * n;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(e / n), j = (int)(e - (long long)i * n);
         const int hi = i > j ? i : j, lo = i > j ? j : i;
-        G[e] = packed[(long long)hi * (hi + 1) / 2 + lo];
+        const double v = packed[(long long)hi * (hi + 1) / 2 + lo];
+        G[e] = v;
+        if (Gh) Gh[e] = v;
     }
 }
 
@@ -295,7 +301,8 @@ __global__ void third_weights_kernel(const double* z, const double* q, double* t
 
 }  // namespace
 
-void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, double scale, const double* z) {
+void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, double scale, const double* z,
+                       double* G_host) {
     const int n = (int)ctx->n;
     const int ntile = (n + GBM - 1) / GBM;
     const int npairs = ntile * (ntile + 1) / 2;
@@ -381,14 +388,15 @@ void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, d
     MVSK_CUDA(cudaLaunchKernel(fn, dim3(npairs, nsplit), dim3(nthr), args, smem, ctx->stream));
     ++ctx->launches;
     gram_finish_kernel<<<dim3(npairs, GBM * GBM / 256), 256, 0, ctx->stream>>>(ctx->gram_part, npairs, nsplit, n, scale,
-                                                                                G_dev, n, packed);
+                                                                                G_dev, n, packed,
+                                                                                packed ? nullptr : G_host);
     MVSK_CUDA(cudaGetLastError());
     ctx->phys += 1;
     if (packed) {
         allreduce_sum(ctx, packed, npk);
         ++ctx->launches;
         const int nb = (int)std::min<long long>(4LL * ctx->nsm, ((long long)n * n + 255) / 256);
-        gram_unpack_kernel<<<nb, 256, 0, ctx->stream>>>(packed, n, G_dev);
+        gram_unpack_kernel<<<nb, 256, 0, ctx->stream>>>(packed, n, G_dev, G_host);
         MVSK_CUDA(cudaGetLastError());
     }
 }

@@ -344,9 +344,10 @@ void op_line_model(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double*
 static void ensure_h_mat(mvsk_gpu_ctx* ctx, size_t elems) {
     if (ctx->h_mat_elems >= elems) return;
     if (ctx->h_mat) MVSK_CUDA(cudaFreeHost(ctx->h_mat));
-    ctx->h_mat = nullptr;
+    ctx->h_mat = ctx->h_mat_dev = nullptr;
     ctx->h_mat_elems = 0;
-    MVSK_CUDA(cudaMallocHost(&ctx->h_mat, elems * sizeof(double)));
+    MVSK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_mat), elems * sizeof(double), cudaHostAllocMapped));
+    MVSK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->h_mat_dev), ctx->h_mat, 0));
     ctx->h_mat_elems = elems;
     ++ctx->epoch;
 }
@@ -358,9 +359,8 @@ void op_weighted_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, double* G)
     ensure_h_mat(ctx, (size_t)ctx->ld * ctx->ld);
     const double* full = ctx->h_mat;
     run_graphed(ctx, kGraphGram, 1, slot, [&] {
-        run_weighted_gram(ctx, nullptr, ctx->gram, 1.0 / (double)ctx->T_global, ctx->slots[slot].z);
-        MVSK_CUDA(cudaMemcpyAsync(ctx->h_mat, ctx->gram, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToHost,
-                                  ctx->stream));
+        // the Gram comes back through the mapped staging buffer (no copy node)
+        run_weighted_gram(ctx, nullptr, ctx->gram, 1.0 / (double)ctx->T_global, ctx->slots[slot].z, ctx->h_mat_dev);
     });
     MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
     const long long m = fm.m;

@@ -1019,6 +1019,21 @@ static bool run_small_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io, Sl
     a.rowv = op == Op::FGRAD ? ctx->zoff_dev : (op == Op::XTW ? io.tw : io.z);
     a.zout = op == Op::FGRAD ? slot->z : io.zout;
     a.fin = finish_args(ctx, op, op == Op::LINESUMS ? 0 : 1, 1, io, slot);
+    static unsigned long long* prof = nullptr;  // MVSK_SMALL_PROF: phase cycle sums, printed at exit
+    if (std::getenv("MVSK_SMALL_PROF")) {
+        if (!prof) {
+            MVSK_CUDA(cudaMallocManaged(&prof, 8 * sizeof(unsigned long long)));
+            std::memset(prof, 0, 8 * sizeof(unsigned long long));
+            std::atexit([] {
+                cudaDeviceSynchronize();
+                const double nn = prof[5] ? (double)prof[5] : 1.0;
+                std::fprintf(stderr, "[small pass] %llu launches, cycles/launch on CTA 0: load %.0f rows %.0f "
+                             "combine %.0f epilogue %.0f exit-sync %.0f\n", prof[5], prof[0] / nn, prof[1] / nn,
+                             prof[2] / nn, prof[3] / nn, prof[4] / nn);
+            });
+        }
+        a.prof = prof;
+    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

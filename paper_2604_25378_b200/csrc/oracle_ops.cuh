@@ -40,7 +40,9 @@ void run_psi2(mvsk_gpu_ctx* ctx, const double* z, double* out, long long T);
 // Weighted Gram G = X^T diag(w) X / T over the full panel (n x n, row-major,
 // symmetric, both triangles written); allreduced across the shard group.
 // G = X^T diag(w) X * scale; with z set, w = psi''(z) computed in the kernel (w_rows unused)
-void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, double scale, const double* z = nullptr);
+// G_host: optional mapped host mirror (device alias) written alongside G_dev
+void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, double scale, const double* z = nullptr,
+                       double* G_host = nullptr);
 
 // q_t = x_t^T P x_t (P: ld x ld, zero outside the face) for this rank's rows
 // with z and tw set: writes the third weights psi3(z) q / T to tw instead of q

@@ -44,6 +44,7 @@ struct SmallPassArgs {
     const double* rowv;  // FGRAD z offset (or null), HVP / THIRD / LINESUMS z, XTW weights
     double* zout;        // FGRAD z, LINESUMS A d (optional)
     FinishArgs fin;      // epilogue targets and constants (k = 1)
+    unsigned long long* prof;  // MVSK_SMALL_PROF: CTA 0 phase cycle sums [load, rows, combine, epilogue, n]
 };
 
 __host__ __device__ constexpr size_t small_pass_smem(long long nloc, int ld) {
@@ -60,6 +61,15 @@ __global__ void __launch_bounds__(kSpW * 32, 1) small_pass_kernel(const SmallPas
     constexpr int M = kSpM, MP = kSpMP, CS = kSpCS, GPW = 32 / LPR, NGC = kSpW * GPW;
     const FinishArgs& f = a.fin;
     if (pass_skipped(f.skip, f.nskip)) return;  // uniform over the cluster
+    const bool prof = a.prof && threadIdx.x == 0 && blockIdx.x == 0;
+    unsigned long long tp = prof ? clock64() : 0;
+    auto mark = [&](int i) {
+        if (prof) {
+            const unsigned long long now = clock64();
+            atomicAdd(a.prof + i, now - tp);
+            tp = now;
+        }
+    };
     cgs::cluster_group cluster = cgs::this_cluster();
     const int crank = (int)cluster.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -115,6 +125,7 @@ __global__ void __launch_bounds__(kSpW * 32, 1) small_pass_kernel(const SmallPas
     const double c2 = f.c2, c3 = f.c3, c4 = f.c4;
     if (nloc > 0) mbar_wait(&bar, 0u);
     __syncthreads();  // sZ
+    mark(0);
 
     for (int lb = warp * GPW; lb < nloc; lb += NGC) {  // warp-uniform trip count
         const int tl = lb + lane / LPR;
@@ -216,6 +227,7 @@ __global__ void __launch_bounds__(kSpW * 32, 1) small_pass_kernel(const SmallPas
             for (int i = 0; i < NS; ++i) sW[warp * MP + M + i] = s[i];
     }
     __syncthreads();
+    mark(1);
     for (int el = tid; el < MP; el += blockDim.x) {  // warps in a fixed order
         if ((el >= ld && el < M) || (el >= M + NS) || (!ACC && el < M)) continue;
         double v = 0.0;
@@ -224,6 +236,7 @@ __global__ void __launch_bounds__(kSpW * 32, 1) small_pass_kernel(const SmallPas
         buf[el] = v;
     }
     cluster.sync();
+    mark(2);
     // ---- columns: CTA c finishes the slice [c * chunk, (c + 1) * chunk)
     if constexpr (ACC) {
         const int chunk = (ld + CS - 1) / CS;
@@ -299,8 +312,12 @@ __global__ void __launch_bounds__(kSpW * 32, 1) small_pass_kernel(const SmallPas
             }
         }
     }
-    if (f.hout) __threadfence_system();
+    // (no system fence for hout: kernel completion orders the mapped writes
+    // before the stream synchronisation the host waits on)
+    mark(3);
     cluster.sync();  // no CTA leaves while its partial may still be read
+    mark(4);
+    if (prof) atomicAdd(a.prof + 5, 1ull);
 }
 
 }  // namespace mvsk_b200
