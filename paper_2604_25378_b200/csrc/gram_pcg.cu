@@ -275,12 +275,24 @@ __host__ __device__ inline size_t gp_w_doubles(int m) {
     const int mm = m - 2;
     return std::max(std::max((size_t)m * m, (size_t)mm * m_stride(mm)), (size_t)kGpMaxCols * mm * 6);
 }
-__host__ __device__ inline size_t gp_region_doubles(int m, int stage_rows) {
-    const int mp = (m + 3) & ~3;
-    return std::max(gp_s_doubles(m) + gp_w_doubles(m), (size_t)stage_rows * mp);
+// staged row stride: the face width padded to whole 8-column DMMA tiles, then
+// to 4 (mod 16) doubles, so the 16 lanes of a half-warp fragment load (4 rows
+// x 4 columns) hit distinct banks
+// Narrow panels (ld <= 128: the compact face contexts) stage whole rows by
+// bulk copy, with a zero column at ld for the tile padding, and the face
+// columns are picked in the fragment loads; wide panels gather the face
+// columns into the staging rows
+__host__ __device__ inline bool gp_bulk_rows(int ld) { return ld <= 128 && ld % 2 == 0; }
+__host__ __device__ inline int gp_stage_stride(int m, int ld) {
+    const int w = gp_bulk_rows(ld) ? (m > ld + 1 ? m : ld + 1) : m;
+    const int mp8 = (w + 7) & ~7;
+    return mp8 + (mp8 % 16 == 0 ? 4 : 12);
 }
-__host__ __device__ inline size_t gp_setup_smem_doubles(int m, int stage_rows) {
-    return gp_region_doubles(m, stage_rows) + (size_t)stage_rows + 6 * (size_t)m + 64;
+__host__ __device__ inline size_t gp_region_doubles(int m, int ld, int stage_rows) {
+    return std::max(gp_s_doubles(m) + gp_w_doubles(m), (size_t)stage_rows * gp_stage_stride(m, ld));
+}
+__host__ __device__ inline size_t gp_setup_smem_doubles(int m, int ld, int stage_rows) {
+    return gp_region_doubles(m, ld, stage_rows) + (size_t)stage_rows + 6 * (size_t)m + 64;
 }
 
 // Everything of the direction that precedes the third-action pass, on one CTA,
@@ -584,6 +596,11 @@ __device__ void direct_phases(const SetupArgs& a, const GpParams& P, double* S, 
     if (tid == 0) a.res[4] = (s_sing & 2) ? 1.0 : 0.0;
 }
 
+__device__ __forceinline__ void gp_dmma(double (&d)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+        : "+d"(d[0]), "+d"(d[1])
+        : "d"(a), "d"(b));
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
                  : "memory");
@@ -611,85 +628,138 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_cluster_kernel(const G
     double* S = sm;
     double* W = S + gp_s_doubles(m);
     double* xs = sm;  // the staging area overlays S | W
-    double* ws = sm + gp_region_doubles(m, SR);
+    double* ws = sm + gp_region_doubles(m, g.ld, SR);
     double* tail = ws + SR;
     const double* par = a.par;
     int* cols = reinterpret_cast<int*>(tail);
     for (int j = tid; j < mp; j += blockDim.x) cols[j] = j < m ? (P.face_active ? (int)par[L.idx + j] : j) : -1;
-    const int nbk = mp / 4;
-    const int nblk = nbk * (nbk + 1) / 2;
-    // RS adjacent lanes share a block, each summing the rows t = part (mod RS);
-    // their partials are combined by a fixed butterfly after the row loop
-    int RS = 1;
-    while (RS < 32 && nblk * RS * 2 <= (int)blockDim.x) RS <<= 1;
-    const int blk = tid / RS, part = tid - (tid / RS) * RS;
-    int bi = -1, bj = -1;
-    if (blk < nblk) {  // lower block triangle, row-major over block rows
-        int r = 0, e = blk;
-        while (e > r) {
-            e -= r + 1;
-            ++r;
-        }
-        bi = r;
-        bj = e;
+    // ---- face Gram on the tensor pipe: 8 x 8 lower-triangle tiles of
+    // sum_t (psi''(z_t) x_t,I)(x_t,J) as mma.m8n8k4 f64 over 4-row k-steps; warp
+    // w owns tiles w, w + nwarps, ... over all of this CTA's rows, so no
+    // cross-warp reduction (fragment layout: A row-major lane -> (l/4, l%4),
+    // B col-major lane -> (l%4, l/4), C lane -> (l/4, 2 (l%4) + {0, 1}))
+    const int ms = gp_stage_stride(m, g.ld);
+    const int nt = (m + 7) / 8, ntiles = nt * (nt + 1) / 2;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = (int)blockDim.x >> 5;
+    const int tpw = (ntiles + nwarps - 1) / nwarps;  // tiles per warp (<= 8: kGpMaxM = 112, 16 warps)
+    static_assert((kGpMaxM / 8) * (kGpMaxM / 8 + 1) / 2 <= 8 * (kGpThreads / 32), "tiles per warp");
+    const bool bulk = gp_bulk_rows(g.ld);
+    __shared__ uint64_t sbar;
+    if (tid == 0) {
+        mbar_init(&sbar, 1);
+        fence_mbar_init();
     }
-    double acc[4][4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int l = 0; l < 4; ++l) acc[k][l] = 0.0;
     __syncthreads();
     const long long r0 = g.T * rank / CS, r1 = g.T * (rank + 1) / CS;
-    for (long long c0 = r0; c0 < r1; c0 += SR) {
-        const int rows = (int)min((long long)SR, r1 - c0);
-        for (int e = tid; e < rows * mp; e += blockDim.x) {
-            const int t = e / mp, j = e - t * mp;
-            if (cols[j] >= 0)
-                cp_async8(xs + e, g.X + (c0 + t) * g.ld + cols[j]);
-            else
-                xs[e] = 0.0;
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        for (int t = tid; t < rows; t += blockDim.x) {
-            const double zt = g.z[c0 + t];
-            ws[t] = 2.0 * g.c2 - 6.0 * g.c3 * zt + 12.0 * g.c4 * (zt * zt);  // oracle.hpp:116-119
-        }
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();
-        if (bi >= 0) {
-#pragma unroll 4
-            for (int t = part; t < rows; t += RS) {
-                const double* xr = xs + (size_t)t * mp;
-                const double wt = ws[t];
-                double av[4], bv[4];
+    long long tq = clock64(), tstage = 0, twait = 0, tmma = 0, tpre = tq - tg0;
+    // the DMMA accumulate chain is long-latency (~440 cycles per dependent
+    // step measured on C4), so every warp keeps ~8 independent chains: TW
+    // tiles x U interleaved k-step accumulators, summed in a fixed order
+    auto run = [&](auto tw_c, auto u_c) {
+        constexpr int TW = decltype(tw_c)::value, U = decltype(u_c)::value;
+        double acc[TW][U][2];
+        int tI[TW], tJ[TW], cI[TW], cJ[TW];  // tiles; this lane's staged column of each
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    av[k] = xr[4 * bi + k] * wt;
-                    bv[k] = xr[4 * bj + k];
+        for (int q = 0; q < TW; ++q) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[q][u][0] = acc[q][u][1] = 0.0;
+            const int tl = warp + q * nwarps;
+            int r = 0, e = tl;
+            while (e > r) {  // lower tile triangle, row-major
+                e -= r + 1;
+                ++r;
+            }
+            tI[q] = tl < ntiles ? r : -1;
+            tJ[q] = e;
+            // bulk rows: the face column of fragment column l/4 (the zero column
+            // ld past the face); gathered rows: the staged position itself
+            const int fi = 8 * r + (lane >> 2), fj = 8 * e + (lane >> 2);
+            cI[q] = !bulk ? fi : (fi < m ? cols[fi] : g.ld);
+            cJ[q] = !bulk ? fj : (fj < m ? cols[fj] : g.ld);
+        }
+        uint32_t phase = 0;
+        for (long long c0 = r0; c0 < r1; c0 += SR) {
+            const int rows = (int)min((long long)SR, r1 - c0);
+            const int rows4 = (rows + 3) & ~3;
+            if (bulk) {
+                if (tid == 0) mbar_arrive_expect_tx(&sbar, (uint32_t)((size_t)rows * g.ld * sizeof(double)));
+                __syncthreads();
+                for (int t = tid; t < rows; t += blockDim.x)
+                    bulk_g2s(xs + (size_t)t * ms, g.X + (c0 + t) * g.ld, (uint32_t)(g.ld * sizeof(double)), &sbar,
+                             policy_evict_last());
+                for (int t = warp; t < rows4; t += nwarps)  // pad columns, pad rows
+                    for (int j = (t < rows ? g.ld : 0) + lane; j < ms; j += 32) xs[(size_t)t * ms + j] = 0.0;
+            } else {  // a warp per row, a lane per column: no index arithmetic per element
+                for (int t = warp; t < rows4; t += nwarps) {
+                    const double* src = g.X + (c0 + t) * g.ld;
+                    for (int j = lane; j < ms; j += 32) {
+                        if (t < rows && j < m)
+                            cp_async8(xs + (size_t)t * ms + j, src + cols[j]);
+                        else
+                            xs[(size_t)t * ms + j] = 0.0;
+                    }
                 }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+            for (int t = tid; t < rows4; t += blockDim.x) {
+                const double zt = t < rows ? g.z[c0 + t] : 0.0;
+                ws[t] = t < rows ? 2.0 * g.c2 - 6.0 * g.c3 * zt + 12.0 * g.c4 * (zt * zt) : 0.0;  // oracle.hpp:116-119
+            }
+            tstage += clock64() - tq;
+            tq = clock64();
+            if (bulk) {
+                mbar_wait(&sbar, phase);
+                phase ^= 1u;
+            } else {
+                asm volatile("cp.async.wait_all;" ::: "memory");
+            }
+            __syncthreads();
+            twait += clock64() - tq;
+            tq = clock64();
+            const int kr = lane & 3;
+            for (int t0 = 0; t0 < rows4; t0 += 4 * U) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
+                for (int u = 0; u < U; ++u) {
+                    const int tk = t0 + 4 * u;
+                    if (tk >= rows4) break;
+                    const double* xr = xs + (size_t)(tk + kr) * ms;
+                    const double wt = ws[tk + kr];
 #pragma unroll
-                    for (int l = 0; l < 4; ++l) acc[k][l] = fma(av[k], bv[l], acc[k][l]);
+                    for (int q = 0; q < TW; ++q) {
+                        if (tI[q] < 0) continue;
+                        const double b = xr[cJ[q]];
+                        const double a = (tI[q] == tJ[q] ? b : xr[cI[q]]) * wt;
+                        gp_dmma(acc[q][u], a, b);
+                    }
+                }
+            }
+            __syncthreads();
+            tmma += clock64() - tq;
+            tq = clock64();
+        }
+        // partial -> W (m x m, lower triangle of the face)
+#pragma unroll
+        for (int q = 0; q < TW; ++q) {
+            if (tI[q] < 0) continue;
+            const int i = 8 * tI[q] + (lane >> 2);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                double v = acc[q][0][h];
+#pragma unroll
+                for (int u = 1; u < U; ++u) v += acc[q][u][h];
+                const int j = 8 * tJ[q] + 2 * (lane & 3) + h;
+                if (i < m && j <= i) W[(size_t)i * m + j] = v;
             }
         }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int l = 0; l < 4; ++l)
-            for (int o = 1; o < RS; o <<= 1) acc[k][l] += __shfl_xor_sync(0xffffffffu, acc[k][l], o);
-    // partial -> W (m x m, lower triangle of the face)
-    if (bi >= 0 && part == 0) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const int i = 4 * bi + k, j = 4 * bj + l;
-                if (i < m && j < m && j <= i) W[(size_t)i * m + j] = acc[k][l];
-            }
-    }
+    };
+    if (tpw <= 1)
+        run(std::integral_constant<int, 1>{}, std::integral_constant<int, 8>{});
+    else if (tpw <= 2)
+        run(std::integral_constant<int, 2>{}, std::integral_constant<int, 4>{});
+    else if (tpw <= 4)
+        run(std::integral_constant<int, 4>{}, std::integral_constant<int, 2>{});
+    else
+        run(std::integral_constant<int, 8>{}, std::integral_constant<int, 1>{});  // kGpMaxM = 112: <= 7 tiles
     const long long tg1 = clock64();
     cluster.sync();
     // ---- each CTA sums a slice of the entries over the cluster (rank order)
@@ -720,6 +790,10 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_cluster_kernel(const G
     if (tid == 0) {
         a.res[48] = (double)(tg1 - tg0);
         a.res[49] = (double)(clock64() - tg1);
+        a.res[58] = (double)tpre;
+        a.res[59] = (double)tstage;
+        a.res[60] = (double)twait;
+        a.res[61] = (double)tmma;
     }
     if constexpr (MODE == 0) {
         for (int e = tid; e < m * m; e += blockDim.x) g.Gout[e] = S[e];
@@ -738,7 +812,7 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_setup_kernel(const dou
     const int m = P.m;
     double* S = sm;
     double* W = S + gp_s_doubles(m);
-    double* tail = sm + gp_region_doubles(m, stage_rows) + stage_rows;
+    double* tail = sm + gp_region_doubles(m, a.ld, stage_rows) + stage_rows;
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) S[e] = Gf[e];
     __syncthreads();
     setup_phases(a, P, S, W, tail);
@@ -903,12 +977,12 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
     const int mm = m - 2;
     // rows staged per chunk: as many as fit beside the setup's vectors, at most
     // one 8-CTA share of this rank's rows
-    const int mp = (m + 3) & ~3;
+    const int mp = gp_stage_stride(m, (int)ctx->ld);
     const long long avail = (long long)(ctx->max_smem / sizeof(double)) - (6LL * m + 64) - 64;
     long long SR = std::min<long long>(avail / (mp + 1), (ctx->T_local + 7) / 8);
-    SR = std::max<long long>(SR, 1);
+    SR = std::max<long long>(SR & ~3LL, 4);  // whole 4-row DMMA k-steps
     const int stage_rows = (int)SR;
-    const size_t setup_smem = gp_setup_smem_doubles(m, stage_rows) * sizeof(double);
+    const size_t setup_smem = gp_setup_smem_doubles(m, (int)ctx->ld, stage_rows) * sizeof(double);
     if (setup_smem > ctx->max_smem || main_smem_bytes(m) > ctx->max_smem) return false;
     if (!ctx->gpcg) ctx->gpcg = new GramPcgWs();
     GramPcgWs& ws = *ctx->gpcg;
@@ -1039,9 +1113,10 @@ bool pcg_direction_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const Pc
     static const bool prof = std::getenv("MVSK_GPCG_PROF") != nullptr;
     if (prof)
         std::fprintf(stderr,
-                     "[gpcg] m=%d np=%d cycles: gram %.0f reduce %.0f | setup h %.0f M %.0f jacobi %.0f probes %.0f "
-                     "| main a %.0f cg %.0f | iters %d\n",
-                     m, np, r[48], r[49], r[52], r[53] - r[52], r[54] - r[53], r[55] - r[54], r[56], r[57], iters);
+                     "[gpcg] m=%d np=%d face_gather %d ld %lld T %lld cycles: gram %.0f reduce %.0f | setup h %.0f M %.0f "
+                     "jacobi %.0f probes %.0f | main a %.0f cg %.0f | iters %d | gram: pre %.0f issue %.0f wait %.0f "
+                     "mma %.0f\n",
+                     m, np, fm.active ? 1 : 0, (long long)ctx->ld, (long long)ctx->T_local, r[48], r[49], r[52], r[53] - r[52], r[54] - r[53], r[55] - r[54], r[56], r[57], iters, r[58], r[59], r[60], r[61]);
     // reference contract (common.hpp:27-37): 2 passes per Hop, 3 per third action
     ctx->fwd += (uint64_t)(hvps + 2LL * np);
     ctx->tr += (uint64_t)(hvps + np);
@@ -1059,12 +1134,12 @@ bool direct_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, con
     static const bool on = std::getenv("MVSK_DEVICE_DIRECT") != nullptr;
     if (!on) return false;
     const int mm = m - 2;
-    const int mp = (m + 3) & ~3;
+    const int mp = gp_stage_stride(m, (int)ctx->ld);
     const long long avail = (long long)(ctx->max_smem / sizeof(double)) - (6LL * m + 64) - 64;
     long long SR = std::min<long long>(avail / (mp + 1), (ctx->T_local + 7) / 8);
-    SR = std::max<long long>(SR, 1);
+    SR = std::max<long long>(SR & ~3LL, 4);  // whole 4-row DMMA k-steps
     const int stage_rows = (int)SR;
-    const size_t setup_smem = gp_setup_smem_doubles(m, stage_rows) * sizeof(double);
+    const size_t setup_smem = gp_setup_smem_doubles(m, (int)ctx->ld, stage_rows) * sizeof(double);
     if (setup_smem > ctx->max_smem) return false;
     const void* cfn = reinterpret_cast<const void*>(&gram_pcg_cluster_kernel<2>);
     int CS = 0;

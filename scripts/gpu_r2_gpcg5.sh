@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+MVSK_GPCG_PROF=1 python scripts/one_solve_prof.py C4 2>&1 | grep -E "gpcg|^ok" | tail -3
+MVSK_GPCG_PROF=1 python scripts/one_solve_prof.py C3 20 2>&1 | grep -E "gpcg|^ok" | tail -3
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -rf > gpurun_out/r2q_pytest.log 2>&1; echo "pytest rc $?"; tail -4 gpurun_out/r2q_pytest.log
