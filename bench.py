@@ -220,6 +220,8 @@ def solve_leg():
             t0 = time.perf_counter()
             xc, rc = po.solve(A, mu, c, cc)
             row.update(cpu_s=time.perf_counter() - t0, cpu_status=int(rc.status), df=abs(rc.f_star - rep.f_star),
+                       dx_inf=float(np.max(np.abs(x - xc))),
+                       same_active=bool(np.array_equal(x <= cfg.tau + 1e-12, xc <= cc.tau + 1e-12)),
                        cpu_iterations=rc.iterations)
             # iteration counts are rounding-chaotic on both sides (the CPU oracle
             # with 2 threads moves them as much: scripts/iter_survey.py), so the

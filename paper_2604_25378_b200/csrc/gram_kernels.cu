@@ -303,6 +303,25 @@ __global__ void third_weights_kernel(const double* z, const double* q, double* t
 
 void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, double scale, const double* z,
                        double* G_host) {
+    if (!w_rows && z && !is_sharded(ctx) && run_small_gram(ctx, z, G_dev, scale, G_host)) return;
+    if (!w_rows && z && is_sharded(ctx)) {  // the same one-cluster Gram, packed for the allreduce
+        const size_t npk = (size_t)ctx->n * (ctx->n + 1) / 2;
+        if (ctx->gram_part_elems < npk) {
+            if (ctx->gram_part) MVSK_CUDA(cudaFree(ctx->gram_part));
+            ctx->gram_part = nullptr;
+            MVSK_CUDA(cudaMalloc(&ctx->gram_part, npk * sizeof(double)));
+            ctx->gram_part_elems = npk;
+            ++ctx->epoch;
+        }
+        if (run_small_gram(ctx, z, G_dev, scale, G_host, ctx->gram_part)) {
+            allreduce_sum(ctx, ctx->gram_part, npk);
+            ++ctx->launches;
+            const int nb = (int)std::min<long long>(4LL * ctx->nsm, ((long long)ctx->n * ctx->n + 255) / 256);
+            gram_unpack_kernel<<<nb, 256, 0, ctx->stream>>>(ctx->gram_part, (int)ctx->n, G_dev, G_host);
+            MVSK_CUDA(cudaGetLastError());
+            return;
+        }
+    }
     const int n = (int)ctx->n;
     const int ntile = (n + GBM - 1) / GBM;
     const int npairs = ntile * (ntile + 1) / 2;

@@ -669,8 +669,9 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_cluster_kernel(const G
                 e -= r + 1;
                 ++r;
             }
-            tI[q] = tl < ntiles ? r : -1;
-            tJ[q] = e;
+            // slots past the last tile redo tile 0 (discarded): branch-free k-loop
+            tI[q] = tl < ntiles ? r : 0;
+            tJ[q] = tl < ntiles ? e : 0;
             // bulk rows: the face column of fragment column l/4 (the zero column
             // ld past the face); gathered rows: the staged position itself
             const int fi = 8 * r + (lane >> 2), fj = 8 * e + (lane >> 2);
@@ -726,9 +727,8 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_cluster_kernel(const G
                     const double wt = ws[tk + kr];
 #pragma unroll
                     for (int q = 0; q < TW; ++q) {
-                        if (tI[q] < 0) continue;
                         const double b = xr[cJ[q]];
-                        const double a = (tI[q] == tJ[q] ? b : xr[cI[q]]) * wt;
+                        const double a = xr[cI[q]] * wt;
                         gp_dmma(acc[q][u], a, b);
                     }
                 }
@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_cluster_kernel(const G
         // partial -> W (m x m, lower triangle of the face)
 #pragma unroll
         for (int q = 0; q < TW; ++q) {
-            if (tI[q] < 0) continue;
+            if (warp + q * nwarps >= ntiles) continue;
             const int i = 8 * tI[q] + (lane >> 2);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -753,13 +753,13 @@ __global__ void __launch_bounds__(kGpThreads, 1) gram_pcg_cluster_kernel(const G
         }
     };
     if (tpw <= 1)
-        run(std::integral_constant<int, 1>{}, std::integral_constant<int, 8>{});
+        run(std::integral_constant<int, 1>{}, std::integral_constant<int, 16>{});
     else if (tpw <= 2)
-        run(std::integral_constant<int, 2>{}, std::integral_constant<int, 4>{});
+        run(std::integral_constant<int, 2>{}, std::integral_constant<int, 8>{});
     else if (tpw <= 4)
-        run(std::integral_constant<int, 4>{}, std::integral_constant<int, 2>{});
+        run(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{});
     else
-        run(std::integral_constant<int, 8>{}, std::integral_constant<int, 1>{});  // kGpMaxM = 112: <= 7 tiles
+        run(std::integral_constant<int, 8>{}, std::integral_constant<int, 2>{});  // kGpMaxM = 112: <= 7 tiles
     const long long tg1 = clock64();
     cluster.sync();
     // ---- each CTA sums a slice of the entries over the cluster (rank order)

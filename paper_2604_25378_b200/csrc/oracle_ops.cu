@@ -985,6 +985,29 @@ static bool run_dmma(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io) {
     return true;
 }
 
+// MVSK_SMALL_PROF: per-phase cycle sums of CTA 0 of the one-cluster kernels
+// (0: small_pass_kernel, 1: small_gram_kernel), printed at exit
+static unsigned long long* small_prof(int which) {
+    static const bool on = std::getenv("MVSK_SMALL_PROF") != nullptr;
+    static unsigned long long* buf = nullptr;
+    if (!on) return nullptr;
+    if (!buf) {
+        MVSK_CUDA(cudaMallocManaged(&buf, 16 * sizeof(unsigned long long)));
+        std::memset(buf, 0, 16 * sizeof(unsigned long long));
+        std::atexit([] {
+            cudaDeviceSynchronize();
+            for (int w = 0; w < 2; ++w) {
+                const unsigned long long* p = buf + 8 * w;
+                const double nn = p[5] ? (double)p[5] : 1.0;
+                std::fprintf(stderr, "[%s] %llu launches, cycles/launch on CTA 0: %.0f | %.0f | %.0f | %.0f | %.0f\n",
+                             w ? "small gram: load | tiles | reduce | exit" : "small pass: load | rows | combine | epilogue | exit",
+                             p[5], p[0] / nn, p[1] / nn, p[2] / nn, p[3] / nn, p[4] / nn);
+            }
+        });
+    }
+    return buf + 8 * which;
+}
+
 template <Op OP>
 static const void* small_pass_fn(int ld) {
     if (ld <= 32) return reinterpret_cast<const void*>(&small_pass_kernel<OP, 2, 16>);
@@ -1019,21 +1042,7 @@ static bool run_small_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io, Sl
     a.rowv = op == Op::FGRAD ? ctx->zoff_dev : (op == Op::XTW ? io.tw : io.z);
     a.zout = op == Op::FGRAD ? slot->z : io.zout;
     a.fin = finish_args(ctx, op, op == Op::LINESUMS ? 0 : 1, 1, io, slot);
-    static unsigned long long* prof = nullptr;  // MVSK_SMALL_PROF: phase cycle sums, printed at exit
-    if (std::getenv("MVSK_SMALL_PROF")) {
-        if (!prof) {
-            MVSK_CUDA(cudaMallocManaged(&prof, 8 * sizeof(unsigned long long)));
-            std::memset(prof, 0, 8 * sizeof(unsigned long long));
-            std::atexit([] {
-                cudaDeviceSynchronize();
-                const double nn = prof[5] ? (double)prof[5] : 1.0;
-                std::fprintf(stderr, "[small pass] %llu launches, cycles/launch on CTA 0: load %.0f rows %.0f "
-                             "combine %.0f epilogue %.0f exit-sync %.0f\n", prof[5], prof[0] / nn, prof[1] / nn,
-                             prof[2] / nn, prof[3] / nn, prof[4] / nn);
-            });
-        }
-        a.prof = prof;
-    }
+    a.prof = small_prof(0);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1054,6 +1063,47 @@ static bool run_small_pass(mvsk_gpu_ctx* ctx, Op op, int k, const PassIO& io, Sl
     ++ctx->launches;
     ctx->phys += 1;
     if (sharded) finish_pass(ctx, op, op == Op::LINESUMS ? 0 : 1, 1, io, slot, true);
+    return true;
+}
+
+bool run_small_gram(mvsk_gpu_ctx* ctx, const double* z, double* G_dev, double scale, double* G_host, double* packed) {
+    static const bool off = std::getenv("MVSK_NO_SMALL_PASS") != nullptr;
+    if (off || !z || (is_sharded(ctx) && !packed) || ctx->ld > kSpM || ctx->T_local < kSpCS) return false;
+    const long long nloc = (ctx->T_local + kSpCS - 1) / kSpCS;
+    const size_t smem = small_gram_smem(nloc, (int)ctx->ld);
+    const void* fn = reinterpret_cast<const void*>(&small_gram_kernel);
+    if (smem > ctx->max_smem || !cluster_fits(fn, kSpCS, kSgW * 32, smem)) return false;
+    set_smem_attr(fn, smem);
+    SmallGramArgs a{};
+    a.X = ctx->X;
+    a.T = ctx->T_local;
+    a.ld = (int)ctx->ld;
+    a.n = (int)ctx->n;
+    a.z = z;
+    a.c2 = ctx->c.c2;
+    a.c3 = ctx->c.c3;
+    a.c4 = ctx->c.c4;
+    a.scale = scale;
+    a.G = G_dev;
+    a.Gh = G_host;
+    a.packed = packed;
+    a.prof = small_prof(1);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kSpCS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(kSpCS);
+    cfg.blockDim = dim3(kSgW * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[] = {&a};
+    MVSK_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+    ++ctx->launches;
+    ctx->phys += 1;
     return true;
 }
 

@@ -40,6 +40,10 @@ void run_psi2(mvsk_gpu_ctx* ctx, const double* z, double* out, long long T);
 // Weighted Gram G = X^T diag(w) X / T over the full panel (n x n, row-major,
 // symmetric, both triangles written); allreduced across the shard group.
 // G = X^T diag(w) X * scale; with z set, w = psi''(z) computed in the kernel (w_rows unused)
+// one-cluster Gram for short narrow panels (small_pass.cuh); false if not eligible
+// (packed: row-sharded groups get the packed lower triangle there instead of G)
+bool run_small_gram(mvsk_gpu_ctx* ctx, const double* z, double* G_dev, double scale, double* G_host,
+                    double* packed = nullptr);
 // G_host: optional mapped host mirror (device alias) written alongside G_dev
 void run_weighted_gram(mvsk_gpu_ctx* ctx, const double* w_rows, double* G_dev, double scale, const double* z = nullptr,
                        double* G_host = nullptr);

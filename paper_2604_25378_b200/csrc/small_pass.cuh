@@ -321,3 +321,197 @@ __global__ void __launch_bounds__(kSpW * 32, 1) small_pass_kernel(const SmallPas
 }
 
 }  // namespace mvsk_b200
+
+namespace mvsk_b200 {
+
+// ---- the direct branch's weighted Gram G = X^T diag(psi''(z)) X / T for the
+// same short narrow panels (affine_normal.hpp:151-170 assemble it from n + 1
+// passes; here one launch): the panel rows staged in the cluster's shared
+// memory as above, 8 x 8 lower-triangle output tiles as mma.m8n8k4 f64 over
+// 4-row k-steps (warp w owns tiles w, w + 8, ..., with enough interleaved
+// accumulators per tile for ~8 independent chains: the accumulate chain is
+// long-latency), the CTA partial tiles summed over DSMEM in cluster-rank
+// order, G written mirrored to device memory and to the mapped host buffer.
+constexpr int kSgW = 8;  // warps per CTA
+
+__host__ __device__ constexpr int small_gram_stride(int ld) {  // 4 (mod 16) doubles: conflict-free fragments
+    return ((ld + 7) & ~7) + ((((ld + 7) & ~7) % 16 == 0) ? 4 : 12);
+}
+__host__ __device__ constexpr size_t small_gram_smem(long long nloc, int ld) {
+    const long long nt = (ld + 7) / 8;
+    return ((size_t)((nloc + 3) & ~3LL) * (small_gram_stride(ld) + 1) + (size_t)(nt * (nt + 1) / 2) * 64) * sizeof(double);
+}
+
+struct SmallGramArgs {
+    const double* X;
+    long long T;
+    int ld, n;
+    const double* z;
+    double c2, c3, c4, scale;
+    double* G;   // n x n device
+    double* Gh;  // n x n mapped host mirror (or null)
+    double* packed;  // row-sharded: the lower triangle packed (n (n + 1) / 2) for the allreduce, instead of G
+    unsigned long long* prof;  // MVSK_SMALL_PROF: CTA 0 phase cycle sums [load, tiles, reduce, exit, -, n]
+};
+
+__device__ __forceinline__ void sg_dmma(double (&d)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+        : "+d"(d[0]), "+d"(d[1])
+        : "d"(a), "d"(b));
+}
+
+template <int TW, int U>
+__device__ __forceinline__ void small_gram_tiles(const double* xs, const double* ws, int ms, int rows4, int ntiles,
+                                                 double* tb) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double acc[TW][U][2];
+    int tI[TW], tJ[TW];
+#pragma unroll
+    for (int q = 0; q < TW; ++q) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[q][u][0] = acc[q][u][1] = 0.0;
+        const int tl = warp + q * kSgW;
+        int r = 0, e = tl;
+        while (e > r) {
+            e -= r + 1;
+            ++r;
+        }
+        // slots past the last tile redo tile 0 (discarded): the k-loop stays
+        // branch-free, so the warp issues its DMMAs back to back
+        tI[q] = tl < ntiles ? r : 0;
+        tJ[q] = tl < ntiles ? e : 0;
+    }
+    const int kr = lane & 3, kc = lane >> 2;
+    for (int t0 = 0; t0 < rows4; t0 += 4 * U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int tk = t0 + 4 * u;
+            if (tk >= rows4) break;
+            const double* xr = xs + (size_t)(tk + kr) * ms + kc;
+            const double wt = ws[tk + kr];
+#pragma unroll
+            for (int q = 0; q < TW; ++q) {
+                const double b = xr[8 * tJ[q]];
+                const double a = xr[8 * tI[q]] * wt;
+                sg_dmma(acc[q][u], a, b);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < TW; ++q) {
+        const int tl = warp + q * kSgW;
+        if (tl >= ntiles) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double v = acc[q][0][h];
+#pragma unroll
+            for (int u = 1; u < U; ++u) v += acc[q][u][h];
+            tb[(size_t)tl * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + h] = v;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kSgW * 32, 1) small_gram_kernel(const SmallGramArgs a) {
+    namespace cgs = cooperative_groups;
+    cgs::cluster_group cluster = cgs::this_cluster();
+    const int crank = (int)cluster.block_rank(), CS = (int)cluster.num_blocks();
+    const int tid = threadIdx.x;
+    const int ld = a.ld, ms = small_gram_stride(ld);
+    const int nt = (a.n + 7) / 8, ntiles = nt * (nt + 1) / 2;
+    const bool prof = a.prof && tid == 0 && blockIdx.x == 0;
+    unsigned long long tp = prof ? clock64() : 0;
+    auto mark = [&](int i) {
+        if (prof) {
+            const unsigned long long now = clock64();
+            atomicAdd(a.prof + i, now - tp);
+            tp = now;
+        }
+    };
+    extern __shared__ __align__(16) double sg[];
+    const long long r0 = a.T * crank / CS, r1 = a.T * (crank + 1) / CS;
+    const int nloc = (int)(r1 - r0), rows4 = (nloc + 3) & ~3;
+    // tb first: the cluster reads it by offset, which must not depend on this
+    // CTA's row count
+    double* tb = sg;                           // [ntiles][64] this CTA's tiles
+    double* xs = tb + (size_t)ntiles * 64;     // [rows4][ms]
+    double* ws = xs + (size_t)rows4 * ms;      // [rows4]
+    __shared__ uint64_t bar;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        if (nloc > 0) mbar_arrive_expect_tx(&bar, (uint32_t)((size_t)nloc * ld * sizeof(double)));
+    }
+    __syncthreads();
+    for (int r = tid; r < nloc; r += blockDim.x)
+        bulk_g2s(xs + (size_t)r * ms, a.X + (r0 + r) * (long long)ld, (uint32_t)(ld * sizeof(double)), &bar,
+                 policy_evict_last());
+    for (int e = tid; e < rows4 * ms; e += blockDim.x) {  // pad columns and pad rows
+        const int t = e / ms, j = e - t * ms;
+        if (t >= nloc || j >= ld) xs[e] = 0.0;
+    }
+    for (int t = tid; t < rows4; t += blockDim.x) {  // oracle.hpp:116-119
+        const double zt = t < nloc ? __ldg(a.z + r0 + t) : 0.0;
+        ws[t] = t < nloc ? 2.0 * a.c2 - 6.0 * a.c3 * zt + 12.0 * a.c4 * (zt * zt) : 0.0;
+    }
+    if (nloc > 0) mbar_wait(&bar, 0u);
+    __syncthreads();
+    mark(0);
+    const int tpw = (ntiles + kSgW - 1) / kSgW;
+    // several independent accumulate chains per warp (the DMMA accumulate
+    // latency is several hundred cycles); past ~12 chains the fragment loads
+    // (2 LDS.64 per DMMA) and the register file bound it instead (C2: 12
+    // tiles x 1 chain 13.4k cycles, 12 x 2 14.8k)
+    if (tpw <= 1)
+        small_gram_tiles<1, 16>(xs, ws, ms, rows4, ntiles, tb);
+    else if (tpw <= 2)
+        small_gram_tiles<2, 12>(xs, ws, ms, rows4, ntiles, tb);
+    else if (tpw <= 4)
+        small_gram_tiles<4, 6>(xs, ws, ms, rows4, ntiles, tb);
+    else if (tpw <= 6)
+        small_gram_tiles<6, 4>(xs, ws, ms, rows4, ntiles, tb);
+    else if (tpw <= 8)
+        small_gram_tiles<8, 2>(xs, ws, ms, rows4, ntiles, tb);
+    else if (tpw <= 12)
+        small_gram_tiles<12, 1>(xs, ws, ms, rows4, ntiles, tb);
+    else
+        small_gram_tiles<17, 1>(xs, ws, ms, rows4, ntiles, tb);  // n <= 128: 136 tiles
+    __syncthreads();
+    mark(1);
+    cluster.sync();
+    // tile entries split over the cluster; each summed over the CTAs in rank order
+    const int tot = ntiles * 64;
+    for (int e = crank * (int)blockDim.x + tid; e < tot; e += CS * (int)blockDim.x) {
+        const int tl = e >> 6, w = e & 63;
+        int ti = 0, tj = tl;
+        while (tj > ti) {
+            tj -= ti + 1;
+            ++ti;
+        }
+        const int i = 8 * ti + (w >> 3), j = 8 * tj + (w & 7);
+        if (i >= a.n || j > i) continue;
+        double pv[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) pv[r] = r < CS ? cluster.map_shared_rank(tb, r)[e] : 0.0;
+        double v = 0.0;
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+            if (r < CS) v += pv[r];
+        v *= a.scale;
+        if (a.packed) {
+            a.packed[(size_t)i * (i + 1) / 2 + j] = v;
+            continue;
+        }
+        a.G[(size_t)i * a.n + j] = v;
+        a.G[(size_t)j * a.n + i] = v;
+        if (a.Gh) {
+            a.Gh[(size_t)i * a.n + j] = v;
+            a.Gh[(size_t)j * a.n + i] = v;
+        }
+    }
+    mark(2);
+    cluster.sync();
+    mark(3);
+    if (prof) atomicAdd(a.prof + 5, 1ull);
+}
+
+}  // namespace mvsk_b200
