@@ -11,7 +11,8 @@ import os
 from pathlib import Path
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "_build" / "libmvsk_b200.so"
+# MVSK_B200_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = Path(os.environ.get("MVSK_B200_LIB") or PKG_DIR / "_build" / "libmvsk_b200.so")
 
 MVSK_GPU_ABI_VERSION = 1
 MVSK_GPU_MAX_SLOTS = 8

@@ -560,7 +560,7 @@ bool make_dmma_ws_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
         for (int w : {64, 80, 128})
             if (!WC && 8 * w >= cw && select_dmma_ws(op, K, w, C)) WC = w;
         if (!WC) continue;
-        const size_t stage = (size_t)8 * (8 * WC + 4) * sizeof(double);
+        const size_t stage = (size_t)8 * kWsRowStride(WC) * sizeof(double);
         size_t head = 256 + (size_t)(2 * 8 * V + 4 * C * V + 128) * sizeof(double);
         head = (head + 127) & ~(size_t)127;
         const int S = (int)std::min<size_t>(8, (ctx->max_smem - head) / stage);

@@ -632,6 +632,21 @@ __device__ __forceinline__ void reg_dealloc_40() { asm volatile("setmaxnreg.dec.
 // V fragments leave no room for held phase-2 fragments): phase 2 reads the
 // tile from the ring slot, which is then released after phase 2 instead of
 // after phase 1 (one fill fewer in flight).
+// Ring layout of the warp-specialised kernel. A staged row r of a slot starts at
+// r * RS + ws_row_swz(r) doubles with RS = 8 WC + 8, i.e. at 16-byte chunk
+// (4 r + 2 ((r >> 1) & 1)) mod 8 of the 128-byte bank window: rows 2a and
+// 2a + 1 sit 64 bytes apart (the phase-1 fragments: a quarter-warp reads 4
+// chunks of each of two adjacent rows) and rows 0..3 / 4..7 start at chunks
+// {0, 4, 2, 6} (the phase-2 fragments: 2 chunks of each of four rows), so both
+// 16-byte fragment loads are bank-conflict-free. With the earlier uniform
+// 8 WC + 4 stride the phase-1 loads were 2-way conflicted (ncu: 82 M conflict
+// wavefronts of 227 M shared-load wavefronts on the C5 8-RHS HVP).
+#ifndef MVSK_WS_SWZ
+#define MVSK_WS_SWZ 1  // 0: the uniform 8 WC + 4 stride (A/B builds only)
+#endif
+__host__ __device__ constexpr int kWsRowStride(int wc) { return 8 * wc + (MVSK_WS_SWZ ? 8 : 4); }
+__device__ __forceinline__ int ws_row_swz(int r) { return MVSK_WS_SWZ ? ((r >> 1) & 1) * 4 : 0; }
+
 template <Op OP, int K, int WC, int C, bool F2REG = true>
 __global__ void __launch_bounds__(384, 1) stream_dmma_ws_kernel(const DmmaArgs a) {
     using Sh = DmmaShape<OP, K>;
@@ -642,7 +657,7 @@ __global__ void __launch_bounds__(384, 1) stream_dmma_ws_kernel(const DmmaArgs a
     constexpr int MP = WC / 16;
     constexpr int MT = 2 * MP;
     constexpr int VPL = (V + 31) / 32;  // dots per reducer lane
-    constexpr int RS = 8 * WC + 4;
+    constexpr int RS = kWsRowStride(WC);
     constexpr int NCH = NT1 >= 2 ? MVSK_NCH2 : MVSK_NCH1;
     static_assert(K <= 8 && WC % 16 == 0 && C % 2 == 0, "shape");
     if (pass_skipped(a.skip, a.nskip)) return;
@@ -714,8 +729,8 @@ __global__ void __launch_bounds__(384, 1) stream_dmma_ws_kernel(const DmmaArgs a
                     const double* src = a.X + (r0 + (long long)s * 8) * ld + col0;
                     double* dst = ring + slot * stage_elems;
                     for (int r = 0; r < rows; ++r)
-                        bulk_g2s(dst + (size_t)r * RS, src + (long long)r * ld, (uint32_t)(cw * sizeof(double)),
-                                 &full[slot], policy);
+                        bulk_g2s(dst + (size_t)r * RS + ws_row_swz(r), src + (long long)r * ld,
+                                 (uint32_t)(cw * sizeof(double)), &full[slot], policy);
                     if (++slot == S) slot = 0;
                 }
             }
@@ -831,8 +846,8 @@ __global__ void __launch_bounds__(384, 1) stream_dmma_ws_kernel(const DmmaArgs a
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
         double f2[F2REG ? 2 : 1][F2REG ? MT : 1];
-        const int p1_off = g4 * RS + wcol + 2 * t4;
-        const int p2_off = t4 * RS + wcol + 2 * g4;
+        const int p1_off = g4 * RS + ws_row_swz(g4) + wcol + 2 * t4;
+        const int p2_off = t4 * RS + ws_row_swz(t4) + wcol + 2 * g4;  // rows t4 and 4 + t4 share the offset
         int slot = 0, prev_slot = 0;
         uint32_t fpar = 0;
         for (int i = 0; i <= nst; ++i) {
