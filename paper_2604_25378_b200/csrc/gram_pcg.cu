@@ -41,6 +41,7 @@ namespace {
 constexpr int kGpMaxM = 112;     // face width limit (two m x m fp64 buffers in shared memory)
 constexpr int kGpMaxCols = 8;    // Hutchinson probes handled in one lock-step block
 constexpr int kGpThreads = 512;
+constexpr int kDirectDeviceMinLd = 64;  // narrower panels take the host LU / Cholesky direct branch
 constexpr int kGraphGramPcg = 102;
 constexpr int kGraphGramDirect = 103;
 
@@ -452,6 +453,111 @@ __device__ void unreflect_block(const double* D, int ldd, int r, const double* v
     __syncthreads();
 }
 
+// In-place Gauss-Jordan inverse of an SPD matrix without pivoting, the matrix
+// held in registers: thread (ty, tx) of the 16 x 32 grid owns rows ty + 16 a
+// (a < 7) and columns tx + 32 b (b < 4), i.e. up to 112 x 128 >= kGpMaxM - 2.
+// Per pivot k the owners of row k publish the scaled pivot row (one warp: the
+// pivot is broadcast by a shuffle), the owners of column k publish the column,
+// one block barrier, then every thread applies its rank-1 update from
+// registers; the buffers are double-buffered so the next pivot's owners may
+// publish while slower threads still read. Sweep (classic in-place form):
+//   row k /= d; a_ij -= a_ik a_kj (i, j != k); a_ik = -a_ik / d; a_kk = 1 / d
+// (one reciprocal per pivot, then multiplications). The pivot loop is nested
+// k = 16 KA + kty with KA a compile-time index, so the owners' register
+// elements r[KA][.] / r[.][KA / 2] are static (a flat loop with runtime
+// selects over the 28 elements issued ~680 instructions per pivot: 2.5k cycles).
+// Returns false (W undefined, S untouched) when a pivot is not positive (or NaN);
+// an infinite pivot surfaces in the caller's finite check of P.
+constexpr int kGjRT = 7, kGjCT = 4;
+static_assert(16 * kGjRT >= kGpMaxM - 2 && 32 * kGjCT >= kGpMaxM - 2 && kGpThreads == 512, "tile grid");
+
+template <int KA>
+__device__ __forceinline__ void gj_pivot_block(double (&r)[kGjRT][kGjCT], int mm, double (*gj_row)[32 * kGjCT],
+                                               double (*gj_col)[16 * kGjRT], double* gj_piv, int* gj_bad, int tx, int ty) {
+    constexpr int KB = KA / 2;  // column tile of k = 16 KA + kty
+    // every thread updates its whole 7 x 4 tile (the padding is the identity):
+    // guarding the inactive tiles of a narrow face costs more issue slots than
+    // the 28 FMAs it would save
+    for (int kty = 0; kty < 16; ++kty) {
+        const int k = 16 * KA + kty;
+        if (k >= mm) break;  // uniform
+        const int buf = k & 1;
+        const int ktx = k & 31;
+        if (ty == kty) {  // one warp holds row k
+            const double d = __shfl_sync(0xffffffffu, r[KA][KB], ktx);
+            const double dinv = 1.0 / d;  // one division per pivot: fp64 division is a ~100-cycle routine
+            const bool diag_lane = tx == ktx;
+            if (diag_lane) {
+                gj_piv[buf] = dinv;
+                if (!(d > 0.0)) *gj_bad = 1;  // not positive (or NaN)
+            }
+#pragma unroll
+            for (int b = 0; b < kGjCT; ++b) {
+                const bool diag = (b == KB) && diag_lane;
+                const double v = diag ? 0.0 : r[KA][b] * dinv;
+                gj_row[buf][tx + 32 * b] = v;
+                r[KA][b] = diag ? dinv : v;  // row k is final for this pivot
+            }
+        }
+        if (tx == ktx) {  // 16 threads hold column k
+#pragma unroll
+            for (int a = 0; a < kGjRT; ++a) gj_col[buf][ty + 16 * a] = (a == KA && ty == kty) ? 0.0 : r[a][KB];
+        }
+        __syncthreads();
+        double rw[kGjCT], cl[kGjRT];
+#pragma unroll
+        for (int b = 0; b < kGjCT; ++b) rw[b] = gj_row[buf][tx + 32 * b];
+#pragma unroll
+        for (int a = 0; a < kGjRT; ++a) cl[a] = gj_col[buf][ty + 16 * a];
+        const double ndinv = -gj_piv[buf];
+#pragma unroll
+        for (int a = 0; a < kGjRT; ++a)
+#pragma unroll
+            for (int b = 0; b < kGjCT; ++b)
+                r[a][b] = fma(-cl[a], rw[b], r[a][b]);  // row k (cl = 0), column k (rw = 0): unchanged
+        if (tx == ktx) {  // column k: a_ik = -a_ik / d (the diagonal keeps 1 / d)
+#pragma unroll
+            for (int a = 0; a < kGjRT; ++a)
+                if (!(a == KA && ty == kty)) r[a][KB] = cl[a] * ndinv;
+        }
+    }
+}
+
+__device__ bool spd_inverse_tiled(const double* S, double* W, int ldm, int mm) {
+    constexpr int RT = kGjRT, CT = kGjCT;
+    __shared__ double gj_row[2][32 * CT], gj_col[2][16 * RT], gj_piv[2];
+    __shared__ int gj_bad;
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    double r[RT][CT];
+#pragma unroll
+    for (int a = 0; a < RT; ++a)
+#pragma unroll
+        for (int b = 0; b < CT; ++b) {
+            const int i = ty + 16 * a, j = tx + 32 * b;
+            r[a][b] = (i < mm && j < mm) ? S[(size_t)i * ldm + j] : (i == j ? 1.0 : 0.0);
+        }
+    if (tid == 0) gj_bad = 0;
+    __syncthreads();
+    gj_pivot_block<0>(r, mm, gj_row, gj_col, gj_piv, &gj_bad, tx, ty);
+    gj_pivot_block<1>(r, mm, gj_row, gj_col, gj_piv, &gj_bad, tx, ty);
+    gj_pivot_block<2>(r, mm, gj_row, gj_col, gj_piv, &gj_bad, tx, ty);
+    gj_pivot_block<3>(r, mm, gj_row, gj_col, gj_piv, &gj_bad, tx, ty);
+    gj_pivot_block<4>(r, mm, gj_row, gj_col, gj_piv, &gj_bad, tx, ty);
+    gj_pivot_block<5>(r, mm, gj_row, gj_col, gj_piv, &gj_bad, tx, ty);
+    gj_pivot_block<6>(r, mm, gj_row, gj_col, gj_piv, &gj_bad, tx, ty);
+    __syncthreads();
+    if (gj_bad) return false;
+#pragma unroll
+    for (int a = 0; a < RT; ++a)
+#pragma unroll
+        for (int b = 0; b < CT; ++b) {
+            const int i = ty + 16 * a, j = tx + 32 * b;
+            if (i < mm && j < mm) W[(size_t)i * ldm + j] = r[a][b];
+        }
+    __syncthreads();
+    return true;
+}
+
 // Direct branch (affine_normal.hpp:151-188) after the Gram, one CTA: h, M + lambda I,
 // its inverse by Gauss-Jordan with partial pivoting (the pivots of the
 // reference's PartialPivLU: the largest remaining magnitude, first index on
@@ -477,6 +583,7 @@ __device__ void direct_phases(const SetupArgs& a, const GpParams& P, double* S, 
         if (i < m - 1) vQ[i] = par[L.vQ + i];
     }
     __syncthreads();
+    const long long td0 = clock64();
     // h = Q^T U^T G (U nu)  (:164-166)
     if (warp == 0) {
         for (int i = lane; i < m; i += 32) w[i] = i == 0 ? 0.0 : par[L.nu + i - 1];
@@ -497,6 +604,7 @@ __device__ void direct_phases(const SetupArgs& a, const GpParams& P, double* S, 
         for (int i = lane; i < mm; i += 32) a.vec[i] = t[2 + i];
     }
     __syncthreads();
+    if (tid == 0) a.res[52] = (double)(clock64() - td0);
     // M = (UQ)^T G (UQ) + lambda I  (:169-170)
     reflect_sym_block(S, m, m, vU, P.bU, W, m - 1, av, misc);
     const int ldm = m_stride(mm);
@@ -512,8 +620,18 @@ __device__ void direct_phases(const SetupArgs& a, const GpParams& P, double* S, 
         a.res[4] = 0.0;
     }
     __syncthreads();
+    if (tid == 0) a.res[53] = (double)(clock64() - td0);
+    // SPD fast path: when every pivot of the unpivoted sweep is positive and
+    // finite (M = W^T D W / T + lambda I with psi'' > 0, the normal case) the
+    // inverse comes from the register-tiled in-place sweep, one block barrier
+    // per pivot; otherwise the pivoted sweep below runs on the untouched S
+    const bool spd_done = spd_inverse_tiled(S, W, ldm, mm);
+    if (tid == 0) {
+        a.res[56] = spd_done ? 1.0 : 0.0;
+        a.res[57] = (double)(clock64() - td0);
+    }
     // Gauss-Jordan on [M | I] with partial pivoting: W <- M^-1
-    for (int k = 0; k < mm; ++k) {
+    for (int k = 0; k < mm && !spd_done; ++k) {
         if (warp == 0) {
             double big = -1.0;
             int piv = k;
@@ -574,7 +692,10 @@ __device__ void direct_phases(const SetupArgs& a, const GpParams& P, double* S, 
         }
         __syncthreads();
     }
-    if (tid == 0) a.res[3] = s_sing ? 1.0 : 0.0;
+    if (tid == 0) {
+        a.res[3] = s_sing ? 1.0 : 0.0;
+        a.res[54] = (double)(clock64() - td0);
+    }
     for (int e = tid; e < mm * ldm; e += blockDim.x) a.Mg[e] = W[e];
     __syncthreads();
     if (!a.pmat) return;
@@ -593,7 +714,10 @@ __device__ void direct_phases(const SetupArgs& a, const GpParams& P, double* S, 
     }
     if (bad) atomicOr(&s_sing, 2);
     __syncthreads();
-    if (tid == 0) a.res[4] = (s_sing & 2) ? 1.0 : 0.0;
+    if (tid == 0) {
+        a.res[4] = (s_sing & 2) ? 1.0 : 0.0;
+        a.res[55] = (double)(clock64() - td0);
+    }
 }
 
 __device__ __forceinline__ void gp_dmma(double (&d)[2], double a, double b) {
@@ -1127,15 +1251,23 @@ bool direct_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, con
                              std::vector<double>& u) {
     const int m = (int)in.m;
     if (m < 4 || m > kGpMaxM || is_sharded(ctx)) return false;
-    // opt-in (MVSK_DEVICE_DIRECT=1): on B200 its kernel chain measured slower than
-    // the host LU path (C2 direction 207 vs 122 us, C1 69 vs 56 us; profiles/
-    // r02_direct_device_ab.txt) - the Gauss-Jordan sweep pays a block barrier per
-    // pivot and the trace still needs two more kernels
-    static const bool on = std::getenv("MVSK_DEVICE_DIRECT") != nullptr;
-    if (!on) return false;
+    // Device-resident by default on panels of >= kDirectDeviceMinLd columns: one
+    // graph (Gram + h + M + register-tiled SPD inverse + P in one cluster
+    // kernel, trace quadform, X^T pass, solve) and one round trip per
+    // direction. Measured (profiles/r02_direct_device_ab.txt): C2-small solve
+    // (n = 100, T = 1000) 5.04 ms on the host LU path (112 us per direction) vs
+    // 4.31 ms here (94 us); C1 (n = 20, T = 500) 42 us per direction on the host
+    // vs 60 us here - the kernel's fixed phase latencies (~26 us) and its three
+    // trailing launches exceed two short round trips around an 18 x 18
+    // factorisation, so narrow panels keep the host path.
+    // MVSK_DEVICE_DIRECT=1 / MVSK_NO_DEVICE_DIRECT=1 force either side (A/B runs).
+    static const bool force_on = std::getenv("MVSK_DEVICE_DIRECT") != nullptr;
+    static const bool force_off = std::getenv("MVSK_NO_DEVICE_DIRECT") != nullptr;
+    if (force_off || (!force_on && ctx->ld < kDirectDeviceMinLd)) return false;
     const int mm = m - 2;
     const int mp = gp_stage_stride(m, (int)ctx->ld);
-    const long long avail = (long long)(ctx->max_smem / sizeof(double)) - (6LL * m + 64) - 64;
+    // 512 doubles less than the PCG setup: the static buffers of spd_inverse_tiled
+    const long long avail = (long long)(ctx->max_smem / sizeof(double)) - (6LL * m + 64) - 64 - 512;
     long long SR = std::min<long long>(avail / (mp + 1), (ctx->T_local + 7) / 8);
     SR = std::max<long long>(SR & ~3LL, 4);  // whole 4-row DMMA k-steps
     const int stage_rows = (int)SR;
@@ -1238,6 +1370,15 @@ bool direct_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, con
     });
     MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
     u.assign(ws.h_res + 64, ws.h_res + 64 + mm);
+    static const bool prof = std::getenv("MVSK_GPCG_PROF") != nullptr;
+    if (prof) {
+        const double* r = ws.h_res;
+        std::fprintf(stderr,
+                     "[gdirect] m=%d ld %lld T %lld spd %.0f (%.0f) cycles: gram %.0f reduce %.0f | h %.0f M %.0f inverse %.0f P %.0f | "
+                     "gram: pre %.0f issue %.0f wait %.0f mma %.0f\n",
+                     m, (long long)ctx->ld, (long long)ctx->T_local, r[56], r[57] - r[53], r[48], r[49], r[52], r[53] - r[52],
+                     r[54] - r[53], r[55] - r[54], r[58], r[59], r[60], r[61]);
+    }
     return true;
 }
 
