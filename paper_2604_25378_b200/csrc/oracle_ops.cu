@@ -449,58 +449,6 @@ const void* select_dmma(Op op, int K, int WC, int D) {
     return nullptr;
 }
 
-template <Op OP, int K, int WC>
-const void* pfn() {
-    return reinterpret_cast<const void*>(&stream_dmma_pipe_kernel<OP, K, WC, 4>);
-}
-
-// pipelined variant (stream_dmma_pipe_kernel, 4-CTA clusters): instantiated
-// where its registers (V fragments + accumulators + the held phase-2
-// fragments) fit one thread's 255
-const void* select_dmma_pipe(Op op, int K, int WC) {
-    if (op == Op::HVP && K == 8) {
-        if (WC == 64) return pfn<Op::HVP, 8, 64>();
-        if (WC == 80) return pfn<Op::HVP, 8, 80>();
-        if (WC == 128) return pfn<Op::HVP, 8, 128>();
-    }
-    if (op == Op::HVP && K == 4) {
-        if (WC == 64) return pfn<Op::HVP, 4, 64>();
-        if (WC == 80) return pfn<Op::HVP, 4, 80>();
-        if (WC == 128) return pfn<Op::HVP, 4, 128>();
-    }
-    if (op == Op::THIRD && K == 4) {
-        if (WC == 64) return pfn<Op::THIRD, 4, 64>();
-        if (WC == 80) return pfn<Op::THIRD, 4, 80>();
-        if (WC == 128) return pfn<Op::THIRD, 4, 128>();
-    }
-    return nullptr;
-}
-
-// C = 4 / WC / S for the pipelined kernel; false when no instantiation fits
-bool make_dmma_pipe_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
-    const int C = 4;
-    const int ndot = op == Op::THIRD ? 2 * K : K;
-    const int V = 8 * ndot;
-    if (ctx->ld % (2 * C)) return false;
-    const int cw = (int)(ctx->ld / C);
-    int WC = 0;
-    for (int w : {64, 80, 128})
-        if (!WC && 8 * w >= cw && select_dmma_pipe(op, K, w)) WC = w;
-    if (!WC) return false;
-    const size_t stage = (size_t)8 * (8 * WC + 4) * sizeof(double);
-    size_t head = 256 + (size_t)(2 * 8 * V + 4 * C * V) * sizeof(double);
-    head = (head + 127) & ~(size_t)127;
-    const int S = (int)std::min<size_t>(8, (ctx->max_smem - head) / stage);
-    if (S < 2) return false;
-    pl.C = C;
-    pl.WC = WC;
-    pl.S = S;
-    pl.smem = head + (size_t)S * stage;
-    pl.fn = select_dmma_pipe(op, K, WC);
-    pl.ncl = std::max(1, ctx->nsm / C);
-    return true;
-}
-
 template <Op OP, int K, int WC, int C, bool F2REG = true>
 const void* wfn() {
     return reinterpret_cast<const void*>(&stream_dmma_ws_kernel<OP, K, WC, C, F2REG>);
@@ -579,12 +527,12 @@ bool make_dmma_ws_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
 
 bool make_dmma_plan(const mvsk_gpu_ctx* ctx, Op op, int K, DPlan& pl) {
     if (std::getenv("MVSK_NO_DMMA")) return false;
-    // warp-specialised kernel first (C5 8-RHS HVP 1.47 ms vs 2.06 pipelined vs
-    // 2.23 v1, profiles/r01_dmma_pipe.txt); MVSK_DMMA_PIPE / MVSK_DMMA_V1 force
-    // the older kernels for A/B runs
+    // warp-specialised kernel first (C5 8-RHS HVP 1.41 ms vs 2.23 v1,
+    // profiles/r01_dmma_pipe.txt, r02_dmma_row_swizzle_ab.txt); v1 serves the
+    // shapes the warp-specialised kernel has no instantiation for (160-column
+    // slices at n = 5000) and MVSK_DMMA_V1 forces it for A/B runs
     const bool v1 = std::getenv("MVSK_DMMA_V1") || std::getenv("MVSK_TUNE_DMMA");
-    if (!v1 && !std::getenv("MVSK_DMMA_PIPE") && make_dmma_ws_plan(ctx, op, K, pl)) return true;
-    if (!v1 && make_dmma_pipe_plan(ctx, op, K, pl)) return true;
+    if (!v1 && make_dmma_ws_plan(ctx, op, K, pl)) return true;
     int forceC = 0, forceD = 0;
     if (const char* e = std::getenv("MVSK_TUNE_DMMA")) std::sscanf(e, "%d,%d", &forceC, &forceD);
     const int ndot = op == Op::THIRD ? 2 * K : K;

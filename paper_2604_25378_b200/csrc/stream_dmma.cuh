@@ -281,334 +281,12 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Pipelined variant: no CTA-wide barrier in the stage loop, the cluster
-// exchange of stage i hidden behind the row dots of stage i+1.
-//
-// The kernel above serialises every stage: phase 1 -> barrier -> reduce ->
-// DSMEM round trip -> barrier -> phase 2, and its 64 KB ring slot stays
-// claimed until phase 2 is done. ncu (profiles/r01_ncu_dmma_v1_stalls.txt):
-// 28 % of warp samples at the two barriers, DRAM at 47 % while the DMMA pipe
-// idles half the time. Here each warp runs, per iteration i,
-//   reduce(i-1)  sum 8 warp partials of its share of the stage-(i-1) dots and
-//                push them to every CTA of the cluster (st.async)
-//   phase1(i)    row dots of stage i from the staged tile (DMMA), partial -> red
-//   phase2(i-1)  wait for the stage-(i-1) dots, W = psi o Y, G += X^T W from the
-//                stage-(i-1) fragments held in REGISTERS
-//   frag(i)      load stage i's phase-2 fragments (transposed tile) into
-//                registers and release the ring slot; the last warp to release
-//                refills it (monotone counter, no waiting warp)
-// so a slot is claimed for one iteration (two fills in flight with S = 3) and
-// the only waits are on data: the TMA fill, the 8 warp partials (mbarrier) and
-// the cluster's partial dots (tx-count mbarrier).
-//
-// Slot-reuse argument. Iteration i runs reduce(i-1) (push), phase1(i),
-// phase2(i-1), frag(i). A push of stage j+2 happens in iteration j+3, after
-// this warp's wait for the complete stage-(j+1) dots, which needs every warp of
-// every CTA to have pushed stage j+1, i.e. to have started iteration j+2 and so
-// finished phase2(j), the last read of exchange slot j % E: E >= 2 suffices (4
-// are kept). A partial of stage i+2 is written after this warp passed the wait
-// for stage i+1's dots, so every local warp has run reduce(i+1) and with it
-// reduce(i): R = 2 suffices. xfull[e] for stage j+E is re-armed by thread 0
-// right after its own wait for stage j completed (bytes arriving earlier only
-// drive the tx-count negative).
-//
-// Measured at C5 (scripts/dmma_ab.py, profiles/r01_dmma_pipe.txt): 8-RHS HVP
-// 2.23 -> 2.06 ms, 4-RHS 2.21 -> 2.02 ms, 4 third actions 2.24 -> 2.18 ms; the
-// 8-pair third action (twice the phase-1 fragments) spills here and stays on
-// the kernel above.
-// ---------------------------------------------------------------------------
-template <Op OP, int K, int WC, int C>
-__global__ void __launch_bounds__(256, 1) stream_dmma_pipe_kernel(const DmmaArgs a) {
-    using Sh = DmmaShape<OP, K>;
-    constexpr int NDOT = Sh::NDOT, NT1 = Sh::NT1, V = Sh::V;
-    constexpr int NW = 8;            // warps
-    constexpr int E = 4;             // exchange ring depth (slot-reuse argument above)
-    constexpr int KP = WC / 8;       // phase-1 k-step pairs per warp (one 16-byte load each)
-    constexpr int MP = WC / 16;      // phase-2 m-tile pairs per warp (one 16-byte load each)
-    constexpr int MT = 2 * MP;
-    constexpr int VPW = V / NW;      // dots reduced + pushed by each warp
-    constexpr int RS = 8 * WC + 4;   // smem row stride (doubles): conflict-free 16-byte fragments
-    constexpr int NCH = NT1 >= 2 ? MVSK_NCH2 : MVSK_NCH1;
-    static_assert(K <= 8, "phase 2 uses one n-tile");
-    static_assert(WC % 16 == 0, "16-byte fragment pairs");
-    static_assert(V % NW == 0 && VPW <= 32, "reduce share");
-    static_assert(C % 2 == 0, "partials read in pairs");
-    if (pass_skipped(a.skip, a.nskip)) return;  // uniform over the whole grid
-    cg::cluster_group cluster = cg::this_cluster();
-    const int crank = (int)cluster.block_rank();
-    const int ncl = gridDim.x / C;
-    const int ci = blockIdx.x / C;
-
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g4 = lane >> 2, t4 = lane & 3;
-    const int cw = a.cw, S = a.S;
-    const long long ld = a.ld;
-    const int col0 = crank * cw;
-    const int wcol = warp * WC;
-
-    // smem: [full 8 | xfull 4 | pfull 2] mbarriers, cnt[8] (256 B) [red 2 x NW x V][xchg E x V x C][ring S x 8 x RS]
-    // xchg is value-major (the C partials of one dot adjacent): 16-byte loads of partial pairs
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
-    uint64_t* xfull = full + 8;
-    uint64_t* pfull = full + 12;
-    unsigned* cnt = reinterpret_cast<unsigned*>(smem_raw + 128);
-    double* red = reinterpret_cast<double*>(smem_raw + 256);
-    double* xchg = red + 2 * NW * V;
-    size_t off = 256 + (size_t)(2 * NW * V + E * C * V) * sizeof(double);
-    off = (off + 127) & ~(size_t)127;
-    constexpr size_t stage_elems = (size_t)8 * RS;
-    double* ring = reinterpret_cast<double*>(smem_raw + off);
-
-    const long long T = a.T;
-    const long long r0 = T * ci / ncl, r1 = T * (ci + 1) / ncl;
-    const long long nrows = r1 - r0;
-    const int nst = (int)((nrows + 7) / 8);
-
-    for (size_t i = tid; i < (size_t)S * stage_elems; i += 256) ring[i] = 0.0;  // pads stay 0, tails finite
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
-        for (int e = 0; e < E; ++e) mbar_init(&xfull[e], 1);
-        for (int r = 0; r < 2; ++r) mbar_init(&pfull[r], NW);
-        for (int s = 0; s < 8; ++s) cnt[s] = 0;
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const uint64_t policy = a.evict_first ? policy_evict_first() : policy_evict_last();
-    auto issue = [&](int s, int slot) {
-        const long long rows = (nrows - (long long)s * 8) < 8 ? (nrows - (long long)s * 8) : 8;
-        mbar_arrive_expect_tx(&full[slot], (uint32_t)(rows * cw * sizeof(double)));
-        const double* src = a.X + (r0 + (long long)s * 8) * ld + col0;
-        double* dst = ring + slot * stage_elems;
-        for (int r = 0; r < rows; ++r)
-            bulk_g2s(dst + (size_t)r * RS, src + (long long)r * ld, (uint32_t)(cw * sizeof(double)), &full[slot], policy);
-    };
-    constexpr uint32_t kXBytes = (uint32_t)(C * V * sizeof(double));
-    if (tid == 0) {
-        const int pre = nst < S ? nst : S;
-        for (int s = 0; s < pre; ++s) issue(s, s);
-        for (int e = 0; e < E && e < nst; ++e) mbar_arrive_expect_tx(&xfull[e], kXBytes);
-    }
-    cluster.sync();  // peers' barriers initialised (and armed) before any push
-
-    // k-step (m, h) of a warp covers columns wcol + 8m + 2*t4 + h: a permutation
-    // inside each 8-column block, applied to A and B alike, so that thread t4
-    // reads its two columns 8m + 2*t4 + {0,1} as one 16-byte load
-    double vb[NT1][2 * KP];
-#pragma unroll
-    for (int nt = 0; nt < NT1; ++nt)
-#pragma unroll
-        for (int ks = 0; ks < 2 * KP; ++ks) {
-            const int c = wcol + 8 * (ks >> 1) + 2 * t4 + (ks & 1);
-            const int j = nt * 8 + g4;
-            double v = 0.0;
-            if (c < cw && j < NDOT) {
-                const double* src = (OP == Op::THIRD && j >= K) ? a.vin2 + (long long)(j - K) * ld
-                                                                 : a.vin + (long long)j * ld;
-                v = src[col0 + c];
-            }
-            vb[nt][ks] = v;
-        }
-    // phase-2 m-tile (p, h) of a warp covers columns wcol + 16p + 2*g4 + h
-    double acc[MT][2];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
-    double f2[2][MT];  // phase-2 A fragments of the previous stage
-    const double c2 = a.c2, c3 = a.c3, c4 = a.c4;
-    double pp[2] = {0.0, 0.0};  // psi2 (HVP) / psi3 (THIRD) of the previous stage's rows t4, 4 + t4
-    int refill = -1, refill_slot = 0;
-    unsigned rel_old = 0;
-    double zn[2];  // z of the next stage's rows t4, 4 + t4
-    zn[0] = (r0 + t4 < r1) ? __ldg(a.z + r0 + t4) : 0.0;
-    zn[1] = (r0 + 4 + t4 < r1) ? __ldg(a.z + r0 + 4 + t4) : 0.0;
-    const int p1_off = g4 * RS + wcol + 2 * t4;  // phase-1 fragment base (doubles)
-    const int p2_off = t4 * RS + wcol + 2 * g4;  // phase-2 fragment base (doubles)
-    const int rd_off = warp * VPW + lane;        // reduce share
-    const uint32_t xb_self = smem_u32(xchg);
-
-    // ---- reduce(j): this warp's VPW dots of stage j -> every CTA of the cluster
-    auto reduce = [&](int j) {
-        if (lane < VPW) {
-            mbar_wait(&pfull[j & 1], (uint32_t)((j >> 1) & 1));
-            const double* rb = red + (size_t)(j & 1) * NW * V + rd_off;
-            double sum = 0.0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) sum += rb[w * V];
-            const uint32_t la = xb_self + (uint32_t)((((j % E) * V + rd_off) * C + crank) * sizeof(double));
-            const uint32_t lb = smem_u32(&xfull[j % E]);
-#pragma unroll
-            for (int r = 0; r < C; ++r) {
-                uint32_t ra, rbar;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(r));
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(lb), "r"(r));
-                st_async_f64(ra, sum, rbar);
-            }
-        }
-    };
-    // ---- phase1(i): row dots of stage i from the staged tile, warp partial -> red
-    auto phase1 = [&](int i, int slot, uint32_t fpar) {
-        mbar_wait(&full[slot], fpar);
-        const double* X = ring + slot * stage_elems + p1_off;
-        double cfr[NCH][NT1][2];
-#pragma unroll
-        for (int h = 0; h < NCH; ++h)
-#pragma unroll
-            for (int nt = 0; nt < NT1; ++nt) cfr[h][nt][0] = cfr[h][nt][1] = 0.0;
-#pragma unroll
-        for (int m = 0; m < KP; ++m) {
-            const double2 av = *reinterpret_cast<const double2*>(X + 8 * m);
-#pragma unroll
-            for (int nt = 0; nt < NT1; ++nt) {
-                dmma884(cfr[(2 * m) % NCH][nt], av.x, vb[nt][2 * m]);
-                dmma884(cfr[(2 * m + 1) % NCH][nt], av.y, vb[nt][2 * m + 1]);
-            }
-        }
-#pragma unroll
-        for (int h = 1; h < NCH; ++h)
-#pragma unroll
-            for (int nt = 0; nt < NT1; ++nt) {
-                cfr[0][nt][0] += cfr[h][nt][0];
-                cfr[0][nt][1] += cfr[h][nt][1];
-            }
-        double* rb = red + (size_t)(i & 1) * NW * V + warp * V + g4 * NDOT;
-#pragma unroll
-        for (int nt = 0; nt < NT1; ++nt)
-            if (nt * 8 + 2 * t4 < NDOT)
-                *reinterpret_cast<double2*>(rb + nt * 8 + 2 * t4) = make_double2(cfr[0][nt][0], cfr[0][nt][1]);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pfull[i & 1]);
-    };
-    // ---- phase2(j): W = psi o Y for stage j, G += X_j^T W from the held fragments
-    auto phase2 = [&](int j) {
-        const int e = j % E;
-        const long long srow0 = r0 + (long long)j * 8;
-        mbar_wait(&xfull[e], (uint32_t)((j / E) & 1));  // CTA scope: the st.async bytes complete here
-        if (tid == 0 && j + E < nst) mbar_arrive_expect_tx(&xfull[e], kXBytes);
-        const double* xb = xchg + (size_t)e * V * C;
-        // both rows' partial pairs are loaded before any add (no branch around
-        // the loads: g4 >= K reads finite neighbours, then is masked)
-        double wf[2];
-        double2 py[2][C / 2], pv[2][C / 2];
-#pragma unroll
-        for (int kh = 0; kh < 2; ++kh) {
-            const double* yp = xb + (size_t)((kh * 4 + t4) * NDOT + (g4 < K ? g4 : 0)) * C;
-#pragma unroll
-            for (int q = 0; q < C / 2; ++q) {
-                py[kh][q] = *reinterpret_cast<const double2*>(yp + 2 * q);
-                if constexpr (OP == Op::THIRD) pv[kh][q] = *reinterpret_cast<const double2*>(yp + (size_t)K * C + 2 * q);
-            }
-        }
-#pragma unroll
-        for (int kh = 0; kh < 2; ++kh) {
-            double y = 0.0, yv = 0.0;
-#pragma unroll
-            for (int q = 0; q < C / 2; ++q) {
-                y += py[kh][q].x;
-                y += py[kh][q].y;
-                if constexpr (OP == Op::THIRD) {
-                    yv += pv[kh][q].x;
-                    yv += pv[kh][q].y;
-                }
-            }
-            const bool valid = (srow0 + kh * 4 + t4 < r1) && g4 < K;
-            double w;
-            if constexpr (OP == Op::HVP)
-                w = pp[kh] * y;
-            else
-                w = pp[kh] * y * yv;
-            wf[kh] = valid ? w : 0.0;
-        }
-#pragma unroll
-        for (int kh = 0; kh < 2; ++kh)
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) dmma884(acc[mt], f2[kh][mt], wf[kh]);
-    };
-    // ---- frag(i): stage i's phase-2 fragments into registers, release the slot
-    auto frag = [&](int i, int slot) {
-        const double* X = ring + slot * stage_elems + p2_off;
-#pragma unroll
-        for (int kh = 0; kh < 2; ++kh)
-#pragma unroll
-            for (int p = 0; p < MP; ++p) {
-                const double2 v = *reinterpret_cast<const double2*>(X + kh * 4 * RS + 16 * p);
-                f2[kh][2 * p] = v.x;
-                f2[kh][2 * p + 1] = v.y;
-            }
-#pragma unroll
-        for (int kh = 0; kh < 2; ++kh) {
-            const double zt = zn[kh];
-            if constexpr (OP == Op::HVP)
-                pp[kh] = 2.0 * c2 - 6.0 * c3 * zt + 12.0 * c4 * (zt * zt);
-            else
-                pp[kh] = -6.0 * c3 + 24.0 * c4 * zt;
-        }
-        __syncwarp();
-        if (lane == 0) {
-            rel_old = atom_add_acq_rel(&cnt[slot], 1u);  // the last warp out refills (checked next step)
-            if (i + S < nst) {
-                refill = i + S;
-                refill_slot = slot;
-            }
-        }
-        // z of stage i+1, a whole iteration ahead and after the release (whose
-        // fence waits for outstanding loads)
-        if (i + 1 < nst) {
-            const long long nrow0 = r0 + (long long)(i + 1) * 8;
-            zn[0] = (nrow0 + t4 < r1) ? __ldg(a.z + nrow0 + t4) : 0.0;
-            zn[1] = (nrow0 + 4 + t4 < r1) ? __ldg(a.z + nrow0 + 4 + t4) : 0.0;
-        }
-    };
-    auto do_refill = [&]() {
-        if (refill >= 0) {  // lane 0 only
-            if ((rel_old + 1) % NW == 0) issue(refill, refill_slot);
-            refill = -1;
-        }
-    };
-
-    if (nst > 0) {
-        phase1(0, 0, 0u);
-        frag(0, 0);
-        int slot = 1, fpar = 0;
-        if (slot == S) {
-            slot = 0;
-            fpar = 1;
-        }
-        for (int i = 1; i < nst; ++i) {
-            do_refill();
-            reduce(i - 1);
-            phase1(i, slot, (uint32_t)fpar);
-            phase2(i - 1);
-            frag(i, slot);
-            if (++slot == S) {
-                slot = 0;
-                fpar ^= 1;
-            }
-        }
-        do_refill();
-        reduce(nst - 1);
-        phase2(nst - 1);
-    }
-
-#pragma unroll
-    for (int p = 0; p < MP; ++p)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int c = wcol + 16 * p + 2 * g4 + h;
-                const int k = 2 * t4 + q;
-                if (c < cw && k < K) a.part_acc[((size_t)ci * K + k) * ld + col0 + c] = acc[2 * p + h][q];
-            }
-    cluster.sync();  // no CTA exits while a peer may still push into it
-}
-
-// ---------------------------------------------------------------------------
 // Warp-specialised variant: 8 math warps + one helper warpgroup.
 //
-// The pipelined kernel above is bounded by its per-stage skeleton running in
-// lock-step with the DMMA phases in all 8 warps (profiles/r01_dmma_pipe.txt).
-// Here the skeleton moves to a helper warpgroup (registers rebalanced with
+// An intermediate generation (barrier-free stage loop, all 8 warps doing skeleton
+// and DMMA in lock-step; profiles/r01_dmma_pipe.txt: 2.06 ms on the C5 8-RHS
+// HVP) was bounded by its per-stage skeleton and has been removed. Here the
+// skeleton moves to a helper warpgroup (registers rebalanced with
 // setmaxnreg: 232 per math thread, 40 per helper thread):
 //   warp 8   TMA producer: refills a ring slot once the 8 math warps released it
 //   warp 9   reducer: sums the 8 warp partials of a stage, pushes the C-CTA

@@ -1,6 +1,7 @@
 """A/B timing of the multi-RHS tensor-core passes: warp-specialised kernel
-(ws, the default) vs pipelined (MVSK_DMMA_PIPE=1) vs v1 (MVSK_DMMA_V1=1), plus a bitwise/relative comparison of the
-two results. python scripts/dmma_ab.py C5 hvp8,third8,hvp4 ws,pipe,v1"""
+(ws, the default) vs v1 (MVSK_DMMA_V1=1), plus a relative comparison of the
+results. python scripts/dmma_ab.py C5 hvp8,third8,hvp4 ws,v1
+(another build of the library: MVSK_B200_LIB=<path> python scripts/dmma_ab.py C5 hvp8 ws)"""
 import os
 import sys
 from pathlib import Path
@@ -13,7 +14,7 @@ from paper_2604_25378_b200.gpu_oracle import GpuOracle  # noqa
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
 ops = sys.argv[2].split(",") if len(sys.argv) > 2 else ["hvp8", "third8"]
-variants = sys.argv[3].split(",") if len(sys.argv) > 3 else ["pipe", "v1"]
+variants = sys.argv[3].split(",") if len(sys.argv) > 3 else ["ws", "v1"]
 spec = CONFIGS[cfg]
 dev = torch.device("cuda", 0)
 X = raw_returns(spec, 5000, device=dev)
@@ -61,10 +62,7 @@ for op in ops:
     res = {}
     for var in variants:
         os.environ.pop("MVSK_DMMA_V1", None)
-        os.environ.pop("MVSK_DMMA_PIPE", None)
-        if var == "pipe":
-            os.environ["MVSK_DMMA_PIPE"] = "1"
-        elif var == "v1":
+        if var == "v1":
             os.environ["MVSK_DMMA_V1"] = "1"
         out.zero_()
         fn()

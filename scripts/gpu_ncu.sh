@@ -1,3 +1,6 @@
+# One `ncu --set full` capture (+ raw / SASS / source pages as CSV) per hot kernel, each after the same
+# command has exited 0 without ncu:  gpurun -- 'bash scripts/gpu_ncu.sh'
+# Summarise a SASS page with scripts/sass_hotspots.py; copy what should be judged into profiles/.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 prof() {  # name op reps cfg kernel-regex skip
@@ -6,11 +9,11 @@ prof() {  # name op reps cfg kernel-regex skip
   echo "$1 rc $?"
   ncu -i /tmp/$1.ncu-rep --page raw --csv > gpurun_out/$1_raw.csv 2>/dev/null
   ncu -i /tmp/$1.ncu-rep --page source --csv --print-source sass > gpurun_out/$1_sass.csv 2>/dev/null
-  ncu -i /tmp/$1.ncu-rep --page source --csv --print-source cuda > gpurun_out/$1_src.csv 2>/dev/null
   ncu -i /tmp/$1.ncu-rep --page details > gpurun_out/$1_details.txt 2>/dev/null
   rm -f /tmp/$1.ncu-rep
 }
-prof r2_c4_fgrad fgrad 4 C4 stream_kernel 3
-prof r2_c5_hvp8 hvp8 3 C5 stream_dmma 2
-prof r2_c5_hvp1 hvp1 4 C5 stream_kernel 3
+prof ncu_c5_hvp1 hvp1 4 C5 stream_kernel 3
+prof ncu_c5_hvp8 hvp8 3 C5 stream_dmma 2
+prof ncu_c5_third8 third8 3 C5 stream_dmma 2
+prof ncu_c4_fgrad fgrad 4 C4 stream_kernel 3
 du -sh gpurun_out
