@@ -139,6 +139,36 @@ def test_descent_identity_and_direction_parity():  # test_affine_normal.cpp:44-7
     assert checked >= 20
 
 
+@pytest.mark.parametrize("kind", ["spd", "indefinite"])
+def test_device_direct_branch_matches_the_reference(kind):  # affine_normal.hpp:151-188
+    """Panels of >= 64 columns run the direct branch on the device (gram_pcg.cu: Gram, h, M, inverse, P in one
+    cluster kernel). "spd": the register-tiled unpivoted sweep; "indefinite": psi'' < 0 on most samples makes M
+    indefinite, the sweep meets a non-positive pivot and the kernel falls back to its partial-pivot sweep, the
+    reference's PartialPivLU semantics. Both against the CPU oracle's direct direction."""
+    from paper_2604_25378_b200.gpu_oracle import tangent_config
+    n, T = 72, 400
+    A, mu = rh.lcg_panel(n, T, 5)
+    c = rh.crra(6.0) if kind == "spd" else np.array([1.0, 0.1, 50.0, 1.0])
+    cpu, gpu = po.CpuOracle(A, mu, c), _gpu(A, mu, c)
+    x = rh.simplex_point(n, 17, 1e-6)
+    cc, gc = cpu.make_cache(x), gpu.make_cache(x)
+    z = A @ x
+    psi2 = 2 * c[1] - 6 * c[2] * z + 12 * c[3] * z * z
+    ev = np.linalg.eigvalsh((A.T * psi2) @ A / T)
+    if kind == "spd":
+        assert ev[0] > 0
+    else:
+        assert ev[2] < 0  # M compresses G to codimension 2: its smallest eigenvalue is <= ev[2] < 0
+    g = cpu.gradient(cc)
+    gn = np.linalg.norm(po.basis_apply_transpose(n, g))
+    dc, diag_c = cpu.yand_direction(cc, po.tangent_config("direct"), 3)
+    dg, diag_g = gpu.yand_direction(gc, tangent_config("direct"), 3)
+    assert diag_g.lambda_fallback == diag_c.lambda_fallback
+    assert abs(g @ dg + gn) <= 1e-9 * (1 + gn)
+    assert abs(dg.sum()) <= 1e-12 * (1 + np.linalg.norm(dg))
+    assert np.max(np.abs(dg - dc)) <= 1e-8 * (1 + np.max(np.abs(dc)))
+
+
 def test_direct_vs_exact_pcg():  # test_affine_normal.cpp:75-100
     from paper_2604_25378_b200.gpu_oracle import tangent_config
     n = 6
