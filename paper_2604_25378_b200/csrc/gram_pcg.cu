@@ -169,17 +169,34 @@ __device__ void cg_warp(const double* M, int ldm, int mm, double lambda, const d
     nh = 0;
     bd = 0;
     while (it < cap && rn > target) {
-        for (int i = lane; i < mm; i += 32) {
-            const double* mr = M + (size_t)i * ldm;
-            double s0 = 0.0, s1 = 0.0;
+        // M p: a lane's rows i, i + 32 run together, four accumulators each, so
+        // eight independent FMA chains hide the fp64 latency (one row at a time
+        // with two chains made the matvec ~80 % of a CG step)
+        for (int i0 = lane; i0 < mm; i0 += 64) {
+            const int i1 = i0 + 32;
+            const bool two = i1 < mm;
+            const double* m0 = M + (size_t)i0 * ldm;
+            const double* m1 = M + (size_t)(two ? i1 : i0) * ldm;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
             int j = 0;
-#pragma unroll 4
-            for (; j + 1 < mm; j += 2) {
-                s0 = fma(mr[j], p[j], s0);
-                s1 = fma(mr[j + 1], p[j + 1], s1);
+#pragma unroll 2
+            for (; j + 3 < mm; j += 4) {
+                const double p0 = p[j], p1 = p[j + 1], p2 = p[j + 2], p3 = p[j + 3];
+                a0 = fma(m0[j], p0, a0);
+                a1 = fma(m0[j + 1], p1, a1);
+                a2 = fma(m0[j + 2], p2, a2);
+                a3 = fma(m0[j + 3], p3, a3);
+                b0 = fma(m1[j], p0, b0);
+                b1 = fma(m1[j + 1], p1, b1);
+                b2 = fma(m1[j + 2], p2, b2);
+                b3 = fma(m1[j + 3], p3, b3);
             }
-            if (j < mm) s0 = fma(mr[j], p[j], s0);
-            hp[i] = (s0 + s1) + lambda * p[i];
+            for (; j < mm; ++j) {
+                a0 = fma(m0[j], p[j], a0);
+                b0 = fma(m1[j], p[j], b0);
+            }
+            hp[i0] = ((a0 + a1) + (a2 + a3)) + lambda * p[i0];
+            if (two) hp[i1] = ((b0 + b1) + (b2 + b3)) + lambda * p[i1];
         }
         __syncwarp();
         const double pHp = warp_dot(p, hp, mm, lane);
