@@ -64,8 +64,10 @@ def timeit(fn, reps=20):
     return a.elapsed_time(b) / reps
 
 
-plans = ["", "0,0,0,0,0,0", "16,2,1,3,0,1", "8,1,2,2,0,0", "8,1,2,3,0,0", "8,1,2,2,0,1", "8,1,2,3,0,1",
-         "8,1,1,3,0,0", "8,1,1,4,0,0", "8,1,1,5,0,0"]
+# MVSK_TUNE fields: Q, G, RG, S, OCC, VS
+plans = ["", "8,1,2,2,0,0", "16,2,1,3,0,1", "16,2,1,2,0,1", "8,1,1,3,0,0"]
+if len(sys.argv) > 2:
+    plans = [""] + sys.argv[2:]
 for op, (fn, get) in FN.items():
     ref = None
     for p in plans:
