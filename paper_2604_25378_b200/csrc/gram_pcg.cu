@@ -42,6 +42,7 @@ constexpr int kGpMaxM = 112;     // face width limit (two m x m fp64 buffers in 
 constexpr int kGpMaxCols = 8;    // Hutchinson probes handled in one lock-step block
 constexpr int kGpThreads = 512;
 constexpr int kDirectDeviceMinLd = 64;  // narrower panels take the host LU / Cholesky direct branch
+constexpr int kDirectDeviceMaxLd = 512;
 constexpr int kGraphGramPcg = 102;
 constexpr int kGraphGramDirect = 103;
 
@@ -1281,6 +1282,9 @@ bool direct_direction_device(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, con
     static const bool force_on = std::getenv("MVSK_DEVICE_DIRECT") != nullptr;
     static const bool force_off = std::getenv("MVSK_NO_DEVICE_DIRECT") != nullptr;
     if (force_off || (!force_on && ctx->ld < kDirectDeviceMinLd)) return false;
+    // P is scattered into a zero-filled ld x ld matrix by one CTA: index-map faces of wide panels (only
+    // reachable with face compaction switched off) stay on the host path
+    if (ctx->ld > kDirectDeviceMaxLd) return false;
     const int mm = m - 2;
     const int mp = gp_stage_stride(m, (int)ctx->ld);
     // 512 doubles less than the PCG setup: the static buffers of spd_inverse_tiled
