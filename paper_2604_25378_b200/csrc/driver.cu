@@ -489,6 +489,30 @@ struct View {
         for (int i = 0; i < k; ++i) out.emplace_back(o.begin() + (size_t)i * fm.m, o.begin() + (size_t)(i + 1) * fm.m);
         return out;
     }
+    // k line models at the same cache in one round trip (op_line_models); a0 = NaN marks a direction the
+    // single call would reject. Logical passes are counted when a model is consumed (count_line_model).
+    std::vector<LineModel> line_models(int slot, const std::vector<const Vec*>& dirs, const std::vector<double>& caps) const {
+        Tick tk(g_prof.line);
+        const int k = (int)dirs.size();
+        Vec D((size_t)k * (size_t)fm.m), o((size_t)k * 14);
+        for (int i = 0; i < k; ++i) std::copy(dirs[(size_t)i]->begin(), dirs[(size_t)i]->end(), D.begin() + (size_t)i * fm.m);
+        op_line_models(ctx, slot, fm, D.data(), k, o.data());
+        std::vector<LineModel> out((size_t)k);
+        for (int i = 0; i < k; ++i) {
+            LineModel& lm = out[(size_t)i];
+            lm.a0 = o[(size_t)i * 14];
+            lm.a1 = o[(size_t)i * 14 + 1];
+            lm.a2 = o[(size_t)i * 14 + 2];
+            lm.a3 = o[(size_t)i * 14 + 3];
+            lm.a4 = o[(size_t)i * 14 + 4];
+            lm.cap = caps[(size_t)i];
+        }
+        return out;
+    }
+    void count_line_model() const {
+        ++g_prof.nline;
+        ctx->fwd += 1;
+    }
     LineModel line_model(int slot, const Vec& d, double cap) const {
         Tick tk(g_prof.line);
         ++g_prof.nline;
@@ -1222,14 +1246,14 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
             rep.krylov += dd.krylov_iters;
             const double amax = alpha_max(xf, d, tau);
             bool moved = false;
-            auto exact_step = [&](const Vec& dir, double cap) {  // :437-446
-                const LineModel lm = face.line_model(kSlotFace, dir, cap);
+            auto step_from = [&](const LineModel& lm) {  // :437-446
                 if (config.armijo) {
-                    auto res = armijo_search([&](double al) { return lm.eval(al); }, lm.a1, std::min(1.0, cap));
+                    auto res = armijo_search([&](double al) { return lm.eval(al); }, lm.a1, std::min(1.0, lm.cap));
                     return std::pair<double, double>{res.first, lm.eval(res.first)};
                 }
                 return minimize_line(lm);
             };
+            auto exact_step = [&](const Vec& dir, double cap) { return step_from(face.line_model(kSlotFace, dir, cap)); };
             if (amax >= t_cur) {
                 auto st = exact_step(d, amax);
                 if (st.first > 0) {
@@ -1241,8 +1265,22 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
                 for (long long i = 0; i < nf; ++i) floor0[(size_t)i] = xf[(size_t)i] <= tau + 1e-12;
                 std::vector<std::vector<char>> zsets;
                 std::vector<long long> zset_sizes;
+                // The ladder's rungs (trial step t_cur / 2^rung, projected) depend on xf, d and the projections
+                // only, never on earlier rungs' line searches, so the loop of :454-562 is walked lazily: rung by
+                // rung as the reference visits them, and once a rung's exact step has failed the line models of
+                // ALL remaining rungs are evaluated in one graph launch and one round trip (k independent
+                // line-sums passes, each bitwise the single-direction pass), then consumed in order.
+                struct Rung {
+                    Vec db;
+                    double cap = 0.0;
+                    bool step = false;  // takes an exact step (else skipped: tiny or non-descent direction)
+                    bool stop = false;  // the ladder ends after this rung (newz == 0)
+                    bool have = false;
+                    LineModel lm;
+                };
+                std::vector<Rung> rungs;
                 double t_len = t_cur;
-                for (int rung = 0; rung < 6; ++rung) {
+                auto next_rung = [&]() {
                     Vec trial(xf.size());
                     for (size_t i = 0; i < xf.size(); ++i) trial[i] = xf[i] + t_len * d[i];
                     const Vec xb = project_slice(trial, tau, mass);
@@ -1257,25 +1295,58 @@ Report solve(mvsk_gpu_ctx* ctx, const SolveCfg& config, Vec x0,
                         zsets.push_back(zb);
                         zset_sizes.push_back(zb_count);
                     }
-                    Vec db(xf.size());
-                    for (size_t i = 0; i < xf.size(); ++i) db[i] = xb[i] - xf[i];
-                    const double dbm = vmean(db);
-                    for (double& v : db) v -= dbm;
-                    const double dbn = norm(db);
-                    if (dbn <= 1e-12 * std::max(1.0, norm(xf)) || dot(gf, db) >= -1e-10 * (1.0 + std::abs(fcur))) {
-                        if (newz == 0) break;
-                        t_len *= 0.5;
-                        continue;
-                    }
-                    const double cap = std::min(1.0, alpha_max(xf, db, tau));
-                    auto st = exact_step(db, cap);
-                    if (st.first > 0 && (rung == 0 || fcur - st.second >= 1e-12 * (1.0 + std::abs(fcur)))) {
-                        axpy(xf, st.first, db);
-                        moved = true;
-                        break;
-                    }
-                    if (newz == 0) break;
+                    Rung R;
+                    R.db.resize(xf.size());
+                    for (size_t i = 0; i < xf.size(); ++i) R.db[i] = xb[i] - xf[i];
+                    const double dbm = vmean(R.db);
+                    for (double& v : R.db) v -= dbm;
+                    const double dbn = norm(R.db);
+                    R.step = !(dbn <= 1e-12 * std::max(1.0, norm(xf)) || dot(gf, R.db) >= -1e-10 * (1.0 + std::abs(fcur)));
+                    if (R.step) R.cap = std::min(1.0, alpha_max(xf, R.db, tau));
+                    R.stop = newz == 0;
+                    rungs.push_back(std::move(R));
                     t_len *= 0.5;
+                };
+                bool any_failed = false;
+                for (int rung = 0; rung < 6; ++rung) {
+                    if ((int)rungs.size() <= rung) next_rung();
+                    if (rungs[(size_t)rung].step) {
+                        if (!rungs[(size_t)rung].have && any_failed) {
+                            while ((int)rungs.size() < 6 && !rungs.back().stop) next_rung();
+                            std::vector<size_t> want;
+                            for (size_t q = (size_t)rung; q < rungs.size(); ++q)
+                                if (rungs[q].step && !rungs[q].have) want.push_back(q);
+                            if (want.size() > 1) {
+                                std::vector<const Vec*> dirs;
+                                std::vector<double> caps;
+                                for (size_t q : want) {
+                                    dirs.push_back(&rungs[q].db);
+                                    caps.push_back(rungs[q].cap);
+                                }
+                                const std::vector<LineModel> lms = face.line_models(kSlotFace, dirs, caps);
+                                for (size_t e = 0; e < want.size(); ++e)
+                                    if (std::isfinite(lms[e].a0)) {
+                                        rungs[want[e]].lm = lms[e];
+                                        rungs[want[e]].have = true;
+                                    }
+                            }
+                        }
+                        Rung& R = rungs[(size_t)rung];
+                        if (R.have) {
+                            face.count_line_model();  // a batch-evaluated rung is consumed: one reference pass
+                        } else {
+                            R.lm = face.line_model(kSlotFace, R.db, R.cap);
+                            R.have = true;
+                        }
+                        auto st = step_from(R.lm);
+                        if (st.first > 0 && (rung == 0 || fcur - st.second >= 1e-12 * (1.0 + std::abs(fcur)))) {
+                            axpy(xf, st.first, R.db);
+                            moved = true;
+                            break;
+                        }
+                        any_failed = true;
+                    }
+                    if (rungs[(size_t)rung].stop) break;
                 }
                 if (!moved) {
                     bool done = false;

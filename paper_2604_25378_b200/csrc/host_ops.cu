@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <functional>
 
 #include "host_ops.hpp"
@@ -339,6 +340,63 @@ void op_line_model(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double*
     out[3] = -c.c3 * s[6] + 4.0 * c.c4 * s[7];
     out[4] = c.c4 * s[8];
     for (int i = 0; i < 9; ++i) out[5 + i] = s[i];
+}
+
+// k line models along k directions at the same cache in ONE graph launch and
+// one round trip: k independent LINESUMS passes, each bitwise the pass
+// op_line_model runs for that direction (the boundary ladder's rungs,
+// solver.hpp:448-562, evaluated together once the first rung has failed). A
+// direction that op_line_model would reject (zero, or not tangent) gets a NaN
+// a0 instead of an exception: the caller re-runs it singly if it is ever
+// consumed. Logical pass counters are left to the caller (only consumed rungs
+// count as reference passes).
+void op_line_models(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* D, int k, double* out) {
+    check_slot(ctx, slot);
+    if (k < 1 || k > 8) throw ApiError(MVSK_DIMENSION_ERROR, "line_models: 1 <= k <= 8");
+    const long long m = fm.m;
+    bool ok[8];
+    for (int j = 0; j < k; ++j) {
+        const double* d = D + (size_t)j * m;
+        double dn2 = 0.0, dsum = 0.0;
+        for (long long i = 0; i < m; ++i) {
+            dn2 += d[i] * d[i];
+            dsum += d[i];
+        }
+        const double dn = std::sqrt(dn2);
+        ok[j] = dn > 0 && !(std::abs(dsum) > 1e-10 * dn);
+    }
+    ensure_host_staging(ctx, (size_t)MVSK_GPU_MAX_RHS * 2 * ctx->ld);
+    stage_host(ctx, fm, D, k, 0.0, 0);
+    constexpr int kGraphLineMulti = 110;
+    run_graphed(ctx, kGraphLineMulti, k, slot, [&] {
+        copy_in(ctx, k, 0);
+        for (int j = 0; j < k; ++j) {
+            PassIO io;
+            io.vin = ctx->vin + (size_t)j * ctx->ld;
+            io.z = ctx->slots[slot].z;
+            io.out = ctx->outd + (size_t)j * 16;
+            io.hout = ctx->h_out_dev + (size_t)j * 16;
+            run_pass(ctx, Op::LINESUMS, 1, io);
+        }
+    });
+    MVSK_CUDA(cudaStreamSynchronize(ctx->stream));
+    const mvsk_coeffs& c = ctx->c;
+    const double f0 = op_value(ctx, slot);
+    for (int j = 0; j < k; ++j) {
+        const double* d = D + (size_t)j * m;
+        double s[9];
+        std::memcpy(s, ctx->h_out + (size_t)j * 16, sizeof(s));
+        double mud = 0.0;  // mu_f' d_f
+        for (long long i = 0; i < m; ++i) mud += ctx->mu[fm.active ? fm.idx[i] : i] * d[i];
+        double* o = out + (size_t)j * 14;
+        // linesearch.hpp:72-78
+        o[0] = ok[j] ? f0 : std::numeric_limits<double>::quiet_NaN();
+        o[1] = -c.c1 * mud + 2.0 * c.c2 * s[0] - 3.0 * c.c3 * s[1] + 4.0 * c.c4 * s[2];
+        o[2] = c.c2 * s[3] - 3.0 * c.c3 * s[4] + 6.0 * c.c4 * s[5];
+        o[3] = -c.c3 * s[6] + 4.0 * c.c4 * s[7];
+        o[4] = c.c4 * s[8];
+        for (int i = 0; i < 9; ++i) o[5 + i] = s[i];
+    }
 }
 
 static void ensure_h_mat(mvsk_gpu_ctx* ctx, size_t elems) {

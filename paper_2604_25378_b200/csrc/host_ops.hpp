@@ -36,6 +36,8 @@ void op_third(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* U, c
 void op_psi2(mvsk_gpu_ctx* ctx, int slot, double* out);
 void op_sample_direction(mvsk_gpu_ctx* ctx, const FaceMap& fm, const double* d, double* out);
 void op_line_model(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* d, double out[14]);
+// k line models in one graph launch (k x 14 doubles out; a0 = NaN marks a direction op_line_model would reject)
+void op_line_models(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, const double* D, int k, double* out);
 // weighted Gram over the face columns: G_f = A_f^T diag(psi''(z)) A_f / T (m x m)
 void op_weighted_gram(mvsk_gpu_ctx* ctx, int slot, const FaceMap& fm, double* G);
 // q_t = a_t^T P a_t for a symmetric face-coordinate P (m x m), then
