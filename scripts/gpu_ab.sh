@@ -9,8 +9,8 @@ for rep in 1 2; do
   set -- "$@"
   args=("$@")
   for ((i=0; i<${#args[@]}; i+=2)); do
-    echo "== new ${args[i]}"; python scripts/dmma_ab.py ${args[i]} ${args[i+1]} ws
-    echo "== base ${args[i]}"; MVSK_B200_LIB=$AB python scripts/dmma_ab.py ${args[i]} ${args[i+1]} ws
+    echo "== new ${args[i]}"; timeout 300 python scripts/dmma_ab.py ${args[i]} ${args[i+1]} ws
+    echo "== base ${args[i]}"; MVSK_B200_LIB=$AB timeout 300 python scripts/dmma_ab.py ${args[i]} ${args[i+1]} ws
   done
 done
 } > $out 2>&1
