@@ -213,6 +213,14 @@ int32_t mvsk_gpu_sample_direction(mvsk_gpu_ctx* ctx, const double* d, double* ou
  * sums s11,s21,s31,s02,s12,s22,s03,s13,s04 (PowerSums, :16-20); 1 pass. */
 int32_t mvsk_gpu_line_model(mvsk_gpu_ctx* ctx, int32_t slot, const double* d, double cap,
                             double out[14]);
+/* k line models at the same cache in one graph launch and one round trip
+ * (1 <= k <= 8): D is k x nf row-major, out is k x 14 laid out as above. Each
+ * model is bitwise what mvsk_gpu_line_model returns for that direction; the
+ * solve driver uses it for the rungs of the boundary ladder
+ * (solver.hpp:448-562). A direction that line_model would reject (zero, or not
+ * tangent to the simplex) gets a0 = NaN instead of a domain_error. Counts k
+ * logical passes. */
+int32_t mvsk_gpu_line_models(mvsk_gpu_ctx* ctx, int32_t slot, const double* D, int32_t k, double* out);
 /* PassCounter (common.hpp:31-37) plus physical streaming passes */
 int32_t mvsk_gpu_passes(const mvsk_gpu_ctx* ctx, uint64_t* forward, uint64_t* transpose,
                         uint64_t* physical);

@@ -158,6 +158,7 @@ SIGNATURES = [
     ("mvsk_gpu_hessian_diag_weights", _I32, [_P, _I32, _D]),
     ("mvsk_gpu_sample_direction", _I32, [_P, _D, _D]),
     ("mvsk_gpu_line_model", _I32, [_P, _I32, _D, C.c_double, _D]),
+    ("mvsk_gpu_line_models", _I32, [_P, _I32, _D, _I32, _D]),
     ("mvsk_gpu_passes", _I32, [_P, _U64P, _U64P, _U64P]),
     ("mvsk_gpu_reset_passes", _I32, [_P]),
     ("mvsk_gpu_launch_count", _I32, [_P, _U64P]),

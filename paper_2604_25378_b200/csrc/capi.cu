@@ -436,6 +436,14 @@ int32_t mvsk_gpu_line_model(mvsk_gpu_ctx* ctx, int32_t slot, const double* d, do
     });
 }
 
+int32_t mvsk_gpu_line_models(mvsk_gpu_ctx* ctx, int32_t slot, const double* D, int32_t k, double* out) {
+    return guard(ctx, [&] {
+        set_device(ctx);
+        op_line_models(ctx, slot, ctx->pub_face, D, k, out);
+        ctx->fwd += (uint64_t)k;
+    });
+}
+
 int32_t mvsk_gpu_weighted_gram(mvsk_gpu_ctx* ctx, int32_t slot, double* G_out) {
     return guard(ctx, [&] {
         set_device(ctx);

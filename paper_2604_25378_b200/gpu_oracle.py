@@ -333,6 +333,17 @@ class GpuOracle:
         self._chk(self.lib.mvsk_gpu_line_model(self._ctx, cache.slot, _p(d), C.c_double(cap), _p(out)))
         return LineModel(*out[:5], cap, out[5:].copy())
 
+    def line_models(self, cache: OracleCache, D, caps):
+        """k line models in one round trip (mvsk_gpu_line_models): D is k x m; a
+        rejected direction comes back with a0 = NaN instead of raising."""
+        D = np.ascontiguousarray(np.asarray(D, dtype=np.float64))
+        if D.ndim != 2 or D.shape[1] != self._m:
+            raise DimensionError("line_models: D must be k x m")
+        k = D.shape[0]
+        out = np.empty((k, 14))
+        self._chk(self.lib.mvsk_gpu_line_models(self._ctx, cache.slot, _p(D), k, _p(out)))
+        return [LineModel(*out[i, :5], float(caps[i]), out[i, 5:].copy()) for i in range(k)]
+
     def yand_direction(self, cache: OracleCache, cfg: mvsk_tangent_config, it_seed: int = 0):
         d = np.empty(self._m)
         diag = mvsk_direction_diag()

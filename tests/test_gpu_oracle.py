@@ -135,6 +135,40 @@ def test_line_model(n, T, seed):
         gpu.line_model(gc, np.zeros(n), 1.0)
 
 
+def test_line_models_batch_is_bitwise_the_single_calls():  # linesearch.hpp:62-81, solver.hpp:448-562
+    """mvsk_gpu_line_models (the boundary ladder's rungs in one round trip) against k single line_model
+    calls: identical bits, on a narrow panel (small-pass kernels), a C2-sized one and a face view; a
+    non-tangent direction comes back marked instead of raising; k passes are counted."""
+    for n, T, face in ((12, 60, False), (100, 400, False), (100, 400, True)):
+        A, mu = rh.lcg_panel(n, T, 3)
+        gpu = _gpu(A, mu, rh.crra(5.0))
+        if face:
+            free = np.arange(0, n, 2)
+            gpu.set_face(free, 1e-4)
+            x = np.full(free.size, (1.0 - 1e-4 * (n - free.size)) / free.size)
+            m = free.size
+        else:
+            x = rh.simplex_point(n, 5, 1e-6)
+            m = n
+        gc = gpu.make_cache(x)
+        rng = np.random.default_rng(7)
+        D = rng.standard_normal((5, m))
+        D -= D.mean(axis=1, keepdims=True)
+        for rep in range(4):  # eager, capture and replay of the k-direction graph
+            singles = [gpu.line_model(gc, D[i], 0.5) for i in range(5)]
+            f0, t0, _ = gpu.passes()
+            batch = gpu.line_models(gc, D, [0.5] * 5)
+            assert gpu.passes()[0] - f0 == 5
+            for a, b in zip(singles, batch):
+                assert (a.a0, a.a1, a.a2, a.a3, a.a4) == (b.a0, b.a1, b.a2, b.a3, b.a4)
+                assert np.array_equal(a.sums, b.sums)
+        bad = D.copy()
+        bad[2] += 1.0  # not tangent
+        out = gpu.line_models(gc, bad, [0.5] * 5)
+        assert np.isnan(out[2].a0) and all(np.isfinite(out[i].a0) for i in (0, 1, 3, 4))
+        gpu.close()
+
+
 def test_pass_count_contract():  # test_oracle.cpp:126-154
     A, mu = rh.lcg_panel(6, 18, 5)
     gpu = _gpu(A, mu, rh.crra(4.0))
