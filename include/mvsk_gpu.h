@@ -36,6 +36,7 @@ extern "C" {
 #define MVSK_GPU_ABI_VERSION 1
 #define MVSK_GPU_MAX_SLOTS 8
 #define MVSK_GPU_MAX_RHS 16
+#define MVSK_GPU_MAX_ASSETS 8192 /* widest panel (columns) a context accepts */
 #define MVSK_NCCL_UNIQUE_ID_BYTES 128
 
 typedef enum {
@@ -127,7 +128,9 @@ int32_t mvsk_gpu_preset(const char* name, mvsk_solver_config* out);
 int32_t mvsk_gpu_nccl_unique_id(void* out /* MVSK_NCCL_UNIQUE_ID_BYTES */);
 
 /* Oracle(const ReturnPanel&, PreferenceCoefficients, ...) (oracle.hpp:31-45):
- * uploads host A (T x n row-major) and mu (n) to `device`. */
+ * uploads host A (T x n row-major) and mu (n) to `device`. Every constructor
+ * returns MVSK_DIMENSION_ERROR for n > MVSK_GPU_MAX_ASSETS (the streaming kernels
+ * stage whole rows; the reference's largest universe has n = 5440). */
 int32_t mvsk_gpu_create(const double* A, int64_t T, int64_t n, const double* mu,
                         const mvsk_coeffs* c, int32_t device, mvsk_gpu_ctx** out);
 /* Row-sharded variant: this rank holds rows [row0, row0 + T_local) of a T_global x n

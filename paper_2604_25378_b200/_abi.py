@@ -17,6 +17,7 @@ LIB_PATH = Path(os.environ.get("MVSK_B200_LIB") or PKG_DIR / "_build" / "libmvsk
 MVSK_GPU_ABI_VERSION = 1
 MVSK_GPU_MAX_SLOTS = 8
 MVSK_GPU_MAX_RHS = 16
+MVSK_GPU_MAX_ASSETS = 8192
 MVSK_NCCL_UNIQUE_ID_BYTES = 128
 
 STATUS_NAMES = {

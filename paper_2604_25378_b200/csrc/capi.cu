@@ -42,6 +42,10 @@ bool finite(const double* v, long long n) {
 mvsk_gpu_ctx* make_ctx(long long T_local, long long row0, long long T_global, long long n, const double* mu,
                        const mvsk_coeffs* c, int device, int nranks, int rank, const void* id) {
     if (n < 1) throw ApiError(MVSK_DIMENSION_ERROR, "oracle: need at least one asset");
+    // the row ring and the per-thread column accumulators of the streaming kernels hold whole rows
+    if (n > MVSK_GPU_MAX_ASSETS)
+        throw ApiError(MVSK_DIMENSION_ERROR, "oracle: this build supports at most " + std::to_string(MVSK_GPU_MAX_ASSETS) +
+                                                 " assets (n = " + std::to_string(n) + ")");
     if (T_global < 1 || T_local < 0 || row0 < 0 || row0 + T_local > T_global)
         throw ApiError(MVSK_DIMENSION_ERROR, "oracle: bad row block");
     if (!mu || !c) throw ApiError(MVSK_DIMENSION_ERROR, "oracle: mu length does not match panel columns");

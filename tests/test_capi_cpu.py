@@ -74,6 +74,15 @@ def test_no_cpu_fallback_without_device():
         GpuOracle(np.zeros((4, 2)), np.zeros(2), [1, 1, 1, 1])
 
 
+def test_width_limit_is_a_dimension_error_at_creation():
+    """n > MVSK_GPU_MAX_ASSETS is rejected by every constructor with the reference's dimension_error
+    (the check precedes any device call, so it also holds on a machine without a GPU)."""
+    from paper_2604_25378_b200.gpu_oracle import DimensionError, GpuOracle
+    n = _abi.MVSK_GPU_MAX_ASSETS + 2
+    with pytest.raises(DimensionError):
+        GpuOracle(np.zeros((2, n)), np.zeros(n), [1, 1, 1, 1])
+
+
 def test_crra_and_centering_mirror():
     from oracle import pyoracle as po
     from paper_2604_25378_b200.gpu_oracle import center_panel, crra_coefficients
