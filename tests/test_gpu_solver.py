@@ -169,6 +169,24 @@ def test_device_direct_branch_matches_the_reference(kind):  # affine_normal.hpp:
     assert np.max(np.abs(dg - dc)) <= 1e-8 * (1 + np.max(np.abs(dc)))
 
 
+@pytest.mark.parametrize("n", [64, 65, 81, 97, 112])
+def test_device_direct_branch_tile_boundaries(n):  # affine_normal.hpp:151-188
+    """The register-tiled inverse owns rows ty + 16 a and columns tx + 32 b: widths around the 16- / 32-wide
+    tile edges up to the m = 112 limit (mm = 62 ... 110), device direct direction against the CPU oracle."""
+    from paper_2604_25378_b200.gpu_oracle import tangent_config
+    T = 300
+    A, mu = rh.lcg_panel(n, T, 11 + n)
+    c = rh.crra(4.0)
+    cpu, gpu = po.CpuOracle(A, mu, c), _gpu(A, mu, c)
+    x = rh.simplex_point(n, 23, 1e-6)
+    cc, gc = cpu.make_cache(x), gpu.make_cache(x)
+    dc, diag_c = cpu.yand_direction(cc, po.tangent_config("direct"), 1)
+    dg, diag_g = gpu.yand_direction(gc, tangent_config("direct"), 1)
+    assert diag_g.lambda_fallback == diag_c.lambda_fallback
+    assert np.max(np.abs(dg - dc)) <= 1e-8 * (1 + np.max(np.abs(dc)))
+    gpu.close()
+
+
 def test_direct_vs_exact_pcg():  # test_affine_normal.cpp:75-100
     from paper_2604_25378_b200.gpu_oracle import tangent_config
     n = 6
