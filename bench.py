@@ -241,6 +241,46 @@ def solve_leg():
     return out
 
 
+def solve_parity_leg():
+    """The north_star solve bar in the bench line itself: GPU solves at epsilon 1e-10 (max_elapsed off) on the
+    seeded BASELINE panels of tests/golden/ref_configs.npz against the solutions the UNMODIFIED reference
+    produced for them (oracle/_ref at fixture time; panels pinned by SHA-256). Per row: status match, same
+    active set, |x - x_ref|_inf (bar: 1e-8) and the relative objective gap. The fixture is test data committed
+    in the repo; nothing under oracle/ or /root/reference is executed here."""
+    import hashlib
+    from paper_2604_25378_b200.datagen import make_panel
+    from paper_2604_25378_b200.gpu_oracle import GpuOracle, preset
+    path = ROOT / "tests" / "golden" / "ref_configs.npz"
+    if not path.exists():
+        return None
+    g = np.load(path)
+    out = []
+    for key, mode in (("C1_s0", "small"), ("C2_k1", "small"), ("C2_k1", "large"), ("C2_k1000", "large"),
+                      ("C3_g5", "large"), ("C3_g20", "large"), ("C4", "large")):
+        if f"{key}__{mode}__x" not in g.files:
+            continue
+        name, seed, kappa, gamma = [str(v) for v in g[f"{key}__spec"]]
+        A, mu, _ = make_panel(name, seed=int(seed), kappa=float(kappa))
+        if hashlib.sha256(np.ascontiguousarray(A).tobytes()).hexdigest() != str(g[f"{key}__sha"]):
+            out.append({"config": key, "preset": mode, "error": "panel generator output changed"})
+            continue
+        go = GpuOracle(A, mu, g[f"{key}__c"])
+        cfg = preset(mode)
+        cfg.has_max_elapsed = 0
+        cfg.epsilon = 1e-10
+        x, rep = go.solve(cfg)
+        xr = g[f"{key}__{mode}__x"]
+        fr, _, sr, itr = [float(v) for v in g[f"{key}__{mode}__meta"]]
+        out.append({"config": key, "preset": mode, "kappa": float(kappa), "gamma": float(gamma), "epsilon": 1e-10,
+                    "dx_inf_vs_reference": float(np.max(np.abs(x - xr))), "bar": 1e-8,
+                    "same_active": bool(np.array_equal(x <= cfg.tau + 1e-12, xr <= cfg.tau + 1e-12)),
+                    "status_match": int(rep.status) == int(sr),
+                    "df_rel": abs(rep.f_star - fr) / max(abs(fr), 1e-300),
+                    "iterations": int(rep.iterations), "reference_iterations": int(itr)})
+        go.close()
+    return out
+
+
 def run_reference(args):
     """--impl reference: the reference's own CPU path on this host's cores, on the
     SAME workload as our arm (full C5 panel: 8 GiB, the same generator and seed,
@@ -518,9 +558,10 @@ def main():
                                  else "C++ restatement (oracle/)")}
 
     # ---- YAND full-solve wall time (the metric's second half), rank 0 at N=1
-    solves = None
+    solves = solve_parity = None
     if rank == 0 and ws == 1 and not args.no_solve:
         solves = solve_leg()
+        solve_parity = solve_parity_leg()
 
     if rank == 0:
         line = {
@@ -537,6 +578,8 @@ def main():
             line["cpu_baseline"] = cpu_base
         if solves is not None:
             line["solve"] = solves
+        if solve_parity is not None:
+            line["solve_parity_eps1e-10"] = solve_parity
         print(json.dumps(line), flush=True)
     gpu.close()
     if ws > 1:
