@@ -167,11 +167,11 @@ def cpu_oracle_module(kind: str):
 def cpu_hvp_full(A: np.ndarray, mu, c, x, v, reps: int = 3):
     """cpu_baseline: ONE thread of the reference's own code (oracle.hpp:92-101,
     reference-faithful build) on the FULL panel: 1 warm-up, lower median of
-    `reps` (bench.hpp:188-191). Returns (HVP/s, seconds per HVP, kind)."""
+    `reps` (bench.hpp:188-191). Returns (HVP/s, seconds per HVP, kind, Hv)."""
     mod, kind = cpu_oracle_module("reference")
     o = mod.CpuOracle(A, mu, c)
     cache = o.make_cache(x)
-    o.hvp(cache, v)
+    hv = np.array(o.hvp(cache, v), dtype=np.float64)
     ts = []
     for _ in range(reps):
         t0 = time.perf_counter()
@@ -179,7 +179,7 @@ def cpu_hvp_full(A: np.ndarray, mu, c, x, v, reps: int = 3):
         ts.append(time.perf_counter() - t0)
     ts.sort()
     t = ts[(len(ts) - 1) // 2]
-    return 1.0 / t, t, kind
+    return 1.0 / t, t, kind, hv
 
 
 def solve_leg():
@@ -548,9 +548,13 @@ def main():
     cpu_base = None
     if rank == 0 and ws == 1:
         A_h = X.cpu().numpy()
-        rate, t_s, kind = cpu_hvp_full(A_h, mu, c, x, V[0])
+        rate, t_s, kind, hv_cpu = cpu_hvp_full(A_h, mu, c, x, V[0])
         del A_h
+        # the same HVP through the C-ABI (the e2e call) against the reference's result: the 1e-11 bar at full size
+        hv_gpu = np.asarray(gpu.hvp(cache0, vh), dtype=np.float64).reshape(-1)
+        hv_err = float(np.max(np.abs(hv_gpu - hv_cpu)) / max(float(np.max(np.abs(hv_cpu))), 1e-300))
         cpu_base = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
+                    "hvp_rel_err_gpu_vs_cpu": hv_err, "hvp_rel_err_bar": 1e-11,
                     "sample": f"one HVP on the full {args.config} panel ({T} x {n}), the reference's two GEMV "
                               f"passes, {t_s:.3f} s each, lower median of 3 after 1 warm-up; "
                               + ("unmodified reference headers over the oracle/ref Eigen stand-in, "
