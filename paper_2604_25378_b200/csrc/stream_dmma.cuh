@@ -306,10 +306,6 @@ __global__ void __launch_bounds__(256, 1) stream_dmma_kernel(const DmmaArgs a) {
 __device__ __forceinline__ void reg_alloc_232() { asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory"); }
 __device__ __forceinline__ void reg_dealloc_40() { asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory"); }
 
-// F2REG = false (the 8 third-action pairs at 128-column slices, whose doubled
-// V fragments leave no room for held phase-2 fragments): phase 2 reads the
-// tile from the ring slot, which is then released after phase 2 instead of
-// after phase 1 (one fill fewer in flight).
 // Ring layout of the warp-specialised kernel. A staged row r of a slot starts at
 // r * RS + ws_row_swz(r) doubles with RS = 8 WC + 8, i.e. at 16-byte chunk
 // (4 r + 2 ((r >> 1) & 1)) mod 8 of the 128-byte bank window: rows 2a and
@@ -325,6 +321,10 @@ __device__ __forceinline__ void reg_dealloc_40() { asm volatile("setmaxnreg.dec.
 __host__ __device__ constexpr int kWsRowStride(int wc) { return 8 * wc + (MVSK_WS_SWZ ? 8 : 4); }
 __device__ __forceinline__ int ws_row_swz(int r) { return MVSK_WS_SWZ ? ((r >> 1) & 1) * 4 : 0; }
 
+// F2REG = false (the 8 third-action pairs at 128-column slices, whose doubled
+// V fragments leave no room for held phase-2 fragments): phase 2 reads the
+// tile from the ring slot, which is then released after phase 2 instead of
+// after phase 1 (one fill fewer in flight).
 template <Op OP, int K, int WC, int C, bool F2REG = true>
 __global__ void __launch_bounds__(384, 1) stream_dmma_ws_kernel(const DmmaArgs a) {
     using Sh = DmmaShape<OP, K>;
