@@ -486,17 +486,17 @@ def main():
     extra = {}
     if not args.no_extra:
         fgrad = lambda: gpu.make_cache_device(0, xd.data_ptr())
-        extra["fgrad_ms"] = timed(fgrad, max(3, args.steps // 2), 2)
-        extra["hvp8_ms"] = timed(lambda: gpu.hvp_device(0, Vd.data_ptr(), 8, out.data_ptr()), max(3, args.steps // 2), 1)
+        extra["fgrad_ms"] = timed(fgrad, max(5, args.steps // 2), 3)
+        extra["hvp8_ms"] = timed(lambda: gpu.hvp_device(0, Vd.data_ptr(), 8, out.data_ptr()), max(5, args.steps // 2), 3)
         extra["hvp8_per_s"] = 8000.0 / extra["hvp8_ms"]
         extra["third_ms"] = timed(lambda: gpu.third_action_device(0, Vd.data_ptr(), Vd[1:].data_ptr(), 1,
-                                                                  out.data_ptr()), max(3, args.steps // 2), 1)
+                                                                  out.data_ptr()), max(5, args.steps // 2), 3)
         extra["linesums_ms"] = timed(lambda: gpu.line_sums_device(0, Vd.data_ptr(), sums.data_ptr()),
-                                     max(3, args.steps // 2), 1)
+                                     max(5, args.steps // 2), 3)
         for k in ("fgrad_ms", "third_ms", "linesums_ms"):
             extra[k.replace("_ms", "_GBps")] = alg_bytes / (extra[k] * 1e-3) / 1e9
         G = torch.empty((n, n), dtype=torch.float64, device=dev)
-        gram_ms = timed(lambda: gpu.weighted_gram_device(0, G.data_ptr()), 1, 1)
+        gram_ms = timed(lambda: gpu.weighted_gram_device(0, G.data_ptr()), 2, 1)  # 149 ms per call
         extra["gram_ms"] = gram_ms
         extra["gram_tflops"] = (T * n * (n + 1.0)) / (gram_ms * 1e-3) / 1e12
         try:  # fp64 tensor-pipe peak measured on this pool (profiles/r01_fp64_peak.json)
@@ -510,7 +510,7 @@ def main():
         # 4*T*n*k (HVP) / 6*T*n*k (THIRD: two row dots per pair) flop on the
         # fp64 tensor pipe; both bounds reported, the larger fraction is binding
         extra["third8_ms"] = timed(lambda: gpu.third_action_device(0, Vd.data_ptr(), Vd.data_ptr(), 8,
-                                                                   out.data_ptr()), max(3, args.steps // 2), 1)
+                                                                   out.data_ptr()), max(5, args.steps // 2), 3)
         extra["hvp8_tflops"] = 4.0 * T_loc * n * 8 / (extra["hvp8_ms"] * 1e-3) / 1e12
         try:
             pk = json.loads((ROOT / "profiles" / "r01_fp64_peak.json").read_text())["dmma_tflops"]
